@@ -1,0 +1,226 @@
+/*
+ * hs_abi.h -- C ABI of the B200 TriForce decode hot path (libhs_b200.so).
+ *
+ * Plain C: device pointers, sizes and a cudaStream_t passed as void*.  No
+ * allocation crosses the boundary (callers own every buffer, including the
+ * workspace), no exceptions: every entry point returns HS_OK or a negative
+ * status whose message is available from hs_last_error().  Statuses map 1:1
+ * onto the reference's exception types (hierspec/errors.py:4-39).
+ *
+ * Each entry point cites the reference operation it replaces
+ * (paths relative to /root/reference/pkg/src/hierspec/).
+ *
+ * Storage model:
+ *   weights   bf16, [out][in] row-major ("K-major"), row stride padded to 64
+ *   norms     fp32
+ *   acts      fp32
+ *   KV        bf16, head-major  [layer][kv_head][slot][head_dim]
+ *   probs     fp64 (matches prob_from_logits, model.py:182-195)
+ */
+#ifndef HS_ABI_H
+#define HS_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_ABI_VERSION 1
+
+/* ---- status codes (errors.py) ----------------------------------------- */
+#define HS_OK            0
+#define HS_ERR_SHAPE    -1   /* ShapeError      errors.py:4   */
+#define HS_ERR_CONTRACT -2   /* ContractError   errors.py:18  */
+#define HS_ERR_CAPACITY -3   /* CapacityError   errors.py:14  */
+#define HS_ERR_FINITE   -4   /* FiniteError     errors.py:8   */
+#define HS_ERR_VALUE    -5   /* ValueError                    */
+#define HS_ERR_CUDA    -10   /* launch / runtime failure      */
+
+const char *hs_last_error(void);
+int hs_abi_version(void);
+int hs_device_sm_count(int device);
+
+/* ---- model descriptor --------------------------------------------------
+ * Replaces ModelWeights.runtime() (model.py:116-143): fused wqkv, fused
+ * gate|up (rows interleaved gate_i, up_i so the SwiGLU epilogue sees both),
+ * transposed to [out][in] bf16.  All pointers are device pointers; layer
+ * tensors are packed with a fixed per-layer stride.                        */
+typedef struct {
+  int n_layers, n_heads, n_kv_heads, head_dim, d_ff, vocab_size, max_seq;
+  int d_model;         /* n_heads * head_dim                         */
+  int ld_d, ld_ff;     /* padded row strides (elements) for K=d, K=d_ff */
+  float norm_eps;
+  const uint16_t *emb;        /* [V][ld_d]                  bf16       */
+  const uint16_t *head;       /* [V][ld_d]   lm_head^T or emb (tied)   */
+  const float *final_norm;    /* [d]                                   */
+  const float *attn_norm;     /* [L][d]                                */
+  const float *mlp_norm;      /* [L][d]                                */
+  const uint16_t *wqkv;       /* [L][(H+2KVH)dh][ld_d]                 */
+  const uint16_t *wo;         /* [L][d][ld_d]                          */
+  const uint16_t *wgu;        /* [L][2 d_ff][ld_d] interleaved         */
+  const uint16_t *wdown;      /* [L][d][ld_ff]                         */
+  const float *rope_cos;      /* [max_seq][dh/2] fp32 (tensor.py:66-76)*/
+  const float *rope_sin;
+} HsModel;
+
+/* ---- KV cache descriptor ------------------------------------------------
+ * One struct covers the three policies of the hot path:
+ *   FullCache       (caches.py:176-221)  kind=HS_KV_LINEAR, slot == position
+ *   RetrievalCache  (caches.py:439-565)  kind=HS_KV_SLOTTED, pos[] per slot
+ *   StreamingCache  (caches.py:224-288)  kind=HS_KV_SLOTTED, ring of slots   */
+#define HS_KV_LINEAR  0
+#define HS_KV_SLOTTED 1
+
+typedef struct {
+  int kind;
+  int n_layers, n_kv_heads, head_dim;
+  int cap;              /* slots per (layer, kv head)                        */
+  uint16_t *k;          /* [L][KVH][cap][dh] bf16                           */
+  uint16_t *v;
+  int32_t *pos;         /* SLOTTED: [L][cap] absolute position, -1 = empty   */
+} HsCache;
+
+/* Per-forward description of where new rows go and what attention sees.
+ *   append: HS_APPEND_POS   slot = position                 (full)
+ *           HS_APPEND_LINEAR slot = append_base + i          (retrieval tail)
+ *           HS_APPEND_RING  slot = p < n_sink ? p : n_sink + (p-n_sink)%ring
+ *   view:   slots [0, n_view) are scanned; a key at position kp is visible
+ *           to the query at position qp iff kp >= 0 && kp <= qp &&
+ *           (window == 0 || kp < n_sink || kp >= max(win_lo, qp-window+1))
+ *           -- the sequential exposure rule of StreamingCache.expose
+ *           (caches.py:246-256) evaluated per query.                         */
+#define HS_APPEND_POS    0
+#define HS_APPEND_LINEAR 1
+#define HS_APPEND_RING   2
+
+typedef struct {
+  int pos0;          /* absolute position of the first new token (frontier) */
+  int append_mode;
+  int append_base;
+  int n_sink;
+  int ring;
+  int n_view;
+  int window;
+  int win_lo;
+  int split;         /* keys per attention split (fixed => t-invariant)    */
+} HsStep;
+
+/* ---- fused forward (model.py:247-331) -----------------------------------
+ * t tokens (device int32) at st->pos0 through all layers: RMSNorm+QKV GEMV,
+ * RoPE + KV append, split-KV attention, wo+residual, RMSNorm+gate|up with a
+ * SwiGLU epilogue, down+residual, final norm + head.  Writes t logits rows
+ * (fp32) and, if q_stash != NULL, the last row's post-RoPE queries per layer
+ * ([L][H][dh], the ForwardRecorder.last_queries of model.py:309).
+ * Row results are independent of t (bitwise), so a batched verify equals a
+ * sequence of decode steps (model.py:366-378 contract).                     */
+size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view, int split);
+int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st,
+               const int32_t *tokens, int t, float *logits, float *q_stash,
+               void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---- building blocks (also used by tests and the per-layer cache API) ---- */
+
+/* y[r][o] (+)= sum_k pro(x)[r][k] * W[o][k]   (tensor.py:26-36 matmul)
+ * prologue: 0 none, 1 rmsnorm with gain (tensor.py:57-63)
+ * epilogue: 0 store, 1 accumulate into y, 2 SwiGLU pairs (y has N/2 cols,
+ *           model.py:320-322)                                              */
+int hs_gemv(const float *x, int ldx, int t, int K, const uint16_t *w, int ldw, int N,
+            int prologue, const float *gain, float eps, int epilogue, float *y, int ldy,
+            void *stream);
+
+/* embedding lookup (model.py:274): x[r] = float(emb[tokens[r]])            */
+int hs_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x,
+             void *stream);
+
+/* RoPE (model.py:235-244) on q,k rows of qkv [t][(H+2KVH)dh] at positions
+ * pos0.., K/V appended to `layer` per st (caches.py append hooks); q written
+ * to q_out [t][H][dh]; last row's q to q_stash[layer] if non-NULL.          */
+int hs_rope_append(const HsModel *m, const HsCache *c, const HsStep *st, int layer,
+                   const float *qkv, int t, float *q_out, float *q_stash, void *stream);
+
+/* raw KV row write for the per-layer cache API (KVCache.append, caches.py:136)
+ * rows [t][KVH][dh] fp32 -> bf16 at slots[i], positions pos[i]             */
+int hs_kv_write(const HsCache *c, int layer, const float *k, const float *v, int t,
+                const int32_t *slots, const int32_t *pos, void *stream);
+
+/* split-KV attention over a cache view (model.py:290-315):
+ * q [t][H][dh] fp32 -> out [t][H*dh] fp32                                   */
+size_t hs_attention_workspace_bytes(int t, int n_heads, int head_dim, int n_view, int split);
+int hs_attention(const HsCache *c, int layer, const HsStep *st, int n_heads,
+                 const float *q, int t, float *out, void *workspace, size_t ws_bytes,
+                 void *stream);
+
+/* chunk scoring, score_chunks (caches.py:414-436), all layers at once.
+ * keys: layer l, kv head h, token i at  keys + l*ls + h*hs + i*ts  (bf16 if
+ * key_bf16 else fp32); queries [L][H][dh] fp32; scores [L][n_chunks] fp64.  */
+int hs_chunk_score(const void *keys, int key_bf16, long long layer_stride, long long head_stride,
+                   long long token_stride, int n_layers, int n_kv_heads, int head_dim, int upto,
+                   int chunk, const float *queries, int n_heads, double *scores, void *stream);
+
+/* chunk selection of RetrievalCache.build (caches.py:474-495) per layer:
+ * top (quota-1) non-last chunks by (-score, id) + the last chunk (all chunks
+ * if clamped).  importance [L][quota] ([last] + rest), chosen [L][quota]
+ * ascending, ring [L][budget]: victim FIFO as slot indices.  n_chosen and
+ * n_exposed are written to out_counts[0..1].                                */
+size_t hs_chunk_select_workspace_bytes(int n_layers, int n_chunks);
+int hs_chunk_select(const double *scores, int n_layers, int n_chunks, int upto, int chunk,
+                    int budget, int32_t *importance, int32_t *chosen, int32_t *ring,
+                    int32_t *out_counts, void *workspace, size_t ws_bytes, void *stream);
+
+/* gather of the chosen chunks into the retrieval cache slots, position order
+ * (st.push(K[sel_idx], ...) caches.py:490-493).  src is a LINEAR cache.     */
+int hs_retrieval_gather(const HsCache *src, const HsCache *dst, const int32_t *chosen,
+                        int chosen_stride, int n_chosen, int chunk, int upto, void *stream);
+
+/* RetrievalCache.commit / _overwrite (caches.py:529-555) for all layers:
+ * spec slots [n_sel, n_sel+n_spec) -- the first `take` move into the victim
+ * slots ring[(head+i) % n_sel]; the rest shift down.                         */
+int hs_retrieval_commit(const HsCache *c, const int32_t *ring, int n_sel, int ring_head,
+                        int n_spec, int take, void *stream);
+
+/* copy a cache's live slots (clone(), caches.py:216-221 / 283-288 / 557-565) */
+int hs_cache_copy(const HsCache *dst, const HsCache *src, int n_slots, void *stream);
+
+/* ---- sampling & verification (model.py:182-206, speculation.py:52-72,187-208)
+ * probs [rows][V] fp64: temperature 0 -> one-hot argmax (lowest index wins) */
+int hs_probs(const float *logits, int rows, int V, double temperature, double *probs,
+             void *stream);
+
+/* inverse-CDF draw consuming one uniform: token = min(#{c_j <= u}, V-1),
+ * u = uniforms[*cursor]; (*cursor)++ (device int).  Writes token to out.    */
+int hs_sample(const double *probs, int V, const double *uniforms, int32_t *cursor,
+              int32_t *out, void *stream);
+
+/* draft step fused: probs of one logits row + sample (draft_round,
+ * speculation.py:221-226).  probs_out may be NULL only if temperature == 0. */
+int hs_draft_sample(const float *logits, int V, double temperature, double *probs_out,
+                    const double *uniforms, int32_t *cursor, int32_t *out, void *stream);
+
+/* _verify_chain (speculation.py:187-208).  tokens[n] (device), qd [n][V],
+ * pd [n+1][V].  result[0..n]: emitted tokens; result[n+1] = count emitted;
+ * result[n+2] = accepted; result[n+3] = status (0 ok, HS_ERR_CONTRACT when
+ * q[x] <= 0, verify_token speculation.py:58-60).                             */
+int hs_verify_chain(const int32_t *tokens, int n, const double *qd, const double *pd, int V,
+                    const double *uniforms, int32_t *cursor, int32_t *result, void *stream);
+
+/* verify_token alone (speculation.py:52-62): result[0] = accepted (0/1),
+ * result[1] = status; one uniform.                                          */
+int hs_verify_token(int32_t x, const double *q, const double *p, const double *uniforms,
+                    int32_t *cursor, int32_t *result, void *stream);
+
+/* correct_token alone (speculation.py:65-72): one uniform.                  */
+int hs_correct_token(const double *q, const double *p, int V, const double *uniforms,
+                     int32_t *cursor, int32_t *out, void *stream);
+
+/* ---- sequence sharding ----------------------------------
+ * merge per-shard partial softmax states in rank order:
+ * parts: [G][rows] (m, l) fp32 and [G][rows][dh] o fp32 (unnormalised).     */
+int hs_shard_merge(const float *m, const float *l, const float *o, int n_shards, int rows,
+                   int head_dim, float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HS_ABI_H */

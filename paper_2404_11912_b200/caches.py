@@ -1,0 +1,575 @@
+"""KV-cache policies on the device -- the drop-in for hierspec/caches.py.
+
+Bookkeeping contract (caches.py:1-19): `frontier` is the next position to
+append, positions >= `committed` are speculative, `rollback_to(n)` drops
+positions >= n, `commit(n)` promotes positions < n and applies the policy's
+eviction/overwrite rule.
+
+Device layout: K and V are bf16 [layer][kv_head][slot][head_dim]
+(head-major, so one head's keys stream contiguously); slotted caches keep
+an int32 absolute position per (layer, slot).
+
+* FullCache        slot == position.
+* StreamingCache   sinks at slots [0, n_sink), the recent window in a ring
+                   slot = n_sink + (p - n_sink) % ring; eviction is a host
+                   watermark (`lo`) -- nothing moves on the device.
+* RetrievalCache   selected chunks in slots [0, n_sel) (position order after
+                   a build), speculative tail in [n_sel, n_sel + n_spec);
+                   the victim FIFO is a fixed ring of slot indices.
+
+The per-layer `append`/`expose` hooks of the reference protocol are kept for
+API compatibility and tests; the fused forward (`hs_forward`) writes and
+reads the caches directly and never materialises `expose()`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from ._abi import (HS_APPEND_LINEAR, HS_APPEND_POS, HS_APPEND_RING, HS_KV_LINEAR, HS_KV_SLOTTED, HsCache,
+                   HsStep, check, lib)
+from .errors import CapacityError, ContractError, ShapeError
+from .runtime import as_device_f32, device, ptr, stream_ptr, workspaces
+
+FULL_SPLIT = 1024     # keys per attention split over the full cache (fixed: t-invariant rows)
+SMALL_SPLIT = 256     # keys per split over retrieval / streaming views
+
+
+@dataclass(frozen=True)
+class StreamingConfig:
+    """caches.py:32-39"""
+    n_sink: int = 4
+    budget: int = 64
+
+    def __post_init__(self):
+        if not 0 <= self.n_sink < self.budget:
+            raise ValueError("need 0 <= n_sink < budget")
+
+
+@dataclass(frozen=True)
+class H2OConfig:
+    """caches.py:42-49 (policy itself is out of scope for the hot path)."""
+    budget: int = 64
+    recent_window: int = 32
+
+    def __post_init__(self):
+        if not 0 <= self.recent_window < self.budget:
+            raise ValueError("need 0 <= recent_window < budget")
+
+
+@dataclass(frozen=True)
+class RetrievalConfig:
+    """caches.py:52-68"""
+    chunk_size: int = 16
+    budget: int = 64
+    rebuild_stride: int = 128
+    rebuild_accept_threshold: float = 0.8
+    rolling_window: int = 16
+
+    def __post_init__(self):
+        if self.chunk_size < 1 or self.budget < self.chunk_size:
+            raise ValueError("need chunk_size >= 1 and budget >= chunk_size")
+        if self.budget % self.chunk_size:
+            raise ValueError("budget must be a multiple of chunk_size")
+        if not 0.0 < self.rebuild_accept_threshold < 1.0:
+            raise ValueError("rebuild_accept_threshold must be in (0, 1)")
+        if self.rebuild_stride < 1 or self.rolling_window < 1:
+            raise ValueError("rebuild_stride and rolling_window must be >= 1")
+
+
+class KVCache:
+    """Base: device buffers, descriptor, bookkeeping helpers."""
+
+    policy = "base"
+    wants_attention = False
+    batched_prefill_ok = True
+    kind = HS_KV_LINEAR
+
+    def __init__(self, n_layers: int, n_kv_heads: int, head_dim: int, cap: int, with_pos: bool):
+        self.n_layers, self.n_kv_heads, self.head_dim = n_layers, n_kv_heads, head_dim
+        self.frontier = 0
+        self.committed = 0
+        self.cap = cap
+        dev = device()
+        self.k = torch.zeros((n_layers, n_kv_heads, cap, head_dim), dtype=torch.bfloat16, device=dev)
+        self.v = torch.zeros_like(self.k)
+        self.pos = torch.full((n_layers, cap), -1, dtype=torch.int32, device=dev) if with_pos else None
+        d = HsCache()
+        d.kind, d.n_layers, d.n_kv_heads, d.head_dim, d.cap = self.kind, n_layers, n_kv_heads, head_dim, cap
+        d.k, d.v, d.pos = self.k.data_ptr(), self.v.data_ptr(), ptr(self.pos)
+        self._desc = d
+        self._ref = C.byref(d)
+
+    @classmethod
+    def from_config(cls, model_config, *args, **kwargs):
+        return cls(model_config.n_layers, model_config.n_kv_heads, model_config.head_dim, *args, **kwargs)
+
+    # -- protocol ----------------------------------------------------------------
+    def observe_attention(self, layer, probs, query_positions):
+        pass
+
+    def _check_kv(self, k, v):
+        if tuple(k.shape) != tuple(v.shape) or k.ndim != 3 or tuple(k.shape[1:]) != (self.n_kv_heads, self.head_dim):
+            raise ShapeError(f"bad kv shape {tuple(k.shape)}")
+
+    def _check_commit(self, n: int):
+        if not self.committed <= n <= self.frontier:
+            raise ContractError(f"commit({n}) outside [{self.committed}, {self.frontier}]")
+
+    def _write_rows(self, layer: int, k, v, slots, positions):
+        kd, vd = as_device_f32(k), as_device_f32(v)
+        s = torch.as_tensor(np.asarray(slots, np.int32)).to(kd.device)
+        p = torch.as_tensor(np.asarray(positions, np.int32)).to(kd.device)
+        check(lib.hs_kv_write(self._ref, layer, ptr(kd), ptr(vd), kd.shape[0], ptr(s), ptr(p), stream_ptr()))
+
+    def _gather_host(self, layer: int, slots: np.ndarray):
+        idx = torch.as_tensor(np.asarray(slots, np.int64), device=self.k.device)
+        K = self.k[layer].index_select(1, idx).permute(1, 0, 2).float().cpu().numpy()
+        V = self.v[layer].index_select(1, idx).permute(1, 0, 2).float().cpu().numpy()
+        return K, V
+
+    def exposed_positions(self, layer: int = 0) -> np.ndarray:
+        return np.asarray(self.expose(layer)[2]).copy()
+
+    def to_json(self) -> dict:
+        return {"policy": self.policy, "frontier": self.frontier, "committed": self.committed,
+                "layers": [{"exposed_positions": np.asarray(self.expose(li)[2]).tolist()}
+                           for li in range(self.n_layers)]}
+
+    # -- fused-forward hooks (overridden) ------------------------------------------
+    def _batches(self, t: int):
+        yield 0, t
+
+    def _step(self, t: int) -> HsStep:
+        raise NotImplementedError
+
+    def _advance(self, t: int) -> None:
+        raise NotImplementedError
+
+
+class FullCache(KVCache):
+    """Keeps every position (caches.py:176-221); capacity = max_entries."""
+
+    policy = "full"
+    kind = HS_KV_LINEAR
+
+    def __init__(self, n_layers: int, n_kv_heads: int, head_dim: int, max_entries: int):
+        super().__init__(n_layers, n_kv_heads, head_dim, max_entries, with_pos=False)
+        self.max_entries = max_entries
+        self._n = [0] * n_layers
+
+    @classmethod
+    def from_config(cls, model_config):
+        return cls(model_config.n_layers, model_config.n_kv_heads, model_config.head_dim, model_config.max_seq)
+
+    def append(self, layer, k, v):
+        self._check_kv(k, v)
+        t = k.shape[0]
+        n = self._n[layer]
+        if n + t > self.max_entries:
+            raise CapacityError(f"full cache overflow past {self.max_entries}")
+        self._write_rows(layer, k, v, np.arange(n, n + t), np.arange(n, n + t))
+        self._n[layer] = n + t
+        if layer == self.n_layers - 1:
+            self.frontier = n + t
+
+    def expose(self, layer, queries=None):
+        n = self._n[layer]
+        K, V = self._gather_host(layer, np.arange(n))
+        return K, V, np.arange(n, dtype=np.int64), None
+
+    def rollback_to(self, n):
+        self._n = [min(x, n) for x in self._n]
+        self.frontier = min(self.frontier, n)
+        self.committed = min(self.committed, n)
+
+    def commit(self, n):
+        self._check_commit(n)
+        self.committed = n
+
+    def clone(self):
+        c = FullCache(self.n_layers, self.n_kv_heads, self.head_dim, self.max_entries)
+        check(lib.hs_cache_copy(c._ref, self._ref, max(self._n + [0]), stream_ptr()))
+        c._n = list(self._n)
+        c.frontier, c.committed = self.frontier, self.committed
+        return c
+
+    def fill_random_(self, n: int, seed: int = 0, std: float = 1.0):
+        """Synthetic context: n committed positions of N(0, std) bf16 K/V
+        (throughput configs)."""
+        if n > self.max_entries:
+            raise CapacityError("fill beyond capacity")
+        g = torch.Generator(device=self.k.device)
+        g.manual_seed(seed)
+        for l in range(self.n_layers):
+            for h in range(self.n_kv_heads):
+                self.k[l, h, :n].normal_(0.0, std, generator=g)
+                self.v[l, h, :n].normal_(0.0, std, generator=g)
+        self._n = [n] * self.n_layers
+        self.frontier = self.committed = n
+
+    # fused forward: append at slot == position, attend to [0, frontier + t)
+    def _step(self, t):
+        s = HsStep()
+        s.pos0 = self.frontier
+        s.append_mode = HS_APPEND_POS
+        s.n_view = self.frontier + t
+        s.split = FULL_SPLIT
+        if s.n_view > self.max_entries:
+            raise CapacityError(f"full cache overflow past {self.max_entries}")
+        return s
+
+    def _advance(self, t):
+        self.frontier += t
+        self._n = [self.frontier] * self.n_layers
+
+
+class StreamingCache(KVCache):
+    """Attention sinks + recent window (caches.py:224-288).
+
+    Store = positions [0, n_sink) U [lo, hi); exposure for a query at p is
+    the sinks plus [max(lo, p - W + 1), p] with W = budget - n_sink -- the
+    reference's `expose` evaluated after appending p.  Commit raises the
+    watermark lo to max(lo, n - W) (keep the last W committed)."""
+
+    policy = "streaming"
+    batched_prefill_ok = False
+    kind = HS_KV_SLOTTED
+
+    def __init__(self, n_layers: int, n_kv_heads: int, head_dim: int, config: StreamingConfig,
+                 slack: int = 128):
+        self.config = config
+        self.window = config.budget - config.n_sink
+        self.ring = self.window + slack
+        self.slack = slack
+        super().__init__(n_layers, n_kv_heads, head_dim, config.n_sink + self.ring, with_pos=True)
+        self.lo = config.n_sink
+        self._hi = [0] * n_layers
+
+    def _slot(self, p: int) -> int:
+        ns = self.config.n_sink
+        return p if p < ns else ns + (p - ns) % self.ring
+
+    def _store(self, hi: int) -> np.ndarray:
+        ns = self.config.n_sink
+        return np.concatenate([np.arange(min(ns, hi)), np.arange(max(self.lo, ns), hi)]).astype(np.int64)
+
+    def _guard(self, first_new: int, last_new: int):
+        """Appending up to last_new overwrites last_new - ring; that position
+        must no longer be exposable (current or after a rollback to committed)."""
+        base = self.committed if self.committed > 0 else first_new
+        lowest = max(self.lo, base - self.window + 1)
+        if last_new - self.ring >= lowest:
+            raise CapacityError(f"streaming ring ({self.ring} slots) too small for the speculative tail; "
+                                f"raise slack")
+
+    def append(self, layer, k, v):
+        self._check_kv(k, v)
+        t = k.shape[0]
+        p0 = self.frontier
+        self._guard(p0, p0 + t - 1)
+        pos = np.arange(p0, p0 + t)
+        self._write_rows(layer, k, v, [self._slot(int(p)) for p in pos], pos)
+        self._hi[layer] = p0 + t
+        if layer == self.n_layers - 1:
+            self.frontier = p0 + t
+
+    def _exposed(self, hi: int) -> np.ndarray:
+        st = self._store(hi)
+        if st.shape[0] <= self.config.budget:
+            return st
+        return np.concatenate([st[:self.config.n_sink], st[-self.window:]])
+
+    def expose(self, layer, queries=None):
+        pos = self._exposed(self._hi[layer])
+        K, V = self._gather_host(layer, [self._slot(int(p)) for p in pos])
+        return K, V, pos, None
+
+    def rollback_to(self, n):
+        if n < self.committed:
+            raise ContractError(f"streaming cache cannot roll below committed {self.committed}")
+        self._hi = [min(h, n) for h in self._hi]
+        self.frontier = min(self.frontier, n)
+
+    def commit(self, n):
+        self._check_commit(n)
+        self.committed = n
+        ns = self.config.n_sink
+        n_comm = min(n, ns) + max(0, n - max(self.lo, ns))
+        if n_comm > self.config.budget:
+            self.lo = max(self.lo, n - self.window)
+
+    def clone(self):
+        c = StreamingCache(self.n_layers, self.n_kv_heads, self.head_dim, self.config, self.slack)
+        check(lib.hs_cache_copy(c._ref, self._ref, self.cap, stream_ptr()))
+        c._hi, c.lo = list(self._hi), self.lo
+        c.frontier, c.committed = self.frontier, self.committed
+        return c
+
+    def fill_random_(self, n: int, seed: int = 0, std: float = 1.0):
+        """Synthetic state equal to 'prefilled n positions and committed'."""
+        ns = self.config.n_sink
+        g = torch.Generator(device=self.k.device)
+        g.manual_seed(seed)
+        self.lo = ns
+        self.frontier = n
+        self._hi = [n] * self.n_layers
+        keep = self._store(n)
+        if keep.shape[0] > self.config.budget:
+            self.lo = n - self.window
+            keep = self._store(n)
+        slots = torch.as_tensor([self._slot(int(p)) for p in keep], device=self.k.device)
+        for l in range(self.n_layers):
+            kk = torch.randn((self.n_kv_heads, len(keep), self.head_dim), generator=g, device=self.k.device) * std
+            vv = torch.randn((self.n_kv_heads, len(keep), self.head_dim), generator=g, device=self.k.device) * std
+            self.k[l][:, slots] = kk.to(torch.bfloat16)
+            self.v[l][:, slots] = vv.to(torch.bfloat16)
+            self.pos[l, slots] = torch.as_tensor(keep, dtype=torch.int32, device=self.k.device)
+        self.committed = n
+
+    # fused forward
+    def _batches(self, t):
+        step = max(1, self.slack // 2)
+        for a in range(0, t, step):
+            yield a, min(t, a + step)
+
+    def _step(self, t):
+        self._guard(self.frontier, self.frontier + t - 1)
+        s = HsStep()
+        s.pos0 = self.frontier
+        s.append_mode = HS_APPEND_RING
+        s.n_sink = self.config.n_sink
+        s.ring = self.ring
+        s.n_view = self.cap
+        s.window = self.window
+        s.win_lo = self.lo
+        s.split = SMALL_SPLIT
+        return s
+
+    def _advance(self, t):
+        self.frontier += t
+        self._hi = [self.frontier] * self.n_layers
+
+
+class ChunkScoreTable:
+    """Per-layer chunk-scoring snapshot of a build (caches.py:399-411).
+    Device results are copied to the host on first access."""
+
+    def __init__(self, chunk_size, upto, n_layers, scores_dev, importance_dev, n_imp, clamped):
+        self.chunk_size = chunk_size
+        self.clamped = clamped
+        n = (upto + chunk_size - 1) // chunk_size
+        b = np.minimum(np.arange(n + 1) * chunk_size, upto).astype(np.int64)
+        self.boundaries = [b.copy() for _ in range(n_layers)]
+        self._scores_dev, self._imp_dev, self._n_imp = scores_dev, importance_dev, n_imp
+        self._scores = self._selected = None
+
+    @property
+    def scores(self):
+        if self._scores is None:
+            h = self._scores_dev.cpu().numpy()
+            self._scores = [h[i].copy() for i in range(h.shape[0])]
+        return self._scores
+
+    @property
+    def selected(self):
+        if self._selected is None:
+            h = self._imp_dev.cpu().numpy()
+            self._selected = [h[i, :self._n_imp].astype(int).tolist() for i in range(h.shape[0])]
+        return self._selected
+
+    def ranking(self, layer: int) -> list:
+        s = self.scores[layer]
+        return sorted(range(len(s)), key=lambda c: (-s[c], c))
+
+
+def _queries_device(queries, n_layers: int) -> torch.Tensor:
+    if isinstance(queries, torch.Tensor):
+        q = queries.to(device=device(), dtype=torch.float32)
+    else:
+        q = torch.from_numpy(np.stack([np.asarray(x, np.float32) for x in queries])).to(device())
+    if q.dim() != 3 or q.shape[0] != n_layers:
+        raise ShapeError(f"queries must be [n_layers, n_heads, head_dim], got {tuple(q.shape)}")
+    return q.contiguous()
+
+
+def score_chunks(keys, queries, chunk_size: int, n_kv_heads: int):
+    """Chunk scores for one layer (caches.py:414-436): mean over query heads
+    of q_h . mean_key[h // g] / sqrt(dh), fp64, on the device.
+    keys [L, KVH, dh] fp32, queries [H, dh]; returns (bounds, scores)."""
+    k = as_device_f32(keys)
+    q = as_device_f32(queries)
+    if k.dim() != 3 or q.dim() != 2 or k.shape[2] != q.shape[1] or k.shape[1] != n_kv_heads:
+        raise ShapeError("score_chunks: keys [L, KVH, dh], queries [H, dh]")
+    L, KVH, dh = k.shape
+    n = (L + chunk_size - 1) // chunk_size
+    out = torch.empty((1, n), dtype=torch.float64, device=k.device)
+    check(lib.hs_chunk_score(ptr(k), 0, 0, dh, KVH * dh, 1, KVH, dh, L, chunk_size, ptr(q), q.shape[0],
+                             ptr(out), stream_ptr()))
+    bounds = np.minimum(np.arange(n + 1) * chunk_size, L).astype(np.int64)
+    return bounds, out[0].cpu().numpy()
+
+
+class RetrievalCache(KVCache):
+    """Budgeted chunk-selected view of a full cache (caches.py:439-565)."""
+
+    policy = "retrieval"
+    batched_prefill_ok = False
+    kind = HS_KV_SLOTTED
+
+    def __init__(self, n_layers: int, n_kv_heads: int, head_dim: int, config: RetrievalConfig,
+                 spec_cap: int = 64):
+        self.config = config
+        self.spec_cap = spec_cap
+        super().__init__(n_layers, n_kv_heads, head_dim, config.budget + spec_cap, with_pos=True)
+        dev = device()
+        self.quota = config.budget // config.chunk_size
+        self.ring = torch.zeros((n_layers, config.budget), dtype=torch.int32, device=dev)
+        self.importance = torch.zeros((n_layers, self.quota), dtype=torch.int32, device=dev)
+        self.chosen = torch.zeros((n_layers, self.quota), dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.n_sel = 0
+        self.ring_head = 0
+        self.n_spec = [0] * n_layers
+        self.table: Optional[ChunkScoreTable] = None
+        self.builds = 0
+
+    def build(self, source: FullCache, queries, upto: int) -> ChunkScoreTable:
+        """Select chunks of source positions [0, upto) with per-layer queries
+        [H, dh]; replaces the selection and the speculative tail; frontier =
+        committed = upto (caches.py:458-502).  Runs entirely on the device."""
+        if upto < 1:
+            raise ContractError("retrieval build needs a non-empty source prefix")
+        if min(source._n) < upto:
+            raise ContractError("source cache shorter than requested build range")
+        cfg = self.config
+        q = _queries_device(queries, self.n_layers)
+        n = (upto + cfg.chunk_size - 1) // cfg.chunk_size
+        scores = torch.empty((self.n_layers, n), dtype=torch.float64, device=q.device)
+        dh = self.head_dim
+        check(lib.hs_chunk_score(ptr(source.k), 1, self.n_kv_heads * source.cap * dh, source.cap * dh, dh,
+                                 self.n_layers, self.n_kv_heads, dh, upto, cfg.chunk_size, ptr(q), q.shape[1],
+                                 ptr(scores), stream_ptr()))
+        check(lib.hs_chunk_select(ptr(scores), self.n_layers, n, upto, cfg.chunk_size, cfg.budget,
+                                  ptr(self.importance), ptr(self.chosen), ptr(self.ring), ptr(self.counts),
+                                  None, 0, stream_ptr()))
+        clamped = cfg.budget >= upto
+        k_sel = min(n - 1, self.quota - 1)
+        n_chosen = k_sel + 1
+        self.n_sel = k_sel * cfg.chunk_size + (upto - (n - 1) * cfg.chunk_size)
+        self.pos.fill_(-1)
+        check(lib.hs_retrieval_gather(source._ref, self._ref, ptr(self.chosen), self.quota, n_chosen,
+                                      cfg.chunk_size, upto, stream_ptr()))
+        self.ring_head = 0
+        self.n_spec = [0] * self.n_layers
+        self.frontier = self.committed = upto
+        self.builds += 1
+        self.table = ChunkScoreTable(cfg.chunk_size, upto, self.n_layers, scores, self.importance, n_chosen,
+                                     clamped)
+        return self.table
+
+    def append(self, layer, k, v):
+        self._check_kv(k, v)
+        t = k.shape[0]
+        ns = self.n_spec[layer]
+        if ns + t > self.spec_cap:
+            raise CapacityError("retrieval speculative tail overflow")
+        p0 = self.frontier
+        self._write_rows(layer, k, v, np.arange(self.n_sel + ns, self.n_sel + ns + t), np.arange(p0, p0 + t))
+        self.n_spec[layer] = ns + t
+        if layer == self.n_layers - 1:
+            self.frontier = p0 + t
+
+    def expose(self, layer, queries=None):
+        pos_all = self.pos[layer, :self.n_sel + self.n_spec[layer]].cpu().numpy().astype(np.int64)
+        sel = pos_all[:self.n_sel]
+        order = np.argsort(sel, kind="stable")     # reference keeps sel position-sorted
+        slots = np.concatenate([order, np.arange(self.n_sel, self.n_sel + self.n_spec[layer])])
+        K, V = self._gather_host(layer, slots)
+        return K, V, pos_all[slots], None
+
+    def rollback_to(self, n):
+        if n < self.committed:
+            raise ContractError(f"retrieval cache cannot roll below committed {self.committed}")
+        self.n_spec = [max(0, min(s, n - self.committed)) for s in self.n_spec]
+        self.frontier = min(self.frontier, n)
+
+    def commit(self, n):
+        self._check_commit(n)
+        take = n - self.committed
+        if take > 0:
+            if self.n_sel < 1:
+                raise ContractError("retrieval cache has no slots")
+            spec = self.n_spec[0]
+            check(lib.hs_retrieval_commit(self._ref, ptr(self.ring), self.n_sel, self.ring_head, spec, take,
+                                          stream_ptr()))
+            self.ring_head = (self.ring_head + take) % self.n_sel
+            self.n_spec = [s - take for s in self.n_spec]
+        self.committed = n
+
+    def clone(self):
+        c = RetrievalCache(self.n_layers, self.n_kv_heads, self.head_dim, self.config, self.spec_cap)
+        check(lib.hs_cache_copy(c._ref, self._ref, self.cap, stream_ptr()))
+        c.ring.copy_(self.ring)
+        c.importance.copy_(self.importance)
+        c.chosen.copy_(self.chosen)
+        c.n_sel, c.ring_head, c.n_spec = self.n_sel, self.ring_head, list(self.n_spec)
+        c.frontier, c.committed, c.table, c.builds = self.frontier, self.committed, self.table, self.builds
+        return c
+
+    # fused forward: tail appended linearly after the selection
+    def _batches(self, t):
+        step = self.spec_cap
+        for a in range(0, t, step):
+            yield a, min(t, a + step)
+
+    def _step(self, t):
+        ns = self.n_spec[0]
+        if ns + t > self.spec_cap:
+            raise CapacityError("retrieval speculative tail overflow")
+        s = HsStep()
+        s.pos0 = self.frontier
+        s.append_mode = HS_APPEND_LINEAR
+        s.append_base = self.n_sel + ns
+        s.n_view = self.n_sel + ns + t
+        s.split = SMALL_SPLIT
+        return s
+
+    def _advance(self, t):
+        self.frontier += t
+        self.n_spec = [s + t for s in self.n_spec]
+
+
+class RollingAcceptance:
+    """Fixed window of per-round acceptance rates (caches.py:655-674)."""
+
+    def __init__(self, window: int):
+        if window < 1:
+            raise ValueError("window must be >= 1")
+        self.window = window
+        self.rates: list = []
+
+    def push(self, rate: float):
+        self.rates.append(float(rate))
+        if len(self.rates) > self.window:
+            self.rates.pop(0)
+
+    @property
+    def full(self) -> bool:
+        return len(self.rates) >= self.window
+
+    def mean(self) -> float:
+        return float(np.mean(self.rates)) if self.rates else 1.0
+
+
+def should_rebuild(config: RetrievalConfig, tokens_since_build: int, rolling: RollingAcceptance) -> bool:
+    """Rebuild at the stride, or when a full window's mean acceptance drops
+    below the threshold (caches.py:677-683)."""
+    if tokens_since_build >= config.rebuild_stride:
+        return True
+    return rolling.full and rolling.mean() < config.rebuild_accept_threshold

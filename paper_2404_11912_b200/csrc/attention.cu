@@ -1,0 +1,270 @@
+// Split-KV ("flash-decoding") attention over a KV-cache view, CUDA cores.
+//
+// Replaces the attention core of the reference forward (model.py:290-315):
+// grouped scores q.K^T, causal / exposure masks, softmax with 1/sqrt(dh),
+// P.V.  The cache is never materialised (no expose()): the kernel scans the
+// view's slots [0, n_view) and applies the exposure rule per query:
+//   visible(qp, kp) = kp >= 0 && kp <= qp &&
+//                     (window == 0 || kp < n_sink || kp >= max(win_lo, qp - window + 1))
+// which is FullCache (window 0), RetrievalCache (sel + spec tail, window 0)
+// and the per-step StreamingCache exposure (caches.py:246-256).
+//
+// Grid: (n_splits, kv_heads, query-row blocks of 16).  Splits are fixed-size
+// ranges of slots, so a query's partial state never depends on how many
+// other queries share the launch; the combine walks splits in index order.
+#include "hs_common.cuh"
+
+namespace hs {
+
+constexpr int ATT_THREADS = 128;
+constexpr int ATT_TILE = 64;     // keys per smem tile
+constexpr int ATT_QROWS = 16;    // query rows per CTA
+
+struct AttnArgs {
+  const float *q;       // [t][H][DH]
+  int t, H, KVH, g;
+  const uint16_t *k;    // layer base [KVH][cap][DH]
+  const uint16_t *v;
+  const int32_t *pos;   // layer [cap] or null (slot == position)
+  int cap, n_view, pos0, window, win_lo, n_sink, split, n_splits;
+  float scale;
+  float *part_m, *part_l, *part_o;   // [n_splits][t*H], [n_splits][t*H][DH]
+};
+
+__device__ __forceinline__ bool visible(int kp, int qp, const AttnArgs &a) {
+  if (kp < 0 || kp > qp) return false;
+  if (a.window == 0 || kp < a.n_sink) return true;
+  int lo = qp - a.window + 1;
+  if (a.win_lo > lo) lo = a.win_lo;
+  return kp >= lo;
+}
+
+template <int DH>
+__global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
+  constexpr int KP = DH + 8;                 // padded K row (bf16) -> conflict-free 16B reads
+  constexpr int NDP = DH / 2;                // dim pairs
+  constexpr int NRG = ATT_THREADS / NDP > ATT_QROWS ? ATT_QROWS : ATT_THREADS / NDP;
+  constexpr int RPT = (ATT_QROWS + NRG - 1) / NRG;   // rows per thread in PV
+  __shared__ __align__(16) uint16_t Ks[ATT_TILE * KP];
+  __shared__ __align__(16) uint16_t Vs[ATT_TILE * DH];
+  __shared__ __align__(16) float qs[ATT_QROWS * DH];
+  __shared__ float S[ATT_QROWS][ATT_TILE];
+  __shared__ int kpos[ATT_TILE];
+  __shared__ float m_s[ATT_QROWS], l_s[ATT_QROWS], f_s[ATT_QROWS];
+  __shared__ int qp_s[ATT_QROWS], head_s[ATT_QROWS], tok_s[ATT_QROWS];
+
+  const int split = blockIdx.x, kh = blockIdx.y, rb = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nrows_total = a.g * a.t;
+  const int r0 = rb * ATT_QROWS;
+  const int nrows = min(ATT_QROWS, nrows_total - r0);
+
+  // query rows: rr = i*g + gi  ->  token i, head kh*g + gi
+  if (tid < ATT_QROWS) {
+    int rr = r0 + tid;
+    if (tid < nrows) {
+      int i = rr / a.g, gi = rr % a.g;
+      tok_s[tid] = i; head_s[tid] = kh * a.g + gi; qp_s[tid] = a.pos0 + i;
+    } else {
+      tok_s[tid] = 0; head_s[tid] = 0; qp_s[tid] = -1;
+    }
+    m_s[tid] = -INFINITY; l_s[tid] = 0.f;
+  }
+  __syncthreads();
+  for (int e = tid; e < ATT_QROWS * DH; e += ATT_THREADS) {
+    int rr = e / DH, d = e % DH;
+    qs[e] = rr < nrows ? a.q[((size_t)tok_s[rr] * a.H + head_s[rr]) * DH + d] : 0.f;
+  }
+
+  float acc[RPT][2];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = 0.f;
+  const int dp = tid % NDP, rg = tid / NDP;
+
+  const int s_lo = split * a.split;
+  const int s_hi = min(a.n_view, s_lo + a.split);
+  const uint16_t *kbase = a.k + (size_t)kh * a.cap * DH;
+  const uint16_t *vbase = a.v + (size_t)kh * a.cap * DH;
+
+  for (int tile = s_lo; tile < s_hi; tile += ATT_TILE) {
+    const int nk = min(ATT_TILE, s_hi - tile);
+    __syncthreads();   // previous tile fully consumed
+    // ---- stage K, V (16-byte vectors) and positions ------------------------
+    constexpr int VPR = DH / 8;  // 16B vectors per row
+    for (int e = tid; e < ATT_TILE * VPR; e += ATT_THREADS) {
+      int kr = e / VPR, c = e % VPR;
+      uint4 kv4 = make_uint4(0, 0, 0, 0), vv4 = make_uint4(0, 0, 0, 0);
+      if (kr < nk) {
+        kv4 = ld_stream(kbase + (size_t)(tile + kr) * DH + c * 8);
+        vv4 = ld_stream(vbase + (size_t)(tile + kr) * DH + c * 8);
+      }
+      *reinterpret_cast<uint4 *>(&Ks[kr * KP + c * 8]) = kv4;
+      *reinterpret_cast<uint4 *>(&Vs[kr * DH + c * 8]) = vv4;
+    }
+    if (tid < ATT_TILE) {
+      int j = tile + tid;
+      kpos[tid] = (tid < nk) ? (a.pos ? a.pos[j] : j) : -1;
+    }
+    __syncthreads();
+    // ---- scores: thread = (key, half of the rows) ---------------------------
+    {
+      const int key = tid & (ATT_TILE - 1), half = tid >> 6;   // ATT_THREADS == 2*ATT_TILE
+      float dot[ATT_QROWS / 2];
+#pragma unroll
+      for (int i = 0; i < ATT_QROWS / 2; ++i) dot[i] = 0.f;
+#pragma unroll 4
+      for (int d = 0; d < DH; d += 8) {
+        float kf[8];
+        unpack8(*reinterpret_cast<const uint4 *>(&Ks[key * KP + d]), kf);
+#pragma unroll
+        for (int i = 0; i < ATT_QROWS / 2; ++i) {
+          const int rr = half + 2 * i;
+          const float4 qa = *reinterpret_cast<const float4 *>(&qs[rr * DH + d]);
+          const float4 qb = *reinterpret_cast<const float4 *>(&qs[rr * DH + d + 4]);
+          float s = dot[i];
+          s = fmaf(qa.x, kf[0], s); s = fmaf(qa.y, kf[1], s);
+          s = fmaf(qa.z, kf[2], s); s = fmaf(qa.w, kf[3], s);
+          s = fmaf(qb.x, kf[4], s); s = fmaf(qb.y, kf[5], s);
+          s = fmaf(qb.z, kf[6], s); s = fmaf(qb.w, kf[7], s);
+          dot[i] = s;
+        }
+      }
+      const int kp = kpos[key];
+#pragma unroll
+      for (int i = 0; i < ATT_QROWS / 2; ++i) {
+        const int rr = half + 2 * i;
+        S[rr][key] = (rr < nrows && key < nk && visible(kp, qp_s[rr], a)) ? dot[i] * a.scale : -INFINITY;
+      }
+    }
+    __syncthreads();
+    // ---- online softmax: one warp per row -------------------------------------
+    for (int rr = warp; rr < ATT_QROWS; rr += ATT_THREADS / 32) {
+      float s0 = S[rr][lane], s1 = S[rr][lane + 32];
+      float tmax = warp_max(fmaxf(s0, s1));
+      float m_old = m_s[rr];
+      float m_new = fmaxf(m_old, tmax);
+      float p0 = 0.f, p1 = 0.f, fac = 1.f;
+      if (m_new != -INFINITY) {
+        p0 = (s0 == -INFINITY) ? 0.f : expf(s0 - m_new);
+        p1 = (s1 == -INFINITY) ? 0.f : expf(s1 - m_new);
+        fac = (m_old == -INFINITY) ? 0.f : expf(m_old - m_new);
+      }
+      float ps = warp_sum(p0 + p1);
+      S[rr][lane] = p0; S[rr][lane + 32] = p1;
+      if (lane == 0) {
+        f_s[rr] = fac; m_s[rr] = m_new; l_s[rr] = l_s[rr] * fac + ps;
+      }
+    }
+    __syncthreads();
+    // ---- P.V: thread = (dim pair, row group) -----------------------------------
+    if (rg < NRG) {
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        const int rr = rg + NRG * i;
+        if (rr < ATT_QROWS) { const float f = f_s[rr]; acc[i][0] *= f; acc[i][1] *= f; }
+      }
+      for (int key = 0; key < nk; ++key) {
+        const uint32_t vw = *reinterpret_cast<const uint32_t *>(&Vs[key * DH + 2 * dp]);
+        const float v0 = bf16_lo(vw), v1 = bf16_hi(vw);
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          const int rr = rg + NRG * i;
+          if (rr < ATT_QROWS) {
+            const float p = S[rr][key];
+            acc[i][0] = fmaf(p, v0, acc[i][0]);
+            acc[i][1] = fmaf(p, v1, acc[i][1]);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- write partial state ------------------------------------------------------
+  const size_t base = (size_t)split * a.t * a.H;
+  if (tid < nrows) {
+    const size_t row = (size_t)tok_s[tid] * a.H + head_s[tid];
+    a.part_m[base + row] = m_s[tid];
+    a.part_l[base + row] = l_s[tid];
+  }
+  if (rg < NRG) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int rr = rg + NRG * i;
+      if (rr < nrows) {
+        const size_t row = (size_t)tok_s[rr] * a.H + head_s[rr];
+        float *o = a.part_o + (base + row) * DH + 2 * dp;
+        o[0] = acc[i][0];
+        o[1] = acc[i][1];
+      }
+    }
+  }
+}
+
+// out[i][h*DH + d] = sum_s w_s o_s / sum_s w_s l_s,  w_s = exp(m_s - M), splits in order
+__global__ void attn_combine_kernel(const float *pm, const float *pl, const float *po, int n_splits,
+                                    int rows, int DH, float *out) {
+  const int row = blockIdx.x;
+  float M = -INFINITY;
+  for (int s = 0; s < n_splits; ++s) M = fmaxf(M, pm[(size_t)s * rows + row]);
+  for (int d = threadIdx.x; d < DH; d += blockDim.x) {
+    float l = 0.f, o = 0.f;
+    for (int s = 0; s < n_splits; ++s) {
+      const float m = pm[(size_t)s * rows + row];
+      if (m == -INFINITY) continue;
+      const float w = expf(m - M);
+      l = fmaf(w, pl[(size_t)s * rows + row], l);
+      o = fmaf(w, po[((size_t)s * rows + row) * DH + d], o);
+    }
+    out[(size_t)row * DH + d] = o / l;
+  }
+}
+
+size_t attention_ws(int t, int H, int DH, int n_view, int split) {
+  size_t ns = (size_t)ceil_div(n_view, split);
+  return ns * t * H * (2 + DH) * sizeof(float) + 256;
+}
+
+int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
+                     float *out, void *ws, size_t ws_bytes, cudaStream_t stream) {
+  const int DH = c->head_dim, KVH = c->n_kv_heads;
+  HS_REQUIRE(H % KVH == 0, HS_ERR_SHAPE, "attention: H %% KVH != 0");
+  HS_REQUIRE(st->split > 0 && st->split % ATT_TILE == 0, HS_ERR_VALUE, "attention: split must be a multiple of %d", ATT_TILE);
+  HS_REQUIRE(st->n_view >= 1 && st->n_view <= c->cap, HS_ERR_CAPACITY, "attention: view %d exceeds capacity %d", st->n_view, c->cap);
+  const int n_splits = ceil_div(st->n_view, st->split);
+  HS_REQUIRE(ws_bytes >= attention_ws(t, H, DH, st->n_view, st->split), HS_ERR_VALUE, "attention: workspace too small");
+  AttnArgs a;
+  a.q = q; a.t = t; a.H = H; a.KVH = KVH; a.g = H / KVH;
+  size_t lay = (size_t)layer * KVH * c->cap * DH;
+  a.k = c->k + lay; a.v = c->v + lay;
+  a.pos = (c->kind == HS_KV_SLOTTED) ? c->pos + (size_t)layer * c->cap : nullptr;
+  a.cap = c->cap; a.n_view = st->n_view; a.pos0 = st->pos0; a.window = st->window;
+  a.win_lo = st->win_lo; a.n_sink = st->n_sink; a.split = st->split; a.n_splits = n_splits;
+  a.scale = (float)(1.0 / sqrt((double)DH));
+  float *wsf = reinterpret_cast<float *>(ws);
+  a.part_m = wsf;
+  a.part_l = wsf + (size_t)n_splits * t * H;
+  a.part_o = wsf + (size_t)2 * n_splits * t * H;
+  dim3 grid(n_splits, KVH, ceil_div(a.g * t, ATT_QROWS));
+  switch (DH) {
+    case 8: attn_partial_kernel<8><<<grid, ATT_THREADS, 0, stream>>>(a); break;
+    case 16: attn_partial_kernel<16><<<grid, ATT_THREADS, 0, stream>>>(a); break;
+    case 32: attn_partial_kernel<32><<<grid, ATT_THREADS, 0, stream>>>(a); break;
+    case 64: attn_partial_kernel<64><<<grid, ATT_THREADS, 0, stream>>>(a); break;
+    case 128: attn_partial_kernel<128><<<grid, ATT_THREADS, 0, stream>>>(a); break;
+    default: return set_error(HS_ERR_SHAPE, "attention: head_dim %d unsupported (8/16/32/64/128)", DH);
+  }
+  attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 0, stream>>>(a.part_m, a.part_l, a.part_o,
+                                                                   n_splits, t * H, DH, out);
+  return check_launch("attention");
+}
+
+}  // namespace hs
+
+extern "C" size_t hs_attention_workspace_bytes(int t, int n_heads, int head_dim, int n_view, int split) {
+  return hs::attention_ws(t, n_heads, head_dim, n_view, split);
+}
+
+extern "C" int hs_attention(const HsCache *c, int layer, const HsStep *st, int n_heads, const float *q,
+                            int t, float *out, void *workspace, size_t ws_bytes, void *stream) {
+  return hs::launch_attention(c, layer, st, n_heads, q, t, out, workspace, ws_bytes, hs::as_stream(stream));
+}

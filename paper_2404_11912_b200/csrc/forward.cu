@@ -1,0 +1,137 @@
+// Native forward driver: one C call runs a whole lane step (model.py:247-331)
+// so the host never pays per-layer launch overhead from Python, and the
+// sequence can be captured into a CUDA graph by the caller.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "hs_common.cuh"
+
+namespace hs {
+
+int launch_gemv(const float *x, int ldx, int t, int K, const uint16_t *w, int ldw, int N, int prologue,
+                const float *gain, float eps, int epilogue, float *y, int ldy, cudaStream_t st);
+int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x, cudaStream_t st);
+int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv, int t,
+                       float *q_out, float *q_stash, cudaStream_t st);
+int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
+                     void *ws, size_t ws_bytes, cudaStream_t stream);
+size_t attention_ws(int t, int H, int DH, int n_view, int split);
+
+// ---- error state -------------------------------------------------------------
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return HS_OK;
+}
+
+struct FwdWs {
+  float *x, *qkv, *q, *attn, *act;
+  void *att_ws;
+  size_t att_bytes;
+};
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+static size_t carve(const HsModel *m, int t, int n_view, int split, char *base, FwdWs *w) {
+  const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char *p = base ? base + off : nullptr; off += align256(bytes); return p; };
+  w->x = (float *)take((size_t)t * d * 4);
+  w->qkv = (float *)take((size_t)t * (H + 2 * KVH) * dh * 4);
+  w->q = (float *)take((size_t)t * H * dh * 4);
+  w->attn = (float *)take((size_t)t * d * 4);
+  w->act = (float *)take((size_t)t * m->d_ff * 4);
+  w->att_bytes = attention_ws(t, H, dh, n_view, split);
+  w->att_ws = take(w->att_bytes);
+  return off;
+}
+
+}  // namespace hs
+
+extern "C" const char *hs_last_error(void) { return hs::g_err; }
+extern "C" int hs_abi_version(void) { return HS_ABI_VERSION; }
+extern "C" int hs_device_sm_count(int device) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return n;
+}
+
+extern "C" size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view, int split) {
+  hs::FwdWs w;
+  return hs::carve(m, t, n_view, split, nullptr, &w);
+}
+
+extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
+                          float *logits, float *q_stash, void *workspace, size_t workspace_bytes, void *stream) {
+  using namespace hs;
+  HS_REQUIRE(t >= 1, HS_ERR_VALUE, "empty token sequence");
+  HS_REQUIRE(c->n_layers == m->n_layers && c->n_kv_heads == m->n_kv_heads && c->head_dim == m->head_dim,
+             HS_ERR_SHAPE, "forward: cache geometry does not match the model");
+  HS_REQUIRE(st->pos0 + t <= m->max_seq, HS_ERR_CAPACITY, "sequence of %d exceeds max_seq %d", st->pos0 + t,
+             m->max_seq);
+  FwdWs w;
+  const size_t need = carve(m, t, st->n_view, st->split, (char *)workspace, &w);
+  HS_REQUIRE(workspace_bytes >= need, HS_ERR_VALUE, "forward: workspace %zu < %zu", workspace_bytes, need);
+  cudaStream_t s = as_stream(stream);
+  const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim;
+  const int nqkv = (H + 2 * KVH) * dh;
+  int rc;
+#define HS_TRY(call) do { if ((rc = (call)) != HS_OK) return rc; } while (0)
+  HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
+  for (int l = 0; l < m->n_layers; ++l) {
+    const size_t lq = (size_t)l * nqkv * m->ld_d;
+    HS_TRY(launch_gemv(w.x, d, t, d, m->wqkv + lq, m->ld_d, nqkv, 1, m->attn_norm + (size_t)l * d, m->norm_eps,
+                       0, w.qkv, nqkv, s));
+    HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
+    HS_TRY(launch_attention(c, l, st, H, w.q, t, w.attn, w.att_ws, w.att_bytes, s));
+    HS_TRY(launch_gemv(w.attn, d, t, d, m->wo + (size_t)l * d * m->ld_d, m->ld_d, d, 0, nullptr, 0.f, 1, w.x, d, s));
+    HS_TRY(launch_gemv(w.x, d, t, d, m->wgu + (size_t)l * 2 * m->d_ff * m->ld_d, m->ld_d, 2 * m->d_ff, 1,
+                       m->mlp_norm + (size_t)l * d, m->norm_eps, 2, w.act, m->d_ff, s));
+    HS_TRY(launch_gemv(w.act, m->d_ff, t, m->d_ff, m->wdown + (size_t)l * d * m->ld_ff, m->ld_ff, d, 0, nullptr, 0.f,
+                       1, w.x, d, s));
+  }
+  HS_TRY(launch_gemv(w.x, d, t, d, m->head, m->ld_d, m->vocab_size, 1, m->final_norm, m->norm_eps, 0, logits,
+                     m->vocab_size, s));
+#undef HS_TRY
+  return HS_OK;
+}
+
+// ---- shard merge: rank-ordered partial-softmax merge ----------
+namespace hs {
+__global__ void shard_merge_kernel(const float *pm, const float *pl, const float *po, int G, int rows, int DH,
+                                   float *out) {
+  const int row = blockIdx.x;
+  float M = -INFINITY;
+  for (int g = 0; g < G; ++g) M = fmaxf(M, pm[(size_t)g * rows + row]);
+  for (int d = threadIdx.x; d < DH; d += blockDim.x) {
+    float l = 0.f, o = 0.f;
+    for (int g = 0; g < G; ++g) {
+      const float m = pm[(size_t)g * rows + row];
+      if (m == -INFINITY) continue;
+      const float wgt = expf(m - M);
+      l = fmaf(wgt, pl[(size_t)g * rows + row], l);
+      o = fmaf(wgt, po[((size_t)g * rows + row) * DH + d], o);
+    }
+    out[(size_t)row * DH + d] = o / l;
+  }
+}
+}  // namespace hs
+
+extern "C" int hs_shard_merge(const float *m, const float *l, const float *o, int n_shards, int rows, int head_dim,
+                              float *out, void *stream) {
+  if (n_shards < 1 || rows < 1) return hs::set_error(HS_ERR_VALUE, "shard_merge: empty");
+  hs::shard_merge_kernel<<<rows, head_dim < 128 ? head_dim : 128, 0, hs::as_stream(stream)>>>(m, l, o, n_shards,
+                                                                                            rows, head_dim, out);
+  return hs::check_launch("shard_merge");
+}

@@ -1,0 +1,435 @@
+"""Decoder-only Llama block on B200: model config, weights, forward entry
+points and sampling -- the drop-in for hierspec/model.py.
+
+Same names, signatures and error behaviour as the reference
+(model.py:28-393); the arithmetic runs in the sm_100a library:
+
+* weights are packed once per device to bf16 [out][in] (`DeviceModel`,
+  replacing `ModelWeights.runtime()`, model.py:116-143);
+* `prefill` / `decode_step` / `decode_chunk` call `hs_forward`, one native
+  call per lane step; `decode_chunk` is a single batched forward whose rows
+  are bit-identical to a `decode_step` loop (the kernels' reductions do not
+  depend on the batch size), which is the reference's own contract
+  (model.py:366-378);
+* sampling (`prob_from_logits`, `sample_from_probs`) runs in fp64 kernels
+  consuming exactly one uniform per draw from the caller's Generator.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import HsModel, check, lib
+from .errors import CapacityError, FiniteError, ShapeError
+from .runtime import (UniformStream, as_device_f32, as_device_f64, device, ptr, stream_ptr,
+                      to_i32_device, workspaces)
+
+BOS = 256
+EOS = 257
+PAD = 258
+TOKENIZER_VOCAB = 259
+
+
+def _pad64(n: int) -> int:
+    return (n + 63) // 64 * 64
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """Architecture hyper-parameters (model.py:28-59)."""
+    n_layers: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    d_ff: int
+    vocab_size: int
+    max_seq: int
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-5
+
+    def __post_init__(self):
+        for name in ("n_layers", "n_heads", "n_kv_heads", "head_dim", "d_ff"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be positive")
+        if self.n_heads % self.n_kv_heads:
+            raise ValueError("n_heads must be a multiple of n_kv_heads")
+        if self.head_dim % 2:
+            raise ValueError("head_dim must be even")
+        if self.max_seq < 1 or self.vocab_size < 2:
+            raise ValueError("max_seq >= 1 and vocab_size >= 2 required")
+        # reals live as f32 in the weight format: canonicalise (model.py:50-53)
+        object.__setattr__(self, "rope_theta", float(np.float32(self.rope_theta)))
+        object.__setattr__(self, "norm_eps", float(np.float32(self.norm_eps)))
+        if self.rope_theta <= 0 or self.norm_eps < 0:
+            raise ValueError("rope_theta must be positive and norm_eps non-negative")
+
+    @property
+    def d_model(self) -> int:
+        return self.n_heads * self.head_dim
+
+
+def tensor_order(config: ModelConfig, tied_head: bool):
+    """Weight tensor names and shapes in file/generation order (model.py:63-82)."""
+    d, kv = config.d_model, config.n_kv_heads * config.head_dim
+    names = [("embedding", (config.vocab_size, d))]
+    for i in range(config.n_layers):
+        for suffix, shape in (("attn_norm", (d,)), ("wq", (d, d)), ("wk", (d, kv)), ("wv", (d, kv)),
+                              ("wo", (d, d)), ("mlp_norm", (d,)), ("w_gate", (d, config.d_ff)),
+                              ("w_up", (d, config.d_ff)), ("w_down", (config.d_ff, d))):
+            names.append((f"layers.{i}.{suffix}", shape))
+    names.append(("final_norm", (d,)))
+    if not tied_head:
+        names.append(("lm_head", (d, config.vocab_size)))
+    return names
+
+
+def rope_tables(n_pos: int, head_dim: int, theta: float):
+    """fp32 cos/sin [n_pos, head_dim/2]: fp64 angles rounded once to fp32
+    (tensor.py:66-76)."""
+    half = head_dim // 2
+    inv = np.power(np.float64(theta), -2.0 * np.arange(half, dtype=np.float64) / np.float64(head_dim))
+    ang = np.arange(n_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+class DeviceModel:
+    """bf16 packing of a model on one CUDA device plus its `HsModel` descriptor.
+
+    Layout (include/hs_abi.h): matrices transposed to [out][in] with the row
+    stride padded to 64 elements; wq|wk|wv fused; gate/up rows interleaved
+    (gate_i, up_i) so the GEMV's SwiGLU epilogue sees both halves; norms and
+    the rope table stay fp32.
+    """
+
+    def __init__(self, config: ModelConfig, tensors: dict, tied_head: bool):
+        self.config = config
+        self.tied_head = tied_head
+        dev = device()
+        L, d, dff, V = config.n_layers, config.d_model, config.d_ff, config.vocab_size
+        kv = config.n_kv_heads * config.head_dim
+        self.ld_d, self.ld_ff = _pad64(d), _pad64(dff)
+        nqkv = d + 2 * kv
+
+        def mat(a, ld):   # numpy [in, out] fp32 -> torch [out, ld] bf16
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).t()
+            out = torch.zeros((t.shape[0], ld), dtype=torch.bfloat16, device=dev)
+            out[:, :t.shape[1]] = t.to(torch.bfloat16)
+            return out
+
+        g = lambda i, n: tensors[f"layers.{i}.{n}"]
+        self.wqkv = torch.empty((L, nqkv, self.ld_d), dtype=torch.bfloat16, device=dev)
+        self.wo = torch.empty((L, d, self.ld_d), dtype=torch.bfloat16, device=dev)
+        self.wgu = torch.empty((L, 2 * dff, self.ld_d), dtype=torch.bfloat16, device=dev)
+        self.wdown = torch.empty((L, d, self.ld_ff), dtype=torch.bfloat16, device=dev)
+        self.attn_norm = torch.empty((L, d), dtype=torch.float32, device=dev)
+        self.mlp_norm = torch.empty((L, d), dtype=torch.float32, device=dev)
+        for i in range(L):
+            self.wqkv[i] = mat(np.concatenate([g(i, "wq"), g(i, "wk"), g(i, "wv")], axis=1), self.ld_d)
+            self.wo[i] = mat(g(i, "wo"), self.ld_d)
+            gu = np.empty((d, 2 * dff), np.float32)
+            gu[:, 0::2] = g(i, "w_gate")
+            gu[:, 1::2] = g(i, "w_up")
+            self.wgu[i] = mat(gu, self.ld_d)
+            self.wdown[i] = mat(g(i, "w_down"), self.ld_ff)
+            self.attn_norm[i] = torch.from_numpy(g(i, "attn_norm").astype(np.float32))
+            self.mlp_norm[i] = torch.from_numpy(g(i, "mlp_norm").astype(np.float32))
+        self.emb = mat(tensors["embedding"].T, self.ld_d)
+        self.head = self.emb if tied_head else mat(tensors["lm_head"], self.ld_d)
+        self.final_norm = torch.from_numpy(tensors["final_norm"].astype(np.float32)).to(dev)
+        self._finish()
+
+    @classmethod
+    def random(cls, config: ModelConfig, seed: int, tied_head: bool = False, std: float = 0.02):
+        """Random-init weights generated directly on the device (bf16), for
+        model sizes whose host fp32 copy is impractical (Llama2-7B shape).
+        Same distribution as generate_weights, different stream."""
+        self = cls.__new__(cls)
+        self.config, self.tied_head = config, tied_head
+        dev = device()
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        L, d, dff, V = config.n_layers, config.d_model, config.d_ff, config.vocab_size
+        kv = config.n_kv_heads * config.head_dim
+        self.ld_d, self.ld_ff = _pad64(d), _pad64(dff)
+
+        def rnd(rows, cols, ld):
+            out = torch.zeros((rows, ld), dtype=torch.bfloat16, device=dev)
+            out[:, :cols] = (torch.randn((rows, cols), generator=gen, device=dev) * std).to(torch.bfloat16)
+            return out
+
+        self.wqkv = torch.stack([rnd(d + 2 * kv, d, self.ld_d) for _ in range(L)])
+        self.wo = torch.stack([rnd(d, d, self.ld_d) for _ in range(L)])
+        self.wgu = torch.empty((L, 2 * dff, self.ld_d), dtype=torch.bfloat16, device=dev)
+        for i in range(L):
+            self.wgu[i] = rnd(2 * dff, d, self.ld_d)
+        self.wdown = torch.stack([rnd(d, dff, self.ld_ff) for _ in range(L)])
+        self.attn_norm = 1.0 + torch.randn((L, d), generator=gen, device=dev) * std
+        self.mlp_norm = 1.0 + torch.randn((L, d), generator=gen, device=dev) * std
+        self.emb = rnd(V, d, self.ld_d)
+        self.head = self.emb if tied_head else rnd(V, d, self.ld_d)
+        self.final_norm = 1.0 + torch.randn((d,), generator=gen, device=dev) * std
+        self._finish()
+        return self
+
+    def _finish(self):
+        cfg = self.config
+        cos, sin = rope_tables(cfg.max_seq, cfg.head_dim, cfg.rope_theta)
+        dev = device()
+        self.rope_cos = torch.from_numpy(cos).to(dev)
+        self.rope_sin = torch.from_numpy(sin).to(dev)
+        s = HsModel()
+        s.n_layers, s.n_heads, s.n_kv_heads = cfg.n_layers, cfg.n_heads, cfg.n_kv_heads
+        s.head_dim, s.d_ff, s.vocab_size, s.max_seq = cfg.head_dim, cfg.d_ff, cfg.vocab_size, cfg.max_seq
+        s.d_model, s.ld_d, s.ld_ff, s.norm_eps = cfg.d_model, self.ld_d, self.ld_ff, cfg.norm_eps
+        for name in ("emb", "head", "final_norm", "attn_norm", "mlp_norm", "wqkv", "wo", "wgu", "wdown",
+                     "rope_cos", "rope_sin"):
+            setattr(s, name, getattr(self, name).data_ptr())
+        self.struct = s
+        self.ref = C.byref(s)
+
+    @property
+    def weight_bytes(self) -> int:
+        """Algorithmic weight bytes streamed per forward (embedding row excluded)."""
+        cfg = self.config
+        kv = cfg.n_kv_heads * cfg.head_dim
+        d, dff, L = cfg.d_model, cfg.d_ff, cfg.n_layers
+        per_layer = (d * (d + 2 * kv) + d * d + 2 * d * dff + dff * d) * 2 + 2 * d * 4
+        return L * per_layer + cfg.vocab_size * d * 2 + d * 4
+
+
+@dataclass
+class ModelWeights:
+    """Host weights in the reference's file layout (model.py:85-143).  The
+    device packing is built once per process on first use (`device()`)."""
+    config: ModelConfig
+    tensors: dict
+    tied_head: bool = True
+    _dev: Optional[DeviceModel] = field(default=None, repr=False, compare=False)
+
+    def validate(self):
+        expected = dict(tensor_order(self.config, self.tied_head))
+        if set(expected) != set(self.tensors):
+            raise ShapeError(f"weight tensor set mismatch: {sorted(set(expected) ^ set(self.tensors))}")
+        for name, shape in expected.items():
+            t = self.tensors[name]
+            if tuple(t.shape) != shape:
+                raise ShapeError(f"{name}: shape {t.shape}, expected {shape}")
+            if t.dtype != np.float32:
+                raise ShapeError(f"{name}: dtype {t.dtype}, expected float32")
+            if not np.isfinite(t).all():
+                raise ShapeError(f"{name}: non-finite entries")
+        return self
+
+    def checksum(self) -> str:
+        h = hashlib.sha256()
+        for name, _ in tensor_order(self.config, self.tied_head):
+            h.update(name.encode())
+            h.update(self.tensors[name].tobytes())
+        return h.hexdigest()
+
+    def device(self) -> DeviceModel:
+        if self._dev is None:
+            self._dev = DeviceModel(self.config, self.tensors, self.tied_head)
+        return self._dev
+
+    def runtime(self) -> DeviceModel:
+        """Reference name for the packed runtime form (model.py:116)."""
+        return self.device()
+
+    def invalidate(self) -> None:
+        """Drop the device packing after mutating `tensors` in place (the
+        reference's `weights._runtime = None`)."""
+        self._dev = None
+
+    def __setattr__(self, name, value):
+        if name == "_runtime" and value is None:   # reference idiom: weights._runtime = None
+            object.__setattr__(self, "_dev", None)
+            return
+        object.__setattr__(self, name, value)
+
+    @classmethod
+    def on_device(cls, dm: DeviceModel) -> "ModelWeights":
+        """Wrap device-only random weights (DeviceModel.random)."""
+        w = cls(dm.config, {}, dm.tied_head)
+        w._dev = dm
+        return w
+
+
+def generate_weights(config: ModelConfig, seed: int, tied_head: bool = True) -> ModelWeights:
+    """Deterministic init, identical stream to the reference (model.py:146-157)."""
+    rng = np.random.default_rng(seed)
+    tensors = {}
+    for name, shape in tensor_order(config, tied_head):
+        draw = rng.standard_normal(shape) * 0.02
+        tensors[name] = (1.0 + draw if "norm" in name else draw).astype(np.float32)
+    return ModelWeights(config, tensors, tied_head).validate()
+
+
+# ---------------------------------------------------------------------------
+# tokenizer (model.py:163-176)
+
+def tokenize(data: bytes) -> list:
+    return [BOS] + list(data)
+
+
+def detokenize(tokens: Sequence[int], vocab_size: int = TOKENIZER_VOCAB) -> bytes:
+    out = bytearray()
+    for t in tokens:
+        if not 0 <= t < vocab_size:
+            raise ValueError(f"token id {t} outside vocab of size {vocab_size}")
+        if t < 256:
+            out.append(t)
+    return bytes(out)
+
+
+# ---------------------------------------------------------------------------
+# sampling (model.py:182-206) -- device kernels, fp64
+
+def prob_from_logits(logits, temperature: float) -> np.ndarray:
+    """fp64 distribution; temperature 0 is a one-hot argmax (lowest index on ties)."""
+    if temperature < 0:
+        raise ValueError("temperature must be >= 0")
+    lg = as_device_f32(logits).reshape(-1)
+    out = torch.empty(lg.numel(), dtype=torch.float64, device=lg.device)
+    check(lib.hs_probs(ptr(lg), 1, lg.numel(), float(temperature), ptr(out), stream_ptr()))
+    return out.cpu().numpy()
+
+
+def sample_from_probs(probs, rng: np.random.Generator) -> int:
+    """Inverse-CDF draw consuming exactly one uniform from `rng`."""
+    p = as_device_f64(probs).reshape(-1)
+    u = torch.tensor([rng.random()], dtype=torch.float64, device=p.device)
+    cur = torch.zeros(1, dtype=torch.int32, device=p.device)
+    out = torch.zeros(1, dtype=torch.int32, device=p.device)
+    check(lib.hs_sample(ptr(p), p.numel(), ptr(u), ptr(cur), ptr(out), stream_ptr()))
+    return int(out.item())
+
+
+def sample(logits, temperature: float, rng: np.random.Generator) -> int:
+    return sample_from_probs(prob_from_logits(logits, temperature), rng)
+
+
+# ---------------------------------------------------------------------------
+# forward passes
+
+@dataclass
+class AttentionProbe:
+    layer: int
+    head: int
+    query_position: int
+    positions: np.ndarray
+    weights: np.ndarray
+
+
+class ForwardRecorder:
+    """Last-row post-RoPE queries of the most recent forward, per layer
+    (model.py:222-233).  Kept on the device ([L, H, dh] fp32) so the
+    retrieval builder reads it without a host round trip."""
+
+    def __init__(self, record_probs: bool = False):
+        if record_probs:
+            raise NotImplementedError("attention-probe recording belongs to the analytics harness "
+                                      "(out of scope for the decode hot path)")
+        self.record_probs = False
+        self.stash: Optional[torch.Tensor] = None
+        self.query_position = -1
+
+    def _buffer(self, cfg: ModelConfig) -> torch.Tensor:
+        shape = (cfg.n_layers, cfg.n_heads, cfg.head_dim)
+        if self.stash is None or tuple(self.stash.shape) != shape:
+            self.stash = torch.zeros(shape, dtype=torch.float32, device=device())
+        return self.stash
+
+    @property
+    def last_queries(self) -> list:
+        if self.stash is None:
+            return []
+        host = self.stash.cpu().numpy()
+        return [host[i].copy() for i in range(host.shape[0])]
+
+    @property
+    def last_probs(self) -> list:
+        return []
+
+
+def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[ForwardRecorder] = None,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Causal forward of `tokens` (host list or device int32 tensor) at
+    cache.frontier; returns device logits [t, V] fp32 (model.py:247-331)."""
+    dm = weights.device()
+    cfg = dm.config
+    tok = to_i32_device(tokens)
+    t = tok.numel()
+    if t == 0:
+        raise ValueError("empty token sequence")
+    if not isinstance(tokens, torch.Tensor):
+        arr = np.asarray(tokens)
+        if arr.min() < 0 or arr.max() >= cfg.vocab_size:
+            raise ValueError("token id outside model vocab")
+    if cache.frontier + t > cfg.max_seq:
+        raise CapacityError(f"sequence of {cache.frontier + t} exceeds max_seq {cfg.max_seq}")
+    if out is None:
+        out = torch.empty((t, cfg.vocab_size), dtype=torch.float32, device=tok.device)
+    stash = recorder._buffer(cfg) if recorder is not None else None
+    for a, b in cache._batches(t):
+        step = cache._step(b - a)
+        nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split)
+        ws = workspaces.get("forward", nbytes)
+        check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), ptr(tok) + 4 * a, b - a,
+                             ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))
+        cache._advance(b - a)
+    if recorder is not None:
+        recorder.query_position = cache.frontier - 1
+    return out
+
+
+def _host_rows(logits: torch.Tensor) -> np.ndarray:
+    host = logits.cpu().numpy()
+    if not np.isfinite(host).all():
+        raise FiniteError("forward produced non-finite logits")
+    return host
+
+
+def prefill(weights: ModelWeights, tokens: Sequence[int], cache,
+            recorder: Optional[ForwardRecorder] = None) -> np.ndarray:
+    """Append every prompt position, commit, return all logits rows
+    (model.py:334-354).  Windowed caches are filled in batches whose
+    per-query exposure equals the reference's token-by-token prefill."""
+    if len(tokens) == 0:
+        raise ValueError("prefill needs at least one token")
+    if cache.frontier + len(tokens) > weights.config.max_seq:
+        raise CapacityError(f"sequence of {cache.frontier + len(tokens)} exceeds max_seq "
+                            f"{weights.config.max_seq}")
+    logits = forward_device(weights, tokens, cache, recorder)
+    cache.commit(cache.frontier)
+    return _host_rows(logits)
+
+
+def decode_step(weights: ModelWeights, token: int, cache,
+                recorder: Optional[ForwardRecorder] = None) -> np.ndarray:
+    """One speculative position; next-token logits row (model.py:357-363)."""
+    if cache.frontier < 1:
+        raise ValueError("decode_step requires a non-empty cache")
+    return _host_rows(forward_device(weights, [int(token)], cache, recorder))[0]
+
+
+def decode_chunk(weights: ModelWeights, tokens: Sequence[int], cache,
+                 recorder: Optional[ForwardRecorder] = None) -> np.ndarray:
+    """One logits row per token, bit-identical to a decode_step loop
+    (model.py:366-378) -- computed as one batched forward."""
+    if len(tokens) == 0:
+        raise ValueError("empty chunk")
+    if cache.frontier < 1:
+        raise ValueError("decode_chunk requires a non-empty cache")
+    return _host_rows(forward_device(weights, list(tokens), cache, recorder))
+
+
+def attention_probe(recorder: ForwardRecorder, layer: int, head: int) -> AttentionProbe:
+    raise ValueError("recorder has no recorded attention (probes are an analytics feature, out of scope)")

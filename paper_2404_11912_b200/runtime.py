@@ -1,0 +1,117 @@
+"""Device plumbing shared by the drop-in modules: the CUDA device/stream,
+reusable workspaces, pinned host staging, and the uniform stream that
+carries the reference's RNG protocol onto the device.
+
+PyTorch is used only for device memory and streams; all compute goes
+through `_abi.lib`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2404_11912_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+class _Workspaces:
+    """Grow-only scratch buffers keyed by purpose (one stream => reuse is safe)."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, key: str, nbytes: int) -> torch.Tensor:
+        b = self.bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device())
+            self.bufs[key] = b
+        return b
+
+
+workspaces = _Workspaces()
+
+
+def to_i32_device(tokens) -> torch.Tensor:
+    if isinstance(tokens, torch.Tensor):
+        return tokens.to(device=device(), dtype=torch.int32)
+    return torch.as_tensor(np.asarray(tokens, dtype=np.int32)).to(device(), non_blocking=False)
+
+
+def as_device_f32(a) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device(), dtype=torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(device())
+
+
+def as_device_f64(a) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device(), dtype=torch.float64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device())
+
+
+class UniformStream:
+    """Uniforms of one numpy PCG64 Generator, in draw order, on the device.
+
+    Kernels consume them through a device cursor (one per sampling event and
+    one per verification, speculation.py:9-12).  The host refills by
+    compacting [cursor, drawn) and appending a fresh block whenever fewer
+    than `margin` remain.  `sync_rng()` rewinds the Generator to its state
+    at creation and re-draws exactly the consumed count, so callers that
+    keep using the Generator see the reference's stream position.
+    """
+
+    def __init__(self, rng: np.random.Generator, block: int = 4096, keep_state: bool = False):
+        self.rng = rng
+        self.block = block
+        self.state0 = rng.bit_generator.state if keep_state else None
+        self.consumed_before = 0          # uniforms consumed before the current buffer
+        host = rng.random(block)
+        self.buf = torch.from_numpy(host).to(device())
+        self.drawn = block                # in the current buffer
+        self.cursor = torch.zeros(1, dtype=torch.int32, device=device())
+        self.host_cursor = 0
+
+    def ensure(self, margin: int, host_cursor: int) -> None:
+        """Call with the cursor value read back at the last sync."""
+        self.host_cursor = host_cursor
+        if self.drawn - host_cursor >= margin:
+            return
+        rest = self.buf[host_cursor:self.drawn]
+        fresh = torch.from_numpy(self.rng.random(self.block)).to(device())
+        self.consumed_before += host_cursor
+        self.buf = torch.cat([rest, fresh])
+        self.drawn = self.buf.numel()
+        self.cursor.zero_()
+        self.host_cursor = 0
+
+    def consumed(self, host_cursor: int) -> int:
+        return self.consumed_before + host_cursor
+
+    def sync_rng(self, host_cursor: int) -> None:
+        if self.state0 is None:
+            return
+        self.rng.bit_generator.state = self.state0
+        n = self.consumed(host_cursor)
+        if n:
+            self.rng.random(n)
+
+
+class Pinned:
+    """Small pinned host buffer for per-round readbacks."""
+
+    def __init__(self, n: int, dtype=torch.int32):
+        self.t = torch.empty(n, dtype=dtype, pin_memory=True)

@@ -1,0 +1,552 @@
+"""Hierarchical speculative decoding on B200 -- the drop-in for
+hierspec/speculation.py (Algorithm 1 of TriForce).
+
+Structure of one outer round (speculation.py:338-368):
+  draft lane (StreamingCache)  -> gamma1 drafted tokens per inner round
+  retrieval lane (RetrievalCache) scores them, verify chain -> x_hat
+  ... until len(x_hat) >= gamma2
+  full lane (FullCache) scores x_hat in ONE batched forward, verify chain.
+
+Device residency: drafted tokens, draft/target distributions (fp64 [rows, V])
+and the uniforms stay on the device; the host reads back only the few
+emitted token ids, the accepted count and the RNG cursor once per inner and
+once per outer round (it needs them for its control flow).  The RNG
+protocol -- one uniform per draft sample, one per verification, one per
+correction/bonus, in loop order from one PCG64 stream -- is the
+reference's (speculation.py:9-12), so traces replay the CPU engine.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from ._abi import check, lib, status_error
+from .caches import (FullCache, KVCache, RetrievalCache, RetrievalConfig, RollingAcceptance, StreamingCache,
+                     StreamingConfig, should_rebuild)
+from .errors import ContractError
+from .model import (ForwardRecorder, ModelWeights, forward_device, prob_from_logits, sample_from_probs)
+from .runtime import UniformStream, as_device_f64, device, ptr, stream_ptr, to_i32_device
+
+
+@dataclass
+class SpecConfig:
+    """Algorithm 1 parameters (speculation.py:35-49)."""
+    target_len: int
+    gamma1: int = 2
+    gamma2: int = 6
+    temperature: float = 0.0
+    seed: int = 0
+    streaming: StreamingConfig = field(default_factory=StreamingConfig)
+    retrieval: RetrievalConfig = field(default_factory=RetrievalConfig)
+
+    def __post_init__(self):
+        if self.gamma1 < 1 or self.gamma2 < 1:
+            raise ValueError("gamma1 and gamma2 must be >= 1")
+        if self.temperature < 0:
+            raise ValueError("temperature must be >= 0")
+
+
+def _one_uniform(rng) -> tuple:
+    u = torch.tensor([rng.random()], dtype=torch.float64, device=device())
+    cur = torch.zeros(1, dtype=torch.int32, device=u.device)
+    return u, cur
+
+
+def verify_token(x: int, q, p, rng: np.random.Generator) -> bool:
+    """Accept x ~ q with probability min(1, p[x]/q[x]); one uniform
+    (speculation.py:52-62).  q[x] <= 0 raises ContractError."""
+    qd, pd = as_device_f64(q).reshape(-1), as_device_f64(p).reshape(-1)
+    if float(qd[int(x)].item()) <= 0.0:
+        raise ContractError(f"verify_token: draft distribution assigns 0 to token {x}")
+    u, cur = _one_uniform(rng)
+    res = torch.zeros(2, dtype=torch.int32, device=u.device)
+    check(lib.hs_verify_token(int(x), ptr(qd), ptr(pd), ptr(u), ptr(cur), ptr(res), stream_ptr()))
+    return bool(res[0].item())
+
+
+def correct_token(q, p, rng: np.random.Generator) -> int:
+    """Sample normalize(max(p - q, 0)), falling back to p when the residual
+    vanishes; one uniform (speculation.py:65-72)."""
+    qd, pd = as_device_f64(q).reshape(-1), as_device_f64(p).reshape(-1)
+    u, cur = _one_uniform(rng)
+    out = torch.zeros(1, dtype=torch.int32, device=u.device)
+    check(lib.hs_correct_token(ptr(qd), ptr(pd), pd.numel(), ptr(u), ptr(cur), ptr(out), stream_ptr()))
+    return int(out.item())
+
+
+class Lane:
+    """Model + cache + frontier logits row (speculation.py:75-130).  The
+    frontier row lives in a device buffer; `None` semantics are tracked on
+    the host."""
+
+    def __init__(self, weights: ModelWeights, cache: KVCache):
+        self.weights = weights
+        self.cache = cache
+        self.recorder = ForwardRecorder(record_probs=False)
+        V = weights.config.vocab_size
+        self._front = torch.zeros(V, dtype=torch.float32, device=device())
+        self._has_front = False
+        self._scratch = None
+
+    @property
+    def frontier(self) -> int:
+        return self.cache.frontier
+
+    @property
+    def frontier_logits(self):
+        return self._front if self._has_front else None
+
+    @frontier_logits.setter
+    def frontier_logits(self, value):
+        if value is None:
+            self._has_front = False
+        else:
+            self._front.copy_(torch.as_tensor(value, dtype=torch.float32).reshape(-1).to(self._front.device))
+            self._has_front = True
+
+    def _logits_buf(self, t: int) -> torch.Tensor:
+        V = self.weights.config.vocab_size
+        if self._scratch is None or self._scratch.shape[0] < t:
+            self._scratch = torch.empty((max(t, 16), V), dtype=torch.float32, device=device())
+        return self._scratch[:t]
+
+    def _forward(self, tokens) -> torch.Tensor:
+        """Forward (host list or device int32 tensor) -> device logits [t, V];
+        updates the frontier row."""
+        t = tokens.numel() if isinstance(tokens, torch.Tensor) else len(tokens)
+        out = forward_device(self.weights, tokens, self.cache, self.recorder, out=self._logits_buf(t))
+        self._front.copy_(out[t - 1])
+        self._has_front = True
+        return out
+
+    def prefill(self, tokens: Sequence[int]) -> None:
+        if len(tokens) == 0:
+            raise ValueError("prefill needs at least one token")
+        self._forward(list(tokens))
+        self.cache.commit(self.cache.frontier)
+
+    def advance(self, tokens: Sequence[int]) -> None:
+        if len(tokens):
+            self._forward(list(tokens))
+
+    def catch_up(self, sequence: Sequence[int]) -> None:
+        if self.frontier < len(sequence):
+            self.advance(list(sequence[self.frontier:]))
+
+    def score(self, tokens: Sequence[int]) -> list:
+        """len(tokens) + 1 logits rows (device), the first being the current
+        frontier row -- one batched forward."""
+        if not self._has_front:
+            raise ContractError("lane has no frontier logits; advance over committed tokens first")
+        rows = [self._front.clone()]
+        if len(tokens):
+            out = self._forward(list(tokens))
+            rows.extend(out[i].clone() for i in range(out.shape[0]))
+        return rows
+
+    def rollback_to(self, n: int) -> None:
+        if n < self.cache.frontier:
+            self._has_front = False
+        self.cache.rollback_to(n)
+
+    def commit(self) -> None:
+        self.cache.commit(self.cache.frontier)
+
+    def last_queries(self) -> list:
+        return self.recorder.last_queries
+
+    def clone(self) -> "Lane":
+        c = Lane(self.weights, self.cache.clone())
+        c._front.copy_(self._front)
+        c._has_front = self._has_front
+        if self.recorder.stash is not None:
+            c.recorder.stash = self.recorder.stash.clone()
+        return c
+
+
+@dataclass
+class LevelStats:
+    proposed: int = 0
+    accepted: int = 0
+    rounds: int = 0
+
+    @property
+    def rejected(self) -> int:
+        return self.proposed - self.accepted
+
+    @property
+    def rate(self) -> float:
+        return self.accepted / self.proposed if self.proposed else 0.0
+
+
+class StepTrace:
+    """Per-token provenance, JSON-lines serialisable (speculation.py:148-184)."""
+
+    def __init__(self):
+        self.records: list = []
+        self.inner = LevelStats()
+        self.outer = LevelStats()
+
+    def add(self, position, token, level, accepted, outer_round):
+        self.records.append({"position": int(position), "token": int(token), "level": level,
+                             "accepted": bool(accepted), "outer_round": int(outer_round)})
+
+    def truncate(self, n_tokens: int):
+        self.records = self.records[:n_tokens]
+
+    def emitted_tokens(self) -> list:
+        return [r["token"] for r in self.records]
+
+    def to_jsonl(self, fp) -> None:
+        for r in self.records:
+            fp.write(json.dumps(r) + "\n")
+
+    def summary(self) -> dict:
+        def lv(s):
+            return {"proposed": s.proposed, "accepted": s.accepted, "rounds": s.rounds, "rate": s.rate}
+        return {"emitted": len(self.records), "inner": lv(self.inner), "outer": lv(self.outer)}
+
+
+# ---------------------------------------------------------------------------
+# device round machinery
+
+class _RoundBuffers:
+    def __init__(self, V: int, gamma1: int, gamma2: int):
+        dev = device()
+        rows = gamma1 + gamma2 + 2
+        self.V = V
+        self.q = torch.empty((gamma1, V), dtype=torch.float64, device=dev)
+        self.dtok = torch.empty(gamma1, dtype=torch.int32, device=dev)
+        self.p = torch.empty((rows, V), dtype=torch.float64, device=dev)
+        self.phat = torch.empty((rows, V), dtype=torch.float64, device=dev)
+        self.xtok = torch.empty(rows, dtype=torch.int32, device=dev)
+        self.res = torch.zeros(rows + 4, dtype=torch.int32, device=dev)
+        self.host = torch.zeros(rows + 5, dtype=torch.int32, pin_memory=True)
+
+
+def _readback(buf: _RoundBuffers, n: int, us: UniformStream):
+    """One device->host sync: chain result for n proposals + RNG cursor."""
+    buf.host[:n + 4].copy_(buf.res[:n + 4], non_blocking=True)
+    buf.host[n + 4:n + 5].copy_(us.cursor, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    h = buf.host.numpy()
+    count, accepted, status, cursor = int(h[n + 1]), int(h[n + 2]), int(h[n + 3]), int(h[n + 4])
+    if status != 0:
+        raise status_error(status, "verify_token: draft distribution assigns 0 to the drafted token")
+    return [int(x) for x in h[:count]], accepted, cursor
+
+
+def _draft_round_dev(lane: Lane, seq: Sequence[int], gamma1: int, T: float, us: UniformStream,
+                     buf: _RoundBuffers) -> None:
+    """draft_round (speculation.py:211-227) with tokens and q rows on device."""
+    lane.catch_up(seq)
+    if not lane._has_front:
+        raise ContractError("lane has no frontier logits; advance over committed tokens first")
+    V = buf.V
+    s = stream_ptr()
+    for g in range(gamma1):
+        check(lib.hs_draft_sample(ptr(lane._front), V, float(T), ptr(buf.q[g]), ptr(us.buf), ptr(us.cursor),
+                                  ptr(buf.dtok[g:g + 1]), s))
+        lane._forward(buf.dtok[g:g + 1])
+
+
+def _score_rows_dev(lane: Lane, seq: Sequence[int], tokens_dev: torch.Tensor, T: float,
+                    out: torch.Tensor) -> None:
+    """lane.catch_up(seq) + lane.score(tokens) as ONE batched forward; the
+    len(tokens)+1 target distributions go to out[0:n+1] (fp64)."""
+    V = lane.weights.config.vocab_size
+    s = stream_ptr()
+    cu = list(seq[lane.frontier:])
+    n = tokens_dev.numel()
+    if not cu:
+        if not lane._has_front:
+            raise ContractError("lane has no frontier logits; advance over committed tokens first")
+        check(lib.hs_probs(ptr(lane._front), 1, V, float(T), ptr(out[0]), s))
+    toks = torch.cat([to_i32_device(cu), tokens_dev]) if cu else tokens_dev
+    logits = lane._forward(toks)
+    if cu:
+        check(lib.hs_probs(ptr(logits[len(cu) - 1]), n + 1, V, float(T), ptr(out[0]), s))
+    else:
+        check(lib.hs_probs(ptr(logits[0]), n, V, float(T), ptr(out[1]), s))
+
+
+def _chain_dev(tokens_dev, n, qd, pd, V, us, buf):
+    check(lib.hs_verify_chain(ptr(tokens_dev), n, ptr(qd), ptr(pd), V, ptr(us.buf), ptr(us.cursor), ptr(buf.res),
+                              stream_ptr()))
+
+
+def _inner_round_dev(retr: Lane, draft: Lane, seq, cfg: SpecConfig, us, buf, phat_off: int):
+    V = buf.V
+    _draft_round_dev(draft, seq, cfg.gamma1, cfg.temperature, us, buf)
+    _score_rows_dev(retr, seq, buf.dtok, cfg.temperature, buf.p)
+    _chain_dev(buf.dtok, cfg.gamma1, buf.q, buf.p, V, us, buf)
+    # p_hat rows of the emitted tokens: copy all gamma1+1, the surplus is overwritten later
+    buf.phat[phat_off:phat_off + cfg.gamma1 + 1].copy_(buf.p[:cfg.gamma1 + 1])
+    return _readback(buf, cfg.gamma1, us)
+
+
+# ---------------------------------------------------------------------------
+# public single-round API (speculation.py:211-275) -- numpy in/out
+
+def _api_buffers(lane: Lane, gamma1: int, gamma2: int) -> _RoundBuffers:
+    return _RoundBuffers(lane.weights.config.vocab_size, gamma1, gamma2)
+
+
+def draft_round(draft_lane: Lane, committed: Sequence[int], gamma1: int, temperature: float,
+                rng: np.random.Generator):
+    """Draft gamma1 tokens; returns (tokens, q distributions as numpy)."""
+    us = UniformStream(rng, block=max(64, gamma1), keep_state=True)
+    buf = _api_buffers(draft_lane, gamma1, 1)
+    _draft_round_dev(draft_lane, list(committed), gamma1, temperature, us, buf)
+    toks = buf.dtok.cpu().numpy().astype(int).tolist()
+    us.sync_rng(gamma1)
+    return toks, [buf.q[i].cpu().numpy() for i in range(gamma1)]
+
+
+def _verify_chain(tokens, draft_dists, target_dists, rng):
+    """(emitted, labels, accepted) -- speculation.py:187-208."""
+    n = len(tokens)
+    V = len(target_dists[0])
+    us = UniformStream(rng, block=max(64, n + 1), keep_state=True)
+    buf = _RoundBuffers(V, max(n, 1), max(n, 1))
+    tok = to_i32_device(list(tokens)) if n else torch.zeros(1, dtype=torch.int32, device=device())
+    qd = torch.stack([as_device_f64(x).reshape(-1) for x in draft_dists]) if n else buf.q
+    pd = torch.stack([as_device_f64(x).reshape(-1) for x in target_dists])
+    _chain_dev(tok, n, qd, pd, V, us, buf)
+    emitted, accepted, cursor = _readback(buf, n, us)
+    us.sync_rng(cursor)
+    labels = ["accepted"] * accepted + (["corrected"] if accepted < n else ["bonus"])
+    return emitted, labels, accepted
+
+
+def inner_speculate(retr_lane: Lane, draft_lane: Lane, committed: Sequence[int], config: SpecConfig,
+                    rng: np.random.Generator, trace: Optional[StepTrace] = None):
+    """Draft rounds verified against the retrieval lane until >= gamma2
+    tokens (speculation.py:230-261).  Returns (x_hat, p_hats, labels)."""
+    V = retr_lane.weights.config.vocab_size
+    us = UniformStream(rng, keep_state=True)
+    buf = _RoundBuffers(V, config.gamma1, config.gamma2)
+    x_hat, labels, cursor = [], [], 0
+    base = len(committed)
+    while len(x_hat) < config.gamma2:
+        us.ensure(2 * config.gamma1 + 2, cursor)
+        emitted, accepted, cursor = _inner_round_dev(retr_lane, draft_lane, list(committed) + x_hat, config, us,
+                                                     buf, len(x_hat))
+        x_hat.extend(emitted)
+        labels.extend(["draft"] * accepted + ["retrieval"])
+        if trace is not None:
+            trace.inner.rounds += 1
+            trace.inner.proposed += config.gamma1
+            trace.inner.accepted += accepted
+        valid = base + len(x_hat) - 1
+        draft_lane.rollback_to(valid)
+        retr_lane.rollback_to(valid)
+    us.sync_rng(cursor)
+    return x_hat, [buf.phat[i].cpu().numpy() for i in range(len(x_hat))], labels
+
+
+def outer_verify(full_lane: Lane, committed: Sequence[int], x_hat: Sequence[int], p_hats, temperature: float,
+                 rng: np.random.Generator):
+    """Score x_hat under the full cache (one batched forward) and verify
+    (speculation.py:264-275).  Returns (emitted, labels, accepted, pdists)."""
+    n = len(x_hat)
+    V = full_lane.weights.config.vocab_size
+    us = UniformStream(rng, block=max(64, n + 1), keep_state=True)
+    buf = _RoundBuffers(V, 1, n)
+    xt = to_i32_device(list(x_hat))
+    _score_rows_dev(full_lane, list(committed), xt, temperature, buf.p)
+    qd = torch.stack([as_device_f64(x).reshape(-1) for x in p_hats])
+    _chain_dev(xt, n, qd, buf.p, V, us, buf)
+    emitted, accepted, cursor = _readback(buf, n, us)
+    us.sync_rng(cursor)
+    labels = ["accepted"] * accepted + (["corrected"] if accepted < n else ["bonus"])
+    return emitted, labels, accepted, [buf.p[i].cpu().numpy() for i in range(n + 1)]
+
+
+# ---------------------------------------------------------------------------
+# the two-level session
+
+class HierarchicalSession:
+    """Prefilled lanes for one (target, draft, prefix) triple
+    (speculation.py:278-368).  Single-threaded; clone() snapshots."""
+
+    def __init__(self, target: ModelWeights, draft: ModelWeights, prefix: Sequence[int], config: SpecConfig,
+                 _prefill: bool = True):
+        if target.config.vocab_size != draft.config.vocab_size:
+            raise ContractError("target and draft models must share a vocabulary")
+        if len(prefix) < 1:
+            raise ValueError("prefix must be non-empty")
+        if config.target_len <= len(prefix):
+            raise ValueError("target_len must exceed the prefix length")
+        self.config = config
+        self.committed = list(prefix)
+        self.full_lane = Lane(target, FullCache.from_config(target.config))
+        self.draft_lane = Lane(draft, StreamingCache.from_config(draft.config, config.streaming))
+        self.retr_lane = Lane(target, RetrievalCache.from_config(target.config, config.retrieval))
+        self.rolling = RollingAcceptance(config.retrieval.rolling_window)
+        self.tokens_since_build = 0
+        self.rebuilds = 0
+        self._buf = _RoundBuffers(target.config.vocab_size, config.gamma1, config.gamma2)
+        if _prefill:
+            self.full_lane.prefill(prefix)
+            self.draft_lane.prefill(prefix)
+            self._initial_build()
+
+    def _initial_build(self):
+        n = len(self.committed)
+        retr: RetrievalCache = self.retr_lane.cache
+        q = self.full_lane.recorder.stash
+        if n >= 2:
+            retr.build(self.full_lane.cache, q, upto=n - 1)
+        else:
+            retr.build(self.full_lane.cache, q, upto=n)
+            self.retr_lane.frontier_logits = self.full_lane.frontier_logits
+
+    @classmethod
+    def synthetic(cls, target: ModelWeights, draft: ModelWeights, context: Sequence[int], config: SpecConfig,
+                  seed: int = 0):
+        """Session over a synthetic long context (throughput configs,
+        SURVEY §7.4 item 6): the full and draft caches are filled with random
+        bf16 K/V for positions [0, n-1); the last context token is then
+        decoded for real on every lane and the initial build uses its queries."""
+        s = cls(target, draft, context, config, _prefill=False)
+        n = len(context)
+        s.full_lane.cache.fill_random_(n - 1, seed=seed)
+        s.draft_lane.cache.fill_random_(n - 1, seed=seed + 1)
+        s.full_lane.advance([context[-1]])
+        s.full_lane.commit()
+        s.draft_lane.advance([context[-1]])
+        s.draft_lane.commit()
+        s._initial_build()
+        return s
+
+    def clone(self) -> "HierarchicalSession":
+        c = object.__new__(HierarchicalSession)
+        c.config = self.config
+        c.committed = list(self.committed)
+        c.full_lane = self.full_lane.clone()
+        c.draft_lane = self.draft_lane.clone()
+        c.retr_lane = self.retr_lane.clone()
+        c.rolling = RollingAcceptance(self.config.retrieval.rolling_window)
+        c.rolling.rates = list(self.rolling.rates)
+        c.tokens_since_build = self.tokens_since_build
+        c.rebuilds = self.rebuilds
+        c._buf = _RoundBuffers(self.full_lane.weights.config.vocab_size, self.config.gamma1, self.config.gamma2)
+        return c
+
+    def _maybe_rebuild(self) -> bool:
+        cache: RetrievalCache = self.retr_lane.cache
+        if not should_rebuild(cache.config, self.tokens_since_build, self.rolling):
+            return False
+        # queries of the last committed token under the OLD exposure
+        # (speculation.py:324-336), then rebuild from the full cache
+        self.retr_lane.catch_up(self.committed)
+        cache.build(self.full_lane.cache, self.retr_lane.recorder.stash, upto=self.full_lane.frontier)
+        self.retr_lane.frontier_logits = None
+        self.tokens_since_build = 0
+        self.rolling.rates.clear()
+        self.rebuilds += 1
+        return True
+
+    def generate(self, seed: Optional[int] = None):
+        """Run the two-level loop until target_len tokens are committed;
+        returns (tokens, StepTrace)."""
+        cfg = self.config
+        rng = np.random.default_rng(cfg.seed if seed is None else seed)
+        us = UniformStream(rng)
+        buf = self._buf
+        trace = StepTrace()
+        cursor = 0
+        V = buf.V
+        while len(self.committed) < cfg.target_len:
+            self._maybe_rebuild()
+            # ---- inner level: draft -> retrieval (speculation.py:230-261)
+            x_hat, ilabels = [], []
+            base = len(self.committed)
+            while len(x_hat) < cfg.gamma2:
+                us.ensure(2 * cfg.gamma1 + 2, cursor)
+                emitted, accepted, cursor = _inner_round_dev(self.retr_lane, self.draft_lane,
+                                                             self.committed + x_hat, cfg, us, buf, len(x_hat))
+                x_hat.extend(emitted)
+                ilabels.extend(["draft"] * accepted + ["retrieval"])
+                trace.inner.rounds += 1
+                trace.inner.proposed += cfg.gamma1
+                trace.inner.accepted += accepted
+                valid = base + len(x_hat) - 1
+                self.draft_lane.rollback_to(valid)
+                self.retr_lane.rollback_to(valid)
+            # ---- outer level: full-cache verify (speculation.py:264-275)
+            n = len(x_hat)
+            us.ensure(n + 2, cursor)
+            buf.xtok[:n].copy_(torch.as_tensor(np.asarray(x_hat, np.int32)), non_blocking=False)
+            _score_rows_dev(self.full_lane, self.committed, buf.xtok[:n], cfg.temperature, buf.p)
+            _chain_dev(buf.xtok[:n], n, buf.phat, buf.p, V, us, buf)
+            emitted, accepted, cursor = _readback(buf, n, us)
+            olabels = ["accepted"] * accepted + (["corrected"] if accepted < n else ["bonus"])
+            trace.outer.rounds += 1
+            trace.outer.proposed += n
+            trace.outer.accepted += accepted
+            emitted = emitted[:cfg.target_len - base]
+            for i, tok in enumerate(emitted):
+                level = ilabels[i] if olabels[i] == "accepted" else olabels[i]
+                trace.add(base + i, tok, level, olabels[i] == "accepted", trace.outer.rounds)
+            self.committed.extend(emitted)
+            valid = base + min(accepted, len(emitted))
+            self.full_lane.rollback_to(valid)
+            self.full_lane.commit()
+            for lane in (self.draft_lane, self.retr_lane):
+                lane.rollback_to(min(lane.frontier, valid))
+                lane.commit()
+            self.rolling.push(accepted / n)
+            self.tokens_since_build += len(emitted)
+        return list(self.committed), trace
+
+
+def hierarchical_generate(target: ModelWeights, draft: ModelWeights, prefix: Sequence[int], config: SpecConfig):
+    """Two-level speculative generation (speculation.py:371-375)."""
+    return HierarchicalSession(target, draft, prefix, config).generate()
+
+
+def autoregressive_generate(weights: ModelWeights, prefix: Sequence[int], target_len: int,
+                            temperature: float = 0.0, seed: int = 0) -> list:
+    """Plain decode over the full cache (speculation.py:378-398); the
+    sampled token never leaves the device until the end."""
+    if len(prefix) < 1:
+        raise ValueError("prefix must be non-empty")
+    if target_len <= len(prefix):
+        raise ValueError("target_len must exceed the prefix length")
+    rng = np.random.default_rng(seed)
+    lane = Lane(weights, FullCache.from_config(weights.config))
+    lane.prefill(list(prefix))
+    return _ar_loop(lane, list(prefix), target_len, temperature, rng)
+
+
+def _ar_loop(lane: Lane, out: list, target_len: int, temperature: float, rng) -> list:
+    V = lane.weights.config.vocab_size
+    n_new = target_len - len(out)
+    us = UniformStream(rng, block=max(64, n_new))
+    toks = torch.empty(n_new, dtype=torch.int32, device=device())
+    probs = torch.empty(V, dtype=torch.float64, device=device())
+    s = stream_ptr()
+    for i in range(n_new):
+        check(lib.hs_draft_sample(ptr(lane._front), V, float(temperature), ptr(probs), ptr(us.buf), ptr(us.cursor),
+                                  ptr(toks[i:i + 1]), s))
+        if i == n_new - 1:
+            break
+        lane._forward(toks[i:i + 1])
+        lane.commit()
+    return out + toks.cpu().numpy().astype(int).tolist()
+
+
+class SingleLevelSession:
+    """Standard one-level speculative decoding harness (speculation.py:401-477);
+    an acceptance-measurement pairing, outside Algorithm 1's hot path."""
+
+    def __init__(self, *a, **k):
+        raise NotImplementedError("SingleLevelSession is an analytics pairing outside the decode hot path "
+                                  "(SURVEY.md §2.1, OUT OF SCOPE)")
