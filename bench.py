@@ -1,0 +1,416 @@
+#!/usr/bin/env python3
+"""Benchmark of the TriForce long-context decode hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json config 2, the metric's configuration): Llama2-7B-128K
+shape (32 layers, d 4096, 32 heads, d_ff 11008, vocab 32000), random-init
+bf16 weights, 122,880-token synthetic context (random N(0,1) bf16 K/V,
+see DESIGN.md), JackFram-68M-shaped draft with a StreamingLLM cache (4 sinks,
+budget 256), retrieval cache budget 4,096 in chunks of 8, gamma1 = 2,
+gamma2 = 4, greedy (T = 0).  One step = one `HierarchicalSession.generate`
+call that commits `--gen` (default 32) more tokens; the retrieval rebuild
+policy (stride 128) runs inside the timed region.
+
+Metric: decode tokens/s (and ms/token) -- whole job, N GPUs.  For N > 1 the
+path runs as independent replicas (one session per GPU, no collective on
+the data path), so scaling is weak.
+
+The KV cache (64 GB/GPU at 122,880 positions) exceeds the 126 MB L2, so no
+L2 flush is needed between iterations.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+TARGET_7B = dict(n_layers=32, n_heads=32, n_kv_heads=32, head_dim=128, d_ff=11008, vocab_size=32000,
+                 max_seq=131072)
+DRAFT_68M = dict(n_layers=2, n_heads=12, n_kv_heads=12, head_dim=64, d_ff=3072, vocab_size=32000,
+                 max_seq=131072)
+CONTEXT = 122880
+BUDGET, CHUNK, SINK, STREAM = 4096, 8, 4, 256
+GAMMA1, GAMMA2 = 2, 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--gen", type=int, default=32, help="tokens committed per step")
+    ap.add_argument("--context", type=int, default=CONTEXT)
+    ap.add_argument("--temperature", type=float, default=0.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no extras)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and the reference arm)
+
+def oracle_sample(context: int, temperature: float, rounds: int, time_budget_s: float = 150.0):
+    """TriForce on the CPU oracle (oracle/hs_oracle.py, a restatement of the
+    reference numpy engine): a 1-layer slice of the Llama2-7B shape over the
+    full synthetic context plus the full 2-layer draft, run for whole outer
+    rounds; target-forward time is scaled x32 layers (the other layers are
+    identical work) and the amortised retrieval build is added.  Returns
+    (tokens_per_s estimate for the 32-layer model, sample description, cores)."""
+    from oracle import hs_oracle as O
+    tcfg = O.OConfig(**{**TARGET_7B, "n_layers": 1})
+    dcfg = O.OConfig(**DRAFT_68M)
+    tgt = O.OModel(tcfg, O.make_tensors(tcfg, 1, tied_head=False), tied_head=False)
+    drf = O.OModel(dcfg, O.make_tensors(dcfg, 2, tied_head=False), tied_head=False)
+    ctx = np.random.default_rng(0).integers(1, 32000, context).tolist()
+    spec = O.OSpec(target_len=context + 10 ** 6, gamma1=GAMMA1, gamma2=GAMMA2, temperature=temperature, seed=0,
+                   n_sink=SINK, stream_budget=STREAM, chunk=CHUNK, retr_budget=BUDGET)
+    t0 = time.perf_counter()
+    sess = O.OSession.synthetic(tgt, drf, ctx, spec, seed=0)
+    setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    sess.retr.cache.build(sess.full.cache, [x.copy() for x in sess.full.rec.last_queries], upto=context - 1)
+    build_s = time.perf_counter() - t0
+    spent = {"target": 0.0, "draft": 0.0}
+    real_forward = O.forward
+
+    def timed_forward(model, *a, **k):
+        s = time.perf_counter()
+        try:
+            return real_forward(model, *a, **k)
+        finally:
+            spent["target" if model is tgt else "draft"] += time.perf_counter() - s
+
+    O.forward = timed_forward
+    per_token = []
+    rng = np.random.default_rng(0)
+    tr = O.OTrace()
+    start = time.perf_counter()
+    try:
+        for _ in range(rounds):
+            spent["target"] = spent["draft"] = 0.0
+            s = time.perf_counter()
+            got = sess.round(rng, tr)
+            wall = time.perf_counter() - s
+            rest = wall - spent["target"] - spent["draft"]
+            est = spent["target"] * TARGET_7B["n_layers"] + spent["draft"] + rest
+            est += build_s * TARGET_7B["n_layers"] * got / 128.0     # rebuild every 128 tokens
+            per_token.append(est / got)
+            if time.perf_counter() - start > time_budget_s:
+                break
+    finally:
+        O.forward = real_forward
+    cores = len(os.sched_getaffinity(0))
+    desc = (f"oracle (numpy port of hierspec) TriForce outer rounds on a 1-layer slice of the Llama2-7B shape "
+            f"over a {context}-token synthetic context + full JF68M draft; target forwards x32 layers, build "
+            f"({build_s:.1f} s/layer) amortised over the 128-token stride; {len(per_token)} round(s), "
+            f"setup {setup:.0f} s")
+    return [1.0 / x for x in per_token], desc, cores
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port; the Python
+    reference cannot travel to the GPU box) on this host's cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=max(1, args.steps))
+    val = statistics.median(rates)
+    out = {"metric": "decode tokens/s (TriForce, Llama2-7B-128K shape @122,880 ctx)", "value": val,
+           "unit": "tokens/s", "n_gpus": 0, "steps": len(rates), "warmup": 0, "ms_per_step": 1000.0 / val,
+           "higher_is_better": True, "impl": "reference", "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": workload_config(args),
+           "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
+           "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def workload_config(args):
+    return {"workload": "TriForce decode, Llama2-7B-128K shape, 122,880-token synthetic context, "
+                        "JF68M-shaped StreamingLLM draft",
+            "context": args.context, "retrieval_budget": BUDGET, "chunk": CHUNK, "stream_sink": SINK,
+            "stream_budget": STREAM, "gamma1": GAMMA1, "gamma2": GAMMA2, "temperature": args.temperature,
+            "tokens_per_step": args.gen, "l2": "inputs larger than L2 (64 GB KV/GPU), no flush",
+            "parallelism": f"replicas x{args.gpus}"}
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2404_11912_b200 as P
+    from paper_2404_11912_b200 import speculation as S
+    from paper_2404_11912_b200._abi import lib
+
+    tcfg, dcfg = P.ModelConfig(**TARGET_7B), P.ModelConfig(**DRAFT_68M)
+    target = P.ModelWeights.on_device(P.DeviceModel.random(tcfg, seed=1 + rank))
+    draft = P.ModelWeights.on_device(P.DeviceModel.random(dcfg, seed=1001 + rank))
+    ctx = np.random.default_rng(rank).integers(1, 32000, args.context).tolist()
+    spec = P.SpecConfig(target_len=args.context + 1, gamma1=GAMMA1, gamma2=GAMMA2, temperature=args.temperature,
+                        seed=rank, streaming=P.StreamingConfig(n_sink=SINK, budget=STREAM),
+                        retrieval=P.RetrievalConfig(chunk_size=CHUNK, budget=BUDGET))
+    sess = P.HierarchicalSession.synthetic(target, draft, ctx, spec, seed=rank)
+    torch.cuda.synchronize()
+
+    def step(i):
+        sess.config.target_len = len(sess.committed) + args.gen
+        sess.generate(seed=1000 * rank + i)
+
+    for i in range(args.warmup):
+        step(i)
+    if args.profile_only:
+        torch.cuda.synchronize()
+        return
+
+    # ---- timed region: K generate() calls -----------------------------------------
+    clocks = ClockSampler(local)
+    stats0 = dict(S.COUNTERS)
+    launches0 = lib.hs_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tokens0 = len(sess.committed)
+    wall0 = time.perf_counter()
+    ev0.record()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    ev1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = lib.hs_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    tokens = len(sess.committed) - tokens0
+    stats = {k: S.COUNTERS[k] - stats0.get(k, 0) for k in S.COUNTERS}
+    t_ms = torch.tensor([ms, wall * 1000.0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms, wall_ms = float(t_ms[0]), float(t_ms[1])
+    total_tokens = tokens * world
+    value = total_tokens / (ms / 1000.0)
+    e2e = total_tokens / (wall_ms / 1000.0)
+
+    extra = {}
+    if rank == 0:
+        extra = measure_kernels(P, sess, tcfg)
+        extra["ar_ms_per_token"] = measure_ar(P, sess)
+    out = None
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        rf = extra.pop("roofline")
+        rf["peak"] = peak
+        rf["frac"] = rf["achieved"] / peak
+        rf["peak_source"] = peak_kind
+        out = {"metric": "decode tokens/s (TriForce, Llama2-7B-128K shape @122,880 ctx)", "value": value,
+               "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": ms / args.steps, "ms_per_token": ms / tokens, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+               "config": workload_config(args),
+               "e2e": {"value": e2e, "unit": "tokens/s",
+                       "h2d_bytes_per_step": stats.get("h2d_bytes", 0) // max(1, args.steps),
+                       "d2h_bytes_per_step": stats.get("d2h_bytes", 0) // max(1, args.steps)},
+               "gpu_launches": int(launches), "clocks": clk, "roofline": rf,
+               "acceptance": {"inner_rounds": stats.get("inner_rounds", 0), "outer_rounds": stats.get("outer_rounds", 0),
+                              "inner_rate": stats.get("inner_accepted", 0) / max(1, stats.get("inner_proposed", 0)),
+                              "outer_rate": stats.get("outer_accepted", 0) / max(1, stats.get("outer_proposed", 0)),
+                              "rebuilds": stats.get("rebuilds", 0)},
+               **extra}
+        if world == 1 and not args.no_cpu_baseline:
+            rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=1, time_budget_s=60)
+            out["cpu_baseline"] = {"value": statistics.median(rates), "unit": "tokens/s", "cores": cores,
+                                   "kind": "port", "sample": desc}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_kernels(P, sess, tcfg):
+    """Per-kernel timing with CUDA events on the launching stream: the verify
+    attention over the full cache (dominant kernel) and per-lane forwards."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2404_11912_b200._abi import HsStep, check, lib
+    from paper_2404_11912_b200.runtime import ptr, stream_ptr, workspaces
+
+    cache = sess.full_lane.cache
+    n = cache.frontier
+    H, dh, kvh = tcfg.n_heads, tcfg.head_dim, tcfg.n_kv_heads
+    res = {}
+    reps = 20
+    for t in (1, 5):
+        q = torch.randn((t, H, dh), device="cuda")
+        out = torch.empty((t, H * dh), device="cuda")
+        st = HsStep()
+        st.pos0, st.n_view, st.split = n - t, n, P.caches.FULL_SPLIT
+        nb = lib.hs_attention_workspace_bytes(t, H, dh, n, st.split)
+        ws = workspaces.get("bench_att", nb)
+        args = (cache._ref, 0, C.byref(st), H, ptr(q), t, ptr(out), ptr(ws), nb, stream_ptr())
+        for _ in range(3):
+            check(lib.hs_attention(*args))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for r in range(reps):
+            check(lib.hs_attention(cache._ref, r % tcfg.n_layers, C.byref(st), H, ptr(q), t, ptr(out), ptr(ws), nb,
+                                   stream_ptr()))
+        e1.record()
+        torch.cuda.synchronize()
+        sec = e0.elapsed_time(e1) / 1000.0 / reps
+        kv_bytes = n * kvh * dh * 2 * 2
+        res[f"attn_full_t{t}"] = {"us": sec * 1e6, "GBps": kv_bytes / sec / 1e9}
+    # lane forwards (device time per forward)
+    dm = sess.full_lane.weights.device()
+
+    def time_forward(lane, t, reps=5):
+        cache = lane.cache
+        toks = torch.ones(t, dtype=torch.int32, device="cuda")
+        f0 = cache.frontier
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lane.rollback_to(f0)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            lane._forward(toks)
+            lane.rollback_to(f0)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    full_ms = time_forward(sess.full_lane, 5)
+    retr_ms = time_forward(sess.retr_lane, 3)
+    draft_ms = time_forward(sess.draft_lane, 1, reps=20)
+    w_bytes = dm.weight_bytes
+    kv_full = (n + 5) * kvh * dh * 2 * 2 * tcfg.n_layers
+    kv_retr = (sess.retr_lane.cache.n_sel + 3) * kvh * dh * 2 * 2 * tcfg.n_layers
+    res["forward_ms"] = {"verify_t5": full_ms, "retrieval_t3": retr_ms, "draft_t1": draft_ms}
+    res["forward_GBps"] = {"verify_t5": (w_bytes + kv_full) / full_ms / 1e6,
+                           "retrieval_t3": (w_bytes + kv_retr) / retr_ms / 1e6}
+    a = res["attn_full_t5"]
+    res["roofline"] = {"bound": "hbm", "kernel": "attn_partial_kernel<128> + combine (verify t=5, full cache)",
+                       "achieved": a["GBps"], "unit": "GB/s",
+                       "bytes_per_launch": n * kvh * dh * 2 * 2, "traffic": read_ncu_traffic()}
+    return res
+
+
+def read_ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("attn_traffic_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def measure_ar(P, sess):
+    """Autoregressive decode over the same full cache: ms per token."""
+    import torch
+    from paper_2404_11912_b200.speculation import _ar_loop
+    lane = sess.full_lane
+    f0 = lane.frontier
+    committed = lane.cache.committed
+    n = 8
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _ar_loop(lane, [], n + 1, 0.0, np.random.default_rng(0))
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / n
+    lane.cache.committed = committed
+    lane.rollback_to(f0)
+    return dt * 1000.0
+
+
+if __name__ == "__main__":
+    main()

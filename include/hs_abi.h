@@ -41,6 +41,8 @@ extern "C" {
 const char *hs_last_error(void);
 int hs_abi_version(void);
 int hs_device_sm_count(int device);
+/* number of kernels this library has launched since it was loaded */
+unsigned long long hs_launch_count(void);
 
 /* ---- model descriptor --------------------------------------------------
  * Replaces ModelWeights.runtime() (model.py:116-143): fused wqkv, fused
@@ -177,7 +179,7 @@ int hs_retrieval_gather(const HsCache *src, const HsCache *dst, const int32_t *c
 /* RetrievalCache.commit / _overwrite (caches.py:529-555) for all layers:
  * spec slots [n_sel, n_sel+n_spec) -- the first `take` move into the victim
  * slots ring[(head+i) % n_sel]; the rest shift down.                         */
-int hs_retrieval_commit(const HsCache *c, const int32_t *ring, int n_sel, int ring_head,
+int hs_retrieval_commit(const HsCache *c, const int32_t *ring, int ring_stride, int n_sel, int ring_head,
                         int n_spec, int take, void *stream);
 
 /* copy a cache's live slots (clone(), caches.py:216-221 / 283-288 / 557-565) */

@@ -61,6 +61,7 @@ _SIGS = {
     "hs_last_error": (C.c_char_p, []),
     "hs_abi_version": (i32, []),
     "hs_device_sm_count": (i32, [i32]),
+    "hs_launch_count": (C.c_ulonglong, []),
     "hs_forward_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32]),
     "hs_forward": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), vp, i32, vp, vp, vp, sz, vp]),
     "hs_gemv": (i32, [vp, i32, i32, i32, vp, i32, i32, i32, vp, f32, i32, vp, i32, vp]),
@@ -73,7 +74,7 @@ _SIGS = {
     "hs_chunk_select_workspace_bytes": (sz, [i32, i32]),
     "hs_chunk_select": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]),
     "hs_retrieval_gather": (i32, [_P(HsCache), _P(HsCache), vp, i32, i32, i32, i32, vp]),
-    "hs_retrieval_commit": (i32, [_P(HsCache), vp, i32, i32, i32, i32, vp]),
+    "hs_retrieval_commit": (i32, [_P(HsCache), vp, i32, i32, i32, i32, i32, vp]),
     "hs_cache_copy": (i32, [_P(HsCache), _P(HsCache), i32, vp]),
     "hs_probs": (i32, [vp, i32, i32, f64, vp, vp]),
     "hs_sample": (i32, [vp, i32, vp, vp, vp, vp]),

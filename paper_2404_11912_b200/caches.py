@@ -506,7 +506,7 @@ class RetrievalCache(KVCache):
             if self.n_sel < 1:
                 raise ContractError("retrieval cache has no slots")
             spec = self.n_spec[0]
-            check(lib.hs_retrieval_commit(self._ref, ptr(self.ring), self.n_sel, self.ring_head, spec, take,
+            check(lib.hs_retrieval_commit(self._ref, ptr(self.ring), self.config.budget, self.n_sel, self.ring_head, spec, take,
                                           stream_ptr()))
             self.ring_head = (self.ring_head + take) % self.n_sel
             self.n_spec = [s - take for s in self.n_spec]

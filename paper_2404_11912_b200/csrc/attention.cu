@@ -255,7 +255,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   }
   attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 0, stream>>>(a.part_m, a.part_l, a.part_o,
                                                                    n_splits, t * H, DH, out);
-  return check_launch("attention");
+  return check_launch("attention", 2);
 }
 
 }  // namespace hs

@@ -29,9 +29,15 @@ int set_error(int code, const char *fmt, ...) {
   return code;
 }
 
-int check_launch(const char *what) {
+// kernels launched by this library since load (gpu_launches evidence for bench.py)
+static unsigned long long g_launches = 0;
+
+void count_launch(int n) { __atomic_add_fetch(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+
+int check_launch(const char *what, int n_kernels) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  count_launch(n_kernels);
   return HS_OK;
 }
 
@@ -61,6 +67,7 @@ static size_t carve(const HsModel *m, int t, int n_view, int split, char *base, 
 
 extern "C" const char *hs_last_error(void) { return hs::g_err; }
 extern "C" int hs_abi_version(void) { return HS_ABI_VERSION; }
+extern "C" unsigned long long hs_launch_count(void) { return __atomic_load_n(&hs::g_launches, __ATOMIC_RELAXED); }
 extern "C" int hs_device_sm_count(int device) {
   int n = 0;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;

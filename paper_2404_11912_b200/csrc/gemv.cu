@@ -289,6 +289,7 @@ int launch_gemv(const float *x, int ldx, int t, int K, const uint16_t *w, int ld
     a.y = y + (size_t)r0 * ldy;
     cudaError_t e = RL == 2 ? launch_gemv_rl<2>(a, row_blocks, st) : launch_gemv_rl<1>(a, row_blocks, st);
     if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "gemv launch: %s", cudaGetErrorString(e));
+    count_launch(1);
   }
   return HS_OK;
 }

@@ -12,7 +12,8 @@ namespace hs {
 
 // ---- error state (hs_abi.cu) ---------------------------------------------
 int set_error(int code, const char *fmt, ...);
-int check_launch(const char *what);
+int check_launch(const char *what, int n_kernels = 1);
+void count_launch(int n);
 
 #define HS_REQUIRE(cond, code, ...)                 \
   do {                                              \

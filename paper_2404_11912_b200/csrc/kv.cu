@@ -97,12 +97,12 @@ __global__ void kv_write_kernel(HsCache c, int layer, const float *k, const floa
 // ---- RetrievalCache.commit (caches.py:529-555) --------------------------------
 // grid (L, KVH); every thread owns fixed dims, so the sequential FIFO order of
 // overwrites (including wrap-around when take > n_sel) is preserved per dim.
-__global__ void retrieval_commit_kernel(HsCache c, const int32_t *ring, int n_sel, int head,
+__global__ void retrieval_commit_kernel(HsCache c, const int32_t *ring, int ring_stride, int n_sel, int head,
                                         int n_spec, int take) {
   const int l = blockIdx.x, kh = blockIdx.y, DH = c.head_dim;
   const size_t rowbase = ((size_t)l * c.n_kv_heads + kh) * c.cap;
   int32_t *pos = c.pos + (size_t)l * c.cap;
-  const int32_t *rg = ring + (size_t)l * n_sel;
+  const int32_t *rg = ring + (size_t)l * ring_stride;
   for (int i = 0; i < take; ++i) {
     const int dst = rg[(head + i) % n_sel];
     const int src = n_sel + i;
@@ -147,14 +147,14 @@ extern "C" int hs_kv_write(const HsCache *c, int layer, const float *k, const fl
   return hs::check_launch("kv_write");
 }
 
-extern "C" int hs_retrieval_commit(const HsCache *c, const int32_t *ring, int n_sel, int ring_head,
+extern "C" int hs_retrieval_commit(const HsCache *c, const int32_t *ring, int ring_stride, int n_sel, int ring_head,
                                    int n_spec, int take, void *stream) {
   if (take < 0 || take > n_spec) return hs::set_error(HS_ERR_CONTRACT, "retrieval commit: take %d outside [0,%d]", take, n_spec);
   if (take > 0 && n_sel < 1) return hs::set_error(HS_ERR_CONTRACT, "retrieval cache has no slots");
   if (n_spec == 0) return HS_OK;
   dim3 grid(c->n_layers, c->n_kv_heads);
   hs::retrieval_commit_kernel<<<grid, c->head_dim < 128 ? c->head_dim : 128, 0, hs::as_stream(stream)>>>(
-      *c, ring, n_sel, ring_head, n_spec, take);
+      *c, ring, ring_stride, n_sel, ring_head, n_spec, take);
   return hs::check_launch("retrieval_commit");
 }
 

@@ -33,6 +33,11 @@ from .model import (ForwardRecorder, ModelWeights, forward_device, prob_from_log
 from .runtime import UniformStream, as_device_f64, device, ptr, stream_ptr, to_i32_device
 
 
+# process-wide counters (bench.py reads them around its timed region)
+COUNTERS = {"inner_rounds": 0, "inner_proposed": 0, "inner_accepted": 0, "outer_rounds": 0, "outer_proposed": 0,
+            "outer_accepted": 0, "rebuilds": 0, "h2d_bytes": 0, "d2h_bytes": 0}
+
+
 @dataclass
 class SpecConfig:
     """Algorithm 1 parameters (speculation.py:35-49)."""
@@ -234,6 +239,7 @@ def _readback(buf: _RoundBuffers, n: int, us: UniformStream):
     buf.host[:n + 4].copy_(buf.res[:n + 4], non_blocking=True)
     buf.host[n + 4:n + 5].copy_(us.cursor, non_blocking=True)
     torch.cuda.current_stream().synchronize()
+    COUNTERS["d2h_bytes"] += 4 * (n + 5)
     h = buf.host.numpy()
     count, accepted, status, cursor = int(h[n + 1]), int(h[n + 2]), int(h[n + 3]), int(h[n + 4])
     if status != 0:
@@ -268,6 +274,7 @@ def _score_rows_dev(lane: Lane, seq: Sequence[int], tokens_dev: torch.Tensor, T:
             raise ContractError("lane has no frontier logits; advance over committed tokens first")
         check(lib.hs_probs(ptr(lane._front), 1, V, float(T), ptr(out[0]), s))
     toks = torch.cat([to_i32_device(cu), tokens_dev]) if cu else tokens_dev
+    COUNTERS["h2d_bytes"] += 4 * len(cu)
     logits = lane._forward(toks)
     if cu:
         check(lib.hs_probs(ptr(logits[len(cu) - 1]), n + 1, V, float(T), ptr(out[0]), s))
@@ -451,6 +458,7 @@ class HierarchicalSession:
         self.tokens_since_build = 0
         self.rolling.rates.clear()
         self.rebuilds += 1
+        COUNTERS["rebuilds"] += 1
         return True
 
     def generate(self, seed: Optional[int] = None):
@@ -477,6 +485,9 @@ class HierarchicalSession:
                 trace.inner.rounds += 1
                 trace.inner.proposed += cfg.gamma1
                 trace.inner.accepted += accepted
+                COUNTERS["inner_rounds"] += 1
+                COUNTERS["inner_proposed"] += cfg.gamma1
+                COUNTERS["inner_accepted"] += accepted
                 valid = base + len(x_hat) - 1
                 self.draft_lane.rollback_to(valid)
                 self.retr_lane.rollback_to(valid)
@@ -484,6 +495,7 @@ class HierarchicalSession:
             n = len(x_hat)
             us.ensure(n + 2, cursor)
             buf.xtok[:n].copy_(torch.as_tensor(np.asarray(x_hat, np.int32)), non_blocking=False)
+            COUNTERS["h2d_bytes"] += 4 * n
             _score_rows_dev(self.full_lane, self.committed, buf.xtok[:n], cfg.temperature, buf.p)
             _chain_dev(buf.xtok[:n], n, buf.phat, buf.p, V, us, buf)
             emitted, accepted, cursor = _readback(buf, n, us)
@@ -491,6 +503,9 @@ class HierarchicalSession:
             trace.outer.rounds += 1
             trace.outer.proposed += n
             trace.outer.accepted += accepted
+            COUNTERS["outer_rounds"] += 1
+            COUNTERS["outer_proposed"] += n
+            COUNTERS["outer_accepted"] += accepted
             emitted = emitted[:cfg.target_len - base]
             for i, tok in enumerate(emitted):
                 level = ilabels[i] if olabels[i] == "accepted" else olabels[i]

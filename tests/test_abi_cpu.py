@@ -19,9 +19,10 @@ def _declared():
 
 
 def test_library_exports_every_declared_symbol():
-    from paper_2404_11912_b200.build import LIB, build
-    build()
-    lib = ctypes.CDLL(LIB)
+    import __graft_entry__
+    b = __graft_entry__._builder()
+    b.build()
+    lib = ctypes.CDLL(b.LIB)
     names = _declared()
     assert len(names) >= 20
     missing = [n for n in names if not hasattr(lib, n)]
