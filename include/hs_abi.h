@@ -118,6 +118,8 @@ typedef struct {
  * Row results are independent of t (bitwise), so a batched verify equals a
  * sequence of decode steps (model.py:366-378 contract).                     */
 size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view, int split);
+/* leading bytes of the forward workspace that must be zero before first use */
+size_t hs_forward_workspace_clean_bytes(const HsModel *m);
 int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st,
                const int32_t *tokens, int t, float *logits, float *q_stash,
                void *workspace, size_t workspace_bytes, void *stream);
@@ -131,6 +133,21 @@ int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st,
 int hs_gemv(const float *x, int ldx, int t, int K, const uint16_t *w, int ldw, int N,
             int prologue, const float *gain, float eps, int epilogue, float *y, int ldy,
             void *stream);
+
+/* Tensor-core GEMV (tcgen05 + TMA, swap-AB): y (+)= W . x for one pass of
+ * t <= 8 activation rows held as an exact 3-way bf16 split xs [24][ldw]
+ * (rows split*8 + r; see hs_split_rows).  epilogue 0 store, 1 accumulate,
+ * 2 SwiGLU pairs (output split of act written to xs_out [24][ld_xs_out] and,
+ * if y != NULL, fp32 act to y).  The workspace head (hs_gemv_tc_workspace_bytes)
+ * must be zero before the first call; kernels leave it zero.              */
+size_t hs_gemv_tc_workspace_bytes(int N, int ldw);
+int hs_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
+               uint16_t *xs_out, int ld_xs_out, void *workspace, size_t ws_bytes, void *stream);
+
+/* activation prep for hs_gemv_tc: optional RMSNorm (gain != NULL,
+ * model.py:282-284) then exact split h = hi + mid + lo into xs [24][ldk]    */
+int hs_split_rows(const float *x, int ldx, int t, int K, int ldk, const float *gain, float eps,
+                  uint16_t *xs, void *stream);
 
 /* embedding lookup (model.py:274): x[r] = float(emb[tokens[r]])            */
 int hs_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x,

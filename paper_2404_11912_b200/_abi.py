@@ -63,6 +63,10 @@ _SIGS = {
     "hs_device_sm_count": (i32, [i32]),
     "hs_launch_count": (C.c_ulonglong, []),
     "hs_forward_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32]),
+    "hs_forward_workspace_clean_bytes": (sz, [_P(HsModel)]),
+    "hs_gemv_tc_workspace_bytes": (sz, [i32, i32]),
+    "hs_gemv_tc": (i32, [vp, i32, vp, i32, i32, i32, vp, i32, vp, i32, vp, sz, vp]),
+    "hs_split_rows": (i32, [vp, i32, i32, i32, i32, vp, f32, vp, vp]),
     "hs_forward": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), vp, i32, vp, vp, vp, sz, vp]),
     "hs_gemv": (i32, [vp, i32, i32, i32, vp, i32, i32, i32, vp, f32, i32, vp, i32, vp]),
     "hs_embed": (i32, [vp, i32, i32, vp, i32, vp, vp]),

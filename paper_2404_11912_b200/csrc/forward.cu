@@ -41,23 +41,52 @@ int check_launch(const char *what, int n_kernels) {
   return HS_OK;
 }
 
+int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const float *gain, float eps, uint16_t *xs,
+                      cudaStream_t st);
+int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
+                   uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st);
+size_t gemv_tc_ws_bytes(int N, int nkb);
+
+// Workspace layout.  The head is position-independent so that the regions
+// which must stay zero/clean between calls never move:
+//   [gemv counters + partials (max over the model's matrices)]
+//   [Xd: 24 x ld_d bf16 split operand][Xf: 24 x ld_ff bf16]
+//   then per-call regions: x, qkv, q, attn, attention partials.
 struct FwdWs {
-  float *x, *qkv, *q, *attn, *act;
+  void *gemv_ws;
+  size_t gemv_bytes;
+  uint16_t *xd, *xf;
+  float *x, *qkv, *q, *attn;
   void *att_ws;
   size_t att_bytes;
 };
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+static size_t gemv_region(const HsModel *m) {
+  const int d = m->d_model, kv = m->n_kv_heads * m->head_dim;
+  size_t g = 0;
+  const int Ns[5] = {d + 2 * kv, d, 2 * m->d_ff, d, m->vocab_size};
+  const int Ks[5] = {m->ld_d, m->ld_d, m->ld_d, m->ld_ff, m->ld_d};
+  for (int i = 0; i < 5; ++i) {
+    size_t b = gemv_tc_ws_bytes(Ns[i], Ks[i] / 64);
+    if (b > g) g = b;
+  }
+  return align256(g);
+}
+
 static size_t carve(const HsModel *m, int t, int n_view, int split, char *base, FwdWs *w) {
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim;
   size_t off = 0;
   auto take = [&](size_t bytes) { char *p = base ? base + off : nullptr; off += align256(bytes); return p; };
+  w->gemv_bytes = gemv_region(m);
+  w->gemv_ws = take(w->gemv_bytes);
+  w->xd = (uint16_t *)take((size_t)24 * m->ld_d * 2);
+  w->xf = (uint16_t *)take((size_t)24 * m->ld_ff * 2);
   w->x = (float *)take((size_t)t * d * 4);
   w->qkv = (float *)take((size_t)t * (H + 2 * KVH) * dh * 4);
   w->q = (float *)take((size_t)t * H * dh * 4);
   w->attn = (float *)take((size_t)t * d * 4);
-  w->act = (float *)take((size_t)t * m->d_ff * 4);
   w->att_bytes = attention_ws(t, H, dh, n_view, split);
   w->att_ws = take(w->att_bytes);
   return off;
@@ -79,6 +108,11 @@ extern "C" size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view
   return hs::carve(m, t, n_view, split, nullptr, &w);
 }
 
+extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
+  // bytes at the head of the workspace that must be zero before the first call
+  return hs::gemv_region(m) + hs::align256((size_t)24 * m->ld_d * 2) + hs::align256((size_t)24 * m->ld_ff * 2);
+}
+
 extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
                           float *logits, float *q_stash, void *workspace, size_t workspace_bytes, void *stream) {
   using namespace hs;
@@ -91,25 +125,43 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
   const size_t need = carve(m, t, st->n_view, st->split, (char *)workspace, &w);
   HS_REQUIRE(workspace_bytes >= need, HS_ERR_VALUE, "forward: workspace %zu < %zu", workspace_bytes, need);
   cudaStream_t s = as_stream(stream);
-  const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim;
+  const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim, ff = m->d_ff;
   const int nqkv = (H + 2 * KVH) * dh;
+  const float eps = m->norm_eps;
   int rc;
 #define HS_TRY(call) do { if ((rc = (call)) != HS_OK) return rc; } while (0)
   HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
   for (int l = 0; l < m->n_layers; ++l) {
-    const size_t lq = (size_t)l * nqkv * m->ld_d;
-    HS_TRY(launch_gemv(w.x, d, t, d, m->wqkv + lq, m->ld_d, nqkv, 1, m->attn_norm + (size_t)l * d, m->norm_eps,
-                       0, w.qkv, nqkv, s));
+    const uint16_t *wqkv = m->wqkv + (size_t)l * nqkv * m->ld_d;
+    const uint16_t *wo = m->wo + (size_t)l * d * m->ld_d;
+    const uint16_t *wgu = m->wgu + (size_t)l * 2 * ff * m->ld_d;
+    const uint16_t *wdn = m->wdown + (size_t)l * d * m->ld_ff;
+    const float *an = m->attn_norm + (size_t)l * d, *mn = m->mlp_norm + (size_t)l * d;
+    for (int r0 = 0; r0 < t; r0 += 8) {
+      const int tp = t - r0 < 8 ? t - r0 : 8;
+      HS_TRY(launch_split_rows(w.x + (size_t)r0 * d, d, tp, d, m->ld_d, an, eps, w.xd, s));
+      HS_TRY(launch_gemv_tc(w.xd, tp, wqkv, m->ld_d, nqkv, 0, w.qkv + (size_t)r0 * nqkv, nqkv, nullptr, 0, w.gemv_ws,
+                            w.gemv_bytes, s));
+    }
     HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
     HS_TRY(launch_attention(c, l, st, H, w.q, t, w.attn, w.att_ws, w.att_bytes, s));
-    HS_TRY(launch_gemv(w.attn, d, t, d, m->wo + (size_t)l * d * m->ld_d, m->ld_d, d, 0, nullptr, 0.f, 1, w.x, d, s));
-    HS_TRY(launch_gemv(w.x, d, t, d, m->wgu + (size_t)l * 2 * m->d_ff * m->ld_d, m->ld_d, 2 * m->d_ff, 1,
-                       m->mlp_norm + (size_t)l * d, m->norm_eps, 2, w.act, m->d_ff, s));
-    HS_TRY(launch_gemv(w.act, m->d_ff, t, m->d_ff, m->wdown + (size_t)l * d * m->ld_ff, m->ld_ff, d, 0, nullptr, 0.f,
-                       1, w.x, d, s));
+    for (int r0 = 0; r0 < t; r0 += 8) {
+      const int tp = t - r0 < 8 ? t - r0 : 8;
+      float *xr = w.x + (size_t)r0 * d;
+      HS_TRY(launch_split_rows(w.attn + (size_t)r0 * d, d, tp, d, m->ld_d, nullptr, 0.f, w.xd, s));
+      HS_TRY(launch_gemv_tc(w.xd, tp, wo, m->ld_d, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
+      HS_TRY(launch_split_rows(xr, d, tp, d, m->ld_d, mn, eps, w.xd, s));
+      HS_TRY(launch_gemv_tc(w.xd, tp, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes,
+                            s));
+      HS_TRY(launch_gemv_tc(w.xf, tp, wdn, m->ld_ff, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
+    }
   }
-  HS_TRY(launch_gemv(w.x, d, t, d, m->head, m->ld_d, m->vocab_size, 1, m->final_norm, m->norm_eps, 0, logits,
-                     m->vocab_size, s));
+  for (int r0 = 0; r0 < t; r0 += 8) {
+    const int tp = t - r0 < 8 ? t - r0 : 8;
+    HS_TRY(launch_split_rows(w.x + (size_t)r0 * d, d, tp, d, m->ld_d, m->final_norm, eps, w.xd, s));
+    HS_TRY(launch_gemv_tc(w.xd, tp, m->head, m->ld_d, m->vocab_size, 0, logits + (size_t)r0 * m->vocab_size,
+                          m->vocab_size, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
+  }
 #undef HS_TRY
   return HS_OK;
 }

@@ -1,0 +1,364 @@
+// Tensor-core weight-streaming GEMV (tcgen05 + TMA), the projection engine of
+// every decode / verify forward (model.py:285, 316, 320-323, 328).
+//
+// Swap-AB: the weight tile is the MMA's A operand (M = 128 output rows, bf16
+// [out][in] = K-major), the activations are B (N = 24 columns).  fp32
+// activations are split EXACTLY into three bf16 terms, x = hi + mid + lo
+// (round-to-nearest splitting captures 8+8+8 significand bits, the full fp32
+// mantissa), laid out as rows [split*8 + r] of a [24][K] bf16 operand; the
+// tensor core forms the exact bf16 x bf16 products and accumulates in fp32
+// in TMEM, so the result matches an fp32 CUDA-core GEMV to rounding.  The
+// epilogue sums the three column groups in a fixed order.
+//
+// Pipeline per CTA (128 threads): warp 0 issues TMA loads of [128 x 64]
+// weight tiles + [24 x 64] activation tiles into a 5-stage ring, warp 1 issues
+// tcgen05.mma (4 x K16 per stage) and tcgen05.commit frees the stage, all four
+// warps drain TMEM (tcgen05.ld) in the epilogue.  K is split over gridDim.y
+// CTAs; partial tiles are reduced by the last-arriving CTA in split order
+// (deterministic; the split depends only on N and K, never on t, so a row's
+// result does not depend on the batch size).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "hs_common.cuh"
+#include "tc_util.cuh"
+
+namespace hs {
+
+constexpr int TC_BM = 128;        // output rows per tile (MMA M)
+constexpr int TC_BK = 64;         // K per stage (one 128-byte swizzle row)
+constexpr int TC_XN = 24;         // activation columns: 3 splits x 8 rows
+constexpr int TC_T = 8;           // activation rows per pass
+constexpr int TC_STAGES = 5;
+constexpr int TC_W_BYTES = TC_BM * TC_BK * 2;    // 16 KB
+constexpr int TC_X_BYTES = TC_XN * TC_BK * 2;    // 3 KB
+constexpr int TC_SMEM = TC_STAGES * (TC_W_BYTES + TC_X_BYTES) + 1024 + 256;
+constexpr int TC_COUNTER_INTS = 16384;           // per-tile arrival counters at the workspace head
+
+// ---------------------------------------------------------------------------
+// host: tensor-map cache
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::mutex g_map_mu;
+struct MapKey {
+  const void *p; uint64_t inner, rows, stride; uint32_t box_rows;
+  bool operator==(const MapKey &o) const {
+    return p == o.p && inner == o.inner && rows == o.rows && stride == o.stride && box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey &k) const {
+    return std::hash<const void *>()(k.p) ^ (k.inner * 1315423911u) ^ (k.rows << 7) ^ k.box_rows;
+  }
+};
+static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+int get_tmap_bf16(const void *ptr, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes, uint32_t box_rows,
+                  CUtensorMap *out) {
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  MapKey key{ptr, inner, rows, row_stride_bytes, box_rows};
+  auto it = g_maps.find(key);
+  if (it != g_maps.end()) { *out = it->second; return HS_OK; }
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return set_error(HS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)TC_BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(HS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps.emplace(key, m);
+  *out = m;
+  return HS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// activation prep: optional RMSNorm, then exact 3-way bf16 split
+__device__ __forceinline__ void split3(float h, uint16_t &a, uint16_t &b, uint16_t &c) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(h);
+  const float r1 = h - __bfloat162float(hi);
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  const float r2 = r1 - __bfloat162float(mid);
+  a = __bfloat16_as_ushort(hi);
+  b = __bfloat16_as_ushort(mid);
+  c = f_to_bf16(r2);
+}
+
+// grid: TC_T blocks (row r); rows >= t are written as zeros
+__global__ void __launch_bounds__(256) split_rows_kernel(const float *x, int ldx, int t, int K, int ldk,
+                                                         const float *gain, float eps, uint16_t *xs) {
+  const int r = blockIdx.x;
+  __shared__ double red[8];
+  __shared__ double scale_s;
+  double scale = 1.0;
+  if (gain != nullptr && r < t) {
+    double ss = 0.0;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      const double v = (double)x[(size_t)r * ldx + k];
+      ss += v * v;
+    }
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < 8; ++w) tot += red[w];
+      scale_s = sqrt(tot / (double)K + (double)eps);   // rms_norm, model.py:282-284
+    }
+    __syncthreads();
+    scale = scale_s;
+  }
+  for (int k = threadIdx.x; k < ldk; k += blockDim.x) {
+    float h = 0.f;
+    if (r < t && k < K) {
+      const float v = x[(size_t)r * ldx + k];
+      h = gain ? (float)(((double)v / scale) * (double)gain[k]) : v;
+    }
+    uint16_t a, b, c;
+    split3(h, a, b, c);
+    xs[(size_t)r * ldk + k] = a;
+    xs[(size_t)(TC_T + r) * ldk + k] = b;
+    xs[(size_t)(2 * TC_T + r) * ldk + k] = c;
+  }
+}
+
+struct GemvTcArgs {
+  int N, nkb, ks, t, epilogue, n_tiles;
+  float *y;
+  int ldy;
+  uint16_t *xs_out;   // swiglu epilogue: split of act written here ([24][ld_xs_out]) if non-null
+  int ld_xs_out;
+  float *partial;     // [ks][n_tiles*128][8]
+  int *counters;      // [n_tiles]
+};
+
+__device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float *v, int lane) {
+  if (a.epilogue == 2) {
+    float up[TC_T];
+#pragma unroll
+    for (int r = 0; r < TC_T; ++r) up[r] = __shfl_down_sync(0xffffffffu, v[r], 1);
+    if ((o & 1) == 0 && o + 1 < a.N) {
+      const int i = o >> 1;
+#pragma unroll
+      for (int r = 0; r < TC_T; ++r) {
+        if (r < a.t) {
+          const double g = (double)v[r];
+          const float act = (float)(g * (0.5 * (tanh(0.5 * g) + 1.0))) * up[r];   // model.py:321-322
+          if (a.y) a.y[(size_t)r * a.ldy + i] = act;
+          if (a.xs_out) {
+            uint16_t h0, h1, h2;
+            split3(act, h0, h1, h2);
+            a.xs_out[(size_t)r * a.ld_xs_out + i] = h0;
+            a.xs_out[(size_t)(TC_T + r) * a.ld_xs_out + i] = h1;
+            a.xs_out[(size_t)(2 * TC_T + r) * a.ld_xs_out + i] = h2;
+          }
+        }
+      }
+    }
+    return;
+  }
+  if (o >= a.N) return;
+#pragma unroll
+  for (int r = 0; r < TC_T; ++r) {
+    if (r < a.t) {
+      float *p = a.y + (size_t)r * a.ldy + o;
+      *p = (a.epilogue == 1) ? (*p + v[r]) : v[r];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                         const __grid_constant__ CUtensorMap tmX, GemvTcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char *sW = base;
+  unsigned char *sX = base + TC_STAGES * TC_W_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sX + TC_STAGES * TC_X_BYTES);
+  uint64_t *empty = full + TC_STAGES;
+  uint64_t *accum = empty + TC_STAGES;
+  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(accum + 1);
+  int *flag = reinterpret_cast<int *>(tmem_base + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int per = a.nkb / a.ks, rem = a.nkb % a.ks;
+  const int kb0 = split * per + min(split, rem);
+  const int nk = per + (split < rem ? 1 : 0);
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmW);
+    tc::tma_prefetch(&tmX);
+    for (int s = 0; s < TC_STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    tc::mbar_init(accum, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<32>(tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t taddr = *tmem_base;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      const uint64_t pol = tc::policy_evict_first();   // weights are streamed exactly once
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % TC_STAGES;
+        const uint32_t ph = (i / TC_STAGES) & 1;
+        tc::mbar_wait(&empty[s], ph ^ 1);
+        tc::mbar_expect_tx(&full[s], TC_W_BYTES + TC_X_BYTES);
+        const int k = (kb0 + i) * TC_BK;
+        tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], k, tile * TC_BM, pol);
+        tc::tma_load_2d(sX + s * TC_X_BYTES, &tmX, &full[s], k, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (tc::elect_one()) {
+      constexpr uint32_t idesc = tc::idesc_bf16(TC_BM, TC_XN, 0, 0);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % TC_STAGES;
+        const uint32_t ph = (i / TC_STAGES) & 1;
+        tc::mbar_wait(&full[s], ph);
+        tc::fence_after();
+        const uint64_t da = tc::desc_k_sw128(sW + s * TC_W_BYTES);
+        const uint64_t db = tc::desc_k_sw128(sX + s * TC_X_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < TC_BK / 16; ++kk)   // +32 bytes per K16 step inside the swizzle row
+          tc::mma_bf16(taddr, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(accum);
+    }
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers ---------------------------------------------------
+  tc::mbar_wait(accum, 0);
+  tc::fence_after();
+  const int row = warp * 32 + lane;
+  const uint32_t tl = taddr + ((uint32_t)(warp * 32) << 16);
+  float h[8], m[8], l[8], v[TC_T];
+  tc::tmem_ld8(tl + 0, h);
+  tc::tmem_ld8(tl + 8, m);
+  tc::tmem_ld8(tl + 16, l);
+  tc::tmem_ld_wait();
+#pragma unroll
+  for (int r = 0; r < TC_T; ++r) v[r] = nk > 0 ? (h[r] + m[r]) + l[r] : 0.f;
+  const int o = tile * TC_BM + row;
+
+  if (a.ks == 1) {
+    finalize(a, o, v, lane);
+  } else {
+    float *pp = a.partial + ((size_t)split * a.n_tiles * TC_BM + o) * TC_T;
+    *reinterpret_cast<float4 *>(pp) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4 *>(pp + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int old = atomicAdd(&a.counters[tile], 1);
+      *flag = (old == a.ks - 1);
+    }
+    __syncthreads();
+    if (*flag) {
+      __threadfence();
+#pragma unroll
+      for (int r = 0; r < TC_T; ++r) v[r] = 0.f;
+      for (int s2 = 0; s2 < a.ks; ++s2) {
+        const float *q = a.partial + ((size_t)s2 * a.n_tiles * TC_BM + o) * TC_T;
+        const float4 x0 = __ldcg(reinterpret_cast<const float4 *>(q));
+        const float4 x1 = __ldcg(reinterpret_cast<const float4 *>(q + 4));
+        v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
+        v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
+      }
+      finalize(a, o, v, lane);
+      if (threadIdx.x == 0) a.counters[tile] = 0;   // self-cleaning for the next launch
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<32>(taddr);
+}
+
+// K split: a function of (N, K) only.  Picks the split count that fills
+// whole waves of 2 CTAs per SM best, with at least 4 K-blocks per CTA.
+int gemv_tc_ksplit(int N, int nkb) {
+  const int tiles = (N + TC_BM - 1) / TC_BM;
+  const int slots = 2 * 148;
+  int best = 1;
+  double best_eff = -1.0;
+  for (int ks = 1; ks <= 16; ++ks) {
+    if (ks > 1 && nkb / ks < 4) break;
+    const int ctas = tiles * ks;
+    const int waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots) - 0.004 * ks;
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = ks; }
+  }
+  return best;
+}
+
+size_t gemv_tc_ws_bytes(int N, int nkb) {
+  const int tiles = (N + TC_BM - 1) / TC_BM;
+  const int ks = gemv_tc_ksplit(N, nkb);
+  return (size_t)TC_COUNTER_INTS * 4 + (ks > 1 ? (size_t)ks * tiles * TC_BM * TC_T * 4 : 0);
+}
+
+int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const float *gain, float eps, uint16_t *xs,
+                      cudaStream_t st) {
+  HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "split_rows: t=%d outside [1,%d]", t, TC_T);
+  split_rows_kernel<<<TC_T, 256, 0, st>>>(x, ldx, t, K, ldk, gain, eps, xs);
+  return check_launch("split_rows");
+}
+
+// y (+)= W . x for one pass of <= 8 rows whose split operand is in xs [24][ldw]
+int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
+                   uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st) {
+  HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "gemv_tc: t=%d outside [1,%d]", t, TC_T);
+  HS_REQUIRE(ldw % TC_BK == 0, HS_ERR_SHAPE, "gemv_tc: ldw %d not a multiple of %d", ldw, TC_BK);
+  HS_REQUIRE(((uintptr_t)w % 16) == 0 && ((uintptr_t)xs % 16) == 0, HS_ERR_VALUE, "gemv_tc: operands must be 16B aligned");
+  HS_REQUIRE(epilogue != 2 || N % 2 == 0, HS_ERR_SHAPE, "gemv_tc: swiglu needs an even N");
+  const int nkb = ldw / TC_BK;
+  const int tiles = (N + TC_BM - 1) / TC_BM;
+  HS_REQUIRE(tiles <= TC_COUNTER_INTS, HS_ERR_SHAPE, "gemv_tc: N too large");
+  HS_REQUIRE(ws_bytes >= gemv_tc_ws_bytes(N, nkb), HS_ERR_VALUE, "gemv_tc: workspace too small");
+  CUtensorMap mw, mx;
+  int rc = get_tmap_bf16(w, (uint64_t)ldw, (uint64_t)N, (uint64_t)ldw * 2, TC_BM, &mw);
+  if (rc != HS_OK) return rc;
+  rc = get_tmap_bf16(xs, (uint64_t)ldw, (uint64_t)TC_XN, (uint64_t)ldw * 2, TC_XN, &mx);
+  if (rc != HS_OK) return rc;
+  GemvTcArgs a;
+  a.N = N; a.nkb = nkb; a.ks = gemv_tc_ksplit(N, nkb); a.t = t; a.epilogue = epilogue; a.n_tiles = tiles;
+  a.y = y; a.ldy = ldy; a.xs_out = xs_out; a.ld_xs_out = ld_xs_out;
+  a.counters = reinterpret_cast<int *>(ws);
+  a.partial = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + (size_t)TC_COUNTER_INTS * 4);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    attr_set = true;
+  }
+  gemv_tc_kernel<<<dim3(tiles, a.ks), 128, TC_SMEM, st>>>(mw, mx, a);
+  return check_launch("gemv_tc");
+}
+
+}  // namespace hs
+
+extern "C" size_t hs_gemv_tc_workspace_bytes(int N, int ldw) { return hs::gemv_tc_ws_bytes(N, ldw / hs::TC_BK); }
+
+extern "C" int hs_split_rows(const float *x, int ldx, int t, int K, int ldk, const float *gain, float eps,
+                             uint16_t *xs, void *stream) {
+  return hs::launch_split_rows(x, ldx, t, K, ldk, gain, eps, xs, hs::as_stream(stream));
+}
+
+extern "C" int hs_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
+                          uint16_t *xs_out, int ld_xs_out, void *workspace, size_t ws_bytes, void *stream) {
+  return hs::launch_gemv_tc(xs, t, w, ldw, N, epilogue, y, ldy, xs_out, ld_xs_out, workspace, ws_bytes,
+                            hs::as_stream(stream));
+}

@@ -381,7 +381,7 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
     for a, b in cache._batches(t):
         step = cache._step(b - a)
         nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split)
-        ws = workspaces.get("forward", nbytes)
+        ws = workspaces.get(f"forward:{id(dm)}", nbytes)
         check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), ptr(tok) + 4 * a, b - a,
                              ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))
         cache._advance(b - a)

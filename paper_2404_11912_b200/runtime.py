@@ -37,7 +37,7 @@ class _Workspaces:
     def get(self, key: str, nbytes: int) -> torch.Tensor:
         b = self.bufs.get(key)
         if b is None or b.numel() < nbytes:
-            b = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device())
+            b = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device())
             self.bufs[key] = b
         return b
 

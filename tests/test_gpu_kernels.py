@@ -254,3 +254,72 @@ def test_verify_and_correct_golden(P, golden):
 def test_abi_exports_loaded_on_device(P):
     from paper_2404_11912_b200._abi import lib
     assert lib.hs_device_sm_count(0) >= 1
+
+
+def _gemv_tc(x, W, gain=None, epilogue=0, y0=None, eps=1e-5):
+    """hs_split_rows (+RMSNorm) then hs_gemv_tc, passes of 8 rows."""
+    from paper_2404_11912_b200._abi import check, lib
+    from paper_2404_11912_b200.runtime import ptr, stream_ptr
+    t, K = x.shape
+    N = W.shape[0]
+    ld = (K + 63) // 64 * 64
+    Wd = torch.zeros((N, ld), dtype=torch.bfloat16, device="cuda")
+    Wd[:, :K] = torch.from_numpy(W).to("cuda").to(torch.bfloat16)
+    xd = torch.from_numpy(x.astype(np.float32)).cuda()
+    xs = torch.zeros((24, ld), dtype=torch.bfloat16, device="cuda")
+    ncol = N // 2 if epilogue == 2 else N
+    y = torch.from_numpy(y0.astype(np.float32)).cuda() if y0 is not None else torch.zeros((t, ncol), device="cuda")
+    g = torch.from_numpy(gain.astype(np.float32)).cuda() if gain is not None else None
+    nb = lib.hs_gemv_tc_workspace_bytes(N, ld)
+    ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+    ldo = (ncol + 63) // 64 * 64
+    xo = torch.zeros((24, ldo), dtype=torch.bfloat16, device="cuda")
+    for r0 in range(0, t, 8):
+        tp = min(8, t - r0)
+        check(lib.hs_split_rows(ptr(xd) + 4 * r0 * K, K, tp, K, ld, ptr(g), eps, ptr(xs), stream_ptr()))
+        check(lib.hs_gemv_tc(ptr(xs), tp, ptr(Wd), ld, N, epilogue, ptr(y) + 4 * r0 * ncol, ncol,
+                             ptr(xo) if epilogue == 2 else None, ldo, ptr(ws), nb, stream_ptr()))
+    assert int(ws[:4 * 16384].view(torch.int32).abs().sum().item()) == 0, "arrival counters not reset"
+    return y.cpu().numpy(), xo
+
+
+@pytest.mark.parametrize("t,K,N", [(1, 4096, 4096), (7, 4096, 12288), (5, 11008, 4096), (3, 256, 260),
+                                   (8, 688, 256), (13, 64, 40), (2, 40, 33), (4, 4096, 32000)])
+def test_gemv_tc_matches_fp64(P, t, K, N):
+    rng = np.random.default_rng(K + N + t + 1)
+    W = _bf16(rng.normal(0, 0.02, (N, K)).astype(np.float32))
+    x = rng.normal(0, 1, (t, K)).astype(np.float32)
+    y, _ = _gemv_tc(x, W)
+    ref = x.astype(np.float64) @ W.astype(np.float64).T
+    err = np.abs(y - ref).max() / np.abs(ref).max()
+    assert err < 2e-6, err
+
+
+def test_gemv_tc_epilogues_and_batch_invariance(P):
+    rng = np.random.default_rng(2)
+    t, K, N = 6, 1024, 640
+    W = _bf16(rng.normal(0, 0.05, (N, K)).astype(np.float32))
+    x = rng.normal(0, 1, (t, K)).astype(np.float32)
+    gain = (1 + rng.normal(0, 0.02, K)).astype(np.float32)
+    eps = float(np.float32(1e-5))
+    x64 = x.astype(np.float64)
+    h = (x64 / np.sqrt(np.square(x64).mean(axis=-1, keepdims=True) + eps) * gain.astype(np.float64)).astype(np.float32)
+    y, _ = _gemv_tc(x, W, gain=gain, eps=eps)
+    assert np.allclose(y, h.astype(np.float64) @ W.astype(np.float64).T, rtol=1e-5, atol=1e-5)
+    y0 = rng.normal(0, 1, (t, N)).astype(np.float32)
+    y, _ = _gemv_tc(x, W, epilogue=1, y0=y0)
+    assert np.allclose(y, y0 + x64 @ W.astype(np.float64).T, rtol=1e-5, atol=1e-5)
+    y, xo = _gemv_tc(x, W, epilogue=2)
+    gu = (x64 @ W.astype(np.float64).T).astype(np.float32)
+    g64 = gu[:, 0::2].astype(np.float64)
+    act = (g64 * (0.5 * (np.tanh(0.5 * g64) + 1.0))).astype(np.float32) * gu[:, 1::2]
+    assert np.allclose(y, act, rtol=1e-5, atol=1e-6)
+    # the split written for the next GEMV reconstructs act exactly
+    xo = xo.float().cpu().numpy()
+    rec = (xo[0:8] + xo[8:16]) + xo[16:24]
+    assert np.array_equal(rec[:t, :N // 2].astype(np.float32), y.astype(np.float32))
+    # rows are bitwise independent of the batch they are computed in
+    full, _ = _gemv_tc(x, W)
+    for r in range(t):
+        one, _ = _gemv_tc(x[r:r + 1], W)
+        assert np.array_equal(one[0], full[r])
