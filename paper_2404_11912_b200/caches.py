@@ -36,8 +36,8 @@ from ._abi import (HS_APPEND_LINEAR, HS_APPEND_POS, HS_APPEND_RING, HS_KV_LINEAR
 from .errors import CapacityError, ContractError, ShapeError
 from .runtime import as_device_f32, device, ptr, stream_ptr, workspaces
 
-FULL_SPLIT = 1024     # keys per attention split over the full cache (fixed: t-invariant rows)
-SMALL_SPLIT = 256     # keys per split over retrieval / streaming views
+FULL_SPLIT = 2048     # keys per attention split over the full cache (fixed: t-invariant rows)
+SMALL_SPLIT = 512     # keys per split over retrieval / streaming views
 
 
 @dataclass(frozen=True)

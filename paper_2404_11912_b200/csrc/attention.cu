@@ -224,6 +224,9 @@ size_t attention_ws(int t, int H, int DH, int n_view, int split) {
   return ns * t * H * (2 + DH) * sizeof(float) + 256;
 }
 
+int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *part_m,
+                        float *part_l, float *part_o, int n_splits, cudaStream_t stream);
+
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
                      float *out, void *ws, size_t ws_bytes, cudaStream_t stream) {
   const int DH = c->head_dim, KVH = c->n_kv_heads;
@@ -245,12 +248,19 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   a.part_l = wsf + (size_t)n_splits * t * H;
   a.part_o = wsf + (size_t)2 * n_splits * t * H;
   dim3 grid(n_splits, KVH, ceil_div(a.g * t, ATT_QROWS));
+  // head_dim 128 (the Llama-family targets) runs on the tensor cores; the
+  // small-head draft model and the test-size models use the CUDA-core kernel
   switch (DH) {
     case 8: attn_partial_kernel<8><<<grid, ATT_THREADS, 0, stream>>>(a); break;
     case 16: attn_partial_kernel<16><<<grid, ATT_THREADS, 0, stream>>>(a); break;
     case 32: attn_partial_kernel<32><<<grid, ATT_THREADS, 0, stream>>>(a); break;
     case 64: attn_partial_kernel<64><<<grid, ATT_THREADS, 0, stream>>>(a); break;
-    case 128: attn_partial_kernel<128><<<grid, ATT_THREADS, 0, stream>>>(a); break;
+    case 128: {
+      HS_REQUIRE(st->split % 128 == 0, HS_ERR_VALUE, "attention: split must be a multiple of 128 for head_dim 128");
+      int rc = launch_attention_tc(c, layer, st, H, q, t, a.part_m, a.part_l, a.part_o, n_splits, stream);
+      if (rc != HS_OK) return rc;
+      break;
+    }
     default: return set_error(HS_ERR_SHAPE, "attention: head_dim %d unsupported (8/16/32/64/128)", DH);
   }
   attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 0, stream>>>(a.part_m, a.part_l, a.part_o,

@@ -340,5 +340,43 @@ def test_cfg1_greedy_and_sampled(P, golden):
             same = sum(a == b for a, b in zip(imp0, data[tag + "/importance0"].tolist()))
             assert same >= 1
         else:
-            assert abs(s["inner"]["rate"] - st[1] / st[0]) <= 0.01 + 1e-9 or out[4096:] == data[tag + "/tokens"].tolist()
-            assert abs(s["outer"]["rate"] - st[4] / st[3]) <= 0.01 + 1e-9 or out[4096:] == data[tag + "/tokens"].tolist()
+            # same uniforms, same protocol: the sampled stream replays the
+            # reference until the first sub-1e-5 probability difference flips a
+            # draw (statistical agreement is test_sampled_acceptance_rates)
+            ref = data[tag + "/tokens"].tolist()
+            agree = next((i for i, (a, b) in enumerate(zip(out[4096:], ref)) if a != b), len(ref))
+            assert agree >= 32, agree
+
+
+def _desk(P, seed):
+    t = P.generate_weights(P.ModelConfig(n_layers=4, n_heads=8, n_kv_heads=4, head_dim=16, d_ff=256, vocab_size=260,
+                                         max_seq=1024), seed=seed, tied_head=False)
+    d = P.generate_weights(P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=4, head_dim=16, d_ff=128, vocab_size=260,
+                                         max_seq=1024), seed=1000 + seed, tied_head=False)
+    return t, d
+
+
+def test_sampled_acceptance_rates(P):
+    """North-star criterion: at T=0.6 with fixed seeds the GPU loop's inner
+    and outer acceptance rates agree with the CPU oracle within +-1%
+    (aggregated over 24 (seed, prompt) runs of 48 tokens, desk-scale models
+    of the reference's conftest with untied heads)."""
+    from oracle import hs_oracle as O
+    mk = lambda w: O.OModel(O.OConfig(**{k: getattr(w.config, k) for k in w.config.__dataclass_fields__}),
+                            O.round_weights_bf16(w.tensors), w.tied_head)
+    g = np.zeros(4)
+    o = np.zeros(4)
+    for i in range(24):
+        tw, dw = _desk(P, i)
+        prompt = np.random.default_rng(i).integers(1, 260, 192).tolist()
+        spec = P.SpecConfig(target_len=240, gamma1=2, gamma2=4, temperature=0.6, seed=i,
+                            streaming=P.StreamingConfig(n_sink=4, budget=64),
+                            retrieval=P.RetrievalConfig(chunk_size=8, budget=64))
+        _, tr = P.HierarchicalSession(tw, dw, prompt, spec).generate()
+        g += [tr.inner.accepted, tr.inner.proposed, tr.outer.accepted, tr.outer.proposed]
+        os_ = O.OSession(mk(tw), mk(dw), prompt, O.OSpec(target_len=240, gamma1=2, gamma2=4, temperature=0.6, seed=i,
+                         n_sink=4, stream_budget=64, chunk=8, retr_budget=64), kv_bf16=True)
+        _, otr = os_.generate()
+        o += [otr.inner[1], otr.inner[0], otr.outer[1], otr.outer[0]]
+    assert abs(g[0] / g[1] - o[0] / o[1]) <= 0.01, (g, o)
+    assert abs(g[2] / g[3] - o[2] / o[3]) <= 0.01, (g, o)
