@@ -10,8 +10,9 @@
 // Per CTA work item (split of 2048/512 slots, kv head, block of <= 16 query
 // rows), per 128-key tile:
 //   S^T[128 keys x 48] = K_tile[128 x 128] . Qsplit^T        (8 x tcgen05.mma K16)
-//   softmax in registers (thread = key = TMEM lane), online max/sum across
-//   the 4 warps, P split exactly into 3 bf16 terms -> smem (K-major, SW128)
+//   softmax in registers (thread = key = TMEM lane), tile max across the 4
+//   warps (redux + one named barrier), P split exactly into 3 bf16 terms ->
+//   smem (K-major, SW128)
 //   O^T[128 dh x 48]   = V_tile^T (MN-major) . Psplit^T      (8 x tcgen05.mma K16)
 //   thread = dh lane accumulates o = o*fac + (hi + mid + lo) in registers.
 // q and p enter the tensor core as exact 3-way bf16 splits, so every product
@@ -19,11 +20,13 @@
 // Each query row is its own MMA column: a row's result does not depend on
 // the other rows in the launch (t-invariance of the verify forward).
 //
-// Warp roles: warps 0-3 own TMEM lane quarters (softmax / accumulate), thread
-// 0 issues the MMAs at the points where the four warps are synchronised;
-// warp 4 is the TMA producer (one K stage + one V stage, 32 KB each), so the
-// next tile's K streams while the current tile's P.V runs.  Two CTAs per SM,
-// persistent over work items.
+// Software pipeline (double-buffered S, P, O in TMEM/smem; 2 K + 2 V stages):
+//   iteration i issues S(i+1), runs softmax(i), issues PV(i), then folds
+//   O(i-1) into the register accumulator -- the tensor core and the TMA
+//   stream run underneath the softmax of the current tile.
+// Warp roles: warps 0-3 own the TMEM lane quarters, thread 0 issues MMAs at
+// the points where the four warps are synchronised; warp 4 is the TMA
+// producer.  One CTA per SM, persistent over work items.
 #include "hs_common.cuh"
 #include "tc_util.cuh"
 
@@ -39,9 +42,11 @@ constexpr int AT_DH = 128;
 constexpr int AT_QR = 16;               // query rows per work item
 constexpr int AT_N = 3 * AT_QR;         // MMA N (3-way split)
 constexpr int AT_HALF = 128 * 64 * 2;   // one [128 rows x 64] bf16 SW128 tile = 16 KB
+constexpr int AT_KV = 2 * AT_HALF;      // one K or V tile (two dh halves) = 32 KB
 constexpr int AT_QP = AT_N * 128;       // one [48 rows x 64] bf16 SW128 atom column = 6 KB
+constexpr int AT_OPND = 2 * AT_QP;      // Q or one P buffer = 12 KB
 constexpr int AT_THREADS = 160;
-constexpr int AT_SMEM = 2 * AT_HALF /*K*/ + 2 * AT_HALF /*V*/ + 2 * AT_QP /*Q*/ + 2 * AT_QP /*P*/ + 2048 + 1024;
+constexpr int AT_SMEM = 2 * AT_KV + 2 * AT_KV + AT_OPND + 2 * AT_OPND + 1024;
 
 struct AttTcArgs {
   const float *q;       // [t][H][128]
@@ -61,43 +66,57 @@ __device__ __forceinline__ bool visible_tc(int kp, int qp, const AttTcArgs &a) {
 }
 
 // byte offset of element (row n, col k) in a K-major SW128 operand made of
-// 64-column atoms of `rows` rows each
-__device__ __forceinline__ uint32_t sw128_off(int n, int k, int rows) {
+// 64-column atoms of AT_N rows each
+__device__ __forceinline__ uint32_t sw128_off(int n, int k) {
   const int atom = k >> 6, kk = k & 63;
-  return (uint32_t)(atom * rows * 128 + n * 128 + ((((kk >> 3) ^ (n & 7)) & 7) << 4) + ((kk & 7) << 1));
+  return (uint32_t)(atom * AT_QP + n * 128 + ((((kk >> 3) ^ (n & 7)) & 7) << 4) + ((kk & 7) << 1));
 }
 
 __device__ __forceinline__ void named_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-__global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_constant__ CUtensorMap tmK,
+// order-preserving float <-> int for redux.sync max
+__device__ __forceinline__ int f2o(float f) { const int i = __float_as_int(f); return i ^ ((i >> 31) & 0x7fffffff); }
+__device__ __forceinline__ float o2f(int i) { return __int_as_float(i ^ ((i >> 31) & 0x7fffffff)); }
+
+__device__ __forceinline__ void split3_store(unsigned char *buf, int n, int k, float v) {
+  const __nv_bfloat16 h0 = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(h0);
+  const __nv_bfloat16 h1 = __float2bfloat16_rn(r1);
+  const __nv_bfloat16 h2 = __float2bfloat16_rn(r1 - __bfloat162float(h1));
+  *reinterpret_cast<__nv_bfloat16 *>(buf + sw128_off(n, k)) = h0;
+  *reinterpret_cast<__nv_bfloat16 *>(buf + sw128_off(AT_QR + n, k)) = h1;
+  *reinterpret_cast<__nv_bfloat16 *>(buf + sw128_off(2 * AT_QR + n, k)) = h2;
+}
+
+__global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV, AttTcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char *sK = base;                        // 2 x 16 KB (dh halves)
-  unsigned char *sV = sK + 2 * AT_HALF;            // 2 x 16 KB
-  unsigned char *sQ = sV + 2 * AT_HALF;            // 2 x 6 KB
-  unsigned char *sP = sQ + 2 * AT_QP;              // 2 x 6 KB (key halves)
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sP + 2 * AT_QP);
-  uint64_t *kfull = bars + 0, *kempty = bars + 1, *vfull = bars + 2, *vempty = bars + 3, *sdone = bars + 4,
-           *odone = bars + 5;
-  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(bars + 8);
-  float *red = reinterpret_cast<float *>(bars + 16);          // [4][AT_QR]
-  int *qp_s = reinterpret_cast<int *>(red + 4 * AT_QR);        // [AT_QR]
+  unsigned char *sK = base;                        // 2 stages x 32 KB
+  unsigned char *sV = sK + 2 * AT_KV;              // 2 stages x 32 KB
+  unsigned char *sQ = sV + 2 * AT_KV;              // 12 KB
+  unsigned char *sP = sQ + AT_OPND;                // 2 buffers x 12 KB
+  __shared__ uint64_t kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], ofull[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ int red[4][AT_QR];
+  __shared__ float redl[4][AT_QR];
+  __shared__ int qp_s[AT_QR];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   if (tid == 0) {
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
-    tc::mbar_init(kfull, 1); tc::mbar_init(kempty, 1); tc::mbar_init(vfull, 1); tc::mbar_init(vempty, 1);
-    tc::mbar_init(sdone, 1); tc::mbar_init(odone, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&kfull[s], 1); tc::mbar_init(&kempty[s], 1); tc::mbar_init(&vfull[s], 1);
+      tc::mbar_init(&vempty[s], 1); tc::mbar_init(&sfull[s], 1); tc::mbar_init(&ofull[s], 1);
+    }
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc<128>(tmem_base);
+  if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tmem = *tmem_base;
-  const uint32_t tS = tmem, tO = tmem + 64;
+  const uint32_t tmem = tmem_base;   // S[b] at b*64, O[b] at 128 + b*64
 
   // ---------------------------------------------------------------- producer
   if (warp == 4) {
@@ -108,14 +127,16 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
         const int row0 = (a.layer * a.KVH + kh) * a.cap;
         for (int tile = lo; tile < hi; tile += AT_KT, ++g) {
-          tc::mbar_wait(kempty, (g & 1) ^ 1);
-          tc::mbar_expect_tx(kfull, 2 * AT_HALF);
-          tc::tma_load_2d(sK, &tmK, kfull, 0, row0 + tile);
-          tc::tma_load_2d(sK + AT_HALF, &tmK, kfull, 64, row0 + tile);
-          tc::mbar_wait(vempty, (g & 1) ^ 1);
-          tc::mbar_expect_tx(vfull, 2 * AT_HALF);
-          tc::tma_load_2d(sV, &tmV, vfull, 0, row0 + tile);
-          tc::tma_load_2d(sV + AT_HALF, &tmV, vfull, 64, row0 + tile);
+          const int s = g & 1;
+          const uint32_t ph = (g >> 1) & 1;
+          tc::mbar_wait(&kempty[s], ph ^ 1);
+          tc::mbar_expect_tx(&kfull[s], AT_KV);
+          tc::tma_load_2d(sK + s * AT_KV, &tmK, &kfull[s], 0, row0 + tile);
+          tc::tma_load_2d(sK + s * AT_KV + AT_HALF, &tmK, &kfull[s], 64, row0 + tile);
+          tc::mbar_wait(&vempty[s], ph ^ 1);
+          tc::mbar_expect_tx(&vfull[s], AT_KV);
+          tc::tma_load_2d(sV + s * AT_KV, &tmV, &vfull[s], 0, row0 + tile);
+          tc::tma_load_2d(sV + s * AT_KV + AT_HALF, &tmV, &vfull[s], 64, row0 + tile);
         }
       }
     }
@@ -126,13 +147,45 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
   constexpr uint32_t idS = tc::idesc_bf16(128, AT_N, 0, 0);
   constexpr uint32_t idO = tc::idesc_bf16(128, AT_N, 1, 0);
   const uint32_t tl = (uint32_t)(warp * 32) << 16;   // this warp's TMEM lane quarter
-  uint32_t g = 0;
+  uint32_t g = 0;   // global tile counter (stage = g & 1, phase = (g >> 1) & 1)
+
+  auto issue_S = [&](uint32_t gg) {   // thread 0
+    const int s = gg & 1;
+    const uint32_t ph = (gg >> 1) & 1;
+    tc::mbar_wait(&kfull[s], ph);
+    tc::fence_after();
+#pragma unroll
+    for (int kk = 0; kk < AT_DH / 16; ++kk) {
+      const uint64_t da = tc::desc_k_sw128(sK + s * AT_KV + (kk >> 2) * AT_HALF) + 2 * (kk & 3);
+      const uint64_t db = tc::desc_k_sw128(sQ + (kk >> 2) * AT_QP) + 2 * (kk & 3);
+      tc::mma_bf16(tmem + s * 64, da, db, idS, kk != 0);
+    }
+    tc::mma_commit(&kempty[s]);
+    tc::mma_commit(&sfull[s]);
+  };
+  auto issue_PV = [&](uint32_t gg) {  // thread 0
+    const int s = gg & 1;
+    const uint32_t ph = (gg >> 1) & 1;
+    tc::mbar_wait(&vfull[s], ph);
+    tc::fence_after();
+#pragma unroll
+    for (int kk = 0; kk < AT_KT / 16; ++kk) {
+      // A = V^T, MN-major: 64-dh blocks 16 KB apart (LBO), 8-key groups 1 KB apart (SBO)
+      const uint64_t da = tc::desc_mn_sw128(sV + s * AT_KV + kk * 2048, AT_HALF, 1024);
+      const uint64_t db = tc::desc_k_sw128(sP + s * AT_OPND + (kk >> 2) * AT_QP) + 2 * (kk & 3);
+      tc::mma_bf16(tmem + 128 + s * 64, da, db, idO, kk != 0);
+    }
+    tc::mma_commit(&vempty[s]);
+    tc::mma_commit(&ofull[s]);
+  };
+
   for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
     const int split = item % a.n_splits, kh = (item / a.n_splits) % a.KVH, qb = item / (a.n_splits * a.KVH);
     const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
     const int r0 = qb * AT_QR;
     const int nrows = min(AT_QR, a.g * a.t - r0);
-    // ---- stage the query split (rows n = s*16 + rr) -------------------------------
+    const int ntiles = (hi - lo + AT_KT - 1) / AT_KT;
+    // ---- stage the query split; zero both P buffers (rows >= nrows stay 0) ----------
     if (tid < AT_QR) qp_s[tid] = tid < nrows ? a.pos0 + (r0 + tid) / a.g : -1;
     for (int e = tid; e < AT_QR * AT_DH; e += 128) {
       const int rr = e >> 7, d = e & 127;
@@ -141,114 +194,118 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         const int i = (r0 + rr) / a.g, head = kh * a.g + (r0 + rr) % a.g;
         v = a.q[((size_t)i * a.H + head) * AT_DH + d];
       }
-      const __nv_bfloat16 h0 = __float2bfloat16_rn(v);
-      const float r1 = v - __bfloat162float(h0);
-      const __nv_bfloat16 h1 = __float2bfloat16_rn(r1);
-      const __nv_bfloat16 h2 = __float2bfloat16_rn(r1 - __bfloat162float(h1));
-      *reinterpret_cast<__nv_bfloat16 *>(sQ + sw128_off(rr, d, AT_N)) = h0;
-      *reinterpret_cast<__nv_bfloat16 *>(sQ + sw128_off(AT_QR + rr, d, AT_N)) = h1;
-      *reinterpret_cast<__nv_bfloat16 *>(sQ + sw128_off(2 * AT_QR + rr, d, AT_N)) = h2;
+      split3_store(sQ, rr, d, v);
     }
+    for (int e = tid; e < 2 * AT_OPND / 16; e += 128) reinterpret_cast<uint4 *>(sP)[e] = make_uint4(0, 0, 0, 0);
     tc::fence_async_smem();
     named_sync();
-    float m_run[AT_QR], l_run[AT_QR], o_acc[AT_QR];
-#pragma unroll
-    for (int r = 0; r < AT_QR; ++r) { m_run[r] = -INFINITY; l_run[r] = 0.f; o_acc[r] = 0.f; }
 
-    for (int tile = lo; tile < hi; tile += AT_KT, ++g) {
-      const uint32_t ph = g & 1;
-      // ---- S^T = K . Qsplit^T ---------------------------------------------------
-      if (tid == 0) {
-        tc::mbar_wait(kfull, ph);
-        tc::fence_after();
+    float m_run[AT_QR], l_run[AT_QR], o_acc[AT_QR], fac_prev[AT_QR];
 #pragma unroll
-        for (int kk = 0; kk < AT_DH / 16; ++kk) {
-          const uint64_t da = tc::desc_k_sw128(sK + (kk >> 2) * AT_HALF) + 2 * (kk & 3);
-          const uint64_t db = tc::desc_k_sw128(sQ + (kk >> 2) * AT_QP) + 2 * (kk & 3);
-          tc::mma_bf16(tS, da, db, idS, kk != 0);
-        }
-        tc::mma_commit(kempty);
-        tc::mma_commit(sdone);
-      }
-      const int key = tile + tid;               // this thread's key slot
-      const bool in_range = key < hi;
-      const int kp = in_range ? (a.pos ? a.pos[key] : key) : -1;
-      tc::mbar_wait(sdone, ph);
+    for (int r = 0; r < AT_QR; ++r) { m_run[r] = -INFINITY; l_run[r] = 0.f; o_acc[r] = 0.f; fac_prev[r] = 1.f; }
+    const uint32_t g0 = g;
+    if (tid == 0) issue_S(g0);
+
+    for (int it = 0; it < ntiles; ++it) {
+      const uint32_t gi = g0 + it;
+      const int s = gi & 1;
+      const uint32_t ph = (gi >> 1) & 1;
+      if (tid == 0 && it + 1 < ntiles) issue_S(gi + 1);   // tensor core runs ahead
+      const int key = lo + it * AT_KT + tid;
+      const int kp = key < hi ? (a.pos ? a.pos[key] : key) : -1;
+      tc::mbar_wait(&sfull[s], ph);
       tc::fence_after();
-      float s[AT_N];
+      float sv[AT_N];
+      if (nrows <= 8) {
+        tc::tmem_ld8(tmem + s * 64 + tl + 0, sv + 0);
+        tc::tmem_ld8(tmem + s * 64 + tl + AT_QR, sv + AT_QR);
+        tc::tmem_ld8(tmem + s * 64 + tl + 2 * AT_QR, sv + 2 * AT_QR);
+      } else {
 #pragma unroll
-      for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tS + tl + c, s + c);
+        for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + s * 64 + tl + c, sv + c);
+      }
       tc::tmem_ld_wait();
-      // ---- masked scores, tile max across the 128 keys ---------------------------
+      // masked scores and tile max across the 128 keys
       float x[AT_QR];
 #pragma unroll
       for (int r = 0; r < AT_QR; ++r) {
-        const bool vis = r < nrows && visible_tc(kp, qp_s[r], a);
-        x[r] = vis ? ((s[r] + s[AT_QR + r]) + s[2 * AT_QR + r]) * a.scale : -INFINITY;
-        float mx = warp_max(x[r]);
-        if (lane == 0) red[warp * AT_QR + r] = mx;
+        if (r < nrows) {
+          const bool vis = visible_tc(kp, qp_s[r], a);
+          x[r] = vis ? ((sv[r] + sv[AT_QR + r]) + sv[2 * AT_QR + r]) * a.scale : -INFINITY;
+          const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
+          if (lane == 0) red[warp][r] = mx;
+        }
       }
       named_sync();
-      float fac[AT_QR], p[AT_QR];
+      float fac[AT_QR];
 #pragma unroll
       for (int r = 0; r < AT_QR; ++r) {
-        const float tmax = fmaxf(fmaxf(red[r], red[AT_QR + r]), fmaxf(red[2 * AT_QR + r], red[3 * AT_QR + r]));
-        const float m_new = fmaxf(m_run[r], tmax);
         fac[r] = 1.f;
-        p[r] = 0.f;
-        if (m_new != -INFINITY) {
-          p[r] = (x[r] == -INFINITY) ? 0.f : expf(x[r] - m_new);
-          fac[r] = (m_run[r] == -INFINITY) ? 0.f : expf(m_run[r] - m_new);
+        if (r < nrows) {
+          const int mi = max(max(red[0][r], red[1][r]), max(red[2][r], red[3][r]));
+          const float m_new = fmaxf(m_run[r], o2f(mi));
+          float p = 0.f;
+          if (m_new != -INFINITY) {
+            p = (x[r] == -INFINITY) ? 0.f : expf(x[r] - m_new);
+            fac[r] = (m_run[r] == -INFINITY) ? 0.f : expf(m_run[r] - m_new);
+          }
+          m_run[r] = m_new;
+          l_run[r] = l_run[r] * fac[r] + p;   // per-thread partial; reduced once per item
+          split3_store(sP + s * AT_OPND, r, tid, p);
         }
-        m_run[r] = m_new;
-      }
-      named_sync();   // everyone read red[] (max) before it is reused for sums
-#pragma unroll
-      for (int r = 0; r < AT_QR; ++r) {
-        const float ps = warp_sum(p[r]);
-        if (lane == 0) red[warp * AT_QR + r] = ps;
-        // P split into smem (K-major over keys): rows r, 16+r, 32+r
-        const __nv_bfloat16 h0 = __float2bfloat16_rn(p[r]);
-        const float r1 = p[r] - __bfloat162float(h0);
-        const __nv_bfloat16 h1 = __float2bfloat16_rn(r1);
-        const __nv_bfloat16 h2 = __float2bfloat16_rn(r1 - __bfloat162float(h1));
-        *reinterpret_cast<__nv_bfloat16 *>(sP + sw128_off(r, tid, AT_N)) = h0;
-        *reinterpret_cast<__nv_bfloat16 *>(sP + sw128_off(AT_QR + r, tid, AT_N)) = h1;
-        *reinterpret_cast<__nv_bfloat16 *>(sP + sw128_off(2 * AT_QR + r, tid, AT_N)) = h2;
       }
       tc::fence_async_smem();
       tc::fence_before();
-      named_sync();
-#pragma unroll
-      for (int r = 0; r < AT_QR; ++r)
-        l_run[r] = l_run[r] * fac[r] + ((red[r] + red[AT_QR + r]) + (red[2 * AT_QR + r] + red[3 * AT_QR + r]));
-      // ---- O^T = V^T . Psplit^T -------------------------------------------------
-      if (tid == 0) {
+      named_sync();   // P(i) complete, red[] free, S(i) drained
+      if (tid == 0) issue_PV(gi);
+      if (it > 0) {   // fold O(i-1): its PV was issued one iteration ago
+        const int sp = (gi - 1) & 1;
+        tc::mbar_wait(&ofull[sp], ((gi - 1) >> 1) & 1);
         tc::fence_after();
-        tc::mbar_wait(vfull, ph);
-        tc::fence_after();
+        float ov[AT_N];
+        if (nrows <= 8) {
+          tc::tmem_ld8(tmem + 128 + sp * 64 + tl + 0, ov + 0);
+          tc::tmem_ld8(tmem + 128 + sp * 64 + tl + AT_QR, ov + AT_QR);
+          tc::tmem_ld8(tmem + 128 + sp * 64 + tl + 2 * AT_QR, ov + 2 * AT_QR);
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < AT_KT / 16; ++kk) {
-          // A = V^T, MN-major: 64-dh blocks 16 KB apart (LBO), 8-key groups 1 KB apart (SBO)
-          const uint64_t da = tc::desc_mn_sw128(sV + kk * 2048, AT_HALF, 1024);
-          const uint64_t db = tc::desc_k_sw128(sP + (kk >> 2) * AT_QP) + 2 * (kk & 3);
-          tc::mma_bf16(tO, da, db, idO, kk != 0);
+          for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 128 + sp * 64 + tl + c, ov + c);
         }
-        tc::mma_commit(vempty);
-        tc::mma_commit(odone);
-      }
-      tc::mbar_wait(odone, ph);
-      tc::fence_after();
-      float o[AT_N];
+        tc::tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tO + tl + c, o + c);
+        for (int r = 0; r < AT_QR; ++r)
+          if (r < nrows) o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_QR + r]) + ov[2 * AT_QR + r]);
+      }
+#pragma unroll
+      for (int r = 0; r < AT_QR; ++r) fac_prev[r] = fac[r];
+    }
+    // drain the last PV
+    {
+      const uint32_t gl = g0 + ntiles - 1;
+      const int sp = gl & 1;
+      tc::mbar_wait(&ofull[sp], (gl >> 1) & 1);
+      tc::fence_after();
+      float ov[AT_N];
+#pragma unroll
+      for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 128 + sp * 64 + tl + c, ov + c);
       tc::tmem_ld_wait();
 #pragma unroll
-      for (int r = 0; r < AT_QR; ++r) o_acc[r] = o_acc[r] * fac[r] + ((o[r] + o[AT_QR + r]) + o[2 * AT_QR + r]);
-      tc::fence_before();
-      named_sync();   // TMEM S/O and smem P free for the next tile
+      for (int r = 0; r < AT_QR; ++r)
+        if (r < nrows) o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_QR + r]) + ov[2 * AT_QR + r]);
     }
-    // ---- partial state of this item ---------------------------------------------------
+    g = g0 + ntiles;
+    // ---- l: sum of the per-thread partials (fixed order), then write partial state ----
+#pragma unroll
+    for (int r = 0; r < AT_QR; ++r) {
+      if (r < nrows) {
+        float v = l_run[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) redl[warp][r] = v;
+      }
+    }
+    tc::fence_before();
+    named_sync();
     const size_t pbase = (size_t)split * a.t * a.H;
 #pragma unroll
     for (int r = 0; r < AT_QR; ++r) {
@@ -256,14 +313,17 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         const int i = (r0 + r) / a.g, head = kh * a.g + (r0 + r) % a.g;
         const size_t row = (size_t)i * a.H + head;
         a.part_o[(pbase + row) * AT_DH + tid] = o_acc[r];
-        if (tid == 0) { a.part_m[pbase + row] = m_run[r]; a.part_l[pbase + row] = l_run[r]; }
+        if (tid == 0) {
+          a.part_m[pbase + row] = m_run[r];
+          a.part_l[pbase + row] = (redl[0][r] + redl[1][r]) + (redl[2][r] + redl[3][r]);
+        }
       }
     }
     named_sync();
   }
   tc::fence_before();
   named_sync();
-  if (warp == 0) tc::tmem_dealloc<128>(tmem);
+  if (warp == 0) tc::tmem_dealloc<256>(tmem);
 }
 
 }  // namespace
@@ -291,9 +351,9 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
     cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);
     attr = true;
   }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int grid = a.n_items < 2 * sms ? a.n_items : 2 * sms;
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = a.n_items < sms ? a.n_items : sms;
   attn_tc_kernel<<<grid, AT_THREADS, AT_SMEM, stream>>>(mk, mv, a);
   return check_launch("attention_tc");
 }

@@ -97,6 +97,7 @@ __device__ __forceinline__ void split3(float h, uint16_t &a, uint16_t &b, uint16
 // grid: TC_T blocks (row r); rows >= t are written as zeros
 __global__ void __launch_bounds__(256) split_rows_kernel(const float *x, int ldx, int t, int K, int ldk,
                                                          const float *gain, float eps, uint16_t *xs) {
+  tc::grid_dep_launch();
   const int r = blockIdx.x;
   __shared__ double red[8];
   __shared__ double scale_s;
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   uint32_t *tmem_base = reinterpret_cast<uint32_t *>(accum + 1);
   int *flag = reinterpret_cast<int *>(tmem_base + 1);
 
+  tc::grid_dep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y;
   const int per = a.nkb / a.ks, rem = a.nkb % a.ks;
@@ -210,8 +212,18 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
 
   if (warp == 0) {
     if (tc::elect_one()) {
+      // Programmatic dependent launch: the weights never depend on the
+      // previous kernel, so the first stages' weight tiles stream in while
+      // that kernel drains; only the activation tiles wait for it.
       const uint64_t pol = tc::policy_evict_first();   // weights are streamed exactly once
-      for (int i = 0; i < nk; ++i) {
+      const int npre = nk < TC_STAGES ? nk : TC_STAGES;
+      for (int i = 0; i < npre; ++i) {
+        tc::mbar_expect_tx(&full[i], TC_W_BYTES + TC_X_BYTES);
+        tc::tma_load_2d_hint(sW + i * TC_W_BYTES, &tmW, &full[i], (kb0 + i) * TC_BK, tile * TC_BM, pol);
+      }
+      tc::grid_dep_wait();
+      for (int i = 0; i < npre; ++i) tc::tma_load_2d(sX + i * TC_X_BYTES, &tmX, &full[i], (kb0 + i) * TC_BK, 0);
+      for (int i = npre; i < nk; ++i) {
         const int s = i % TC_STAGES;
         const uint32_t ph = (i / TC_STAGES) & 1;
         tc::mbar_wait(&empty[s], ph ^ 1);
@@ -220,6 +232,8 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
         tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], k, tile * TC_BM, pol);
         tc::tma_load_2d(sX + s * TC_X_BYTES, &tmX, &full[s], k, 0);
       }
+    } else {
+      tc::grid_dep_wait();
     }
   } else if (warp == 1) {
     if (tc::elect_one()) {
@@ -239,6 +253,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
       tc::mma_commit(accum);
     }
   }
+  if (warp != 0) tc::grid_dep_wait();   // epilogue reads y written by earlier kernels
   __syncwarp();
 
   // ---- epilogue: TMEM -> registers ---------------------------------------------------
@@ -344,7 +359,18 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
     cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     attr_set = true;
   }
-  gemv_tc_kernel<<<dim3(tiles, a.ks), 128, TC_SMEM, st>>>(mw, mx, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles, a.ks, 1);
+  cfg.blockDim = dim3(128, 1, 1);
+  cfg.dynamicSmemBytes = TC_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_tc_kernel, mw, mx, a);
+  if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "gemv_tc launch: %s", cudaGetErrorString(e));
   return check_launch("gemv_tc");
 }
 

@@ -51,29 +51,25 @@ def main():
     d, ff = 4096, 11008
     out = {"gemv": {}, "attn": {}}
     s = stream_ptr()
-    shapes = {"wqkv": (dm.wqkv, 12288, d, dm.ld_d, 1, 0), "wo": (dm.wo, d, d, dm.ld_d, 0, 1),
-              "wgu": (dm.wgu, 2 * ff, d, dm.ld_d, 1, 2), "wdown": (dm.wdown, d, ff, dm.ld_ff, 0, 1)}
+    shapes = {"wqkv": (dm.wqkv, 12288, d, dm.ld_d, 0), "wo": (dm.wo, d, d, dm.ld_d, 1),
+              "wgu": (dm.wgu, 2 * ff, d, dm.ld_d, 2), "wdown": (dm.wdown, d, ff, dm.ld_ff, 1),
+              "head": (dm.head.unsqueeze(0), 32000, d, dm.ld_d, 0)}
+    xs = torch.zeros((24, dm.ld_ff), dtype=torch.bfloat16, device="cuda")
+    xo = torch.zeros((24, dm.ld_ff), dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros((8, 32000), device="cuda")
     for t in (1, 3, 5, 8):
-        x = torch.randn((t, ff), device="cuda")
-        y = torch.zeros((t, 2 * ff), device="cuda")
-        for name, (w, N, K, ld, pro, epi) in shapes.items():
+        for name, (w, N, K, ld, epi) in shapes.items():
             if a.only and a.only not in name:
                 continue
-            per_layer = w[0].numel() * 2
+            nb = lib.hs_gemv_tc_workspace_bytes(N, ld)
+            ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+            nl = w.shape[0]
 
-            def fn(r, w=w, N=N, K=K, ld=ld, pro=pro, epi=epi):
-                check(lib.hs_gemv(ptr(x), K, t, K, ptr(w[r % L]), ld, N, pro, ptr(dm.attn_norm[0]), 1e-5, epi, ptr(y),
-                                  N // 2 if epi == 2 else N, s))
+            def fn(r, w=w, N=N, ld=ld, epi=epi, nb=nb, ws=ws, nl=nl):
+                check(lib.hs_gemv_tc(ptr(xs), t, ptr(w[r % nl]), ld, N, epi, ptr(y) if epi != 2 else None,
+                                     N, ptr(xo) if epi == 2 else None, dm.ld_ff, ptr(ws), nb, s))
             us = timeit(fn)
             out["gemv"][f"{name}_t{t}"] = {"us": us, "GBps": N * K * 2 / us / 1e3}
-        if not a.only or "head" in a.only:
-            yh = torch.zeros((t, 32000), device="cuda")
-
-            def fnh(r):
-                check(lib.hs_gemv(ptr(x), d, t, d, ptr(dm.head), dm.ld_d, 32000, 1, ptr(dm.final_norm), 1e-5, 0,
-                                  ptr(yh), 32000, s))
-            us = timeit(fnh)
-            out["gemv"][f"head_t{t}"] = {"us": us, "GBps": 32000 * d * 2 / us / 1e3}
     # attention over a full cache
     if not a.only or "attn" in a.only:
         n = a.ctx
