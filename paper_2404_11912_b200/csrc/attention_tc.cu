@@ -45,7 +45,7 @@ constexpr int AT_HALF = 128 * 64 * 2;   // one [128 rows x 64] bf16 SW128 tile =
 constexpr int AT_KV = 2 * AT_HALF;      // one K or V tile (two dh halves) = 32 KB
 constexpr int AT_QP = AT_N * 128;       // one [48 rows x 64] bf16 SW128 atom column = 6 KB
 constexpr int AT_OPND = 2 * AT_QP;      // Q or one P buffer = 12 KB
-constexpr int AT_THREADS = 160;
+constexpr int AT_THREADS = 192;
 constexpr int AT_SMEM = 2 * AT_KV + 2 * AT_KV + AT_OPND + 2 * AT_OPND + 1024;
 
 struct AttTcArgs {
@@ -96,9 +96,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
   unsigned char *sV = sK + 2 * AT_KV;              // 2 stages x 32 KB
   unsigned char *sQ = sV + 2 * AT_KV;              // 12 KB
   unsigned char *sP = sQ + AT_OPND;                // 2 buffers x 12 KB
-  __shared__ uint64_t kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], ofull[2];
+  // TMA <-> MMA: kfull/kempty/vfull/vempty; MMA <-> softmax warps: sfull/sfree,
+  // pfull, ofull/ofree, qfull (per item).  Per-tile barriers alternate on
+  // buffer b = g & 1 with phase (g >> 1) & 1.
+  __shared__ uint64_t kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], sfree[2], pfull[2], ofull[2], ofree[2];
+  __shared__ uint64_t qfull;
   __shared__ uint32_t tmem_base;
-  __shared__ int red[4][AT_QR];
+  __shared__ int red[2][4][AT_QR];
   __shared__ float redl[4][AT_QR];
   __shared__ int qp_s[AT_QR];
 
@@ -108,8 +112,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
     tc::tma_prefetch(&tmV);
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&kfull[s], 1); tc::mbar_init(&kempty[s], 1); tc::mbar_init(&vfull[s], 1);
-      tc::mbar_init(&vempty[s], 1); tc::mbar_init(&sfull[s], 1); tc::mbar_init(&ofull[s], 1);
+      tc::mbar_init(&vempty[s], 1); tc::mbar_init(&sfull[s], 1); tc::mbar_init(&sfree[s], 4);
+      tc::mbar_init(&pfull[s], 4); tc::mbar_init(&ofull[s], 1); tc::mbar_init(&ofree[s], 4);
     }
+    tc::mbar_init(&qfull, 4);
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
@@ -117,8 +123,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;   // S[b] at b*64, O[b] at 128 + b*64
+  tc::grid_dep_wait();               // K/V rows appended by the previous kernel
 
-  // ---------------------------------------------------------------- producer
+  // ---------------------------------------------------------------- TMA producer (warp 4)
   if (warp == 4) {
     if (tc::elect_one()) {
       uint32_t g = 0;
@@ -143,42 +150,63 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
     return;
   }
 
-  // ---------------------------------------------------------------- consumers (warps 0-3)
-  constexpr uint32_t idS = tc::idesc_bf16(128, AT_N, 0, 0);
-  constexpr uint32_t idO = tc::idesc_bf16(128, AT_N, 1, 0);
+  // ---------------------------------------------------------------- MMA issuer (warp 5)
+  if (warp == 5) {
+    if (tc::elect_one()) {
+      constexpr uint32_t idS = tc::idesc_bf16(128, AT_N, 0, 0);
+      constexpr uint32_t idO = tc::idesc_bf16(128, AT_N, 1, 0);
+      auto issue_S = [&](uint32_t g) {
+        const int s = g & 1;
+        const uint32_t ph = (g >> 1) & 1;
+        tc::mbar_wait(&kfull[s], ph);
+        tc::mbar_wait(&sfree[s], ph ^ 1);
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_DH / 16; ++kk) {
+          const uint64_t da = tc::desc_k_sw128(sK + s * AT_KV + (kk >> 2) * AT_HALF) + 2 * (kk & 3);
+          const uint64_t db = tc::desc_k_sw128(sQ + (kk >> 2) * AT_QP) + 2 * (kk & 3);
+          tc::mma_bf16(tmem + s * 64, da, db, idS, kk != 0);
+        }
+        tc::mma_commit(&kempty[s]);
+        tc::mma_commit(&sfull[s]);
+      };
+      auto issue_PV = [&](uint32_t g) {
+        const int s = g & 1;
+        const uint32_t ph = (g >> 1) & 1;
+        tc::mbar_wait(&pfull[s], ph);
+        tc::mbar_wait(&vfull[s], ph);
+        tc::mbar_wait(&ofree[s], ph ^ 1);
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_KT / 16; ++kk) {
+          // A = V^T, MN-major: 64-dh blocks 16 KB apart (LBO), 8-key groups 1 KB apart (SBO)
+          const uint64_t da = tc::desc_mn_sw128(sV + s * AT_KV + kk * 2048, AT_HALF, 1024);
+          const uint64_t db = tc::desc_k_sw128(sP + s * AT_OPND + (kk >> 2) * AT_QP) + 2 * (kk & 3);
+          tc::mma_bf16(tmem + 128 + s * 64, da, db, idO, kk != 0);
+        }
+        tc::mma_commit(&vempty[s]);
+        tc::mma_commit(&ofull[s]);
+      };
+      uint32_t g = 0, nitem = 0;
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x, ++nitem) {
+        const int split = item % a.n_splits;
+        const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
+        const int ntiles = (hi - lo + AT_KT - 1) / AT_KT;
+        tc::mbar_wait(&qfull, nitem & 1);          // this item's query split is staged
+        issue_S(g);
+        for (int it = 0; it < ntiles; ++it) {       // S runs one tile ahead of P.V
+          if (it + 1 < ntiles) issue_S(g + it + 1);
+          issue_PV(g + it);
+        }
+        g += ntiles;
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- softmax warps 0-3
   const uint32_t tl = (uint32_t)(warp * 32) << 16;   // this warp's TMEM lane quarter
-  uint32_t g = 0;   // global tile counter (stage = g & 1, phase = (g >> 1) & 1)
-
-  auto issue_S = [&](uint32_t gg) {   // thread 0
-    const int s = gg & 1;
-    const uint32_t ph = (gg >> 1) & 1;
-    tc::mbar_wait(&kfull[s], ph);
-    tc::fence_after();
-#pragma unroll
-    for (int kk = 0; kk < AT_DH / 16; ++kk) {
-      const uint64_t da = tc::desc_k_sw128(sK + s * AT_KV + (kk >> 2) * AT_HALF) + 2 * (kk & 3);
-      const uint64_t db = tc::desc_k_sw128(sQ + (kk >> 2) * AT_QP) + 2 * (kk & 3);
-      tc::mma_bf16(tmem + s * 64, da, db, idS, kk != 0);
-    }
-    tc::mma_commit(&kempty[s]);
-    tc::mma_commit(&sfull[s]);
-  };
-  auto issue_PV = [&](uint32_t gg) {  // thread 0
-    const int s = gg & 1;
-    const uint32_t ph = (gg >> 1) & 1;
-    tc::mbar_wait(&vfull[s], ph);
-    tc::fence_after();
-#pragma unroll
-    for (int kk = 0; kk < AT_KT / 16; ++kk) {
-      // A = V^T, MN-major: 64-dh blocks 16 KB apart (LBO), 8-key groups 1 KB apart (SBO)
-      const uint64_t da = tc::desc_mn_sw128(sV + s * AT_KV + kk * 2048, AT_HALF, 1024);
-      const uint64_t db = tc::desc_k_sw128(sP + s * AT_OPND + (kk >> 2) * AT_QP) + 2 * (kk & 3);
-      tc::mma_bf16(tmem + 128 + s * 64, da, db, idO, kk != 0);
-    }
-    tc::mma_commit(&vempty[s]);
-    tc::mma_commit(&ofull[s]);
-  };
-
+  uint32_t g = 0;
   for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
     const int split = item % a.n_splits, kh = (item / a.n_splits) % a.KVH, qb = item / (a.n_splits * a.KVH);
     const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
@@ -186,6 +214,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
     const int nrows = min(AT_QR, a.g * a.t - r0);
     const int ntiles = (hi - lo + AT_KT - 1) / AT_KT;
     // ---- stage the query split; zero both P buffers (rows >= nrows stay 0) ----------
+    // (all S/P.V MMAs of the previous item completed: its tiles were all consumed)
     if (tid < AT_QR) qp_s[tid] = tid < nrows ? a.pos0 + (r0 + tid) / a.g : -1;
     for (int e = tid; e < AT_QR * AT_DH; e += 128) {
       const int rr = e >> 7, d = e & 127;
@@ -199,101 +228,108 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
     for (int e = tid; e < 2 * AT_OPND / 16; e += 128) reinterpret_cast<uint4 *>(sP)[e] = make_uint4(0, 0, 0, 0);
     tc::fence_async_smem();
     named_sync();
+    if (lane == 0) tc::mbar_arrive(&qfull);
 
     float m_run[AT_QR], l_run[AT_QR], o_acc[AT_QR], fac_prev[AT_QR];
 #pragma unroll
     for (int r = 0; r < AT_QR; ++r) { m_run[r] = -INFINITY; l_run[r] = 0.f; o_acc[r] = 0.f; fac_prev[r] = 1.f; }
-    const uint32_t g0 = g;
-    if (tid == 0) issue_S(g0);
 
-    for (int it = 0; it < ntiles; ++it) {
-      const uint32_t gi = g0 + it;
-      const int s = gi & 1;
-      const uint32_t ph = (gi >> 1) & 1;
-      if (tid == 0 && it + 1 < ntiles) issue_S(gi + 1);   // tensor core runs ahead
-      const int key = lo + it * AT_KT + tid;
-      const int kp = key < hi ? (a.pos ? a.pos[key] : key) : -1;
-      tc::mbar_wait(&sfull[s], ph);
-      tc::fence_after();
-      float sv[AT_N];
-      if (nrows <= 8) {
-        tc::tmem_ld8(tmem + s * 64 + tl + 0, sv + 0);
-        tc::tmem_ld8(tmem + s * 64 + tl + AT_QR, sv + AT_QR);
-        tc::tmem_ld8(tmem + s * 64 + tl + 2 * AT_QR, sv + 2 * AT_QR);
-      } else {
-#pragma unroll
-        for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + s * 64 + tl + c, sv + c);
-      }
-      tc::tmem_ld_wait();
-      // masked scores and tile max across the 128 keys
-      float x[AT_QR];
-#pragma unroll
-      for (int r = 0; r < AT_QR; ++r) {
-        if (r < nrows) {
-          const bool vis = visible_tc(kp, qp_s[r], a);
-          x[r] = vis ? ((sv[r] + sv[AT_QR + r]) + sv[2 * AT_QR + r]) * a.scale : -INFINITY;
-          const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
-          if (lane == 0) red[warp][r] = mx;
-        }
-      }
-      named_sync();
-      float fac[AT_QR];
-#pragma unroll
-      for (int r = 0; r < AT_QR; ++r) {
-        fac[r] = 1.f;
-        if (r < nrows) {
-          const int mi = max(max(red[0][r], red[1][r]), max(red[2][r], red[3][r]));
-          const float m_new = fmaxf(m_run[r], o2f(mi));
-          float p = 0.f;
-          if (m_new != -INFINITY) {
-            p = (x[r] == -INFINITY) ? 0.f : expf(x[r] - m_new);
-            fac[r] = (m_run[r] == -INFINITY) ? 0.f : expf(m_run[r] - m_new);
-          }
-          m_run[r] = m_new;
-          l_run[r] = l_run[r] * fac[r] + p;   // per-thread partial; reduced once per item
-          split3_store(sP + s * AT_OPND, r, tid, p);
-        }
-      }
-      tc::fence_async_smem();
-      tc::fence_before();
-      named_sync();   // P(i) complete, red[] free, S(i) drained
-      if (tid == 0) issue_PV(gi);
-      if (it > 0) {   // fold O(i-1): its PV was issued one iteration ago
-        const int sp = (gi - 1) & 1;
-        tc::mbar_wait(&ofull[sp], ((gi - 1) >> 1) & 1);
+    for (int it = 0; it <= ntiles; ++it) {
+      if (it < ntiles) {
+        const uint32_t gi = g + it;
+        const int s = gi & 1;
+        const uint32_t ph = (gi >> 1) & 1;
+        const int key = lo + it * AT_KT + tid;
+        const int kp = key < hi ? (a.pos ? a.pos[key] : key) : -1;
+        tc::mbar_wait(&sfull[s], ph);
         tc::fence_after();
-        float ov[AT_N];
+        float sv[AT_N];
         if (nrows <= 8) {
-          tc::tmem_ld8(tmem + 128 + sp * 64 + tl + 0, ov + 0);
-          tc::tmem_ld8(tmem + 128 + sp * 64 + tl + AT_QR, ov + AT_QR);
-          tc::tmem_ld8(tmem + 128 + sp * 64 + tl + 2 * AT_QR, ov + 2 * AT_QR);
+          tc::tmem_ld8(tmem + s * 64 + tl + 0, sv + 0);
+          tc::tmem_ld8(tmem + s * 64 + tl + AT_QR, sv + AT_QR);
+          tc::tmem_ld8(tmem + s * 64 + tl + 2 * AT_QR, sv + 2 * AT_QR);
         } else {
 #pragma unroll
-          for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 128 + sp * 64 + tl + c, ov + c);
+          for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + s * 64 + tl + c, sv + c);
         }
         tc::tmem_ld_wait();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&sfree[s]);
+        // masked scores and tile max across the 128 keys
+        float x[AT_QR];
+#pragma unroll
+        for (int r = 0; r < AT_QR; ++r) {
+          if (r < nrows) {
+            const bool vis = visible_tc(kp, qp_s[r], a);
+            x[r] = vis ? ((sv[r] + sv[AT_QR + r]) + sv[2 * AT_QR + r]) * a.scale : -INFINITY;
+            const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
+            if (lane == 0) red[s][warp][r] = mx;
+          }
+        }
+        named_sync();
+        float fac[AT_QR];
+#pragma unroll
+        for (int r = 0; r < AT_QR; ++r) {
+          fac[r] = 1.f;
+          if (r < nrows) {
+            const int mi = max(max(red[s][0][r], red[s][1][r]), max(red[s][2][r], red[s][3][r]));
+            const float m_new = fmaxf(m_run[r], o2f(mi));
+            float p = 0.f;
+            if (m_new != -INFINITY) {
+              p = (x[r] == -INFINITY) ? 0.f : expf(x[r] - m_new);
+              fac[r] = (m_run[r] == -INFINITY) ? 0.f : expf(m_run[r] - m_new);
+            }
+            m_run[r] = m_new;
+            l_run[r] = l_run[r] * fac[r] + p;   // per-thread partial; reduced once per item
+            split3_store(sP + s * AT_OPND, r, tid, p);
+          }
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&pfull[s]);
+        if (it > 0) {   // fold O(it-1) with the previous tile's rescale factor
+          const uint32_t gp = gi - 1;
+          const int sp = gp & 1;
+          tc::mbar_wait(&ofull[sp], (gp >> 1) & 1);
+          tc::fence_after();
+          float ov[AT_N];
+          if (nrows <= 8) {
+            tc::tmem_ld8(tmem + 128 + sp * 64 + tl + 0, ov + 0);
+            tc::tmem_ld8(tmem + 128 + sp * 64 + tl + AT_QR, ov + AT_QR);
+            tc::tmem_ld8(tmem + 128 + sp * 64 + tl + 2 * AT_QR, ov + 2 * AT_QR);
+          } else {
+#pragma unroll
+            for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 128 + sp * 64 + tl + c, ov + c);
+          }
+          tc::tmem_ld_wait();
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&ofree[sp]);
+#pragma unroll
+          for (int r = 0; r < AT_QR; ++r)
+            if (r < nrows) o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_QR + r]) + ov[2 * AT_QR + r]);
+        }
+#pragma unroll
+        for (int r = 0; r < AT_QR; ++r) fac_prev[r] = fac[r];
+      } else {        // drain O(last)
+        const uint32_t gp = g + ntiles - 1;
+        const int sp = gp & 1;
+        tc::mbar_wait(&ofull[sp], (gp >> 1) & 1);
+        tc::fence_after();
+        float ov[AT_N];
+#pragma unroll
+        for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 128 + sp * 64 + tl + c, ov + c);
+        tc::tmem_ld_wait();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&ofree[sp]);
 #pragma unroll
         for (int r = 0; r < AT_QR; ++r)
           if (r < nrows) o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_QR + r]) + ov[2 * AT_QR + r]);
       }
-#pragma unroll
-      for (int r = 0; r < AT_QR; ++r) fac_prev[r] = fac[r];
     }
-    // drain the last PV
-    {
-      const uint32_t gl = g0 + ntiles - 1;
-      const int sp = gl & 1;
-      tc::mbar_wait(&ofull[sp], (gl >> 1) & 1);
-      tc::fence_after();
-      float ov[AT_N];
-#pragma unroll
-      for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 128 + sp * 64 + tl + c, ov + c);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int r = 0; r < AT_QR; ++r)
-        if (r < nrows) o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_QR + r]) + ov[2 * AT_QR + r]);
-    }
-    g = g0 + ntiles;
+    g += ntiles;
     // ---- l: sum of the per-thread partials (fixed order), then write partial state ----
 #pragma unroll
     for (int r = 0; r < AT_QR; ++r) {
@@ -304,7 +340,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
         if (lane == 0) redl[warp][r] = v;
       }
     }
-    tc::fence_before();
     named_sync();
     const size_t pbase = (size_t)split * a.t * a.H;
 #pragma unroll
