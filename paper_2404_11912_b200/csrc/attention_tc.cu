@@ -39,21 +39,22 @@ namespace {
 
 constexpr int AT_KT = 128;              // keys per tile (MMA M of S^T)
 constexpr int AT_DH = 128;
-constexpr int AT_QR = 16;               // query rows per work item
+constexpr int AT_QR = 8;                // query rows per work item (more rows -> more items)
 constexpr int AT_N = 3 * AT_QR;         // MMA N (3-way split)
 constexpr int AT_HALF = 128 * 64 * 2;   // one [128 rows x 64] bf16 SW128 tile = 16 KB
 constexpr int AT_KV = 2 * AT_HALF;      // one K or V tile (two dh halves) = 32 KB
-constexpr int AT_QP = AT_N * 128;       // one [48 rows x 64] bf16 SW128 atom column = 6 KB
-constexpr int AT_OPND = 2 * AT_QP;      // Q or one P buffer = 12 KB
+constexpr int AT_QP = AT_N * 128;       // one [24 rows x 64] bf16 SW128 atom column = 3 KB
+constexpr int AT_OPND = 2 * AT_QP;      // Q or one P buffer = 6 KB
 constexpr int AT_THREADS = 192;
-constexpr int AT_SMEM = 2 * AT_KV + 2 * AT_KV + AT_OPND + 2 * AT_OPND + 1024;
+constexpr int AT_KSTAGES = 1, AT_VSTAGES = 1;
+constexpr int AT_SMEM = AT_KSTAGES * AT_KV + AT_VSTAGES * AT_KV + AT_OPND + 2 * AT_OPND + 1024;
 
 struct AttTcArgs {
   const float *q;       // [t][H][128]
   int t, H, KVH, g;
   const int32_t *pos;   // layer [cap] or null
   int cap, layer, n_view, pos0, window, win_lo, n_sink, split, n_splits, n_qb, n_items;
-  float scale;
+  float scale_log2;     // log2(e) / sqrt(dh)
   float *part_m, *part_l, *part_o;
 };
 
@@ -72,6 +73,12 @@ __device__ __forceinline__ uint32_t sw128_off(int n, int k) {
   return (uint32_t)(atom * AT_QP + n * 128 + ((((kk >> 3) ^ (n & 7)) & 7) << 4) + ((kk & 7) << 1));
 }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void named_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // order-preserving float <-> int for redux.sync max
@@ -88,13 +95,13 @@ __device__ __forceinline__ void split3_store(unsigned char *buf, int n, int k, f
   *reinterpret_cast<__nv_bfloat16 *>(buf + sw128_off(2 * AT_QR + n, k)) = h2;
 }
 
-__global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmK,
+__global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV, AttTcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char *sK = base;                        // 2 stages x 32 KB
-  unsigned char *sV = sK + 2 * AT_KV;              // 2 stages x 32 KB
-  unsigned char *sQ = sV + 2 * AT_KV;              // 12 KB
+  unsigned char *sK = base;                        // AT_KSTAGES x 32 KB
+  unsigned char *sV = sK + AT_KSTAGES * AT_KV;     // AT_VSTAGES x 32 KB
+  unsigned char *sQ = sV + AT_VSTAGES * AT_KV;     // 12 KB
   unsigned char *sP = sQ + AT_OPND;                // 2 buffers x 12 KB
   // TMA <-> MMA: kfull/kempty/vfull/vempty; MMA <-> softmax warps: sfull/sfree,
   // pfull, ofull/ofree, qfull (per item).  Per-tile barriers alternate on
@@ -118,11 +125,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
     tc::mbar_init(&qfull, 4);
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
+  if (warp == 0) tc::tmem_alloc<128>(&tmem_base);   // S[b] at b*32, O[b] at 64 + b*32
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tmem = tmem_base;   // S[b] at b*64, O[b] at 128 + b*64
+  const uint32_t tmem = tmem_base;
   tc::grid_dep_wait();               // K/V rows appended by the previous kernel
 
   // ---------------------------------------------------------------- TMA producer (warp 4)
@@ -134,16 +141,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
         const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
         const int row0 = (a.layer * a.KVH + kh) * a.cap;
         for (int tile = lo; tile < hi; tile += AT_KT, ++g) {
-          const int s = g & 1;
-          const uint32_t ph = (g >> 1) & 1;
-          tc::mbar_wait(&kempty[s], ph ^ 1);
-          tc::mbar_expect_tx(&kfull[s], AT_KV);
-          tc::tma_load_2d(sK + s * AT_KV, &tmK, &kfull[s], 0, row0 + tile);
-          tc::tma_load_2d(sK + s * AT_KV + AT_HALF, &tmK, &kfull[s], 64, row0 + tile);
-          tc::mbar_wait(&vempty[s], ph ^ 1);
-          tc::mbar_expect_tx(&vfull[s], AT_KV);
-          tc::tma_load_2d(sV + s * AT_KV, &tmV, &vfull[s], 0, row0 + tile);
-          tc::tma_load_2d(sV + s * AT_KV + AT_HALF, &tmV, &vfull[s], 64, row0 + tile);
+          const int ks = g % AT_KSTAGES, vs = g % AT_VSTAGES;
+          const uint32_t kph = (g / AT_KSTAGES) & 1, vph = (g / AT_VSTAGES) & 1;
+          tc::mbar_wait(&kempty[ks], kph ^ 1);
+          tc::mbar_expect_tx(&kfull[ks], AT_KV);
+          tc::tma_load_2d(sK + ks * AT_KV, &tmK, &kfull[ks], 0, row0 + tile);
+          tc::tma_load_2d(sK + ks * AT_KV + AT_HALF, &tmK, &kfull[ks], 64, row0 + tile);
+          tc::mbar_wait(&vempty[vs], vph ^ 1);
+          tc::mbar_expect_tx(&vfull[vs], AT_KV);
+          tc::tma_load_2d(sV + vs * AT_KV, &tmV, &vfull[vs], 0, row0 + tile);
+          tc::tma_load_2d(sV + vs * AT_KV + AT_HALF, &tmV, &vfull[vs], 64, row0 + tile);
         }
       }
     }
@@ -156,35 +163,35 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
       constexpr uint32_t idS = tc::idesc_bf16(128, AT_N, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16(128, AT_N, 1, 0);
       auto issue_S = [&](uint32_t g) {
-        const int s = g & 1;
+        const int s = g & 1, ks = g % AT_KSTAGES;
         const uint32_t ph = (g >> 1) & 1;
-        tc::mbar_wait(&kfull[s], ph);
+        tc::mbar_wait(&kfull[ks], (g / AT_KSTAGES) & 1);
         tc::mbar_wait(&sfree[s], ph ^ 1);
         tc::fence_after();
 #pragma unroll
         for (int kk = 0; kk < AT_DH / 16; ++kk) {
-          const uint64_t da = tc::desc_k_sw128(sK + s * AT_KV + (kk >> 2) * AT_HALF) + 2 * (kk & 3);
+          const uint64_t da = tc::desc_k_sw128(sK + ks * AT_KV + (kk >> 2) * AT_HALF) + 2 * (kk & 3);
           const uint64_t db = tc::desc_k_sw128(sQ + (kk >> 2) * AT_QP) + 2 * (kk & 3);
-          tc::mma_bf16(tmem + s * 64, da, db, idS, kk != 0);
+          tc::mma_bf16(tmem + s * 32, da, db, idS, kk != 0);
         }
-        tc::mma_commit(&kempty[s]);
+        tc::mma_commit(&kempty[ks]);
         tc::mma_commit(&sfull[s]);
       };
       auto issue_PV = [&](uint32_t g) {
-        const int s = g & 1;
+        const int s = g & 1, vs = g % AT_VSTAGES;
         const uint32_t ph = (g >> 1) & 1;
         tc::mbar_wait(&pfull[s], ph);
-        tc::mbar_wait(&vfull[s], ph);
+        tc::mbar_wait(&vfull[vs], (g / AT_VSTAGES) & 1);
         tc::mbar_wait(&ofree[s], ph ^ 1);
         tc::fence_after();
 #pragma unroll
         for (int kk = 0; kk < AT_KT / 16; ++kk) {
           // A = V^T, MN-major: 64-dh blocks 16 KB apart (LBO), 8-key groups 1 KB apart (SBO)
-          const uint64_t da = tc::desc_mn_sw128(sV + s * AT_KV + kk * 2048, AT_HALF, 1024);
+          const uint64_t da = tc::desc_mn_sw128(sV + vs * AT_KV + kk * 2048, AT_HALF, 1024);
           const uint64_t db = tc::desc_k_sw128(sP + s * AT_OPND + (kk >> 2) * AT_QP) + 2 * (kk & 3);
-          tc::mma_bf16(tmem + 128 + s * 64, da, db, idO, kk != 0);
+          tc::mma_bf16(tmem + 64 + s * 32, da, db, idO, kk != 0);
         }
-        tc::mma_commit(&vempty[s]);
+        tc::mma_commit(&vempty[vs]);
         tc::mma_commit(&ofull[s]);
       };
       uint32_t g = 0, nitem = 0;
@@ -244,14 +251,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
         tc::mbar_wait(&sfull[s], ph);
         tc::fence_after();
         float sv[AT_N];
-        if (nrows <= 8) {
-          tc::tmem_ld8(tmem + s * 64 + tl + 0, sv + 0);
-          tc::tmem_ld8(tmem + s * 64 + tl + AT_QR, sv + AT_QR);
-          tc::tmem_ld8(tmem + s * 64 + tl + 2 * AT_QR, sv + 2 * AT_QR);
-        } else {
 #pragma unroll
-          for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + s * 64 + tl + c, sv + c);
-        }
+        for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + s * 32 + tl + c, sv + c);
         tc::tmem_ld_wait();
         tc::fence_before();
         __syncwarp();
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
         for (int r = 0; r < AT_QR; ++r) {
           if (r < nrows) {
             const bool vis = visible_tc(kp, qp_s[r], a);
-            x[r] = vis ? ((sv[r] + sv[AT_QR + r]) + sv[2 * AT_QR + r]) * a.scale : -INFINITY;
+            x[r] = vis ? ((sv[r] + sv[AT_QR + r]) + sv[2 * AT_QR + r]) * a.scale_log2 : -INFINITY;
             const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
             if (lane == 0) red[s][warp][r] = mx;
           }
@@ -277,8 +278,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
             const float m_new = fmaxf(m_run[r], o2f(mi));
             float p = 0.f;
             if (m_new != -INFINITY) {
-              p = (x[r] == -INFINITY) ? 0.f : expf(x[r] - m_new);
-              fac[r] = (m_run[r] == -INFINITY) ? 0.f : expf(m_run[r] - m_new);
+              p = (x[r] == -INFINITY) ? 0.f : ex2(x[r] - m_new);       // exp(s - m) in the log2 domain
+              fac[r] = (m_run[r] == -INFINITY) ? 0.f : ex2(m_run[r] - m_new);
             }
             m_run[r] = m_new;
             l_run[r] = l_run[r] * fac[r] + p;   // per-thread partial; reduced once per item
@@ -294,14 +295,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
           tc::mbar_wait(&ofull[sp], (gp >> 1) & 1);
           tc::fence_after();
           float ov[AT_N];
-          if (nrows <= 8) {
-            tc::tmem_ld8(tmem + 128 + sp * 64 + tl + 0, ov + 0);
-            tc::tmem_ld8(tmem + 128 + sp * 64 + tl + AT_QR, ov + AT_QR);
-            tc::tmem_ld8(tmem + 128 + sp * 64 + tl + 2 * AT_QR, ov + 2 * AT_QR);
-          } else {
 #pragma unroll
-            for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 128 + sp * 64 + tl + c, ov + c);
-          }
+          for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 64 + sp * 32 + tl + c, ov + c);
           tc::tmem_ld_wait();
           tc::fence_before();
           __syncwarp();
@@ -319,7 +314,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
         tc::fence_after();
         float ov[AT_N];
 #pragma unroll
-        for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 128 + sp * 64 + tl + c, ov + c);
+        for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 64 + sp * 32 + tl + c, ov + c);
         tc::tmem_ld_wait();
         tc::fence_before();
         __syncwarp();
@@ -349,7 +344,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
         const size_t row = (size_t)i * a.H + head;
         a.part_o[(pbase + row) * AT_DH + tid] = o_acc[r];
         if (tid == 0) {
-          a.part_m[pbase + row] = m_run[r];
+          a.part_m[pbase + row] = m_run[r] * 0.69314718055994530942f;   // back to natural-log units
           a.part_l[pbase + row] = (redl[0][r] + redl[1][r]) + (redl[2][r] + redl[3][r]);
         }
       }
@@ -358,7 +353,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_tc_kernel(const __grid_con
   }
   tc::fence_before();
   named_sync();
-  if (warp == 0) tc::tmem_dealloc<256>(tmem);
+  if (warp == 0) tc::tmem_dealloc<128>(tmem);
 }
 
 }  // namespace
@@ -379,7 +374,7 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
   a.win_lo = st->win_lo; a.n_sink = st->n_sink; a.split = st->split; a.n_splits = n_splits;
   a.n_qb = ceil_div(a.g * t, AT_QR);
   a.n_items = n_splits * a.KVH * a.n_qb;
-  a.scale = (float)(1.0 / sqrt((double)AT_DH));
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)AT_DH));
   a.part_m = part_m; a.part_l = part_l; a.part_o = part_o;
   static bool attr = false;
   if (!attr) {
@@ -388,7 +383,7 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
   }
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int grid = a.n_items < sms ? a.n_items : sms;
+  const int grid = a.n_items < 2 * sms ? a.n_items : 2 * sms;
   attn_tc_kernel<<<grid, AT_THREADS, AT_SMEM, stream>>>(mk, mv, a);
   return check_launch("attention_tc");
 }
