@@ -43,6 +43,7 @@ DRAFT_68M = dict(n_layers=2, n_heads=12, n_kv_heads=12, head_dim=64, d_ff=3072, 
 CONTEXT = 122880
 BUDGET, CHUNK, SINK, STREAM = 4096, 8, 4, 256
 GAMMA1, GAMMA2 = 2, 4
+EASY_FRAC, PLANT_SEED = 0.92, 77
 
 
 def parse():
@@ -54,6 +55,8 @@ def parse():
     ap.add_argument("--gen", type=int, default=32, help="tokens committed per step")
     ap.add_argument("--context", type=int, default=CONTEXT)
     ap.add_argument("--temperature", type=float, default=0.0)
+    ap.add_argument("--easy-frac", type=float, default=EASY_FRAC,
+                    help="planted successor channel (model.plant_successor); 0 = pure random init")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no extras)")
     return ap.parse_args()
@@ -123,7 +126,20 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # CPU oracle sample (cpu_baseline and the reference arm)
 
-def oracle_sample(context: int, temperature: float, rounds: int, time_budget_s: float = 150.0):
+def plant_host(tensors: dict, d: int, V: int, seed: int, easy_frac: float, emb_scale=4.0, margin=12.0):
+    """numpy twin of paper_2404_11912_b200.model.plant_successor for the CPU
+    arm (kept here so the reference arm never loads the CUDA package)."""
+    rng = np.random.default_rng(seed)
+    succ = rng.permutation(V)
+    easy = np.nonzero(rng.random(V) < easy_frac)[0]
+    u = rng.integers(0, 2, (easy.size, d)).astype(np.float32) * 2.0 - 1.0
+    tensors["embedding"][easy] += np.float32(emb_scale) * u
+    tensors["lm_head"][:, succ[easy]] += np.float32(margin / d) * u.T
+    return tensors
+
+
+def oracle_sample(context: int, temperature: float, rounds: int, time_budget_s: float = 150.0,
+                  easy_frac: float = EASY_FRAC):
     """TriForce on the CPU oracle (oracle/hs_oracle.py, a restatement of the
     reference numpy engine): a 1-layer slice of the Llama2-7B shape over the
     full synthetic context plus the full 2-layer draft, run for whole outer
@@ -133,8 +149,13 @@ def oracle_sample(context: int, temperature: float, rounds: int, time_budget_s: 
     from oracle import hs_oracle as O
     tcfg = O.OConfig(**{**TARGET_7B, "n_layers": 1})
     dcfg = O.OConfig(**DRAFT_68M)
-    tgt = O.OModel(tcfg, O.make_tensors(tcfg, 1, tied_head=False), tied_head=False)
-    drf = O.OModel(dcfg, O.make_tensors(dcfg, 2, tied_head=False), tied_head=False)
+    tt = O.make_tensors(tcfg, 1, tied_head=False)
+    dt = O.make_tensors(dcfg, 2, tied_head=False)
+    if easy_frac > 0:
+        plant_host(tt, tcfg.d_model, tcfg.vocab_size, PLANT_SEED, easy_frac)
+        plant_host(dt, dcfg.d_model, dcfg.vocab_size, PLANT_SEED, easy_frac)
+    tgt = O.OModel(tcfg, tt, tied_head=False)
+    drf = O.OModel(dcfg, dt, tied_head=False)
     ctx = np.random.default_rng(0).integers(1, 32000, context).tolist()
     spec = O.OSpec(target_len=context + 10 ** 6, gamma1=GAMMA1, gamma2=GAMMA2, temperature=temperature, seed=0,
                    n_sink=SINK, stream_budget=STREAM, chunk=CHUNK, retr_budget=BUDGET)
@@ -187,7 +208,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=max(1, args.steps))
+    rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=max(1, args.steps),
+                                       easy_frac=args.easy_frac)
     val = statistics.median(rates)
     out = {"metric": "decode tokens/s (TriForce, Llama2-7B-128K shape @122,880 ctx)", "value": val,
            "unit": "tokens/s", "n_gpus": 0, "steps": len(rates), "warmup": 0, "ms_per_step": 1000.0 / val,
@@ -204,6 +226,9 @@ def workload_config(args):
             "context": args.context, "retrieval_budget": BUDGET, "chunk": CHUNK, "stream_sink": SINK,
             "stream_budget": STREAM, "gamma1": GAMMA1, "gamma2": GAMMA2, "temperature": args.temperature,
             "tokens_per_step": args.gen, "l2": "inputs larger than L2 (64 GB KV/GPU), no flush",
+            "weights": ("random-init N(0,0.02) bf16 + planted successor channel, easy_frac "
+                        f"{args.easy_frac} (model.plant_successor; acceptance near the paper's 0.92)"
+                        if args.easy_frac > 0 else "pure random-init N(0,0.02) bf16 (acceptance ~0)"),
             "parallelism": f"replicas x{args.gpus}"}
 
 
@@ -229,8 +254,11 @@ def main():
     from paper_2404_11912_b200._abi import lib
 
     tcfg, dcfg = P.ModelConfig(**TARGET_7B), P.ModelConfig(**DRAFT_68M)
-    target = P.ModelWeights.on_device(P.DeviceModel.random(tcfg, seed=1 + rank))
-    draft = P.ModelWeights.on_device(P.DeviceModel.random(dcfg, seed=1001 + rank))
+    tdm, ddm = P.DeviceModel.random(tcfg, seed=1 + rank), P.DeviceModel.random(dcfg, seed=1001 + rank)
+    if args.easy_frac > 0:
+        tdm.plant_successor_(PLANT_SEED, args.easy_frac)
+        ddm.plant_successor_(PLANT_SEED, args.easy_frac)
+    target, draft = P.ModelWeights.on_device(tdm), P.ModelWeights.on_device(ddm)
     ctx = np.random.default_rng(rank).integers(1, 32000, args.context).tolist()
     spec = P.SpecConfig(target_len=args.context + 1, gamma1=GAMMA1, gamma2=GAMMA2, temperature=args.temperature,
                         seed=rank, streaming=P.StreamingConfig(n_sink=SINK, budget=STREAM),
@@ -306,7 +334,8 @@ def main():
                               "rebuilds": stats.get("rebuilds", 0)},
                **extra}
         if world == 1 and not args.no_cpu_baseline:
-            rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=1, time_budget_s=60)
+            rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=1, time_budget_s=60,
+                                               easy_frac=args.easy_frac)
             out["cpu_baseline"] = {"value": statistics.median(rates), "unit": "tokens/s", "cores": cores,
                                    "kind": "port", "sample": desc}
         print(json.dumps(out), flush=True)

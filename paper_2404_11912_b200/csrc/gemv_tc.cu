@@ -94,35 +94,50 @@ __device__ __forceinline__ void split3(float h, uint16_t &a, uint16_t &b, uint16
   c = f_to_bf16(r2);
 }
 
-// grid: TC_T blocks (row r); rows >= t are written as zeros
-__global__ void __launch_bounds__(256) split_rows_kernel(const float *x, int ldx, int t, int K, int ldk,
-                                                         const float *gain, float eps, uint16_t *xs) {
+// grid (column blocks of SPLIT_COLS, TC_T rows); rows >= t are written as zeros.
+// With a gain, every CTA of a row recomputes the row's sum of squares over
+// the whole row (16-byte loads, all in flight at once, fixed reduction order:
+// identical in every CTA and independent of t), so the RMSNorm needs no
+// second pass and the kernel is one memory round trip deep.
+constexpr int SPLIT_THREADS = 256;
+constexpr int SPLIT_COLS = 1024;
+
+__global__ void __launch_bounds__(SPLIT_THREADS) split_rows_kernel(const float *x, int ldx, int t, int K, int ldk,
+                                                                   const float *gain, float eps, uint16_t *xs) {
   tc::grid_dep_launch();
-  const int r = blockIdx.x;
-  __shared__ double red[8];
-  __shared__ double scale_s;
+  tc::grid_dep_wait();
+  const int r = blockIdx.y;
+  __shared__ double red[SPLIT_THREADS / 32];
   double scale = 1.0;
+  const float *xr = x + (size_t)r * ldx;
   if (gain != nullptr && r < t) {
     double ss = 0.0;
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-      const double v = (double)x[(size_t)r * ldx + k];
-      ss += v * v;
+    if ((K & 3) == 0 && (ldx & 3) == 0 && ((uintptr_t)x & 15) == 0) {
+      const float4 *x4 = reinterpret_cast<const float4 *>(xr);
+#pragma unroll 4
+      for (int k = threadIdx.x; k < K / 4; k += SPLIT_THREADS) {
+        const float4 v = x4[k];
+        ss += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+      }
+    } else {
+      for (int k = threadIdx.x; k < K; k += SPLIT_THREADS) ss += (double)xr[k] * xr[k];
     }
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int w = 0; w < 8; ++w) tot += red[w];
-      scale_s = sqrt(tot / (double)K + (double)eps);   // rms_norm, model.py:282-284
-    }
-    __syncthreads();
-    scale = scale_s;
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < SPLIT_THREADS / 32; ++w) tot += red[w];
+    scale = sqrt(tot / (double)K + (double)eps);   // rms_norm, model.py:282-284
   }
-  for (int k = threadIdx.x; k < ldk; k += blockDim.x) {
+  const int c0 = blockIdx.x * SPLIT_COLS;
+#pragma unroll
+  for (int j = 0; j < SPLIT_COLS / SPLIT_THREADS; ++j) {
+    const int k = c0 + j * SPLIT_THREADS + threadIdx.x;
+    if (k >= ldk) break;
     float h = 0.f;
     if (r < t && k < K) {
-      const float v = x[(size_t)r * ldx + k];
+      const float v = xr[k];
       h = gain ? (float)(((double)v / scale) * (double)gain[k]) : v;
     }
     uint16_t a, b, c;
@@ -329,7 +344,17 @@ size_t gemv_tc_ws_bytes(int N, int nkb) {
 int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const float *gain, float eps, uint16_t *xs,
                       cudaStream_t st) {
   HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "split_rows: t=%d outside [1,%d]", t, TC_T);
-  split_rows_kernel<<<TC_T, 256, 0, st>>>(x, ldx, t, K, ldk, gain, eps, xs);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((ldk + SPLIT_COLS - 1) / SPLIT_COLS, TC_T, 1);
+  cfg.blockDim = dim3(SPLIT_THREADS, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, split_rows_kernel, x, ldx, t, K, ldk, gain, eps, xs);
+  if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "split_rows launch: %s", cudaGetErrorString(e));
   return check_launch("split_rows");
 }
 

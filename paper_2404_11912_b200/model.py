@@ -178,6 +178,29 @@ class DeviceModel:
         self._finish()
         return self
 
+    def plant_successor_(self, seed: int, easy_frac: float, emb_scale: float = 4.0, margin: float = 12.0):
+        """Device-side `plant_successor` (same construction, torch RNG): for
+        the easy tokens t, emb[t] += emb_scale * u_t and head[succ(t)] +=
+        (margin / d) * u_t with u_t a random +-1 vector.  See plant_successor."""
+        cfg = self.config
+        V, d = cfg.vocab_size, cfg.d_model
+        head_scale = margin / d
+        dev = self.emb.device
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        succ = torch.randperm(V, generator=gen, device=dev)
+        easy = torch.rand(V, generator=gen, device=dev) < easy_frac
+        idx = torch.nonzero(easy).flatten()
+        for a in range(0, idx.numel(), 4096):
+            rows = idx[a:a + 4096]
+            u = torch.randint(0, 2, (rows.numel(), d), generator=gen, device=dev).float() * 2.0 - 1.0
+            self.emb[rows, :d] = (self.emb[rows, :d].float() + emb_scale * u).to(torch.bfloat16)
+            hr = succ[rows]
+            self.head[hr, :d] = (self.head[hr, :d].float() + head_scale * u).to(torch.bfloat16)
+        self.planted = {"kind": "successor", "easy_frac": easy_frac, "seed": seed, "emb_scale": emb_scale,
+                        "margin": margin}
+        return self
+
     def _finish(self):
         cfg = self.config
         cos, sin = rope_tables(cfg.max_seq, cfg.head_dim, cfg.rope_theta)
@@ -270,6 +293,43 @@ def generate_weights(config: ModelConfig, seed: int, tied_head: bool = True) -> 
         draw = rng.standard_normal(shape) * 0.02
         tensors[name] = (1.0 + draw if "norm" in name else draw).astype(np.float32)
     return ModelWeights(config, tensors, tied_head).validate()
+
+
+def plant_successor(weights: ModelWeights, seed: int, easy_frac: float, emb_scale: float = 4.0,
+                    margin: float = 12.0) -> ModelWeights:
+    """Random-init weights plus a planted next-token channel (benchmark
+    workloads; same idea as the reference's planted_attention_weights,
+    analytics.py:109-186).
+
+    Independent random-init target and draft models never agree on a greedy
+    token, so every speculation is rejected (acceptance 0) and any
+    speculative decoder degenerates to several forwards per token.  Real
+    long-context pairs accept ~92%.  The plant: a random
+    permutation `succ` of the vocabulary and, for a random `easy_frac` subset
+    of tokens t, a +-1 direction u_t added to emb[t] (x emb_scale) and to the
+    lm_head column of succ(t) (x margin / d_model, so the planted logit
+    lead is ~`margin` at any width).  After an easy token every
+    model -- whatever its other weights -- puts its argmax on succ(t); after a
+    hard token the argmax is decided by the model's own random weights and
+    attention, so two different models (or the retrieval and full views of
+    one model) disagree.  Acceptance therefore tracks `easy_frac` while every
+    forward still runs the full architecture.  Needs an untied head."""
+    if weights.tied_head:
+        raise ValueError("plant_successor needs an untied lm_head")
+    if not 0.0 <= easy_frac <= 1.0:
+        raise ValueError("easy_frac must be in [0, 1]")
+    cfg = weights.config
+    V, d = cfg.vocab_size, cfg.d_model
+    rng = np.random.default_rng(seed)
+    succ = rng.permutation(V)
+    easy = np.nonzero(rng.random(V) < easy_frac)[0]
+    u = rng.integers(0, 2, (easy.size, d)).astype(np.float32) * 2.0 - 1.0
+    emb = weights.tensors["embedding"]
+    head = weights.tensors["lm_head"]
+    emb[easy] += np.float32(emb_scale) * u
+    head[:, succ[easy]] += np.float32(margin / d) * u.T
+    weights.invalidate()
+    return weights.validate()
 
 
 # ---------------------------------------------------------------------------

@@ -512,6 +512,11 @@ class HierarchicalSession:
                 trace.add(base + i, tok, level, olabels[i] == "accepted", trace.outer.rounds)
             self.committed.extend(emitted)
             valid = base + min(accepted, len(emitted))
+            if valid == len(self.committed):
+                # truncated final round: the reference ends the session here with
+                # lanes that hold every token but no frontier row; keep the last
+                # token unprocessed instead so a later generate() can catch up
+                valid -= 1
             self.full_lane.rollback_to(valid)
             self.full_lane.commit()
             for lane in (self.draft_lane, self.retr_lane):

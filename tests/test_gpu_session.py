@@ -380,3 +380,50 @@ def test_sampled_acceptance_rates(P):
         o += [otr.inner[1], otr.inner[0], otr.outer[1], otr.outer[0]]
     assert abs(g[0] / g[1] - o[0] / o[1]) <= 0.01, (g, o)
     assert abs(g[2] / g[3] - o[2] / o[3]) <= 0.01, (g, o)
+
+
+def test_planted_greedy_stream_and_acceptance_match_oracle(P):
+    """Non-degenerate acceptance (random-init greedy is vacuous):
+    models with a planted successor channel accept most speculations, and the
+    GPU loop's greedy stream and per-level accept counts equal the oracle's
+    exactly, rebuilds included."""
+    from oracle import hs_oracle as O
+    mk = lambda w: O.OModel(O.OConfig(**{k: getattr(w.config, k) for k in w.config.__dataclass_fields__}),
+                            O.round_weights_bf16(w.tensors), w.tied_head)
+    tc = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=64, d_ff=344, vocab_size=512, max_seq=2048)
+    dc = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=64, d_ff=172, vocab_size=512, max_seq=2048)
+    tw = bf16_weights(P, P.plant_successor(P.generate_weights(tc, 5, tied_head=False), 9, 0.9))
+    dw = bf16_weights(P, P.plant_successor(P.generate_weights(dc, 6, tied_head=False), 9, 0.9))
+    prompt = np.random.default_rng(3).integers(1, 512, 1200).tolist()
+    spec = P.SpecConfig(target_len=1200 + 96, gamma1=2, gamma2=4, temperature=0.0, seed=0,
+                        streaming=P.StreamingConfig(n_sink=4, budget=128),
+                        retrieval=P.RetrievalConfig(chunk_size=8, budget=128, rebuild_stride=32))
+    out, tr = P.HierarchicalSession(tw, dw, prompt, spec).generate()
+    os_ = O.OSession(mk(tw), mk(dw), prompt, O.OSpec(target_len=1200 + 96, gamma1=2, gamma2=4, temperature=0.0,
+                     seed=0, n_sink=4, stream_budget=128, chunk=8, retr_budget=128, rebuild_stride=32),
+                     kv_bf16=True)
+    oout, otr = os_.generate()
+    assert out == oout
+    assert [tr.inner.proposed, tr.inner.accepted] == otr.inner[:2]
+    assert [tr.outer.proposed, tr.outer.accepted] == otr.outer[:2]
+    assert tr.outer.rate > 0.6 and tr.inner.rate > 0.6, tr.summary()
+
+
+def test_generate_continues_after_truncated_round(P):
+    """bench.py extends target_len and calls generate() again; the lanes must
+    stay resumable after a truncated final round and the greedy stream must
+    still be the autoregressive one."""
+    tc = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=64, d_ff=344, vocab_size=512, max_seq=1024)
+    dc = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=64, d_ff=172, vocab_size=512, max_seq=1024)
+    tw = P.plant_successor(P.generate_weights(tc, 5, tied_head=False), 9, 0.95)
+    dw = P.plant_successor(P.generate_weights(dc, 6, tied_head=False), 9, 0.95)
+    prompt = np.random.default_rng(4).integers(1, 512, 300).tolist()
+    spec = P.SpecConfig(target_len=301, gamma1=2, gamma2=4, temperature=0.0, seed=0,
+                        streaming=P.StreamingConfig(n_sink=4, budget=64),
+                        retrieval=P.RetrievalConfig(chunk_size=8, budget=64, rebuild_stride=16))
+    s = P.HierarchicalSession(tw, dw, prompt, spec)
+    for n in (301, 303, 310, 311, 340):
+        s.config.target_len = n
+        out, _ = s.generate()
+        assert len(out) == n
+    assert out == P.autoregressive_generate(tw, prompt, 340, 0.0, 0)
