@@ -126,7 +126,7 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # CPU oracle sample (cpu_baseline and the reference arm)
 
-def plant_host(tensors: dict, d: int, V: int, seed: int, easy_frac: float, emb_scale=4.0, margin=12.0):
+def plant_host(tensors: dict, d: int, V: int, seed: int, easy_frac: float, emb_scale=32.0, margin=24.0):
     """numpy twin of paper_2404_11912_b200.model.plant_successor for the CPU
     arm (kept here so the reference arm never loads the CUDA package)."""
     rng = np.random.default_rng(seed)

@@ -178,7 +178,7 @@ class DeviceModel:
         self._finish()
         return self
 
-    def plant_successor_(self, seed: int, easy_frac: float, emb_scale: float = 4.0, margin: float = 12.0):
+    def plant_successor_(self, seed: int, easy_frac: float, emb_scale: float = 32.0, margin: float = 24.0):
         """Device-side `plant_successor` (same construction, torch RNG): for
         the easy tokens t, emb[t] += emb_scale * u_t and head[succ(t)] +=
         (margin / d) * u_t with u_t a random +-1 vector.  See plant_successor."""
@@ -295,8 +295,8 @@ def generate_weights(config: ModelConfig, seed: int, tied_head: bool = True) -> 
     return ModelWeights(config, tensors, tied_head).validate()
 
 
-def plant_successor(weights: ModelWeights, seed: int, easy_frac: float, emb_scale: float = 4.0,
-                    margin: float = 12.0) -> ModelWeights:
+def plant_successor(weights: ModelWeights, seed: int, easy_frac: float, emb_scale: float = 32.0,
+                    margin: float = 24.0) -> ModelWeights:
     """Random-init weights plus a planted next-token channel (benchmark
     workloads; same idea as the reference's planted_attention_weights,
     analytics.py:109-186).
