@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define HS_ABI_VERSION 1
+#define HS_ABI_VERSION 2
 
 /* ---- status codes (errors.py) ----------------------------------------- */
 #define HS_OK            0
@@ -107,7 +107,31 @@ typedef struct {
   int window;
   int win_lo;
   int split;         /* keys per attention split (fixed => t-invariant)    */
+  int pos_base;      /* LINEAR caches: absolute position of slot 0 (start of
+                        this rank's sequence shard; 0 when unsharded)       */
+  int own_hi;        /* HS_APPEND_POS: rows at positions < pos_base or >=
+                        own_hi are not stored on this rank (0 = no bound)   */
 } HsStep;
+
+/* ---- sequence sharding of the full cache -----------------
+ * Rank r stores the full-cache positions [pos_base, own_hi); every rank runs
+ * the same forward, attends over its own slots, and the per-rank partial
+ * softmax states (m, l, unnormalised o) of every query row are all-gathered
+ * over NCCL and merged in rank order, so all ranks hold bit-identical
+ * attention outputs.  comm is an ncclComm_t made by hs_comm_init.          */
+typedef struct {
+  void *comm;
+  int rank, world;
+} HsShard;
+
+size_t hs_comm_id_bytes(void);
+int hs_comm_unique_id(void *id);                       /* rank 0; ship id to the others */
+int hs_comm_init(void **comm, const void *id, int world, int rank);
+int hs_comm_destroy(void *comm);
+/* recv [world][bytes] <- every rank's send [bytes], rank order            */
+int hs_all_gather(void *comm, const void *send, void *recv, size_t bytes, void *stream);
+/* in-place sum; dtype 0 bf16, 1 f32, 2 f64, 3 i32                          */
+int hs_all_reduce_sum(void *comm, void *buf, size_t count, int dtype, void *stream);
 
 /* ---- fused forward (model.py:247-331) -----------------------------------
  * t tokens (device int32) at st->pos0 through all layers: RMSNorm+QKV GEMV,
@@ -117,10 +141,13 @@ typedef struct {
  * ([L][H][dh], the ForwardRecorder.last_queries of model.py:309).
  * Row results are independent of t (bitwise), so a batched verify equals a
  * sequence of decode steps (model.py:366-378 contract).                     */
-size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view, int split);
+size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view, int split, int world);
 /* leading bytes of the forward workspace that must be zero before first use */
 size_t hs_forward_workspace_clean_bytes(const HsModel *m);
-int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st,
+/* sh == NULL: unsharded.  Otherwise c is this rank's shard of a FULL cache
+ * (kind LINEAR, st->pos_base / st->own_hi set) and attention is merged
+ * across sh->world ranks per layer.                                          */
+int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                const int32_t *tokens, int t, float *logits, float *q_stash,
                void *workspace, size_t workspace_bytes, void *stream);
 
@@ -170,6 +197,12 @@ size_t hs_attention_workspace_bytes(int t, int n_heads, int head_dim, int n_view
 int hs_attention(const HsCache *c, int layer, const HsStep *st, int n_heads,
                  const float *q, int t, float *out, void *workspace, size_t ws_bytes,
                  void *stream);
+/* same, but writes this view's partial softmax state per query row instead
+ * of the normalised output: packed [t*H][2 + dh] = (m, l, o[dh]) with o
+ * unnormalised and m = -inf, l = 0 for rows that see no key (shard input). */
+int hs_attention_partial(const HsCache *c, int layer, const HsStep *st, int n_heads,
+                         const float *q, int t, float *packed, void *workspace, size_t ws_bytes,
+                         void *stream);
 
 /* chunk scoring, score_chunks (caches.py:414-436), all layers at once.
  * keys: layer l, kv head h, token i at  keys + l*ls + h*hs + i*ts  (bf16 if
@@ -189,9 +222,13 @@ int hs_chunk_select(const double *scores, int n_layers, int n_chunks, int upto, 
                     int32_t *out_counts, void *workspace, size_t ws_bytes, void *stream);
 
 /* gather of the chosen chunks into the retrieval cache slots, position order
- * (st.push(K[sel_idx], ...) caches.py:490-493).  src is a LINEAR cache.     */
+ * (st.push(K[sel_idx], ...) caches.py:490-493).  src is a LINEAR cache
+ * holding positions [src_lo, src_hi) (a sequence shard; 0, 0 = unsharded);
+ * chunks outside it are written as zeros (a sum all-reduce then assembles
+ * the selection across shards).                                             */
 int hs_retrieval_gather(const HsCache *src, const HsCache *dst, const int32_t *chosen,
-                        int chosen_stride, int n_chosen, int chunk, int upto, void *stream);
+                        int chosen_stride, int n_chosen, int chunk, int upto, int src_lo, int src_hi,
+                        void *stream);
 
 /* RetrievalCache.commit / _overwrite (caches.py:529-555) for all layers:
  * spec slots [n_sel, n_sel+n_spec) -- the first `take` move into the victim
@@ -234,10 +271,9 @@ int hs_correct_token(const double *q, const double *p, int V, const double *unif
                      int32_t *cursor, int32_t *out, void *stream);
 
 /* ---- sequence sharding ----------------------------------
- * merge per-shard partial softmax states in rank order:
- * parts: [G][rows] (m, l) fp32 and [G][rows][dh] o fp32 (unnormalised).     */
-int hs_shard_merge(const float *m, const float *l, const float *o, int n_shards, int rows,
-                   int head_dim, float *out, void *stream);
+ * merge per-shard packed partial states [G][rows][2 + dh] in rank order:
+ * M = max m_s, out = sum_s e^{m_s-M} o_s / sum_s e^{m_s-M} l_s.            */
+int hs_shard_merge(const float *parts, int n_shards, int rows, int head_dim, float *out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -53,7 +53,12 @@ class HsCache(C.Structure):
 
 class HsStep(C.Structure):
     _fields_ = [("pos0", i32), ("append_mode", i32), ("append_base", i32), ("n_sink", i32), ("ring", i32),
-                ("n_view", i32), ("window", i32), ("win_lo", i32), ("split", i32)]
+                ("n_view", i32), ("window", i32), ("win_lo", i32), ("split", i32), ("pos_base", i32),
+                ("own_hi", i32)]
+
+
+class HsShard(C.Structure):
+    _fields_ = [("comm", vp), ("rank", i32), ("world", i32)]
 
 
 _P = C.POINTER
@@ -62,22 +67,23 @@ _SIGS = {
     "hs_abi_version": (i32, []),
     "hs_device_sm_count": (i32, [i32]),
     "hs_launch_count": (C.c_ulonglong, []),
-    "hs_forward_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32]),
+    "hs_forward_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32, i32]),
     "hs_forward_workspace_clean_bytes": (sz, [_P(HsModel)]),
     "hs_gemv_tc_workspace_bytes": (sz, [i32, i32]),
     "hs_gemv_tc": (i32, [vp, i32, vp, i32, i32, i32, vp, i32, vp, i32, vp, sz, vp]),
     "hs_split_rows": (i32, [vp, i32, i32, i32, i32, vp, f32, vp, vp]),
-    "hs_forward": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), vp, i32, vp, vp, vp, sz, vp]),
+    "hs_forward": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), _P(HsShard), vp, i32, vp, vp, vp, sz, vp]),
     "hs_gemv": (i32, [vp, i32, i32, i32, vp, i32, i32, i32, vp, f32, i32, vp, i32, vp]),
     "hs_embed": (i32, [vp, i32, i32, vp, i32, vp, vp]),
     "hs_rope_append": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), i32, vp, i32, vp, vp, vp]),
     "hs_kv_write": (i32, [_P(HsCache), i32, vp, vp, i32, vp, vp, vp]),
     "hs_attention_workspace_bytes": (sz, [i32, i32, i32, i32, i32]),
     "hs_attention": (i32, [_P(HsCache), i32, _P(HsStep), i32, vp, i32, vp, vp, sz, vp]),
+    "hs_attention_partial": (i32, [_P(HsCache), i32, _P(HsStep), i32, vp, i32, vp, vp, sz, vp]),
     "hs_chunk_score": (i32, [vp, i32, i64, i64, i64, i32, i32, i32, i32, i32, vp, i32, vp, vp]),
     "hs_chunk_select_workspace_bytes": (sz, [i32, i32]),
     "hs_chunk_select": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]),
-    "hs_retrieval_gather": (i32, [_P(HsCache), _P(HsCache), vp, i32, i32, i32, i32, vp]),
+    "hs_retrieval_gather": (i32, [_P(HsCache), _P(HsCache), vp, i32, i32, i32, i32, i32, i32, vp]),
     "hs_retrieval_commit": (i32, [_P(HsCache), vp, i32, i32, i32, i32, i32, vp]),
     "hs_cache_copy": (i32, [_P(HsCache), _P(HsCache), i32, vp]),
     "hs_probs": (i32, [vp, i32, i32, f64, vp, vp]),
@@ -86,7 +92,13 @@ _SIGS = {
     "hs_verify_chain": (i32, [vp, i32, vp, vp, i32, vp, vp, vp, vp]),
     "hs_verify_token": (i32, [i32, vp, vp, vp, vp, vp, vp]),
     "hs_correct_token": (i32, [vp, vp, i32, vp, vp, vp, vp]),
-    "hs_shard_merge": (i32, [vp, vp, vp, i32, i32, i32, vp, vp]),
+    "hs_shard_merge": (i32, [vp, i32, i32, i32, vp, vp]),
+    "hs_comm_id_bytes": (sz, []),
+    "hs_comm_unique_id": (i32, [vp]),
+    "hs_comm_init": (i32, [_P(vp), vp, i32, i32]),
+    "hs_comm_destroy": (i32, [vp]),
+    "hs_all_gather": (i32, [vp, vp, vp, sz, vp]),
+    "hs_all_reduce_sum": (i32, [vp, vp, sz, i32, vp]),
 }
 
 
@@ -100,7 +112,7 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.hs_abi_version() != 1:
+    if lib.hs_abi_version() != 2:
         raise ImportError("libhs_b200.so ABI version mismatch")
     return lib
 

@@ -22,6 +22,20 @@ LIB = os.path.join(HERE, "libhs_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_root() -> str:
+    """NCCL 2.28 shipped with torch (nvidia-nccl wheel); /usr/include has 2.27."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        root = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(root, "include", "nccl.h")):
+            return root
+    raise RuntimeError("nccl.h not found (expected the nvidia-nccl wheel next to torch)")
+
+
+NCCL = _nccl_root()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xptxas", "-O3"]
 
@@ -47,11 +61,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     extra = ["-Xptxas", "-v"] if verbose else []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(NCCL, "include"),
+               "-c", src, "-o", obj]
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
+    nccl_lib = os.path.join(NCCL, "lib")
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-L", nccl_lib, "-l:libnccl.so.2",
+                    "-Xlinker", "-rpath," + nccl_lib], check=True)
     os.replace(tmp, LIB)
     return LIB
 

@@ -153,19 +153,49 @@ class KVCache:
 
 
 class FullCache(KVCache):
-    """Keeps every position (caches.py:176-221); capacity = max_entries."""
+    """Keeps every position (caches.py:176-221); capacity = max_entries.
+
+    Sequence-sharded form (`FullCache.shard`): this rank
+    stores positions [lo, hi) (hi None = the tail, up to max_entries) in
+    slots 0.. ; frontier / committed stay global and every forward merges
+    the per-rank attention states over NCCL (shard.py)."""
 
     policy = "full"
     kind = HS_KV_LINEAR
 
-    def __init__(self, n_layers: int, n_kv_heads: int, head_dim: int, max_entries: int):
-        super().__init__(n_layers, n_kv_heads, head_dim, max_entries, with_pos=False)
+    def __init__(self, n_layers: int, n_kv_heads: int, head_dim: int, max_entries: int,
+                 shards=None, lo: int = 0, hi: Optional[int] = None):
+        if lo < 0 or (hi is not None and not lo < hi <= max_entries) or lo >= max_entries:
+            raise ValueError(f"bad shard range [{lo}, {hi}) for max_entries {max_entries}")
+        local = (hi if hi is not None else max_entries) - lo
+        super().__init__(n_layers, n_kv_heads, head_dim, local, with_pos=False)
         self.max_entries = max_entries
+        self.shards, self.lo, self.hi = shards, lo, hi
+        self.bounds = [(lo, hi)]
         self._n = [0] * n_layers
 
     @classmethod
     def from_config(cls, model_config):
         return cls(model_config.n_layers, model_config.n_kv_heads, model_config.head_dim, model_config.max_seq)
+
+    @classmethod
+    def shard(cls, model_config, shards, n_context: int, chunk: int):
+        """This rank's shard of a full cache whose first n_context positions
+        are split by shard.shard_plan (chunk-aligned)."""
+        plan = shards.plan(n_context, chunk)
+        lo, hi = plan[shards.rank]
+        c = cls(model_config.n_layers, model_config.n_kv_heads, model_config.head_dim, model_config.max_seq,
+                shards, lo, hi)
+        c.bounds = plan
+        return c
+
+    @property
+    def sharded(self) -> bool:
+        return self.shards is not None
+
+    def _local(self, n: int) -> int:
+        """slots of this rank holding positions < n"""
+        return max(0, min(n - self.lo, self.cap))
 
     def append(self, layer, k, v):
         self._check_kv(k, v)
@@ -173,15 +203,21 @@ class FullCache(KVCache):
         n = self._n[layer]
         if n + t > self.max_entries:
             raise CapacityError(f"full cache overflow past {self.max_entries}")
-        self._write_rows(layer, k, v, np.arange(n, n + t), np.arange(n, n + t))
+        pos = np.arange(n, n + t)
+        keep = (pos >= self.lo) & (pos < self.lo + self.cap)
+        if keep.any():
+            kd, vd = as_device_f32(k), as_device_f32(v)
+            idx = torch.as_tensor(np.nonzero(keep)[0], device=kd.device)
+            self._write_rows(layer, kd.index_select(0, idx), vd.index_select(0, idx), pos[keep] - self.lo, pos[keep])
         self._n[layer] = n + t
         if layer == self.n_layers - 1:
             self.frontier = n + t
 
     def expose(self, layer, queries=None):
-        n = self._n[layer]
-        K, V = self._gather_host(layer, np.arange(n))
-        return K, V, np.arange(n, dtype=np.int64), None
+        """This rank's positions (all of them when unsharded)."""
+        m = self._local(self._n[layer])
+        K, V = self._gather_host(layer, np.arange(m))
+        return K, V, np.arange(self.lo, self.lo + m, dtype=np.int64), None
 
     def rollback_to(self, n):
         self._n = [min(x, n) for x in self._n]
@@ -193,35 +229,40 @@ class FullCache(KVCache):
         self.committed = n
 
     def clone(self):
-        c = FullCache(self.n_layers, self.n_kv_heads, self.head_dim, self.max_entries)
-        check(lib.hs_cache_copy(c._ref, self._ref, max(self._n + [0]), stream_ptr()))
+        c = FullCache(self.n_layers, self.n_kv_heads, self.head_dim, self.max_entries, self.shards, self.lo, self.hi)
+        c.bounds = list(self.bounds)
+        check(lib.hs_cache_copy(c._ref, self._ref, self._local(max(self._n + [0])), stream_ptr()))
         c._n = list(self._n)
         c.frontier, c.committed = self.frontier, self.committed
         return c
 
     def fill_random_(self, n: int, seed: int = 0, std: float = 1.0):
         """Synthetic context: n committed positions of N(0, std) bf16 K/V
-        (throughput configs)."""
+        (throughput configs).  Each shard fills its own
+        positions from a stream keyed by (seed, lo)."""
         if n > self.max_entries:
             raise CapacityError("fill beyond capacity")
         g = torch.Generator(device=self.k.device)
-        g.manual_seed(seed)
+        g.manual_seed(seed * 1000003 + self.lo)
+        m = self._local(n)
         for l in range(self.n_layers):
             for h in range(self.n_kv_heads):
-                self.k[l, h, :n].normal_(0.0, std, generator=g)
-                self.v[l, h, :n].normal_(0.0, std, generator=g)
+                self.k[l, h, :m].normal_(0.0, std, generator=g)
+                self.v[l, h, :m].normal_(0.0, std, generator=g)
         self._n = [n] * self.n_layers
         self.frontier = self.committed = n
 
-    # fused forward: append at slot == position, attend to [0, frontier + t)
+    # fused forward: append at slot == position - lo, attend to this rank's slots
     def _step(self, t):
         s = HsStep()
         s.pos0 = self.frontier
         s.append_mode = HS_APPEND_POS
-        s.n_view = self.frontier + t
-        s.split = FULL_SPLIT
-        if s.n_view > self.max_entries:
+        if self.frontier + t > self.max_entries:
             raise CapacityError(f"full cache overflow past {self.max_entries}")
+        s.n_view = self._local(self.frontier + t)
+        s.split = FULL_SPLIT
+        s.pos_base = self.lo
+        s.own_hi = self.hi if self.hi is not None else 0
         return s
 
     def _advance(self, t):
@@ -450,11 +491,7 @@ class RetrievalCache(KVCache):
         cfg = self.config
         q = _queries_device(queries, self.n_layers)
         n = (upto + cfg.chunk_size - 1) // cfg.chunk_size
-        scores = torch.empty((self.n_layers, n), dtype=torch.float64, device=q.device)
-        dh = self.head_dim
-        check(lib.hs_chunk_score(ptr(source.k), 1, self.n_kv_heads * source.cap * dh, source.cap * dh, dh,
-                                 self.n_layers, self.n_kv_heads, dh, upto, cfg.chunk_size, ptr(q), q.shape[1],
-                                 ptr(scores), stream_ptr()))
+        scores = self._score(source, q, upto, n)
         check(lib.hs_chunk_select(ptr(scores), self.n_layers, n, upto, cfg.chunk_size, cfg.budget,
                                   ptr(self.importance), ptr(self.chosen), ptr(self.ring), ptr(self.counts),
                                   None, 0, stream_ptr()))
@@ -464,7 +501,12 @@ class RetrievalCache(KVCache):
         self.n_sel = k_sel * cfg.chunk_size + (upto - (n - 1) * cfg.chunk_size)
         self.pos.fill_(-1)
         check(lib.hs_retrieval_gather(source._ref, self._ref, ptr(self.chosen), self.quota, n_chosen,
-                                      cfg.chunk_size, upto, stream_ptr()))
+                                      cfg.chunk_size, upto, source.lo, source.hi or 0, stream_ptr()))
+        if source.sharded:
+            # every rank wrote the chunks it owns and zeros elsewhere: x + 0 is
+            # exact in bf16, so the sum assembles the selection on every rank
+            source.shards.all_reduce_sum_(self.k)
+            source.shards.all_reduce_sum_(self.v)
         self.ring_head = 0
         self.n_spec = [0] * self.n_layers
         self.frontier = self.committed = upto
@@ -472,6 +514,40 @@ class RetrievalCache(KVCache):
         self.table = ChunkScoreTable(cfg.chunk_size, upto, self.n_layers, scores, self.importance, n_chosen,
                                      clamped)
         return self.table
+
+    def _score(self, source: FullCache, q: torch.Tensor, upto: int, n: int) -> torch.Tensor:
+        """fp64 chunk scores [L, n] of source positions [0, upto).  Sharded:
+        each rank scores the chunks it stores (chunk-aligned shards), the
+        per-rank rows are all-gathered and concatenated in rank order --
+        bit-identical to the unsharded scores (chunks are independent)."""
+        cfg, dh = self.config, self.head_dim
+        dev = q.device
+
+        def local_scores(count, local_upto):
+            out = torch.empty((self.n_layers, count), dtype=torch.float64, device=dev)
+            if count:
+                check(lib.hs_chunk_score(ptr(source.k), 1, self.n_kv_heads * source.cap * dh, source.cap * dh, dh,
+                                         self.n_layers, self.n_kv_heads, dh, local_upto, cfg.chunk_size, ptr(q),
+                                         q.shape[1], ptr(out), stream_ptr()))
+            return out
+
+        if not source.sharded:
+            return local_scores(n, upto)
+        from .shard import shard_chunk_counts
+        sh = source.shards
+        if any(lo % cfg.chunk_size for lo, _ in source.bounds):
+            raise ContractError("shard boundaries must be multiples of the retrieval chunk size")
+        counts = shard_chunk_counts(source.bounds, upto, cfg.chunk_size)
+        cmax = max(counts)
+        mine = counts[sh.rank]
+        send = torch.zeros((self.n_layers, cmax), dtype=torch.float64, device=dev)
+        if mine:
+            send[:, :mine] = local_scores(mine, min(upto, source.lo + source.cap) - source.lo)
+        recv = sh.all_gather(send)
+        scores = torch.cat([recv[r, :, :counts[r]] for r in range(sh.world)], dim=1).contiguous()
+        if scores.shape[1] != n:
+            raise ContractError(f"sharded scores cover {scores.shape[1]} chunks, expected {n}")
+        return scores
 
     def append(self, layer, k, v):
         self._check_kv(k, v)

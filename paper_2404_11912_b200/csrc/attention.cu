@@ -26,7 +26,7 @@ struct AttnArgs {
   const uint16_t *k;    // layer base [KVH][cap][DH]
   const uint16_t *v;
   const int32_t *pos;   // layer [cap] or null (slot == position)
-  int cap, n_view, pos0, window, win_lo, n_sink, split, n_splits;
+  int cap, n_view, pos0, window, win_lo, n_sink, split, n_splits, pos_base;
   float scale;
   float *part_m, *part_l, *part_o;   // [n_splits][t*H], [n_splits][t*H][DH]
 };
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
     }
     if (tid < ATT_TILE) {
       int j = tile + tid;
-      kpos[tid] = (tid < nk) ? (a.pos ? a.pos[j] : j) : -1;
+      kpos[tid] = (tid < nk) ? (a.pos ? a.pos[j] : j + a.pos_base) : -1;
     }
     __syncthreads();
     // ---- scores: thread = (key, half of the rows) ---------------------------
@@ -200,12 +200,15 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
   }
 }
 
-// out[i][h*DH + d] = sum_s w_s o_s / sum_s w_s l_s,  w_s = exp(m_s - M), splits in order
+// out[i][h*DH + d] = sum_s w_s o_s / sum_s w_s l_s,  w_s = exp(m_s - M), splits in order.
+// packed != nullptr: write the view's partial state (M, l, o unnormalised)
+// as [rows][2 + DH] instead (sequence-shard input, hs_attention_partial).
 __global__ void attn_combine_kernel(const float *pm, const float *pl, const float *po, int n_splits,
-                                    int rows, int DH, float *out) {
+                                    int rows, int DH, float *out, float *packed) {
   const int row = blockIdx.x;
   float M = -INFINITY;
   for (int s = 0; s < n_splits; ++s) M = fmaxf(M, pm[(size_t)s * rows + row]);
+  float lsum = 0.f;
   for (int d = threadIdx.x; d < DH; d += blockDim.x) {
     float l = 0.f, o = 0.f;
     for (int s = 0; s < n_splits; ++s) {
@@ -215,8 +218,42 @@ __global__ void attn_combine_kernel(const float *pm, const float *pl, const floa
       l = fmaf(w, pl[(size_t)s * rows + row], l);
       o = fmaf(w, po[((size_t)s * rows + row) * DH + d], o);
     }
+    if (packed) packed[(size_t)row * (DH + 2) + 2 + d] = o;
+    else out[(size_t)row * DH + d] = o / l;
+    lsum = l;
+  }
+  if (packed && threadIdx.x == 0) {
+    packed[(size_t)row * (DH + 2)] = M;
+    packed[(size_t)row * (DH + 2) + 1] = lsum;
+  }
+}
+
+// rank-ordered merge of packed partial states [G][rows][2 + DH];
+// the same arithmetic as attn_combine_kernel, so a 1-rank merge of a packed
+// partial reproduces the unsharded output bit for bit.
+__global__ void shard_merge_kernel(const float *parts, int G, int rows, int DH, float *out) {
+  const int row = blockIdx.x;
+  const size_t stride = (size_t)rows * (DH + 2);
+  float M = -INFINITY;
+  for (int g = 0; g < G; ++g) M = fmaxf(M, parts[g * stride + (size_t)row * (DH + 2)]);
+  for (int d = threadIdx.x; d < DH; d += blockDim.x) {
+    float l = 0.f, o = 0.f;
+    for (int g = 0; g < G; ++g) {
+      const float *p = parts + g * stride + (size_t)row * (DH + 2);
+      const float m = p[0];
+      if (m == -INFINITY) continue;
+      const float w = expf(m - M);
+      l = fmaf(w, p[1], l);
+      o = fmaf(w, p[2 + d], o);
+    }
     out[(size_t)row * DH + d] = o / l;
   }
+}
+
+int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, cudaStream_t st) {
+  HS_REQUIRE(G >= 1 && rows >= 1, HS_ERR_VALUE, "shard_merge: empty");
+  shard_merge_kernel<<<rows, DH < 128 ? DH : 128, 0, st>>>(parts, G, rows, DH, out);
+  return check_launch("shard_merge");
 }
 
 size_t attention_ws(int t, int H, int DH, int n_view, int split) {
@@ -228,11 +265,12 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
                         float *part_l, float *part_o, int n_splits, cudaStream_t stream);
 
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
-                     float *out, void *ws, size_t ws_bytes, cudaStream_t stream) {
+                     float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream) {
   const int DH = c->head_dim, KVH = c->n_kv_heads;
   HS_REQUIRE(H % KVH == 0, HS_ERR_SHAPE, "attention: H %% KVH != 0");
   HS_REQUIRE(st->split > 0 && st->split % ATT_TILE == 0, HS_ERR_VALUE, "attention: split must be a multiple of %d", ATT_TILE);
-  HS_REQUIRE(st->n_view >= 1 && st->n_view <= c->cap, HS_ERR_CAPACITY, "attention: view %d exceeds capacity %d", st->n_view, c->cap);
+  HS_REQUIRE(st->n_view >= (packed ? 0 : 1) && st->n_view <= c->cap, HS_ERR_CAPACITY,
+             "attention: view %d outside [1, capacity %d]", st->n_view, c->cap);
   const int n_splits = ceil_div(st->n_view, st->split);
   HS_REQUIRE(ws_bytes >= attention_ws(t, H, DH, st->n_view, st->split), HS_ERR_VALUE, "attention: workspace too small");
   AttnArgs a;
@@ -242,12 +280,18 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   a.pos = (c->kind == HS_KV_SLOTTED) ? c->pos + (size_t)layer * c->cap : nullptr;
   a.cap = c->cap; a.n_view = st->n_view; a.pos0 = st->pos0; a.window = st->window;
   a.win_lo = st->win_lo; a.n_sink = st->n_sink; a.split = st->split; a.n_splits = n_splits;
+  a.pos_base = st->pos_base;
   a.scale = (float)(1.0 / sqrt((double)DH));
   float *wsf = reinterpret_cast<float *>(ws);
   a.part_m = wsf;
   a.part_l = wsf + (size_t)n_splits * t * H;
   a.part_o = wsf + (size_t)2 * n_splits * t * H;
   dim3 grid(n_splits, KVH, ceil_div(a.g * t, ATT_QROWS));
+  if (n_splits == 0) {   // empty shard view: partial state (-inf, 0, 0) for every row
+    attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 0, stream>>>(a.part_m, a.part_l, a.part_o, 0, t * H, DH,
+                                                                     nullptr, packed);
+    return check_launch("attention(empty)");
+  }
   // head_dim 128 (the Llama-family targets) runs on the tensor cores; the
   // small-head draft model and the test-size models use the CUDA-core kernel
   switch (DH) {
@@ -264,7 +308,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
     default: return set_error(HS_ERR_SHAPE, "attention: head_dim %d unsupported (8/16/32/64/128)", DH);
   }
   attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 0, stream>>>(a.part_m, a.part_l, a.part_o,
-                                                                   n_splits, t * H, DH, out);
+                                                                   n_splits, t * H, DH, out, packed);
   return check_launch("attention", 2);
 }
 
@@ -276,5 +320,15 @@ extern "C" size_t hs_attention_workspace_bytes(int t, int n_heads, int head_dim,
 
 extern "C" int hs_attention(const HsCache *c, int layer, const HsStep *st, int n_heads, const float *q,
                             int t, float *out, void *workspace, size_t ws_bytes, void *stream) {
-  return hs::launch_attention(c, layer, st, n_heads, q, t, out, workspace, ws_bytes, hs::as_stream(stream));
+  return hs::launch_attention(c, layer, st, n_heads, q, t, out, nullptr, workspace, ws_bytes, hs::as_stream(stream));
+}
+
+extern "C" int hs_attention_partial(const HsCache *c, int layer, const HsStep *st, int n_heads, const float *q,
+                                    int t, float *packed, void *workspace, size_t ws_bytes, void *stream) {
+  return hs::launch_attention(c, layer, st, n_heads, q, t, nullptr, packed, workspace, ws_bytes,
+                              hs::as_stream(stream));
+}
+
+extern "C" int hs_shard_merge(const float *parts, int n_shards, int rows, int head_dim, float *out, void *stream) {
+  return hs::launch_shard_merge(parts, n_shards, rows, head_dim, out, hs::as_stream(stream));
 }

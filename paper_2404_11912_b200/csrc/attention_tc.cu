@@ -53,7 +53,7 @@ struct AttTcArgs {
   const float *q;       // [t][H][128]
   int t, H, KVH, g;
   const int32_t *pos;   // layer [cap] or null
-  int cap, layer, n_view, pos0, window, win_lo, n_sink, split, n_splits, n_qb, n_items;
+  int cap, layer, n_view, pos0, window, win_lo, n_sink, split, n_splits, n_qb, n_items, pos_base;
   float scale_log2;     // log2(e) / sqrt(dh)
   float *part_m, *part_l, *part_o;
 };
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         const int s = gi & 1;
         const uint32_t ph = (gi >> 1) & 1;
         const int key = lo + it * AT_KT + tid;
-        const int kp = key < hi ? (a.pos ? a.pos[key] : key) : -1;
+        const int kp = key < hi ? (a.pos ? a.pos[key] : key + a.pos_base) : -1;
         tc::mbar_wait(&sfull[s], ph);
         tc::fence_after();
         float sv[AT_N];
@@ -372,6 +372,7 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
   a.pos = (c->kind == HS_KV_SLOTTED) ? c->pos + (size_t)layer * c->cap : nullptr;
   a.cap = c->cap; a.layer = layer; a.n_view = st->n_view; a.pos0 = st->pos0; a.window = st->window;
   a.win_lo = st->win_lo; a.n_sink = st->n_sink; a.split = st->split; a.n_splits = n_splits;
+  a.pos_base = st->pos_base;
   a.n_qb = ceil_div(a.g * t, AT_QR);
   a.n_items = n_splits * a.KVH * a.n_qb;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)AT_DH));

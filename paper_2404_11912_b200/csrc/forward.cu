@@ -3,6 +3,7 @@
 // sequence can be captured into a CUDA graph by the caller.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "hs_common.cuh"
@@ -15,7 +16,9 @@ int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int 
 int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv, int t,
                        float *q_out, float *q_stash, cudaStream_t st);
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
-                     void *ws, size_t ws_bytes, cudaStream_t stream);
+                     float *packed, void *ws, size_t ws_bytes, cudaStream_t stream);
+int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, cudaStream_t st);
+int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
 
 // ---- error state -------------------------------------------------------------
@@ -31,6 +34,15 @@ int set_error(int code, const char *fmt, ...) {
 
 // kernels launched by this library since load (gpu_launches evidence for bench.py)
 static unsigned long long g_launches = 0;
+
+int pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("HS_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v;
+}
 
 void count_launch(int n) { __atomic_add_fetch(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
 
@@ -51,7 +63,8 @@ size_t gemv_tc_ws_bytes(int N, int nkb);
 // which must stay zero/clean between calls never move:
 //   [gemv counters + partials (max over the model's matrices)]
 //   [Xd: 24 x ld_d bf16 split operand][Xf: 24 x ld_ff bf16]
-//   then per-call regions: x, qkv, q, attn, attention partials.
+//   then per-call regions: x, qkv, q, attn, attention partials and, when
+//   sharded, the packed per-rank partial states (send) and their gather (recv).
 struct FwdWs {
   void *gemv_ws;
   size_t gemv_bytes;
@@ -59,6 +72,7 @@ struct FwdWs {
   float *x, *qkv, *q, *attn;
   void *att_ws;
   size_t att_bytes;
+  float *send, *recv;
 };
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -75,7 +89,7 @@ static size_t gemv_region(const HsModel *m) {
   return align256(g);
 }
 
-static size_t carve(const HsModel *m, int t, int n_view, int split, char *base, FwdWs *w) {
+static size_t carve(const HsModel *m, int t, int n_view, int split, int world, char *base, FwdWs *w) {
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim;
   size_t off = 0;
   auto take = [&](size_t bytes) { char *p = base ? base + off : nullptr; off += align256(bytes); return p; };
@@ -89,6 +103,9 @@ static size_t carve(const HsModel *m, int t, int n_view, int split, char *base, 
   w->attn = (float *)take((size_t)t * d * 4);
   w->att_bytes = attention_ws(t, H, dh, n_view, split);
   w->att_ws = take(w->att_bytes);
+  const size_t part = (size_t)t * H * (dh + 2) * 4;
+  w->send = world > 0 ? (float *)take(part) : nullptr;
+  w->recv = world > 0 ? (float *)take(part * world) : nullptr;
   return off;
 }
 
@@ -103,9 +120,9 @@ extern "C" int hs_device_sm_count(int device) {
   return n;
 }
 
-extern "C" size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view, int split) {
+extern "C" size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view, int split, int world) {
   hs::FwdWs w;
-  return hs::carve(m, t, n_view, split, nullptr, &w);
+  return hs::carve(m, t, n_view, split, world, nullptr, &w);
 }
 
 extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
@@ -113,16 +130,24 @@ extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
   return hs::gemv_region(m) + hs::align256((size_t)24 * m->ld_d * 2) + hs::align256((size_t)24 * m->ld_ff * 2);
 }
 
-extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
-                          float *logits, float *q_stash, void *workspace, size_t workspace_bytes, void *stream) {
+extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
+                          const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
+                          size_t workspace_bytes, void *stream) {
   using namespace hs;
   HS_REQUIRE(t >= 1, HS_ERR_VALUE, "empty token sequence");
   HS_REQUIRE(c->n_layers == m->n_layers && c->n_kv_heads == m->n_kv_heads && c->head_dim == m->head_dim,
              HS_ERR_SHAPE, "forward: cache geometry does not match the model");
   HS_REQUIRE(st->pos0 + t <= m->max_seq, HS_ERR_CAPACITY, "sequence of %d exceeds max_seq %d", st->pos0 + t,
              m->max_seq);
+  const bool sharded = sh != nullptr;
+  if (sharded) {
+    HS_REQUIRE(sh->comm != nullptr && sh->world >= 1 && sh->rank >= 0 && sh->rank < sh->world, HS_ERR_VALUE,
+               "forward: bad shard descriptor (rank %d of %d)", sh->rank, sh->world);
+    HS_REQUIRE(c->kind == HS_KV_LINEAR && st->append_mode == HS_APPEND_POS, HS_ERR_VALUE,
+               "forward: only a full (linear) cache can be sequence-sharded");
+  }
   FwdWs w;
-  const size_t need = carve(m, t, st->n_view, st->split, (char *)workspace, &w);
+  const size_t need = carve(m, t, st->n_view, st->split, sharded ? sh->world : 0, (char *)workspace, &w);
   HS_REQUIRE(workspace_bytes >= need, HS_ERR_VALUE, "forward: workspace %zu < %zu", workspace_bytes, need);
   cudaStream_t s = as_stream(stream);
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim, ff = m->d_ff;
@@ -144,7 +169,15 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
                             w.gemv_bytes, s));
     }
     HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
-    HS_TRY(launch_attention(c, l, st, H, w.q, t, w.attn, w.att_ws, w.att_bytes, s));
+    if (sharded) {
+      // this rank's partial softmax state -> all ranks -> rank-ordered merge
+      const size_t part = (size_t)t * H * (dh + 2) * 4;
+      HS_TRY(launch_attention(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s));
+      HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
+      HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, w.attn, s));
+    } else {
+      HS_TRY(launch_attention(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s));
+    }
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
       float *xr = w.x + (size_t)r0 * d;
@@ -166,31 +199,3 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
   return HS_OK;
 }
 
-// ---- shard merge: rank-ordered partial-softmax merge ----------
-namespace hs {
-__global__ void shard_merge_kernel(const float *pm, const float *pl, const float *po, int G, int rows, int DH,
-                                   float *out) {
-  const int row = blockIdx.x;
-  float M = -INFINITY;
-  for (int g = 0; g < G; ++g) M = fmaxf(M, pm[(size_t)g * rows + row]);
-  for (int d = threadIdx.x; d < DH; d += blockDim.x) {
-    float l = 0.f, o = 0.f;
-    for (int g = 0; g < G; ++g) {
-      const float m = pm[(size_t)g * rows + row];
-      if (m == -INFINITY) continue;
-      const float wgt = expf(m - M);
-      l = fmaf(wgt, pl[(size_t)g * rows + row], l);
-      o = fmaf(wgt, po[((size_t)g * rows + row) * DH + d], o);
-    }
-    out[(size_t)row * DH + d] = o / l;
-  }
-}
-}  // namespace hs
-
-extern "C" int hs_shard_merge(const float *m, const float *l, const float *o, int n_shards, int rows, int head_dim,
-                              float *out, void *stream) {
-  if (n_shards < 1 || rows < 1) return hs::set_error(HS_ERR_VALUE, "shard_merge: empty");
-  hs::shard_merge_kernel<<<rows, head_dim < 128 ? head_dim : 128, 0, hs::as_stream(stream)>>>(m, l, o, n_shards,
-                                                                                            rows, head_dim, out);
-  return hs::check_launch("shard_merge");
-}

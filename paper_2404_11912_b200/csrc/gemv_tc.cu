@@ -352,7 +352,7 @@ int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const floa
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled();
   cudaError_t e = cudaLaunchKernelEx(&cfg, split_rows_kernel, x, ldx, t, K, ldk, gain, eps, xs);
   if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "split_rows launch: %s", cudaGetErrorString(e));
   return check_launch("split_rows");
@@ -393,7 +393,7 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled();
   cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_tc_kernel, mw, mx, a);
   if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "gemv_tc launch: %s", cudaGetErrorString(e));
   return check_launch("gemv_tc");

@@ -58,6 +58,9 @@ __device__ __forceinline__ float warp_max(float v) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// programmatic dependent launch on/off (HS_NO_PDL=1 disables it: debugging aid)
+int pdl_enabled();
+
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 }  // namespace hs

@@ -17,8 +17,13 @@ int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int 
   return check_launch("embed");
 }
 
+// slot of the i-th new row at position p, or -1 when this rank does not store
+// it (sequence shard of a full cache: positions [pos_base, own_hi))
 __device__ __forceinline__ int append_slot(const HsStep &s, int i, int p) {
-  if (s.append_mode == HS_APPEND_POS) return p;
+  if (s.append_mode == HS_APPEND_POS) {
+    if (p < s.pos_base || (s.own_hi > 0 && p >= s.own_hi)) return -1;
+    return p - s.pos_base;
+  }
   if (s.append_mode == HS_APPEND_LINEAR) return s.append_base + i;
   return p < s.n_sink ? p : s.n_sink + (p - s.n_sink) % s.ring;
 }
@@ -52,6 +57,7 @@ __global__ void rope_append_kernel(HsModel m, HsCache c, HsStep s, int layer, co
     } else {
       const int kh = hh - H;
       const int slot = append_slot(s, i, p);
+      if (slot < 0) return;
       uint16_t *kd = c.k + (((size_t)layer * KVH + kh) * c.cap + slot) * DH + 2 * pr;
       kd[0] = f_to_bf16(y0); kd[1] = f_to_bf16(y1);
       if (kh == 0 && pr == 0 && c.kind == HS_KV_SLOTTED) c.pos[(size_t)layer * c.cap + slot] = p;
@@ -59,6 +65,7 @@ __global__ void rope_append_kernel(HsModel m, HsCache c, HsStep s, int layer, co
   } else {
     const int kh = hh - H - KVH;
     const int slot = append_slot(s, i, p);
+    if (slot < 0) return;
     const int col = (H + KVH + kh) * DH + 2 * pr;
     uint16_t *vd = c.v + (((size_t)layer * KVH + kh) * c.cap + slot) * DH + 2 * pr;
     vd[0] = f_to_bf16(row[col]); vd[1] = f_to_bf16(row[col + 1]);
@@ -69,8 +76,10 @@ int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int 
                        int t, float *q_out, float *q_stash, cudaStream_t st) {
   HS_REQUIRE(m->head_dim % 2 == 0 && m->head_dim <= 256, HS_ERR_SHAPE, "rope: bad head_dim");
   HS_REQUIRE(s->pos0 + t <= m->max_seq, HS_ERR_CAPACITY, "sequence of %d exceeds max_seq %d", s->pos0 + t, m->max_seq);
-  if (s->append_mode == HS_APPEND_POS)
-    HS_REQUIRE(s->pos0 + t <= c->cap, HS_ERR_CAPACITY, "full cache overflow past %d", c->cap);
+  if (s->append_mode == HS_APPEND_POS) {
+    const int hi = s->own_hi > 0 && s->own_hi < s->pos0 + t ? s->own_hi : s->pos0 + t;
+    HS_REQUIRE(hi - s->pos_base <= c->cap, HS_ERR_CAPACITY, "full cache overflow past %d", s->pos_base + c->cap);
+  }
   if (s->append_mode == HS_APPEND_LINEAR)
     HS_REQUIRE(s->append_base + t <= c->cap, HS_ERR_CAPACITY, "retrieval spec tail overflow (%d slots)", c->cap);
   if (s->append_mode == HS_APPEND_RING)

@@ -229,20 +229,31 @@ __global__ void __launch_bounds__(SEL_THREADS) chunk_select_kernel(
 }
 
 // grid (n_chosen, KVH, L): copy chunk tokens (position order) into slots j*chunk..
+// src holds positions [src_lo, src_hi) (a sequence shard; src_hi 0 = no bound);
+// chosen chunks outside it are written as zeros so that a sum all-reduce over
+// the shards assembles the full selection (chunks never straddle shards).
 __global__ void retrieval_gather_kernel(HsCache src, HsCache dst, const int32_t *chosen, int quota,
-                                        int chunk, int upto) {
+                                        int chunk, int upto, int src_lo, int src_hi) {
   const int j = blockIdx.x, kh = blockIdx.y, l = blockIdx.z, DH = src.head_dim;
   const int cid = chosen[(size_t)l * quota + j];
   const int p0 = cid * chunk, p1 = min(upto, p0 + chunk);
   const int n = p1 - p0;
-  const uint16_t *ks = src.k + (((size_t)l * src.n_kv_heads + kh) * src.cap + p0) * DH;
-  const uint16_t *vs = src.v + (((size_t)l * src.n_kv_heads + kh) * src.cap + p0) * DH;
+  const bool mine = p0 >= src_lo && (src_hi == 0 || p0 < src_hi);
   uint16_t *kd = dst.k + (((size_t)l * dst.n_kv_heads + kh) * dst.cap + (size_t)j * chunk) * DH;
   uint16_t *vd = dst.v + (((size_t)l * dst.n_kv_heads + kh) * dst.cap + (size_t)j * chunk) * DH;
   const int nvec = n * DH / 8;
-  for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
-    reinterpret_cast<uint4 *>(kd)[e] = ld_stream(reinterpret_cast<const uint4 *>(ks) + e);
-    reinterpret_cast<uint4 *>(vd)[e] = ld_stream(reinterpret_cast<const uint4 *>(vs) + e);
+  if (mine) {
+    const uint16_t *ks = src.k + (((size_t)l * src.n_kv_heads + kh) * src.cap + (p0 - src_lo)) * DH;
+    const uint16_t *vs = src.v + (((size_t)l * src.n_kv_heads + kh) * src.cap + (p0 - src_lo)) * DH;
+    for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
+      reinterpret_cast<uint4 *>(kd)[e] = ld_stream(reinterpret_cast<const uint4 *>(ks) + e);
+      reinterpret_cast<uint4 *>(vd)[e] = ld_stream(reinterpret_cast<const uint4 *>(vs) + e);
+    }
+  } else {
+    for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
+      reinterpret_cast<uint4 *>(kd)[e] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4 *>(vd)[e] = make_uint4(0, 0, 0, 0);
+    }
   }
   if (kh == 0)
     for (int u = threadIdx.x; u < n; u += blockDim.x) dst.pos[(size_t)l * dst.cap + j * chunk + u] = p0 + u;
@@ -291,13 +302,17 @@ extern "C" int hs_chunk_select(const double *scores, int n_layers, int n_chunks,
 }
 
 extern "C" int hs_retrieval_gather(const HsCache *src, const HsCache *dst, const int32_t *chosen, int chosen_stride,
-                                   int n_chosen, int chunk, int upto, void *stream) {
+                                   int n_chosen, int chunk, int upto, int src_lo, int src_hi, void *stream) {
   if (dst->kind != HS_KV_SLOTTED) return hs::set_error(HS_ERR_VALUE, "gather: destination must be slotted");
   if ((long long)n_chosen * chunk > dst->cap) return hs::set_error(HS_ERR_CAPACITY, "gather: %d chunks exceed capacity", n_chosen);
   if (src->head_dim != dst->head_dim || src->n_kv_heads != dst->n_kv_heads || src->n_layers != dst->n_layers)
     return hs::set_error(HS_ERR_SHAPE, "gather: geometry mismatch");
-  if (upto > src->cap) return hs::set_error(HS_ERR_CONTRACT, "source cache shorter than requested build range");
+  if ((src_hi > 0 ? (src_hi < upto ? src_hi : upto) : upto) - src_lo > src->cap)
+    return hs::set_error(HS_ERR_CONTRACT, "source cache shorter than requested build range");
+  if (src_lo % chunk != 0 || (src_hi > 0 && src_hi % chunk != 0))
+    return hs::set_error(HS_ERR_VALUE, "gather: shard bounds [%d, %d) not chunk-aligned", src_lo, src_hi);
   dim3 grid(n_chosen, src->n_kv_heads, src->n_layers);
-  hs::retrieval_gather_kernel<<<grid, 128, 0, hs::as_stream(stream)>>>(*src, *dst, chosen, chosen_stride, chunk, upto);
+  hs::retrieval_gather_kernel<<<grid, 128, 0, hs::as_stream(stream)>>>(*src, *dst, chosen, chosen_stride, chunk, upto,
+                                                                        src_lo, src_hi);
   return hs::check_launch("retrieval_gather");
 }

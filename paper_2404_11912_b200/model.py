@@ -217,6 +217,18 @@ class DeviceModel:
         self.struct = s
         self.ref = C.byref(s)
 
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        """This model's forward workspace.  Its head (GEMV arrival counters and
+        K-split partials, hs_forward_workspace_clean_bytes) must be zero
+        before first use and is left zero by every call; the layout of that
+        head depends on the model's matrix shapes, so the buffer is owned by
+        the model and never shared with another one."""
+        ws = getattr(self, "_ws", None)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=self.emb.device)
+            self._ws = ws
+        return ws
+
     @property
     def weight_bytes(self) -> int:
         """Algorithmic weight bytes streamed per forward (embedding row excluded)."""
@@ -438,11 +450,14 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
     if out is None:
         out = torch.empty((t, cfg.vocab_size), dtype=torch.float32, device=tok.device)
     stash = recorder._buffer(cfg) if recorder is not None else None
+    shards = getattr(cache, "shards", None)
+    shard_ref = shards.ref if shards is not None else None
+    world = shards.world if shards is not None else 0
     for a, b in cache._batches(t):
         step = cache._step(b - a)
-        nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split)
-        ws = workspaces.get(f"forward:{id(dm)}", nbytes)
-        check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), ptr(tok) + 4 * a, b - a,
+        nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split, world)
+        ws = dm.workspace(nbytes)
+        check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), shard_ref, ptr(tok) + 4 * a, b - a,
                              ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))
         cache._advance(b - a)
     if recorder is not None:

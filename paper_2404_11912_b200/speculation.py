@@ -383,7 +383,10 @@ class HierarchicalSession:
     (speculation.py:278-368).  Single-threaded; clone() snapshots."""
 
     def __init__(self, target: ModelWeights, draft: ModelWeights, prefix: Sequence[int], config: SpecConfig,
-                 _prefill: bool = True):
+                 _prefill: bool = True, shards=None):
+        """shards: a shard.SequenceShards -- the full cache is then split
+        along the sequence over its ranks (every rank runs this session with
+        the same arguments).  None = one GPU."""
         if target.config.vocab_size != draft.config.vocab_size:
             raise ContractError("target and draft models must share a vocabulary")
         if len(prefix) < 1:
@@ -392,7 +395,9 @@ class HierarchicalSession:
             raise ValueError("target_len must exceed the prefix length")
         self.config = config
         self.committed = list(prefix)
-        self.full_lane = Lane(target, FullCache.from_config(target.config))
+        full = (FullCache.from_config(target.config) if shards is None else
+                FullCache.shard(target.config, shards, len(prefix), config.retrieval.chunk_size))
+        self.full_lane = Lane(target, full)
         self.draft_lane = Lane(draft, StreamingCache.from_config(draft.config, config.streaming))
         self.retr_lane = Lane(target, RetrievalCache.from_config(target.config, config.retrieval))
         self.rolling = RollingAcceptance(config.retrieval.rolling_window)
@@ -416,12 +421,12 @@ class HierarchicalSession:
 
     @classmethod
     def synthetic(cls, target: ModelWeights, draft: ModelWeights, context: Sequence[int], config: SpecConfig,
-                  seed: int = 0):
+                  seed: int = 0, shards=None):
         """Session over a synthetic long context (throughput configs,
         SURVEY §7.4 item 6): the full and draft caches are filled with random
         bf16 K/V for positions [0, n-1); the last context token is then
         decoded for real on every lane and the initial build uses its queries."""
-        s = cls(target, draft, context, config, _prefill=False)
+        s = cls(target, draft, context, config, _prefill=False, shards=shards)
         n = len(context)
         s.full_lane.cache.fill_random_(n - 1, seed=seed)
         s.draft_lane.cache.fill_random_(n - 1, seed=seed + 1)
@@ -533,15 +538,18 @@ def hierarchical_generate(target: ModelWeights, draft: ModelWeights, prefix: Seq
 
 
 def autoregressive_generate(weights: ModelWeights, prefix: Sequence[int], target_len: int,
-                            temperature: float = 0.0, seed: int = 0) -> list:
+                            temperature: float = 0.0, seed: int = 0, shards=None, chunk: int = 16) -> list:
     """Plain decode over the full cache (speculation.py:378-398); the
-    sampled token never leaves the device until the end."""
+    sampled token never leaves the device until the end.  shards: sequence-
+    shard the full cache (shard.SequenceShards, boundaries aligned to chunk)."""
     if len(prefix) < 1:
         raise ValueError("prefix must be non-empty")
     if target_len <= len(prefix):
         raise ValueError("target_len must exceed the prefix length")
     rng = np.random.default_rng(seed)
-    lane = Lane(weights, FullCache.from_config(weights.config))
+    cache = (FullCache.from_config(weights.config) if shards is None else
+             FullCache.shard(weights.config, shards, len(prefix), chunk))
+    lane = Lane(weights, cache)
     lane.prefill(list(prefix))
     return _ar_loop(lane, list(prefix), target_len, temperature, rng)
 

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 20
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.hs_abi_version() == 1
+    assert lib.hs_abi_version() == 2
 
 
 def test_python_binding_covers_the_header():

@@ -1,0 +1,172 @@
+"""Sequence-sharded full cache on one B200 (`-m gpu`).
+
+The driver's GPU boxes have one GPU, so the multi-rank exchange is checked
+in two halves: (1) the NCCL code path itself runs with a one-rank
+communicator and must reproduce the unsharded path bit for bit; (2) the
+math of G shards -- per-shard partial states merged in rank order, per-shard
+chunk scores, zero-padded per-shard gathers summed -- runs on one device and
+must equal the unsharded results.  The world-size-2 protocol over real
+collectives is covered on CPU with gloo (tests/test_shard_cpu.py)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2404_11912_b200 as pkg
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def one_rank(P):
+    from paper_2404_11912_b200.shard import SequenceShards
+    sh = SequenceShards.single()
+    yield sh
+    sh.destroy()
+
+
+def _planted(P, seed=5):
+    tc = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=128, d_ff=344, vocab_size=512, max_seq=2048)
+    dc = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=64, d_ff=172, vocab_size=512, max_seq=2048)
+    tw = P.plant_successor(P.generate_weights(tc, seed, tied_head=False), 9, 0.9)
+    dw = P.plant_successor(P.generate_weights(dc, seed + 1, tied_head=False), 9, 0.9)
+    return tw, dw
+
+
+def test_one_rank_sharded_forward_is_bitwise_unsharded(P, one_rank):
+    tw, _ = _planted(P)
+    prompt = np.random.default_rng(0).integers(1, 512, 700).tolist()
+    a = P.FullCache.from_config(tw.config)
+    b = P.FullCache.shard(tw.config, one_rank, len(prompt), 8)
+    la = P.prefill(tw, prompt, a)
+    lb = P.prefill(tw, prompt, b)
+    assert np.array_equal(la, lb)
+    for tok in (3, 17, 400):
+        assert np.array_equal(P.decode_step(tw, tok, a), P.decode_step(tw, tok, b))
+    assert np.array_equal(P.decode_chunk(tw, [5, 6, 7, 8, 9], a), P.decode_chunk(tw, [5, 6, 7, 8, 9], b))
+
+
+def test_one_rank_sharded_session_matches_unsharded(P, one_rank):
+    tw, dw = _planted(P)
+    prompt = np.random.default_rng(1).integers(1, 512, 900).tolist()
+    spec = P.SpecConfig(target_len=900 + 80, gamma1=2, gamma2=4, temperature=0.6, seed=3,
+                        streaming=P.StreamingConfig(n_sink=4, budget=128),
+                        retrieval=P.RetrievalConfig(chunk_size=8, budget=128, rebuild_stride=24))
+    out_a, tr_a = P.HierarchicalSession(tw, dw, prompt, spec).generate()
+    out_b, tr_b = P.HierarchicalSession(tw, dw, prompt, spec, shards=one_rank).generate()
+    assert out_a == out_b
+    assert tr_a.summary() == tr_b.summary()
+    ar = P.autoregressive_generate(tw, prompt, 900 + 20, 0.0, 0, shards=one_rank, chunk=8)
+    assert ar == P.autoregressive_generate(tw, prompt, 900 + 20, 0.0, 0)
+
+
+def _fill(cache, K, V, positions):
+    """write rows at absolute positions into a (possibly sharded) full cache"""
+    for l in range(cache.n_layers):
+        cache._n[l] = 0
+        cache.append(l, K[l], V[l])
+    cache.frontier = cache.committed = len(positions)
+
+
+def test_shard_partials_merge_equals_unsharded_attention(P):
+    """G shard caches over one sequence: hs_attention_partial per shard +
+    hs_shard_merge (rank order) == hs_attention over the whole cache."""
+    from paper_2404_11912_b200._abi import HsStep, check, lib
+    from paper_2404_11912_b200.runtime import ptr, stream_ptr, workspaces
+    from paper_2404_11912_b200.shard import shard_plan
+    rng = np.random.default_rng(7)
+    L, kvh, H, dh = 1, 4, 8, 128
+    for n, G, t, dh in ((6000, 4, 7, 128), (5000, 3, 1, 128), (777, 2, 5, 64), (333, 4, 3, 64)):
+        K = rng.normal(0, 1, (L, n, kvh, dh)).astype(np.float32)
+        V = rng.normal(0, 1, (L, n, kvh, dh)).astype(np.float32)
+        q = torch.from_numpy(rng.normal(0, 1, (t, H, dh)).astype(np.float32)).cuda()
+        full = P.FullCache(L, kvh, dh, n + 64)
+        _fill(full, K, V, range(n))
+        st = HsStep()
+        st.pos0, st.n_view, st.split = n - t, n, 1024
+        nb = lib.hs_attention_workspace_bytes(t, H, dh, n, 1024)
+        ws = workspaces.get("shard_t", nb)
+        ref = torch.zeros((t, H * dh), device="cuda")
+        check(lib.hs_attention(full._ref, 0, C.byref(st), H, ptr(q), t, ptr(ref), ptr(ws), nb, stream_ptr()))
+        parts = torch.zeros((G, t * H, dh + 2), device="cuda")
+        for r, (lo, hi) in enumerate(shard_plan(n, G, 8)):
+            sc = P.FullCache(L, kvh, dh, n + 64, None, lo, hi)
+            end = n if hi is None else min(n, hi)
+            if end > lo:
+                for l in range(L):
+                    sc._write_rows(l, K[l, lo:end], V[l, lo:end], np.arange(end - lo), np.arange(lo, end))
+            s2 = HsStep()
+            s2.pos0, s2.n_view, s2.split, s2.pos_base = n - t, max(0, end - lo), 1024, lo
+            check(lib.hs_attention_partial(sc._ref, 0, C.byref(s2), H, ptr(q), t, ptr(parts[r]), ptr(ws), nb,
+                                           stream_ptr()))
+        out = torch.zeros((t, H * dh), device="cuda")
+        check(lib.hs_shard_merge(ptr(parts), G, t * H, dh, ptr(out), stream_ptr()))
+        a, b = out.cpu().numpy(), ref.cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max(), (n, G, t)
+
+
+def test_shard_scores_and_gathers_assemble_the_unsharded_build(P):
+    """Per-shard chunk scores concatenated in rank order are bit-identical to
+    the unsharded scores; per-shard gathers (zeros for foreign chunks) sum to
+    the unsharded retrieval buffer."""
+    from paper_2404_11912_b200._abi import check, lib
+    from paper_2404_11912_b200.runtime import ptr, stream_ptr
+    from paper_2404_11912_b200.shard import shard_chunk_counts, shard_plan
+    rng = np.random.default_rng(11)
+    L, kvh, H, dh, chunk, budget = 2, 2, 4, 64, 8, 256
+    for n, G in ((3001, 2), (4096, 4), (999, 3)):
+        K = rng.normal(0, 1, (L, n, kvh, dh)).astype(np.float32)
+        V = rng.normal(0, 1, (L, n, kvh, dh)).astype(np.float32)
+        q = rng.normal(0, 1, (L, H, dh)).astype(np.float32)
+        full = P.FullCache(L, kvh, dh, n + 64)
+        _fill(full, K, V, range(n))
+        rc = P.RetrievalCache(L, kvh, dh, P.RetrievalConfig(chunk_size=chunk, budget=budget))
+        table = rc.build(full, q, n)
+        want_scores = np.stack(table.scores)
+        plan = shard_plan(n, G, chunk)
+        counts = shard_chunk_counts(plan, n, chunk)
+        qd = torch.from_numpy(q).cuda()
+        got, acc_k, acc_v = [], torch.zeros_like(rc.k, dtype=torch.float32), torch.zeros_like(rc.v, dtype=torch.float32)
+        for r, (lo, hi) in enumerate(plan):
+            sc = P.FullCache(L, kvh, dh, n + 64, None, lo, hi)
+            end = n if hi is None else min(n, hi)
+            for l in range(L):
+                if end > lo:
+                    sc._write_rows(l, K[l, lo:end], V[l, lo:end], np.arange(end - lo), np.arange(lo, end))
+            out = torch.empty((L, counts[r]), dtype=torch.float64, device="cuda")
+            if counts[r]:
+                check(lib.hs_chunk_score(ptr(sc.k), 1, kvh * sc.cap * dh, sc.cap * dh, dh, L, kvh, dh, end - lo,
+                                         chunk, ptr(qd), H, ptr(out), stream_ptr()))
+            got.append(out.cpu().numpy())
+            part = P.RetrievalCache(L, kvh, dh, P.RetrievalConfig(chunk_size=chunk, budget=budget))
+            part.chosen.copy_(rc.chosen)
+            nch = int(rc.table._n_imp)
+            check(lib.hs_retrieval_gather(sc._ref, part._ref, ptr(part.chosen), part.quota, nch, chunk, n, lo,
+                                          hi or 0, stream_ptr()))
+            acc_k += part.k.float()
+            acc_v += part.v.float()
+            assert torch.equal(part.pos[:, :rc.n_sel], rc.pos[:, :rc.n_sel])
+        assert np.array_equal(np.concatenate(got, axis=1), want_scores)
+        assert torch.equal(acc_k[:, :, :rc.n_sel].to(torch.bfloat16), rc.k[:, :, :rc.n_sel])
+        assert torch.equal(acc_v[:, :, :rc.n_sel].to(torch.bfloat16), rc.v[:, :, :rc.n_sel])
+
+
+def test_sharded_cache_rejects_misaligned_bounds(P):
+    from paper_2404_11912_b200._abi import check, lib
+    from paper_2404_11912_b200.runtime import ptr, stream_ptr
+    src = P.FullCache(1, 2, 64, 512, None, 4, 260)
+    dst = P.RetrievalCache(1, 2, 64, P.RetrievalConfig(chunk_size=8, budget=64))
+    with pytest.raises(ValueError):
+        check(lib.hs_retrieval_gather(src._ref, dst._ref, ptr(dst.chosen), dst.quota, 1, 8, 100, 4, 260,
+                                      stream_ptr()))
