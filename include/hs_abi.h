@@ -204,6 +204,13 @@ int hs_attention_partial(const HsCache *c, int layer, const HsStep *st, int n_he
                          const float *q, int t, float *packed, void *workspace, size_t ws_bytes,
                          void *stream);
 
+/* live timing of the dominant kernel for bench.py: while enabled, every
+ * attention launch of hs_forward over a view of >= min_view keys is
+ * bracketed by CUDA events on its stream; read returns the summed device
+ * time, the algorithmic K+V bytes and the launch count (enable resets).     */
+int hs_profile_attention(int enable, int min_view);
+int hs_profile_attention_read(double *ms_total, long long *bytes_total, int *launches);
+
 /* chunk scoring, score_chunks (caches.py:414-436), all layers at once.
  * keys: layer l, kv head h, token i at  keys + l*ls + h*hs + i*ts  (bf16 if
  * key_bf16 else fp32); queries [L][H][dh] fp32; scores [L][n_chunks] fp64.  */

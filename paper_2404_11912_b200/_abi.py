@@ -93,6 +93,8 @@ _SIGS = {
     "hs_verify_token": (i32, [i32, vp, vp, vp, vp, vp, vp]),
     "hs_correct_token": (i32, [vp, vp, i32, vp, vp, vp, vp]),
     "hs_shard_merge": (i32, [vp, i32, i32, i32, vp, vp]),
+    "hs_profile_attention": (i32, [i32, i32]),
+    "hs_profile_attention_read": (i32, [_P(f64), _P(i64), _P(i32)]),
     "hs_comm_id_bytes": (sz, []),
     "hs_comm_unique_id": (i32, [vp]),
     "hs_comm_init": (i32, [_P(vp), vp, i32, i32]),

@@ -34,7 +34,7 @@ import torch
 from ._abi import (HS_APPEND_LINEAR, HS_APPEND_POS, HS_APPEND_RING, HS_KV_LINEAR, HS_KV_SLOTTED, HsCache,
                    HsStep, check, lib)
 from .errors import CapacityError, ContractError, ShapeError
-from .runtime import as_device_f32, device, ptr, stream_ptr, workspaces
+from .runtime import STATS, as_device_f32, device, ptr, stream_ptr, workspaces
 
 FULL_SPLIT = 2048     # keys per attention split over the full cache (fixed: t-invariant rows)
 SMALL_SPLIT = 512     # keys per split over retrieval / streaming views
@@ -511,6 +511,8 @@ class RetrievalCache(KVCache):
         self.n_spec = [0] * self.n_layers
         self.frontier = self.committed = upto
         self.builds += 1
+        row = self.n_kv_heads * self.head_dim * 2 * self.n_layers
+        STATS["alg_bytes"] += source._local(upto) * row + self.n_sel * row * 4   # K read + K,V gather r/w
         self.table = ChunkScoreTable(cfg.chunk_size, upto, self.n_layers, scores, self.importance, n_chosen,
                                      clamped)
         return self.table

@@ -12,6 +12,8 @@
 // Grid: (n_splits, kv_heads, query-row blocks of 16).  Splits are fixed-size
 // ranges of slots, so a query's partial state never depends on how many
 // other queries share the launch; the combine walks splits in index order.
+#include <vector>
+
 #include "hs_common.cuh"
 
 namespace hs {
@@ -264,6 +266,35 @@ size_t attention_ws(int t, int H, int DH, int n_view, int split) {
 int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *part_m,
                         float *part_l, float *part_o, int n_splits, cudaStream_t stream);
 
+// ---- live timing of the dominant kernel (bench.py roofline) --------------------
+// When enabled, every attention launch over a view of >= min_view keys is
+// bracketed by CUDA events on its own stream; bench.py reads the summed
+// durations and algorithmic bytes after its timed region.
+struct ProfPair { cudaEvent_t a, b; long long bytes; };
+static std::vector<ProfPair> g_prof;
+static size_t g_prof_used = 0;
+static int g_prof_on = 0, g_prof_min = 0, g_prof_dropped = 0;
+
+static ProfPair *prof_begin(const HsCache *c, const HsStep *st, cudaStream_t stream) {
+  if (!g_prof_on || st->n_view < g_prof_min) return nullptr;
+  if (g_prof_used == g_prof.size()) { ++g_prof_dropped; return nullptr; }
+  ProfPair *p = &g_prof[g_prof_used++];
+  p->bytes = (long long)st->n_view * c->n_kv_heads * c->head_dim * 2 * 2;
+  cudaEventRecord(p->a, stream);
+  return p;
+}
+
+int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
+                     float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream);
+
+int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
+                           float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream) {
+  ProfPair *p = prof_begin(c, st, stream);
+  const int rc = launch_attention(c, layer, st, H, q, t, out, packed, ws, ws_bytes, stream);
+  if (p) cudaEventRecord(p->b, stream);
+  return rc;
+}
+
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
                      float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream) {
   const int DH = c->head_dim, KVH = c->n_kv_heads;
@@ -313,6 +344,42 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
 }
 
 }  // namespace hs
+
+extern "C" int hs_profile_attention(int enable, int min_view) {
+  using namespace hs;
+  if (enable) {
+    if (g_prof.empty()) {
+      g_prof.resize(16384);
+      for (auto &p : g_prof) {
+        if (cudaEventCreate(&p.a) != cudaSuccess || cudaEventCreate(&p.b) != cudaSuccess)
+          return set_error(HS_ERR_CUDA, "profile: cudaEventCreate failed");
+      }
+    }
+    g_prof_used = 0;
+    g_prof_dropped = 0;
+    g_prof_min = min_view;
+  }
+  g_prof_on = enable;
+  return HS_OK;
+}
+
+extern "C" int hs_profile_attention_read(double *ms_total, long long *bytes_total, int *launches) {
+  using namespace hs;
+  double ms = 0.0;
+  long long bytes = 0;
+  for (size_t i = 0; i < g_prof_used; ++i) {
+    float e = 0.f;
+    if (cudaEventSynchronize(g_prof[i].b) != cudaSuccess || cudaEventElapsedTime(&e, g_prof[i].a, g_prof[i].b) != cudaSuccess)
+      return set_error(HS_ERR_CUDA, "profile: event read failed");
+    ms += e;
+    bytes += g_prof[i].bytes;
+  }
+  *ms_total = ms;
+  *bytes_total = bytes;
+  *launches = (int)g_prof_used;
+  return g_prof_dropped ? set_error(HS_ERR_VALUE, "profile: %d launches not recorded (pool full)", g_prof_dropped)
+                        : HS_OK;
+}
 
 extern "C" size_t hs_attention_workspace_bytes(int t, int n_heads, int head_dim, int n_view, int split) {
   return hs::attention_ws(t, n_heads, head_dim, n_view, split);

@@ -15,8 +15,8 @@ int launch_gemv(const float *x, int ldx, int t, int K, const uint16_t *w, int ld
 int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x, cudaStream_t st);
 int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv, int t,
                        float *q_out, float *q_stash, cudaStream_t st);
-int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
-                     float *packed, void *ws, size_t ws_bytes, cudaStream_t stream);
+int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
+                           float *packed, void *ws, size_t ws_bytes, cudaStream_t stream);
 int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, cudaStream_t st);
 int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
@@ -172,11 +172,11 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
     if (sharded) {
       // this rank's partial softmax state -> all ranks -> rank-ordered merge
       const size_t part = (size_t)t * H * (dh + 2) * 4;
-      HS_TRY(launch_attention(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s));
+      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s));
       HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
       HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, w.attn, s));
     } else {
-      HS_TRY(launch_attention(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s));
+      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s));
     }
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;

@@ -28,7 +28,7 @@ import torch
 from . import _abi
 from ._abi import HsModel, check, lib
 from .errors import CapacityError, FiniteError, ShapeError
-from .runtime import (UniformStream, as_device_f32, as_device_f64, device, ptr, stream_ptr,
+from .runtime import (STATS, UniformStream, as_device_f32, as_device_f64, device, ptr, stream_ptr,
                       to_i32_device, workspaces)
 
 BOS = 256
@@ -459,6 +459,7 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
         ws = dm.workspace(nbytes)
         check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), shard_ref, ptr(tok) + 4 * a, b - a,
                              ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))
+        STATS["alg_bytes"] += dm.weight_bytes + step.n_view * cfg.n_kv_heads * cfg.head_dim * 4 * cfg.n_layers
         cache._advance(b - a)
     if recorder is not None:
         recorder.query_position = cache.frontier - 1

@@ -14,6 +14,12 @@ import numpy as np
 import torch
 
 
+# algorithmic HBM bytes of the work issued so far (weights + K/V views of every
+# forward, K reads + gathers of every retrieval build); bench.py differences it
+# around its timed region for the per-token roofline
+STATS = {"alg_bytes": 0}
+
+
 def device() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2404_11912_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
