@@ -37,7 +37,8 @@ from .errors import CapacityError, ContractError, ShapeError
 from .runtime import STATS, as_device_f32, device, ptr, stream_ptr, workspaces
 
 FULL_SPLIT = 2048     # keys per attention split over the full cache (fixed: t-invariant rows)
-SMALL_SPLIT = 512     # keys per split over retrieval / streaming views
+SMALL_SPLIT = 512     # keys per split over the retrieval view
+STREAM_SPLIT = 64     # keys per split over the (small) streaming window: one CTA per 64 keys
 
 
 @dataclass(frozen=True)
@@ -389,7 +390,7 @@ class StreamingCache(KVCache):
         s.n_view = self.cap
         s.window = self.window
         s.win_lo = self.lo
-        s.split = SMALL_SPLIT
+        s.split = STREAM_SPLIT
         return s
 
     def _advance(self, t):

@@ -59,37 +59,17 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
                    uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t gemv_tc_ws_bytes(int N, int nkb);
 
-struct ChainSpec {
-  const uint16_t *w;
-  int ldw, N, K, epilogue;
-  const float *src;
-  int ld_src;
-  const float *gain;
-  int ssq_parts;
-  float *y;
-  int ldy;
-};
-int launch_chain(const ChainSpec *ps, int n, int t, float eps, void *ws, size_t ws_bytes, cudaStream_t st);
-
-static ChainSpec chain_spec(const uint16_t *w, int ldw, int N, int K, int epilogue, const float *src, int ld_src,
-                            const float *gain, int ssq_parts, float *y, int ldy) {
-  ChainSpec c;
-  c.w = w; c.ldw = ldw; c.N = N; c.K = K; c.epilogue = epilogue; c.src = src; c.ld_src = ld_src;
-  c.gain = gain; c.ssq_parts = ssq_parts; c.y = y; c.ldy = ldy;
-  return c;
-}
-size_t chain_ws_for_model(const HsModel *m);
-
 // Workspace layout.  The head is position-independent so that the regions
-// which must stay zero between calls (chain K-split counters and grid
-// barriers, left zero by every launch) never move:
-//   [chain region: counters | barriers | row sums of squares | K-split partials]
-//   then per-call regions: x, qkv, q, attn, act, attention partials and, when
+// which must stay zero/clean between calls never move:
+//   [gemv counters + partials (max over the model's matrices)]
+//   [Xd: 24 x ld_d bf16 split operand][Xf: 24 x ld_ff bf16]
+//   then per-call regions: x, qkv, q, attn, attention partials and, when
 //   sharded, the packed per-rank partial states (send) and their gather (recv).
 struct FwdWs {
-  void *chain_ws;
-  size_t chain_bytes;
-  float *x, *qkv, *q, *attn, *act;
+  void *gemv_ws;
+  size_t gemv_bytes;
+  uint16_t *xd, *xf;
+  float *x, *qkv, *q, *attn;
   void *att_ws;
   size_t att_bytes;
   float *send, *recv;
@@ -97,17 +77,30 @@ struct FwdWs {
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+static size_t gemv_region(const HsModel *m) {
+  const int d = m->d_model, kv = m->n_kv_heads * m->head_dim;
+  size_t g = 0;
+  const int Ns[5] = {d + 2 * kv, d, 2 * m->d_ff, d, m->vocab_size};
+  const int Ks[5] = {m->ld_d, m->ld_d, m->ld_d, m->ld_ff, m->ld_d};
+  for (int i = 0; i < 5; ++i) {
+    size_t b = gemv_tc_ws_bytes(Ns[i], Ks[i] / 64);
+    if (b > g) g = b;
+  }
+  return align256(g);
+}
+
 static size_t carve(const HsModel *m, int t, int n_view, int split, int world, char *base, FwdWs *w) {
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim;
   size_t off = 0;
   auto take = [&](size_t bytes) { char *p = base ? base + off : nullptr; off += align256(bytes); return p; };
-  w->chain_bytes = align256(chain_ws_for_model(m));
-  w->chain_ws = take(w->chain_bytes);
+  w->gemv_bytes = gemv_region(m);
+  w->gemv_ws = take(w->gemv_bytes);
+  w->xd = (uint16_t *)take((size_t)24 * m->ld_d * 2);
+  w->xf = (uint16_t *)take((size_t)24 * m->ld_ff * 2);
   w->x = (float *)take((size_t)t * d * 4);
   w->qkv = (float *)take((size_t)t * (H + 2 * KVH) * dh * 4);
   w->q = (float *)take((size_t)t * H * dh * 4);
   w->attn = (float *)take((size_t)t * d * 4);
-  w->act = (float *)take((size_t)t * m->d_ff * 4);
   w->att_bytes = attention_ws(t, H, dh, n_view, split);
   w->att_ws = take(w->att_bytes);
   const size_t part = (size_t)t * H * (dh + 2) * 4;
@@ -133,9 +126,9 @@ extern "C" size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view
 }
 
 extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
-  return 16384 * 4 + 2048;   // chain counters, barriers and claim counters at the workspace head
+  // bytes at the head of the workspace that must be zero before the first call
+  return hs::gemv_region(m) + hs::align256((size_t)24 * m->ld_d * 2) + hs::align256((size_t)24 * m->ld_ff * 2);
 }
-
 
 extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                           const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
@@ -163,19 +156,18 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
   int rc;
 #define HS_TRY(call) do { if ((rc = (call)) != HS_OK) return rc; } while (0)
   HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
-  const int d_tiles = (d + 127) / 128;
-  // layer 0's RMSNorm + wqkv (statistics from the embedding rows)
-  for (int r0 = 0; r0 < t; r0 += 8) {
-    const int tp = t - r0 < 8 ? t - r0 : 8;
-    ChainSpec qkv0 = chain_spec(m->wqkv, m->ld_d, nqkv, d, 0, w.x + (size_t)r0 * d, d, m->attn_norm, 0,
-                                w.qkv + (size_t)r0 * nqkv, nqkv);
-    HS_TRY(launch_chain(&qkv0, 1, tp, eps, w.chain_ws, w.chain_bytes, s));
-  }
   for (int l = 0; l < m->n_layers; ++l) {
+    const uint16_t *wqkv = m->wqkv + (size_t)l * nqkv * m->ld_d;
     const uint16_t *wo = m->wo + (size_t)l * d * m->ld_d;
     const uint16_t *wgu = m->wgu + (size_t)l * 2 * ff * m->ld_d;
     const uint16_t *wdn = m->wdown + (size_t)l * d * m->ld_ff;
-    const float *mn = m->mlp_norm + (size_t)l * d;
+    const float *an = m->attn_norm + (size_t)l * d, *mn = m->mlp_norm + (size_t)l * d;
+    for (int r0 = 0; r0 < t; r0 += 8) {
+      const int tp = t - r0 < 8 ? t - r0 : 8;
+      HS_TRY(launch_split_rows(w.x + (size_t)r0 * d, d, tp, d, m->ld_d, an, eps, w.xd, s));
+      HS_TRY(launch_gemv_tc(w.xd, tp, wqkv, m->ld_d, nqkv, 0, w.qkv + (size_t)r0 * nqkv, nqkv, nullptr, 0, w.gemv_ws,
+                            w.gemv_bytes, s));
+    }
     HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
     if (sharded) {
       // this rank's partial softmax state -> all ranks -> rank-ordered merge
@@ -186,24 +178,22 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
     } else {
       HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s));
     }
-    // one persistent chain: wo (+res) -> norm + gate|up (SwiGLU) -> down (+res)
-    // -> norm + next layer's wqkv (or final norm + lm_head)
-    const bool last = l + 1 == m->n_layers;
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
       float *xr = w.x + (size_t)r0 * d;
-      ChainSpec ph[4];
-      ph[0] = chain_spec(wo, m->ld_d, d, d, 1, w.attn + (size_t)r0 * d, d, nullptr, 0, xr, d);
-      ph[1] = chain_spec(wgu, m->ld_d, 2 * ff, d, 2, xr, d, mn, d_tiles, w.act + (size_t)r0 * ff, ff);
-      ph[2] = chain_spec(wdn, m->ld_ff, d, ff, 1, w.act + (size_t)r0 * ff, ff, nullptr, 0, xr, d);
-      if (last)
-        ph[3] = chain_spec(m->head, m->ld_d, m->vocab_size, d, 0, xr, d, m->final_norm, d_tiles,
-                           logits + (size_t)r0 * m->vocab_size, m->vocab_size);
-      else
-        ph[3] = chain_spec(m->wqkv + (size_t)(l + 1) * nqkv * m->ld_d, m->ld_d, nqkv, d, 0, xr, d,
-                           m->attn_norm + (size_t)(l + 1) * d, d_tiles, w.qkv + (size_t)r0 * nqkv, nqkv);
-      HS_TRY(launch_chain(ph, 4, tp, eps, w.chain_ws, w.chain_bytes, s));
+      HS_TRY(launch_split_rows(w.attn + (size_t)r0 * d, d, tp, d, m->ld_d, nullptr, 0.f, w.xd, s));
+      HS_TRY(launch_gemv_tc(w.xd, tp, wo, m->ld_d, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
+      HS_TRY(launch_split_rows(xr, d, tp, d, m->ld_d, mn, eps, w.xd, s));
+      HS_TRY(launch_gemv_tc(w.xd, tp, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes,
+                            s));
+      HS_TRY(launch_gemv_tc(w.xf, tp, wdn, m->ld_ff, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
     }
+  }
+  for (int r0 = 0; r0 < t; r0 += 8) {
+    const int tp = t - r0 < 8 ? t - r0 : 8;
+    HS_TRY(launch_split_rows(w.x + (size_t)r0 * d, d, tp, d, m->ld_d, m->final_norm, eps, w.xd, s));
+    HS_TRY(launch_gemv_tc(w.xd, tp, m->head, m->ld_d, m->vocab_size, 0, logits + (size_t)r0 * m->vocab_size,
+                          m->vocab_size, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
   }
 #undef HS_TRY
   return HS_OK;

@@ -19,8 +19,6 @@
 // result does not depend on the batch size).
 #include <cudaTypedefs.h>
 
-#include <stdlib.h>
-
 #include <mutex>
 #include <unordered_map>
 
@@ -33,8 +31,7 @@ constexpr int TC_BM = 128;        // output rows per tile (MMA M)
 constexpr int TC_BK = 64;         // K per stage (one 128-byte swizzle row)
 constexpr int TC_XN = 24;         // activation columns: 3 splits x 8 rows
 constexpr int TC_T = 8;           // activation rows per pass
-constexpr int TC_STAGES = 3;
-constexpr int TC_THREADS = 192;
+constexpr int TC_STAGES = 5;
 constexpr int TC_W_BYTES = TC_BM * TC_BK * 2;    // 16 KB
 constexpr int TC_X_BYTES = TC_XN * TC_BK * 2;    // 3 KB
 constexpr int TC_SMEM = TC_STAGES * (TC_W_BYTES + TC_X_BYTES) + 1024 + 256;
@@ -152,7 +149,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS) split_rows_kernel(const float *
 }
 
 struct GemvTcArgs {
-  int N, nkb, ks, t, epilogue, n_tiles, n_items, blocked;
+  int N, nkb, ks, t, epilogue, n_tiles;
   float *y;
   int ldy;
   uint16_t *xs_out;   // swiglu epilogue: split of act written here ([24][ld_xs_out]) if non-null
@@ -196,44 +193,33 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
   }
 }
 
-// Persistent kernel: CTA b owns the work items b, b + G, b + 2G, ... (item =
-// (tile, K split)); the TMA ring runs across item boundaries, so a CTA streams
-// its whole share of the matrix without draining the pipeline, and the TMEM
-// accumulator is double-buffered so the epilogue of item j overlaps the MMAs
-// of item j + 1.  Warp 0: TMA producer; warp 1: MMA issuer; warps 2-5:
-// epilogue (warp w reads TMEM lanes 32 * (w % 4) ..).
-__global__ void __launch_bounds__(TC_THREADS, 2) gemv_tc_kernel(const __grid_constant__ CUtensorMap tmW,
-                                                                const __grid_constant__ CUtensorMap tmX,
-                                                                GemvTcArgs a) {
+__global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                         const __grid_constant__ CUtensorMap tmX, GemvTcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *sW = base;
   unsigned char *sX = base + TC_STAGES * TC_W_BYTES;
   uint64_t *full = reinterpret_cast<uint64_t *>(sX + TC_STAGES * TC_X_BYTES);
   uint64_t *empty = full + TC_STAGES;
-  uint64_t *tfull = empty + TC_STAGES;     // [2] accumulator ready
-  uint64_t *tempty = tfull + 2;            // [2] accumulator drained (4 epilogue warps)
-  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *accum = empty + TC_STAGES;
+  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(accum + 1);
   int *flag = reinterpret_cast<int *>(tmem_base + 1);
 
   tc::grid_dep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, split = blockIdx.y;
   const int per = a.nkb / a.ks, rem = a.nkb % a.ks;
-  auto item_range = [&](int item, int &tile, int &kb0, int &nk) {
-    tile = item / a.ks;
-    const int split = item % a.ks;
-    kb0 = split * per + min(split, rem);
-    nk = per + (split < rem ? 1 : 0);
-  };
+  const int kb0 = split * per + min(split, rem);
+  const int nk = per + (split < rem ? 1 : 0);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmW);
     tc::tma_prefetch(&tmX);
     for (int s = 0; s < TC_STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { tc::mbar_init(&tfull[b], 1); tc::mbar_init(&tempty[b], 4); }
+    tc::mbar_init(accum, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc<64>(tmem_base);
+  if (warp == 1) tc::tmem_alloc<32>(tmem_base);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -242,38 +228,24 @@ __global__ void __launch_bounds__(TC_THREADS, 2) gemv_tc_kernel(const __grid_con
   if (warp == 0) {
     if (tc::elect_one()) {
       // Programmatic dependent launch: the weights never depend on the
-      // previous kernel, so the first TC_STAGES weight tiles stream in while
-      // that kernel drains; the activation tiles wait for it.
+      // previous kernel, so the first stages' weight tiles stream in while
+      // that kernel drains; only the activation tiles wait for it.
       const uint64_t pol = tc::policy_evict_first();   // weights are streamed exactly once
-      int pend_k[TC_STAGES];
-      int npend = 0;
-      bool waited = false;
-      uint32_t g = 0;
-      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-        int tile, kb0, nk;
-        item_range(item, tile, kb0, nk);
-        for (int i = 0; i < nk; ++i, ++g) {
-          const int s = g % TC_STAGES;
-          const uint32_t ph = (g / TC_STAGES) & 1;
-          const int k = (kb0 + i) * TC_BK;
-          if (!waited && g == TC_STAGES) {
-            tc::grid_dep_wait();
-            for (int j = 0; j < npend; ++j) tc::tma_load_2d(sX + j * TC_X_BYTES, &tmX, &full[j], pend_k[j], 0);
-            waited = true;
-          }
-          tc::mbar_wait(&empty[s], ph ^ 1);
-          tc::mbar_expect_tx(&full[s], TC_W_BYTES + TC_X_BYTES);
-          if (a.blocked)
-            tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], 0, (tile * a.nkb + kb0 + i) * TC_BM, pol);
-          else
-            tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], k, tile * TC_BM, pol);
-          if (waited) tc::tma_load_2d(sX + s * TC_X_BYTES, &tmX, &full[s], k, 0);
-          else pend_k[npend++] = k;
-        }
+      const int npre = nk < TC_STAGES ? nk : TC_STAGES;
+      for (int i = 0; i < npre; ++i) {
+        tc::mbar_expect_tx(&full[i], TC_W_BYTES + TC_X_BYTES);
+        tc::tma_load_2d_hint(sW + i * TC_W_BYTES, &tmW, &full[i], (kb0 + i) * TC_BK, tile * TC_BM, pol);
       }
-      if (!waited) {
-        tc::grid_dep_wait();
-        for (int j = 0; j < npend; ++j) tc::tma_load_2d(sX + j * TC_X_BYTES, &tmX, &full[j], pend_k[j], 0);
+      tc::grid_dep_wait();
+      for (int i = 0; i < npre; ++i) tc::tma_load_2d(sX + i * TC_X_BYTES, &tmX, &full[i], (kb0 + i) * TC_BK, 0);
+      for (int i = npre; i < nk; ++i) {
+        const int s = i % TC_STAGES;
+        const uint32_t ph = (i / TC_STAGES) & 1;
+        tc::mbar_wait(&empty[s], ph ^ 1);
+        tc::mbar_expect_tx(&full[s], TC_W_BYTES + TC_X_BYTES);
+        const int k = (kb0 + i) * TC_BK;
+        tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], k, tile * TC_BM, pol);
+        tc::tma_load_2d(sX + s * TC_X_BYTES, &tmX, &full[s], k, 0);
       }
     } else {
       tc::grid_dep_wait();
@@ -281,86 +253,69 @@ __global__ void __launch_bounds__(TC_THREADS, 2) gemv_tc_kernel(const __grid_con
   } else if (warp == 1) {
     if (tc::elect_one()) {
       constexpr uint32_t idesc = tc::idesc_bf16(TC_BM, TC_XN, 0, 0);
-      uint32_t g = 0, j = 0;
-      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x, ++j) {
-        int tile, kb0, nk;
-        item_range(item, tile, kb0, nk);
-        const int b = j & 1;
-        tc::mbar_wait(&tempty[b], ((j >> 1) & 1) ^ 1);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % TC_STAGES;
+        const uint32_t ph = (i / TC_STAGES) & 1;
+        tc::mbar_wait(&full[s], ph);
         tc::fence_after();
-        for (int i = 0; i < nk; ++i, ++g) {
-          const int s = g % TC_STAGES;
-          tc::mbar_wait(&full[s], (g / TC_STAGES) & 1);
-          tc::fence_after();
-          const uint64_t da = tc::desc_k_sw128(sW + s * TC_W_BYTES);
-          const uint64_t db = tc::desc_k_sw128(sX + s * TC_X_BYTES);
+        const uint64_t da = tc::desc_k_sw128(sW + s * TC_W_BYTES);
+        const uint64_t db = tc::desc_k_sw128(sX + s * TC_X_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / 16; ++kk)   // +32 bytes per K16 step inside the swizzle row
-            tc::mma_bf16(taddr + b * 32, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
-          tc::mma_commit(&empty[s]);
-        }
-        tc::mma_commit(&tfull[b]);
+        for (int kk = 0; kk < TC_BK / 16; ++kk)   // +32 bytes per K16 step inside the swizzle row
+          tc::mma_bf16(taddr, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+        tc::mma_commit(&empty[s]);
       }
+      tc::mma_commit(accum);
     }
+  }
+  if (warp != 0) tc::grid_dep_wait();   // epilogue reads y written by earlier kernels
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers ---------------------------------------------------
+  tc::mbar_wait(accum, 0);
+  tc::fence_after();
+  const int row = warp * 32 + lane;
+  const uint32_t tl = taddr + ((uint32_t)(warp * 32) << 16);
+  float h[8], m[8], l[8], v[TC_T];
+  tc::tmem_ld8(tl + 0, h);
+  tc::tmem_ld8(tl + 8, m);
+  tc::tmem_ld8(tl + 16, l);
+  tc::tmem_ld_wait();
+#pragma unroll
+  for (int r = 0; r < TC_T; ++r) v[r] = nk > 0 ? (h[r] + m[r]) + l[r] : 0.f;
+  const int o = tile * TC_BM + row;
+
+  if (a.ks == 1) {
+    finalize(a, o, v, lane);
   } else {
-    // ---- epilogue warps: TMEM -> registers -> partial / finalize ----------------------
-    tc::grid_dep_wait();   // y, partials and counters are touched by earlier kernels
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const int etid = threadIdx.x - 64;   // 0..127
-    uint32_t j = 0;
-    for (int item = blockIdx.x; item < a.n_items; item += gridDim.x, ++j) {
-      int tile, kb0, nk;
-      item_range(item, tile, kb0, nk);
-      const int b = j & 1;
-      tc::mbar_wait(&tfull[b], (j >> 1) & 1);
-      tc::fence_after();
-      const uint32_t tl = taddr + b * 32 + ((uint32_t)(q * 32) << 16);
-      float h[8], m[8], l[8], v[TC_T];
-      tc::tmem_ld8(tl + 0, h);
-      tc::tmem_ld8(tl + 8, m);
-      tc::tmem_ld8(tl + 16, l);
-      tc::tmem_ld_wait();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[b]);
-#pragma unroll
-      for (int r = 0; r < TC_T; ++r) v[r] = (h[r] + m[r]) + l[r];
-      const int o = tile * TC_BM + row;
-      if (a.ks == 1) {
-        finalize(a, o, v, lane);
-        continue;
-      }
-      const int split = item % a.ks;
-      float *pp = a.partial + ((size_t)split * a.n_tiles * TC_BM + o) * TC_T;
-      *reinterpret_cast<float4 *>(pp) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4 *>(pp + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    float *pp = a.partial + ((size_t)split * a.n_tiles * TC_BM + o) * TC_T;
+    *reinterpret_cast<float4 *>(pp) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4 *>(pp + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int old = atomicAdd(&a.counters[tile], 1);
+      *flag = (old == a.ks - 1);
+    }
+    __syncthreads();
+    if (*flag) {
       __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (etid == 0) {
-        const int old = atomicAdd(&a.counters[tile], 1);
-        *flag = (old == a.ks - 1);
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (*flag) {
-        __threadfence();
 #pragma unroll
-        for (int r = 0; r < TC_T; ++r) v[r] = 0.f;
-        for (int s2 = 0; s2 < a.ks; ++s2) {
-          const float *qq = a.partial + ((size_t)s2 * a.n_tiles * TC_BM + o) * TC_T;
-          const float4 x0 = __ldcg(reinterpret_cast<const float4 *>(qq));
-          const float4 x1 = __ldcg(reinterpret_cast<const float4 *>(qq + 4));
-          v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
-          v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
-        }
-        finalize(a, o, v, lane);
-        if (etid == 0) a.counters[tile] = 0;   // self-cleaning for the next launch
+      for (int r = 0; r < TC_T; ++r) v[r] = 0.f;
+      for (int s2 = 0; s2 < a.ks; ++s2) {
+        const float *q = a.partial + ((size_t)s2 * a.n_tiles * TC_BM + o) * TC_T;
+        const float4 x0 = __ldcg(reinterpret_cast<const float4 *>(q));
+        const float4 x1 = __ldcg(reinterpret_cast<const float4 *>(q + 4));
+        v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
+        v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
       }
+      finalize(a, o, v, lane);
+      if (threadIdx.x == 0) a.counters[tile] = 0;   // self-cleaning for the next launch
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc<64>(taddr);
+  if (warp == 1) tc::tmem_dealloc<32>(taddr);
 }
 
 // K split: a function of (N, K) only.  Picks the split count that fills
@@ -415,17 +370,12 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   HS_REQUIRE(tiles <= TC_COUNTER_INTS, HS_ERR_SHAPE, "gemv_tc: N too large");
   HS_REQUIRE(ws_bytes >= gemv_tc_ws_bytes(N, nkb), HS_ERR_VALUE, "gemv_tc: workspace too small");
   CUtensorMap mw, mx;
-  static int blocked_test = -1;
-  if (blocked_test < 0) { const char *e = getenv("HS_GEMV_BLOCKED_TEST"); blocked_test = e && e[0] == '1'; }
-  int rc = blocked_test ? get_tmap_bf16(w, (uint64_t)TC_BK, (uint64_t)N * (ldw / TC_BK), (uint64_t)TC_BK * 2, TC_BM, &mw)
-                        : get_tmap_bf16(w, (uint64_t)ldw, (uint64_t)N, (uint64_t)ldw * 2, TC_BM, &mw);
+  int rc = get_tmap_bf16(w, (uint64_t)ldw, (uint64_t)N, (uint64_t)ldw * 2, TC_BM, &mw);
   if (rc != HS_OK) return rc;
   rc = get_tmap_bf16(xs, (uint64_t)ldw, (uint64_t)TC_XN, (uint64_t)ldw * 2, TC_XN, &mx);
   if (rc != HS_OK) return rc;
   GemvTcArgs a;
   a.N = N; a.nkb = nkb; a.ks = gemv_tc_ksplit(N, nkb); a.t = t; a.epilogue = epilogue; a.n_tiles = tiles;
-  a.n_items = tiles * a.ks;
-  a.blocked = blocked_test;
   a.y = y; a.ldy = ldy; a.xs_out = xs_out; a.ld_xs_out = ld_xs_out;
   a.counters = reinterpret_cast<int *>(ws);
   a.partial = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + (size_t)TC_COUNTER_INTS * 4);
@@ -435,10 +385,8 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
-  static int sms = 0;
-  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  cfg.gridDim = dim3(a.n_items < 2 * sms ? a.n_items : 2 * sms, 1, 1);
-  cfg.blockDim = dim3(TC_THREADS, 1, 1);
+  cfg.gridDim = dim3(tiles, a.ks, 1);
+  cfg.blockDim = dim3(128, 1, 1);
   cfg.dynamicSmemBytes = TC_SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

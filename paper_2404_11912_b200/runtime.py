@@ -51,10 +51,50 @@ class _Workspaces:
 workspaces = _Workspaces()
 
 
+class _PinnedStaging:
+    """Ring of pinned host buffers for the small per-step host->device
+    copies (token ids, uniforms).  A copy from pageable memory makes torch
+    synchronise the stream -- the GPU would drain and idle while the host
+    prepares the next step; a pinned, non-blocking copy is stream-ordered and
+    returns at once.  A slot is reused only after its previous copy ran."""
+
+    def __init__(self, slots: int = 32, cap: int = 8192):
+        self.slots, self.cap = slots, cap
+        self.bufs = {}
+        self.events = [None] * slots
+        self.i = 0
+
+    def to_device(self, arr: np.ndarray) -> torch.Tensor:
+        arr = np.ascontiguousarray(arr)
+        if arr.size > self.cap:
+            return torch.from_numpy(arr).to(device())
+        slot = self.i
+        self.i = (self.i + 1) % self.slots
+        ev = self.events[slot]
+        if ev is not None:
+            ev.synchronize()
+        key = (slot, arr.dtype.str)
+        buf = self.bufs.get(key)
+        if buf is None:
+            buf = torch.empty(self.cap, dtype=torch.from_numpy(arr[:0]).dtype, pin_memory=True)
+            self.bufs[key] = buf
+        host = buf[:arr.size]
+        host.numpy()[:] = arr.reshape(-1)
+        out = torch.empty(arr.shape, dtype=host.dtype, device=device())
+        out.view(-1).copy_(host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events[slot] = ev
+        return out
+
+
+staging = _PinnedStaging()
+
+
 def to_i32_device(tokens) -> torch.Tensor:
     if isinstance(tokens, torch.Tensor):
         return tokens.to(device=device(), dtype=torch.int32)
-    return torch.as_tensor(np.asarray(tokens, dtype=np.int32)).to(device(), non_blocking=False)
+    return staging.to_device(np.asarray(tokens, dtype=np.int32))
 
 
 def as_device_f32(a) -> torch.Tensor:
@@ -85,8 +125,7 @@ class UniformStream:
         self.block = block
         self.state0 = rng.bit_generator.state if keep_state else None
         self.consumed_before = 0          # uniforms consumed before the current buffer
-        host = rng.random(block)
-        self.buf = torch.from_numpy(host).to(device())
+        self.buf = staging.to_device(rng.random(block))
         self.drawn = block                # in the current buffer
         self.cursor = torch.zeros(1, dtype=torch.int32, device=device())
         self.host_cursor = 0
@@ -97,7 +136,7 @@ class UniformStream:
         if self.drawn - host_cursor >= margin:
             return
         rest = self.buf[host_cursor:self.drawn]
-        fresh = torch.from_numpy(self.rng.random(self.block)).to(device())
+        fresh = staging.to_device(self.rng.random(self.block))
         self.consumed_before += host_cursor
         self.buf = torch.cat([rest, fresh])
         self.drawn = self.buf.numel()

@@ -56,6 +56,26 @@ class SpecConfig:
             raise ValueError("temperature must be >= 0")
 
 
+class _Cat:
+    """committed + x_hat without copying the (100K+ token) committed list:
+    lanes only take len() and a tail slice of the sequence."""
+
+    __slots__ = ("head", "tail")
+
+    def __init__(self, head, tail):
+        self.head, self.tail = head, tail
+
+    def __len__(self):
+        return len(self.head) + len(self.tail)
+
+    def __getitem__(self, sl):
+        if not isinstance(sl, slice) or sl.step not in (None, 1) or sl.stop is not None:
+            raise TypeError("_Cat supports tail slices only")
+        a = sl.start or 0
+        n = len(self.head)
+        return (list(self.head[a:]) if a < n else []) + list(self.tail[max(0, a - n):])
+
+
 def _one_uniform(rng) -> tuple:
     u = torch.tensor([rng.random()], dtype=torch.float64, device=device())
     cur = torch.zeros(1, dtype=torch.int32, device=u.device)
@@ -342,7 +362,7 @@ def inner_speculate(retr_lane: Lane, draft_lane: Lane, committed: Sequence[int],
     base = len(committed)
     while len(x_hat) < config.gamma2:
         us.ensure(2 * config.gamma1 + 2, cursor)
-        emitted, accepted, cursor = _inner_round_dev(retr_lane, draft_lane, list(committed) + x_hat, config, us,
+        emitted, accepted, cursor = _inner_round_dev(retr_lane, draft_lane, _Cat(committed, x_hat), config, us,
                                                      buf, len(x_hat))
         x_hat.extend(emitted)
         labels.extend(["draft"] * accepted + ["retrieval"])
@@ -484,7 +504,7 @@ class HierarchicalSession:
             while len(x_hat) < cfg.gamma2:
                 us.ensure(2 * cfg.gamma1 + 2, cursor)
                 emitted, accepted, cursor = _inner_round_dev(self.retr_lane, self.draft_lane,
-                                                             self.committed + x_hat, cfg, us, buf, len(x_hat))
+                                                             _Cat(self.committed, x_hat), cfg, us, buf, len(x_hat))
                 x_hat.extend(emitted)
                 ilabels.extend(["draft"] * accepted + ["retrieval"])
                 trace.inner.rounds += 1
@@ -499,7 +519,7 @@ class HierarchicalSession:
             # ---- outer level: full-cache verify (speculation.py:264-275)
             n = len(x_hat)
             us.ensure(n + 2, cursor)
-            buf.xtok[:n].copy_(torch.as_tensor(np.asarray(x_hat, np.int32)), non_blocking=False)
+            buf.xtok[:n].copy_(to_i32_device(x_hat))
             COUNTERS["h2d_bytes"] += 4 * n
             _score_rows_dev(self.full_lane, self.committed, buf.xtok[:n], cfg.temperature, buf.p)
             _chain_dev(buf.xtok[:n], n, buf.phat, buf.p, V, us, buf)
