@@ -205,28 +205,51 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
 // out[i][h*DH + d] = sum_s w_s o_s / sum_s w_s l_s,  w_s = exp(m_s - M), splits in order.
 // packed != nullptr: write the view's partial state (M, l, o unnormalised)
 // as [rows][2 + DH] instead (sequence-shard input, hs_attention_partial).
+// The split weights are computed once into shared memory; the per-dim sums
+// run in split order with the partial-o loads issued 8 at a time (the loop is
+// otherwise one dependent L2 round trip per split).
 __global__ void attn_combine_kernel(const float *pm, const float *pl, const float *po, int n_splits,
                                     int rows, int DH, float *out, float *packed) {
-  const int row = blockIdx.x;
+  extern __shared__ float comb_s[];          // [n_splits] weights | [n_splits] l
+  float *sw = comb_s, *sl = comb_s + n_splits;
+  __shared__ float red[32];
+  const int row = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  float mx = -INFINITY;
+  for (int s = tid; s < n_splits; s += nt) mx = fmaxf(mx, pm[(size_t)s * rows + row]);
+  mx = warp_max(mx);
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  __syncthreads();
   float M = -INFINITY;
-  for (int s = 0; s < n_splits; ++s) M = fmaxf(M, pm[(size_t)s * rows + row]);
-  float lsum = 0.f;
-  for (int d = threadIdx.x; d < DH; d += blockDim.x) {
-    float l = 0.f, o = 0.f;
-    for (int s = 0; s < n_splits; ++s) {
-      const float m = pm[(size_t)s * rows + row];
-      if (m == -INFINITY) continue;
-      const float w = expf(m - M);
-      l = fmaf(w, pl[(size_t)s * rows + row], l);
-      o = fmaf(w, po[((size_t)s * rows + row) * DH + d], o);
+  for (int w = 0; w < (nt + 31) / 32; ++w) M = fmaxf(M, red[w]);
+  for (int s = tid; s < n_splits; s += nt) {
+    const float m = pm[(size_t)s * rows + row];
+    sw[s] = (m == -INFINITY) ? 0.f : expf(m - M);
+    sl[s] = (m == -INFINITY) ? 0.f : pl[(size_t)s * rows + row];
+  }
+  __syncthreads();
+  float l = 0.f;
+  for (int s = 0; s < n_splits; ++s)
+    if (sw[s] != 0.f) l = fmaf(sw[s], sl[s], l);
+  for (int d = tid; d < DH; d += nt) {
+    float o = 0.f;
+    const float *pd = po + (size_t)row * DH + d;
+    int s = 0;
+    for (; s + 8 <= n_splits; s += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = pd[(size_t)(s + u) * rows * DH];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (sw[s + u] != 0.f) o = fmaf(sw[s + u], v[u], o);
     }
+    for (; s < n_splits; ++s)
+      if (sw[s] != 0.f) o = fmaf(sw[s], pd[(size_t)s * rows * DH], o);
     if (packed) packed[(size_t)row * (DH + 2) + 2 + d] = o;
     else out[(size_t)row * DH + d] = o / l;
-    lsum = l;
   }
-  if (packed && threadIdx.x == 0) {
+  if (packed && tid == 0) {
     packed[(size_t)row * (DH + 2)] = M;
-    packed[(size_t)row * (DH + 2) + 1] = lsum;
+    packed[(size_t)row * (DH + 2) + 1] = l;
   }
 }
 
@@ -319,7 +342,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   a.part_o = wsf + (size_t)2 * n_splits * t * H;
   dim3 grid(n_splits, KVH, ceil_div(a.g * t, ATT_QROWS));
   if (n_splits == 0) {   // empty shard view: partial state (-inf, 0, 0) for every row
-    attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 0, stream>>>(a.part_m, a.part_l, a.part_o, 0, t * H, DH,
+    attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 16, stream>>>(a.part_m, a.part_l, a.part_o, 0, t * H, DH,
                                                                      nullptr, packed);
     return check_launch("attention(empty)");
   }
@@ -338,7 +361,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
     }
     default: return set_error(HS_ERR_SHAPE, "attention: head_dim %d unsupported (8/16/32/64/128)", DH);
   }
-  attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 0, stream>>>(a.part_m, a.part_l, a.part_o,
+  attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 2 * n_splits * sizeof(float), stream>>>(a.part_m, a.part_l, a.part_o,
                                                                    n_splits, t * H, DH, out, packed);
   return check_launch("attention", 2);
 }
