@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
 #pragma unroll
     for (int r = 0; r < AT_QR; ++r) { m_run[r] = -INFINITY; l_run[r] = 0.f; o_acc[r] = 0.f; fac_prev[r] = 1.f; }
 
+    const int qmin = a.pos0 + r0 / a.g;   // smallest query position of this block
     for (int it = 0; it <= ntiles; ++it) {
       if (it < ntiles) {
         const uint32_t gi = g + it;
@@ -257,13 +258,16 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&sfree[s]);
-        // masked scores and tile max across the 128 keys
+        // masked scores and tile max across the 128 keys; a full tile of a
+        // linear (full-cache) view entirely below every query needs no mask
+        const int tile_last = lo + it * AT_KT + AT_KT - 1;
+        const bool allvis = a.pos == nullptr && a.window == 0 && tile_last < hi && tile_last + a.pos_base <= qmin;
         float x[AT_QR];
 #pragma unroll
         for (int r = 0; r < AT_QR; ++r) {
           if (r < nrows) {
-            const bool vis = visible_tc(kp, qp_s[r], a);
-            x[r] = vis ? ((sv[r] + sv[AT_QR + r]) + sv[2 * AT_QR + r]) * a.scale_log2 : -INFINITY;
+            const float sc = ((sv[r] + sv[AT_QR + r]) + sv[2 * AT_QR + r]) * a.scale_log2;
+            x[r] = (allvis || visible_tc(kp, qp_s[r], a)) ? sc : -INFINITY;
             const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
             if (lane == 0) red[s][warp][r] = mx;
           }
@@ -278,8 +282,10 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
             const float m_new = fmaxf(m_run[r], o2f(mi));
             float p = 0.f;
             if (m_new != -INFINITY) {
-              p = (x[r] == -INFINITY) ? 0.f : ex2(x[r] - m_new);       // exp(s - m) in the log2 domain
-              fac[r] = (m_run[r] == -INFINITY) ? 0.f : ex2(m_run[r] - m_new);
+              // exp(s - m) in the log2 domain; ex2(-inf) = +0 covers masked keys
+              // and the first visible tile (m_run = -inf)
+              p = ex2(x[r] - m_new);
+              fac[r] = ex2(m_run[r] - m_new);
             }
             m_run[r] = m_new;
             l_run[r] = l_run[r] * fac[r] + p;   // per-thread partial; reduced once per item
