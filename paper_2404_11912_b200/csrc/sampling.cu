@@ -92,6 +92,12 @@ __device__ void row_probs(const float *logits, int V, double T, double *p) {
 
 // inverse CDF: min(#{j : cumsum(w/scale)_j <= u}, V-1); w optionally the
 // residual max(p - q, 0) (computed on the fly); whole block participates.
+// Each thread owns a contiguous segment of up to SEG_REG entries held in
+// registers (one pass over memory, loads all in flight); the cumulative sum
+// is segment-sequential after an exclusive block scan of segment totals --
+// a fixed order, so the draw is deterministic.
+constexpr int SEG_REG = 32;
+
 __device__ int inv_cdf(const double *p, const double *q, double scale, int V, double u) {
   __shared__ double seg[64];
   const int per = (V + blockDim.x - 1) / blockDim.x;
@@ -100,8 +106,16 @@ __device__ int inv_cdf(const double *p, const double *q, double scale, int V, do
     double x = q ? fmax(p[j] - q[j], 0.0) : p[j];
     return scale == 1.0 ? x : x / scale;
   };
+  double wr[SEG_REG];
   double local = 0.0;
-  for (int j = j0; j < j1; ++j) local += w(j);
+  if (per <= SEG_REG) {
+#pragma unroll
+    for (int i = 0; i < SEG_REG; ++i) wr[i] = (i < per && j0 + i < j1) ? w(j0 + i) : 0.0;
+#pragma unroll
+    for (int i = 0; i < SEG_REG; ++i) local += wr[i];
+  } else {
+    for (int j = j0; j < j1; ++j) local += w(j);
+  }
   // exclusive scan of the segment totals: warp scan, then scan of warp totals
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double incl = local;
@@ -129,9 +143,19 @@ __device__ int inv_cdf(const double *p, const double *q, double scale, int V, do
   if (lane == 0) excl = 0.0;
   double c = seg[32 + wid] + excl;
   int cnt = 0;
-  for (int j = j0; j < j1; ++j) {
-    c += w(j);
-    cnt += (c <= u) ? 1 : 0;
+  if (per <= SEG_REG) {
+#pragma unroll
+    for (int i = 0; i < SEG_REG; ++i) {
+      if (i < per && j0 + i < j1) {
+        c += wr[i];
+        cnt += (c <= u) ? 1 : 0;
+      }
+    }
+  } else {
+    for (int j = j0; j < j1; ++j) {
+      c += w(j);
+      cnt += (c <= u) ? 1 : 0;
+    }
   }
   cnt = block_count(cnt);
   return cnt < V - 1 ? cnt : V - 1;
@@ -153,6 +177,16 @@ __global__ void __launch_bounds__(SMP_THREADS) draft_sample_kernel(const float *
                                                                    double *probs, const double *U,
                                                                    int32_t *cursor, int32_t *out) {
   const int cur = *cursor;
+  if (T == 0.0) {
+    // one-hot argmax row; its inverse CDF at any u in [0, 1) is the argmax
+    // itself (model.py:198-202 with a one-hot p), so skip the scan
+    ArgMax best = {-INFINITY, 0x7fffffff};
+    for (int j = threadIdx.x; j < V; j += blockDim.x) best = amax(best, ArgMax{(double)logits[j], j});
+    best = block_argmax(best);
+    for (int j = threadIdx.x; j < V; j += blockDim.x) probs[j] = (j == best.i) ? 1.0 : 0.0;
+    if (threadIdx.x == 0) { *out = best.i < V ? best.i : V - 1; *cursor = cur + 1; }
+    return;
+  }
   row_probs(logits, V, T, probs);
   const int tok = inv_cdf(probs, nullptr, 1.0, V, U[cur]);
   __syncthreads();
