@@ -43,6 +43,8 @@ int hs_abi_version(void);
 int hs_device_sm_count(int device);
 /* number of kernels this library has launched since it was loaded */
 unsigned long long hs_launch_count(void);
+/* add n to that count (kernels launched by replaying a captured CUDA graph) */
+void hs_note_launches(unsigned long long n);
 
 /* ---- model descriptor --------------------------------------------------
  * Replaces ModelWeights.runtime() (model.py:116-143): fused wqkv, fused
@@ -111,6 +113,10 @@ typedef struct {
                         this rank's sequence shard; 0 when unsharded)       */
   int own_hi;        /* HS_APPEND_POS: rows at positions < pos_base or >=
                         own_hi are not stored on this rank (0 = no bound)   */
+  const int32_t *dyn;  /* optional device int32[2] read at run time: the
+                          frontier (added to pos0) and win_lo -- lets a
+                          captured CUDA graph replay a lane step at any
+                          position; NULL = use pos0 / win_lo as given       */
 } HsStep;
 
 /* ---- sequence sharding of the full cache -----------------

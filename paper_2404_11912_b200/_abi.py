@@ -54,7 +54,7 @@ class HsCache(C.Structure):
 class HsStep(C.Structure):
     _fields_ = [("pos0", i32), ("append_mode", i32), ("append_base", i32), ("n_sink", i32), ("ring", i32),
                 ("n_view", i32), ("window", i32), ("win_lo", i32), ("split", i32), ("pos_base", i32),
-                ("own_hi", i32)]
+                ("own_hi", i32), ("dyn", vp)]
 
 
 class HsShard(C.Structure):
@@ -67,6 +67,7 @@ _SIGS = {
     "hs_abi_version": (i32, []),
     "hs_device_sm_count": (i32, [i32]),
     "hs_launch_count": (C.c_ulonglong, []),
+    "hs_note_launches": (None, [C.c_ulonglong]),
     "hs_forward_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32, i32]),
     "hs_forward_workspace_clean_bytes": (sz, [_P(HsModel)]),
     "hs_gemv_tc_workspace_bytes": (sz, [i32, i32]),

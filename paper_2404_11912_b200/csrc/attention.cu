@@ -29,6 +29,7 @@ struct AttnArgs {
   const uint16_t *v;
   const int32_t *pos;   // layer [cap] or null (slot == position)
   int cap, n_view, pos0, window, win_lo, n_sink, split, n_splits, pos_base;
+  const int32_t *dyn;   // HsStep.dyn: run-time frontier / win_lo (graph replay)
   float scale;
   float *part_m, *part_l, *part_o;   // [n_splits][t*H], [n_splits][t*H][DH]
 };
@@ -43,6 +44,7 @@ __device__ __forceinline__ bool visible(int kp, int qp, const AttnArgs &a) {
 
 template <int DH>
 __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
+  if (a.dyn) { a.pos0 += a.dyn[0]; a.win_lo = a.dyn[1]; }
   constexpr int KP = DH + 8;                 // padded K row (bf16) -> conflict-free 16B reads
   constexpr int NDP = DH / 2;                // dim pairs
   constexpr int NRG = ATT_THREADS / NDP > ATT_QROWS ? ATT_QROWS : ATT_THREADS / NDP;
@@ -335,6 +337,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   a.cap = c->cap; a.n_view = st->n_view; a.pos0 = st->pos0; a.window = st->window;
   a.win_lo = st->win_lo; a.n_sink = st->n_sink; a.split = st->split; a.n_splits = n_splits;
   a.pos_base = st->pos_base;
+  a.dyn = st->dyn;
   a.scale = (float)(1.0 / sqrt((double)DH));
   float *wsf = reinterpret_cast<float *>(ws);
   a.part_m = wsf;
@@ -355,6 +358,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
     case 64: attn_partial_kernel<64><<<grid, ATT_THREADS, 0, stream>>>(a); break;
     case 128: {
       HS_REQUIRE(st->split % 128 == 0, HS_ERR_VALUE, "attention: split must be a multiple of 128 for head_dim 128");
+      HS_REQUIRE(st->dyn == nullptr, HS_ERR_VALUE, "attention: run-time positions need head_dim < 128");
       int rc = launch_attention_tc(c, layer, st, H, q, t, a.part_m, a.part_l, a.part_o, n_splits, stream);
       if (rc != HS_OK) return rc;
       break;

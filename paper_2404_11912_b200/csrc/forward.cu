@@ -114,6 +114,7 @@ static size_t carve(const HsModel *m, int t, int n_view, int split, int world, c
 extern "C" const char *hs_last_error(void) { return hs::g_err; }
 extern "C" int hs_abi_version(void) { return HS_ABI_VERSION; }
 extern "C" unsigned long long hs_launch_count(void) { return __atomic_load_n(&hs::g_launches, __ATOMIC_RELAXED); }
+extern "C" void hs_note_launches(unsigned long long n) { hs::count_launch((int)n); }
 extern "C" int hs_device_sm_count(int device) {
   int n = 0;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;

@@ -37,7 +37,7 @@ __global__ void rope_append_kernel(HsModel m, HsCache c, HsStep s, int layer, co
   const int i = blockIdx.x, hh = blockIdx.y, pr = threadIdx.x;
   const int H = m.n_heads, KVH = m.n_kv_heads, DH = m.head_dim, half = DH / 2;
   if (pr >= half) return;
-  const int p = s.pos0 + i;
+  const int p = (s.dyn ? s.dyn[0] : 0) + s.pos0 + i;
   const int ncols = (H + 2 * KVH) * DH;
   const float *row = qkv + (size_t)i * ncols;
   if (hh < H + KVH) {

@@ -64,6 +64,27 @@ class _PinnedStaging:
         self.events = [None] * slots
         self.i = 0
 
+    def copy_into(self, dst: torch.Tensor, arr) -> None:
+        """Stream-ordered copy of a small host array into an existing device
+        tensor (fixed address: inputs of captured CUDA graphs)."""
+        arr = np.ascontiguousarray(arr, dtype=torch.empty(0, dtype=dst.dtype).numpy().dtype)
+        slot = self.i
+        self.i = (self.i + 1) % self.slots
+        ev = self.events[slot]
+        if ev is not None:
+            ev.synchronize()
+        key = (slot, arr.dtype.str)
+        buf = self.bufs.get(key)
+        if buf is None:
+            buf = torch.empty(self.cap, dtype=dst.dtype, pin_memory=True)
+            self.bufs[key] = buf
+        host = buf[:arr.size]
+        host.numpy()[:] = arr.reshape(-1)
+        dst.view(-1)[:arr.size].copy_(host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events[slot] = ev
+
     def to_device(self, arr: np.ndarray) -> torch.Tensor:
         arr = np.ascontiguousarray(arr)
         if arr.size > self.cap:

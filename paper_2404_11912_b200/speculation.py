@@ -30,7 +30,65 @@ from .caches import (FullCache, KVCache, RetrievalCache, RetrievalConfig, Rollin
                      StreamingConfig, should_rebuild)
 from .errors import ContractError
 from .model import (ForwardRecorder, ModelWeights, forward_device, prob_from_logits, sample_from_probs)
-from .runtime import UniformStream, as_device_f64, device, ptr, stream_ptr, to_i32_device
+from .runtime import STATS, UniformStream, as_device_f64, device, ptr, staging, stream_ptr, to_i32_device
+
+import ctypes as C
+import os
+
+from ._abi import HsModel  # noqa: F401  (ctypes layout shared with model.py)
+
+# CUDA-graph replay of the draft lane's one-token steps (HS_NO_GRAPHS=1 turns
+# it off: every step is then a regular hs_forward call with the same kernels)
+USE_GRAPHS = os.environ.get("HS_NO_GRAPHS", "0") != "1"
+
+
+class _StepGraph:
+    """One-token forward of a streaming-cache lane captured as a CUDA graph.
+
+    The draft model is tiny (JF68M shape: 2 layers), so its step is bound by
+    the host launching ~25 kernels, not by the GPU.  The graph reads its
+    token from a fixed device slot and the frontier / window watermark from a
+    device int32[2] (HsStep.dyn) refreshed before each replay, so one capture
+    serves every position.  It keeps references to every buffer it was
+    captured with (workspace, logits rows) so later re-allocations elsewhere
+    cannot invalidate it."""
+
+    def __init__(self, lane: "Lane", tok: torch.Tensor):
+        cache = lane.cache
+        dm = lane.weights.device()
+        cfg = dm.config
+        self.lane, self.tok = lane, tok
+        self.dyn = torch.zeros(2, dtype=torch.int32, device=device())
+        step = cache._step(1)
+        step.pos0, step.win_lo, step.dyn = 0, 0, self.dyn.data_ptr()
+        self.step = step
+        self.nbytes = lib.hs_forward_workspace_bytes(dm.ref, 1, step.n_view, step.split, 0)
+        self.ws = dm.workspace(self.nbytes)
+        self.out = torch.empty((1, cfg.vocab_size), dtype=torch.float32, device=device())
+        self.stash = lane.recorder._buffer(cfg)
+        self.alg_bytes = dm.weight_bytes + step.n_view * cfg.n_kv_heads * cfg.head_dim * 4 * cfg.n_layers
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        n0 = lib.hs_launch_count()
+        with torch.cuda.graph(self.graph, stream=side):
+            check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), None, ptr(tok), 1, ptr(self.out), ptr(self.stash),
+                                 ptr(self.ws), self.nbytes, stream_ptr()))
+            lane._front.copy_(self.out[0])
+        self.n_launch = lib.hs_launch_count() - n0
+        torch.cuda.current_stream().wait_stream(side)
+
+    def run(self) -> None:
+        lane, cache = self.lane, self.lane.cache
+        cache._step(1)                                    # guard / capacity checks on the live state
+        staging.copy_into(self.dyn, [cache.frontier, cache.lo])
+        self.graph.replay()
+        lib.hs_note_launches(self.n_launch)
+        STATS["alg_bytes"] += self.alg_bytes
+        cache._advance(1)
+        lane._has_front = True
+        lane.recorder.query_position = cache.frontier - 1
+
 
 
 # process-wide counters (bench.py reads them around its timed region)
@@ -117,6 +175,15 @@ class Lane:
         self._front = torch.zeros(V, dtype=torch.float32, device=device())
         self._has_front = False
         self._scratch = None
+        self._graphs = {}
+
+    def step_graph(self, tok: torch.Tensor) -> "_StepGraph":
+        """Captured one-token step reading its token from `tok` (a fixed
+        device slot)."""
+        g = self._graphs.get(tok.data_ptr())
+        if g is None:
+            g = self._graphs[tok.data_ptr()] = _StepGraph(self, tok)
+        return g
 
     @property
     def frontier(self) -> int:
@@ -275,10 +342,14 @@ def _draft_round_dev(lane: Lane, seq: Sequence[int], gamma1: int, T: float, us: 
         raise ContractError("lane has no frontier logits; advance over committed tokens first")
     V = buf.V
     s = stream_ptr()
+    graphs = USE_GRAPHS and isinstance(lane.cache, StreamingCache)
     for g in range(gamma1):
         check(lib.hs_draft_sample(ptr(lane._front), V, float(T), ptr(buf.q[g]), ptr(us.buf), ptr(us.cursor),
                                   ptr(buf.dtok[g:g + 1]), s))
-        lane._forward(buf.dtok[g:g + 1])
+        if graphs:
+            lane.step_graph(buf.dtok[g:g + 1]).run()
+        else:
+            lane._forward(buf.dtok[g:g + 1])
 
 
 def _score_rows_dev(lane: Lane, seq: Sequence[int], tokens_dev: torch.Tensor, T: float,

@@ -427,3 +427,29 @@ def test_generate_continues_after_truncated_round(P):
         out, _ = s.generate()
         assert len(out) == n
     assert out == P.autoregressive_generate(tw, prompt, 340, 0.0, 0)
+
+
+def test_draft_step_graphs_match_direct_forwards(P):
+    """The draft lane's captured one-token step (CUDA graph, run-time
+    frontier via HsStep.dyn) gives the same session, bit for bit, as direct
+    hs_forward calls."""
+    from paper_2404_11912_b200 import speculation as S
+    tc = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=64, d_ff=344, vocab_size=512, max_seq=2048)
+    dc = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=4, head_dim=64, d_ff=172, vocab_size=512, max_seq=2048)
+    tw = P.plant_successor(P.generate_weights(tc, 5, tied_head=False), 9, 0.8)
+    dw = P.plant_successor(P.generate_weights(dc, 6, tied_head=False), 9, 0.8)
+    prompt = np.random.default_rng(8).integers(1, 512, 700).tolist()
+    res = []
+    for graphs in (False, True):
+        S.USE_GRAPHS = graphs
+        try:
+            spec = P.SpecConfig(target_len=700 + 90, gamma1=3, gamma2=5, temperature=0.7, seed=2,
+                                streaming=P.StreamingConfig(n_sink=4, budget=96),
+                                retrieval=P.RetrievalConfig(chunk_size=8, budget=128, rebuild_stride=40))
+            s = P.HierarchicalSession(tw, dw, prompt, spec)
+            out, tr = s.generate()
+            res.append((out, tr.summary(), s.draft_lane.cache.k.clone(), s.draft_lane._front.clone()))
+        finally:
+            S.USE_GRAPHS = True
+    assert res[0][0] == res[1][0] and res[0][1] == res[1][1]
+    assert torch.equal(res[0][2], res[1][2]) and torch.equal(res[0][3], res[1][3])
