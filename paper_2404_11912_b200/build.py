@@ -1,6 +1,6 @@
 """In-tree build of the sm_100a C-ABI library `libhs_b200.so`.
 
-    python -m paper_2404_11912_b200.build          # or __graft_entry__.build()
+    python paper_2404_11912_b200/build.py          # or __graft_entry__.build()
 
 Compiles every `csrc/*.cu` with nvcc for `-gencode arch=compute_100a,code=sm_100a`
 into one shared library next to this file (git-ignored, travels to the GPU box
