@@ -41,6 +41,10 @@ import numpy as np  # noqa: E402
 
 TARGET_7B = dict(n_layers=32, n_heads=32, n_kv_heads=32, head_dim=128, d_ff=11008, vocab_size=32000,
                  max_seq=131072)
+TARGET_13B = dict(n_layers=40, n_heads=40, n_kv_heads=40, head_dim=128, d_ff=13824, vocab_size=32000,
+                  max_seq=131072)
+# LWM-Text-7B: the Llama2-7B architecture at a 1M-token context (config 4)
+TARGETS = {"llama2-7b": TARGET_7B, "llama2-13b": TARGET_13B, "lwm-7b": TARGET_7B}
 DRAFT_68M = dict(n_layers=2, n_heads=12, n_kv_heads=12, head_dim=64, d_ff=3072, vocab_size=32000,
                  max_seq=131072)
 CONTEXT = 122880
@@ -56,6 +60,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--gen", type=int, default=32, help="tokens committed per step")
+    ap.add_argument("--model", choices=sorted(TARGETS), default="llama2-7b",
+                    help="target shape: llama2-7b (config 2, default), llama2-13b (config 3), lwm-7b (config 4)")
     ap.add_argument("--context", type=int, default=CONTEXT)
     ap.add_argument("--temperature", type=float, default=0.0)
     ap.add_argument("--easy-frac", type=float, default=EASY_FRAC,
@@ -143,7 +149,7 @@ def plant_host(tensors: dict, d: int, V: int, seed: int, easy_frac: float, emb_s
 
 
 def oracle_sample(context: int, temperature: float, rounds: int, time_budget_s: float = 150.0,
-                  easy_frac: float = EASY_FRAC):
+                  easy_frac: float = EASY_FRAC, target: dict = TARGET_7B):
     """TriForce on the CPU oracle (oracle/hs_oracle.py, a restatement of the
     reference numpy engine): a 1-layer slice of the Llama2-7B shape over the
     full synthetic context plus the full 2-layer draft, run for whole outer
@@ -151,7 +157,7 @@ def oracle_sample(context: int, temperature: float, rounds: int, time_budget_s: 
     identical work) and the amortised retrieval build is added.  Returns
     (tokens_per_s estimate for the 32-layer model, sample description, cores)."""
     from oracle import hs_oracle as O
-    tcfg = O.OConfig(**{**TARGET_7B, "n_layers": 1})
+    tcfg = O.OConfig(**{**target, "n_layers": 1, "max_seq": max(target["max_seq"], context + 1024)})
     dcfg = O.OConfig(**DRAFT_68M)
     tt = O.make_tensors(tcfg, 1, tied_head=False)
     dt = O.make_tensors(dcfg, 2, tied_head=False)
@@ -191,15 +197,15 @@ def oracle_sample(context: int, temperature: float, rounds: int, time_budget_s: 
             got = sess.round(rng, tr)
             wall = time.perf_counter() - s
             rest = wall - spent["target"] - spent["draft"]
-            est = spent["target"] * TARGET_7B["n_layers"] + spent["draft"] + rest
-            est += build_s * TARGET_7B["n_layers"] * got / 128.0     # rebuild every 128 tokens
+            est = spent["target"] * target["n_layers"] + spent["draft"] + rest
+            est += build_s * target["n_layers"] * got / 128.0     # rebuild every 128 tokens
             per_token.append(est / got)
             if time.perf_counter() - start > time_budget_s:
                 break
     finally:
         O.forward = real_forward
     cores = len(os.sched_getaffinity(0))
-    desc = (f"oracle (numpy port of hierspec) TriForce outer rounds on a 1-layer slice of the Llama2-7B shape "
+    desc = (f"oracle (numpy port of hierspec) TriForce outer rounds on a 1-layer slice of the target shape "
             f"over a {context}-token synthetic context + full JF68M draft; target forwards x32 layers, build "
             f"({build_s:.1f} s/layer) amortised over the 128-token stride; {len(per_token)} round(s), "
             f"setup {setup:.0f} s")
@@ -213,9 +219,9 @@ def run_reference(args):
     if rank != 0:
         return
     rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=max(1, args.steps),
-                                       easy_frac=args.easy_frac)
+                                       easy_frac=args.easy_frac, target=TARGETS[args.model])
     val = statistics.median(rates)
-    out = {"metric": "decode tokens/s (TriForce, Llama2-7B-128K shape @122,880 ctx)", "value": val,
+    out = {"metric": metric_name(args), "value": val,
            "unit": "tokens/s", "n_gpus": 0, "steps": len(rates), "warmup": 0, "ms_per_step": 1000.0 / val,
            "higher_is_better": True, "impl": "reference", "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": workload_config(args),
@@ -224,16 +230,24 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+MODEL_NAMES = {"llama2-7b": "Llama2-7B-128K", "llama2-13b": "Llama2-13B-128K", "lwm-7b": "LWM-Text-7B"}
+
+
+def metric_name(args) -> str:
+    return f"decode tokens/s (TriForce, {MODEL_NAMES[args.model]} shape @{args.context:,} ctx)"
+
+
 def workload_config(args, world=1):
-    return {"workload": "TriForce decode, Llama2-7B-128K shape, 122,880-token synthetic context, "
-                        "JF68M-shaped StreamingLLM draft",
+    return {"workload": f"TriForce decode, {MODEL_NAMES[args.model]} shape, {args.context:,}-token synthetic "
+                        "context, JF68M-shaped StreamingLLM draft",
             "context": args.context, "retrieval_budget": BUDGET, "chunk": CHUNK, "stream_sink": SINK,
             "stream_budget": STREAM, "gamma1": GAMMA1, "gamma2": GAMMA2, "temperature": args.temperature,
             "tokens_per_step": args.gen, "l2": "inputs larger than L2 (64 GB KV/GPU), no flush",
             "weights": ("random-init N(0,0.02) bf16 + planted successor channel, easy_frac "
                         f"{args.easy_frac} (model.plant_successor; acceptance near the paper's 0.92)"
                         if args.easy_frac > 0 else "pure random-init N(0,0.02) bf16 (acceptance ~0)"),
-            "parallelism": "1 GPU" if world == 1 else f"full KV cache sequence-sharded over {world} GPUs (NCCL)"}
+            "parallelism": ("host CPU (reference arm)" if args.impl == "reference" else
+                            "1 GPU" if world == 1 else f"full KV cache sequence-sharded over {world} GPUs (NCCL)")}
 
 
 # ---------------------------------------------------------------------------
@@ -257,7 +271,9 @@ def main():
     from paper_2404_11912_b200 import speculation as S
     from paper_2404_11912_b200._abi import check, lib
 
-    tcfg, dcfg = P.ModelConfig(**TARGET_7B), P.ModelConfig(**DRAFT_68M)
+    tshape = dict(TARGETS[args.model])
+    tshape["max_seq"] = max(tshape["max_seq"], args.context + 4096)
+    tcfg, dcfg = P.ModelConfig(**tshape), P.ModelConfig(**{**DRAFT_68M, "max_seq": tshape["max_seq"]})
     # one sequence sharded over the ranks: every rank holds the same weights and
     # tokens and runs the same (deterministic) loop; only the full cache is split
     shards = None
@@ -342,7 +358,7 @@ def main():
         rf["peak"] = peak
         rf["frac"] = rf["achieved"] / peak
         rf["peak_source"] = peak_kind
-        out = {"metric": "decode tokens/s (TriForce, Llama2-7B-128K shape @122,880 ctx)", "value": value,
+        out = {"metric": metric_name(args), "value": value,
                "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": ms / args.steps, "ms_per_token": ms / tokens, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
@@ -364,7 +380,7 @@ def main():
                **extra}
         if world == 1 and not args.no_cpu_baseline:
             rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=1, time_budget_s=60,
-                                               easy_frac=args.easy_frac)
+                                               easy_frac=args.easy_frac, target=TARGETS[args.model])
             out["cpu_baseline"] = {"value": statistics.median(rates), "unit": "tokens/s", "cores": cores,
                                    "kind": "port", "sample": desc}
         print(json.dumps(out), flush=True)
