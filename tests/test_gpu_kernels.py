@@ -370,3 +370,38 @@ def test_attention_tc_slotted_windowed_and_batch_invariant(P):
         for i in range(5):
             one = _run_attention(P, cache, 1, H, q[i:i + 1], pos0 + i, n, 512, window, win_lo, n_sink)
             assert np.array_equal(one[0], got[i])
+
+
+def test_attention_full_context_122880_keys(P):
+    """BASELINE context length: tensor-core split-KV attention over 122,880
+    bf16 keys (60 splits) for t = 7 verify queries vs an fp64 softmax, max rel
+    err <= 1e-4 (north-star bar 2e-2)."""
+    import ctypes as C
+
+    from paper_2404_11912_b200._abi import HsStep, check, lib
+    from paper_2404_11912_b200.runtime import ptr, stream_ptr, workspaces
+    n, t, kvh, H, dh = 122880, 7, 2, 4, 128
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    cache = P.FullCache(1, kvh, dh, n + 64)
+    cache.k[0, :, :n].normal_(generator=g)
+    cache.v[0, :, :n].normal_(generator=g)
+    cache._n = [n]
+    cache.frontier = cache.committed = n
+    q = torch.randn((t, H, dh), generator=g, device="cuda") * 0.3
+    out = torch.zeros((t, H * dh), device="cuda")
+    st = HsStep()
+    st.pos0, st.n_view, st.split = n - t, n, P.caches.FULL_SPLIT
+    nb = lib.hs_attention_workspace_bytes(t, H, dh, n, st.split)
+    ws = workspaces.get("t_full", nb)
+    check(lib.hs_attention(cache._ref, 0, C.byref(st), H, ptr(q), t, ptr(out), ptr(ws), nb, stream_ptr()))
+    got = out.view(t, H, dh).double()
+    K, V, qd = cache.k[0, :, :n].double(), cache.v[0, :, :n].double(), q.double()
+    for i in range(t):
+        vis = n - t + i + 1
+        for h in range(H):
+            s = (K[h // (H // kvh), :vis] @ qd[i, h]) / dh ** 0.5
+            p = torch.softmax(s, 0)
+            ref = p @ V[h // (H // kvh), :vis]
+            rel = ((got[i, h] - ref).abs().max() / ref.abs().max()).item()
+            assert rel <= 1e-4, (i, h, rel)
