@@ -45,7 +45,8 @@ constexpr int AT_HALF = 128 * 64 * 2;   // one [128 rows x 64] bf16 SW128 tile =
 constexpr int AT_KV = 2 * AT_HALF;      // one K or V tile (two dh halves) = 32 KB
 constexpr int AT_QP = AT_N * 128;       // one [24 rows x 64] bf16 SW128 atom column = 3 KB
 constexpr int AT_OPND = 2 * AT_QP;      // Q or one P buffer = 6 KB
-constexpr int AT_THREADS = 192;
+constexpr int AT_THREADS = 320;          // 2 softmax groups x 4 warps, TMA warp, MMA warp
+constexpr int AT_GR = 4;                 // query rows per softmax group
 constexpr int AT_KSTAGES = 1, AT_VSTAGES = 1;
 constexpr int AT_SMEM = AT_KSTAGES * AT_KV + AT_VSTAGES * AT_KV + AT_OPND + 2 * AT_OPND + 1024;
 
@@ -79,7 +80,9 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__device__ __forceinline__ void named_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// all 8 softmax warps / the 4 warps of one softmax group
+__device__ __forceinline__ void softmax_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void group_sync(int grp) { asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory"); }
 
 // order-preserving float <-> int for redux.sync max
 __device__ __forceinline__ int f2o(float f) { const int i = __float_as_int(f); return i ^ ((i >> 31) & 0x7fffffff); }
@@ -119,10 +122,10 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
     tc::tma_prefetch(&tmV);
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&kfull[s], 1); tc::mbar_init(&kempty[s], 1); tc::mbar_init(&vfull[s], 1);
-      tc::mbar_init(&vempty[s], 1); tc::mbar_init(&sfull[s], 1); tc::mbar_init(&sfree[s], 4);
-      tc::mbar_init(&pfull[s], 4); tc::mbar_init(&ofull[s], 1); tc::mbar_init(&ofree[s], 4);
+      tc::mbar_init(&vempty[s], 1); tc::mbar_init(&sfull[s], 1); tc::mbar_init(&sfree[s], 8);
+      tc::mbar_init(&pfull[s], 8); tc::mbar_init(&ofull[s], 1); tc::mbar_init(&ofree[s], 8);
     }
-    tc::mbar_init(&qfull, 4);
+    tc::mbar_init(&qfull, 8);
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<128>(&tmem_base);   // S[b] at b*32, O[b] at 64 + b*32
@@ -211,19 +214,27 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
     return;
   }
 
-  // ---------------------------------------------------------------- softmax warps 0-3
-  const uint32_t tl = (uint32_t)(warp * 32) << 16;   // this warp's TMEM lane quarter
+  // ------------------------------------------------ softmax warps 0-3 (rows 0-3), 6-9 (rows 4-7)
+  // Two groups of four warps split the (up to) 8 query rows of a work item,
+  // halving each thread's per-tile softmax work; warp w reads TMEM lane
+  // quarter w % 4, so thread ltid = key (S) / head dim (O) index.
+  const int grp = warp < 4 ? 0 : 1;
+  const int ltid = (warp & 3) * 32 + lane;
+  const int stid = grp * 128 + ltid;                 // 0..255 over both groups
+  const int rb = grp * AT_GR;                        // first row of this group
+  const uint32_t tl = (uint32_t)((warp & 3) * 32) << 16;   // this warp's TMEM lane quarter
   uint32_t g = 0;
   for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
     const int split = item % a.n_splits, kh = (item / a.n_splits) % a.KVH, qb = item / (a.n_splits * a.KVH);
     const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
     const int r0 = qb * AT_QR;
     const int nrows = min(AT_QR, a.g * a.t - r0);
+    const bool active = rb < nrows;                  // uniform per group
     const int ntiles = (hi - lo + AT_KT - 1) / AT_KT;
     // ---- stage the query split; zero both P buffers (rows >= nrows stay 0) ----------
     // (all S/P.V MMAs of the previous item completed: its tiles were all consumed)
-    if (tid < AT_QR) qp_s[tid] = tid < nrows ? a.pos0 + (r0 + tid) / a.g : -1;
-    for (int e = tid; e < AT_QR * AT_DH; e += 128) {
+    if (stid < AT_QR) qp_s[stid] = stid < nrows ? a.pos0 + (r0 + stid) / a.g : -1;
+    for (int e = stid; e < AT_QR * AT_DH; e += 256) {
       const int rr = e >> 7, d = e & 127;
       float v = 0.f;
       if (rr < nrows) {
@@ -232,14 +243,14 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
       }
       split3_store(sQ, rr, d, v);
     }
-    for (int e = tid; e < 2 * AT_OPND / 16; e += 128) reinterpret_cast<uint4 *>(sP)[e] = make_uint4(0, 0, 0, 0);
+    for (int e = stid; e < 2 * AT_OPND / 16; e += 256) reinterpret_cast<uint4 *>(sP)[e] = make_uint4(0, 0, 0, 0);
     tc::fence_async_smem();
-    named_sync();
+    softmax_sync();
     if (lane == 0) tc::mbar_arrive(&qfull);
 
-    float m_run[AT_QR], l_run[AT_QR], o_acc[AT_QR], fac_prev[AT_QR];
+    float m_run[AT_GR], l_run[AT_GR], o_acc[AT_GR], fac_prev[AT_GR];
 #pragma unroll
-    for (int r = 0; r < AT_QR; ++r) { m_run[r] = -INFINITY; l_run[r] = 0.f; o_acc[r] = 0.f; fac_prev[r] = 1.f; }
+    for (int r = 0; r < AT_GR; ++r) { m_run[r] = -INFINITY; l_run[r] = 0.f; o_acc[r] = 0.f; fac_prev[r] = 1.f; }
 
     const int qmin = a.pos0 + r0 / a.g;   // smallest query position of this block
     for (int it = 0; it <= ntiles; ++it) {
@@ -247,52 +258,58 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         const uint32_t gi = g + it;
         const int s = gi & 1;
         const uint32_t ph = (gi >> 1) & 1;
-        const int key = lo + it * AT_KT + tid;
+        const int key = lo + it * AT_KT + ltid;
         const int kp = key < hi ? (a.pos ? a.pos[key] : key + a.pos_base) : -1;
         tc::mbar_wait(&sfull[s], ph);
         tc::fence_after();
-        float sv[AT_N];
+        float sv[3 * AT_GR];
+        if (active) {
 #pragma unroll
-        for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + s * 32 + tl + c, sv + c);
-        tc::tmem_ld_wait();
+          for (int c = 0; c < 3; ++c) tc::tmem_ld4(tmem + s * 32 + tl + c * AT_QR + rb, sv + c * AT_GR);
+          tc::tmem_ld_wait();
+        }
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&sfree[s]);
-        // masked scores and tile max across the 128 keys; a full tile of a
-        // linear (full-cache) view entirely below every query needs no mask
-        const int tile_last = lo + it * AT_KT + AT_KT - 1;
-        const bool allvis = a.pos == nullptr && a.window == 0 && tile_last < hi && tile_last + a.pos_base <= qmin;
-        float x[AT_QR];
+        float fac[AT_GR];
 #pragma unroll
-        for (int r = 0; r < AT_QR; ++r) {
-          if (r < nrows) {
-            const float sc = ((sv[r] + sv[AT_QR + r]) + sv[2 * AT_QR + r]) * a.scale_log2;
-            x[r] = (allvis || visible_tc(kp, qp_s[r], a)) ? sc : -INFINITY;
-            const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
-            if (lane == 0) red[s][warp][r] = mx;
-          }
-        }
-        named_sync();
-        float fac[AT_QR];
+        for (int r = 0; r < AT_GR; ++r) fac[r] = 1.f;
+        if (active) {
+          // masked scores and tile max across the 128 keys; a full tile of a
+          // linear (full-cache) view entirely below every query needs no mask
+          const int tile_last = lo + it * AT_KT + AT_KT - 1;
+          const bool allvis = a.pos == nullptr && a.window == 0 && tile_last < hi && tile_last + a.pos_base <= qmin;
+          float x[AT_GR];
 #pragma unroll
-        for (int r = 0; r < AT_QR; ++r) {
-          fac[r] = 1.f;
-          if (r < nrows) {
-            const int mi = max(max(red[s][0][r], red[s][1][r]), max(red[s][2][r], red[s][3][r]));
-            const float m_new = fmaxf(m_run[r], o2f(mi));
-            float p = 0.f;
-            if (m_new != -INFINITY) {
-              // exp(s - m) in the log2 domain; ex2(-inf) = +0 covers masked keys
-              // and the first visible tile (m_run = -inf)
-              p = ex2(x[r] - m_new);
-              fac[r] = ex2(m_run[r] - m_new);
+          for (int r = 0; r < AT_GR; ++r) {
+            if (rb + r < nrows) {
+              const float sc = ((sv[r] + sv[AT_GR + r]) + sv[2 * AT_GR + r]) * a.scale_log2;
+              x[r] = (allvis || visible_tc(kp, qp_s[rb + r], a)) ? sc : -INFINITY;
+              const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
+              if (lane == 0) red[s][warp & 3][rb + r] = mx;
             }
-            m_run[r] = m_new;
-            l_run[r] = l_run[r] * fac[r] + p;   // per-thread partial; reduced once per item
-            split3_store(sP + s * AT_OPND, r, tid, p);
           }
+          group_sync(grp);
+#pragma unroll
+          for (int r = 0; r < AT_GR; ++r) {
+            const int rr = rb + r;
+            if (rr < nrows) {
+              const int mi = max(max(red[s][0][rr], red[s][1][rr]), max(red[s][2][rr], red[s][3][rr]));
+              const float m_new = fmaxf(m_run[r], o2f(mi));
+              float p = 0.f;
+              if (m_new != -INFINITY) {
+                // exp(s - m) in the log2 domain; ex2(-inf) = +0 covers masked keys
+                // and the first visible tile (m_run = -inf)
+                p = ex2(x[r] - m_new);
+                fac[r] = ex2(m_run[r] - m_new);
+              }
+              m_run[r] = m_new;
+              l_run[r] = l_run[r] * fac[r] + p;   // per-thread partial; reduced once per item
+              split3_store(sP + s * AT_OPND, rr, ltid, p);
+            }
+          }
+          tc::fence_async_smem();
         }
-        tc::fence_async_smem();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&pfull[s]);
         if (it > 0) {   // fold O(it-1) with the previous tile's rescale factor
@@ -300,65 +317,72 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
           const int sp = gp & 1;
           tc::mbar_wait(&ofull[sp], (gp >> 1) & 1);
           tc::fence_after();
-          float ov[AT_N];
+          float ov[3 * AT_GR];
+          if (active) {
 #pragma unroll
-          for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 64 + sp * 32 + tl + c, ov + c);
-          tc::tmem_ld_wait();
+            for (int c = 0; c < 3; ++c) tc::tmem_ld4(tmem + 64 + sp * 32 + tl + c * AT_QR + rb, ov + c * AT_GR);
+            tc::tmem_ld_wait();
+          }
           tc::fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&ofree[sp]);
 #pragma unroll
-          for (int r = 0; r < AT_QR; ++r)
-            if (r < nrows) o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_QR + r]) + ov[2 * AT_QR + r]);
+          for (int r = 0; r < AT_GR; ++r)
+            if (rb + r < nrows)
+              o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_GR + r]) + ov[2 * AT_GR + r]);
         }
 #pragma unroll
-        for (int r = 0; r < AT_QR; ++r) fac_prev[r] = fac[r];
+        for (int r = 0; r < AT_GR; ++r) fac_prev[r] = fac[r];
       } else {        // drain O(last)
         const uint32_t gp = g + ntiles - 1;
         const int sp = gp & 1;
         tc::mbar_wait(&ofull[sp], (gp >> 1) & 1);
         tc::fence_after();
-        float ov[AT_N];
+        float ov[3 * AT_GR];
+        if (active) {
 #pragma unroll
-        for (int c = 0; c < AT_N; c += 8) tc::tmem_ld8(tmem + 64 + sp * 32 + tl + c, ov + c);
-        tc::tmem_ld_wait();
+          for (int c = 0; c < 3; ++c) tc::tmem_ld4(tmem + 64 + sp * 32 + tl + c * AT_QR + rb, ov + c * AT_GR);
+          tc::tmem_ld_wait();
+        }
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&ofree[sp]);
 #pragma unroll
-        for (int r = 0; r < AT_QR; ++r)
-          if (r < nrows) o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_QR + r]) + ov[2 * AT_QR + r]);
+        for (int r = 0; r < AT_GR; ++r)
+          if (rb + r < nrows)
+            o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_GR + r]) + ov[2 * AT_GR + r]);
       }
     }
     g += ntiles;
     // ---- l: sum of the per-thread partials (fixed order), then write partial state ----
 #pragma unroll
-    for (int r = 0; r < AT_QR; ++r) {
-      if (r < nrows) {
+    for (int r = 0; r < AT_GR; ++r) {
+      if (rb + r < nrows) {
         float v = l_run[r];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) redl[warp][r] = v;
+        if (lane == 0) redl[warp & 3][rb + r] = v;
       }
     }
-    named_sync();
+    group_sync(grp);
     const size_t pbase = (size_t)split * a.t * a.H;
 #pragma unroll
-    for (int r = 0; r < AT_QR; ++r) {
-      if (r < nrows) {
-        const int i = (r0 + r) / a.g, head = kh * a.g + (r0 + r) % a.g;
+    for (int r = 0; r < AT_GR; ++r) {
+      const int rr = rb + r;
+      if (rr < nrows) {
+        const int i = (r0 + rr) / a.g, head = kh * a.g + (r0 + rr) % a.g;
         const size_t row = (size_t)i * a.H + head;
-        a.part_o[(pbase + row) * AT_DH + tid] = o_acc[r];
-        if (tid == 0) {
+        a.part_o[(pbase + row) * AT_DH + ltid] = o_acc[r];
+        if (ltid == 0) {
           a.part_m[pbase + row] = m_run[r] * 0.69314718055994530942f;   // back to natural-log units
-          a.part_l[pbase + row] = (redl[0][r] + redl[1][r]) + (redl[2][r] + redl[3][r]);
+          a.part_l[pbase + row] = (redl[0][rr] + redl[1][rr]) + (redl[2][rr] + redl[3][rr]);
         }
       }
     }
-    named_sync();
+    softmax_sync();
   }
   tc::fence_before();
-  named_sync();
+  softmax_sync();
   if (warp == 0) tc::tmem_dealloc<128>(tmem);
 }
 
