@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
 // run in split order with the partial-o loads issued 8 at a time (the loop is
 // otherwise one dependent L2 round trip per split).
 __global__ void attn_combine_kernel(const float *pm, const float *pl, const float *po, int n_splits,
-                                    int rows, int DH, float *out, float *packed) {
+                                    int rows, int DH, float *out, float *packed, uint16_t *xs, int ldxs, int H) {
   extern __shared__ float comb_s[];          // [n_splits] weights | [n_splits] l
   float *sw = comb_s, *sl = comb_s + n_splits;
   __shared__ float red[32];
@@ -246,8 +246,13 @@ __global__ void attn_combine_kernel(const float *pm, const float *pl, const floa
     }
     for (; s < n_splits; ++s)
       if (sw[s] != 0.f) o = fmaf(sw[s], pd[(size_t)s * rows * DH], o);
-    if (packed) packed[(size_t)row * (DH + 2) + 2 + d] = o;
-    else out[(size_t)row * DH + d] = o / l;
+    if (packed) {
+      packed[(size_t)row * (DH + 2) + 2 + d] = o;
+    } else {
+      const float v = o / l;
+      if (out) out[(size_t)row * DH + d] = v;
+      if (xs) store_split(xs, ldxs, row / H, (row % H) * DH + d, v);
+    }
   }
   if (packed && tid == 0) {
     packed[(size_t)row * (DH + 2)] = M;
@@ -258,7 +263,8 @@ __global__ void attn_combine_kernel(const float *pm, const float *pl, const floa
 // rank-ordered merge of packed partial states [G][rows][2 + DH];
 // the same arithmetic as attn_combine_kernel, so a 1-rank merge of a packed
 // partial reproduces the unsharded output bit for bit.
-__global__ void shard_merge_kernel(const float *parts, int G, int rows, int DH, float *out) {
+__global__ void shard_merge_kernel(const float *parts, int G, int rows, int DH, float *out, uint16_t *xs, int ldxs,
+                                   int H) {
   const int row = blockIdx.x;
   const size_t stride = (size_t)rows * (DH + 2);
   float M = -INFINITY;
@@ -273,13 +279,16 @@ __global__ void shard_merge_kernel(const float *parts, int G, int rows, int DH, 
       l = fmaf(w, p[1], l);
       o = fmaf(w, p[2 + d], o);
     }
-    out[(size_t)row * DH + d] = o / l;
+    const float v = o / l;
+    if (out) out[(size_t)row * DH + d] = v;
+    if (xs) store_split(xs, ldxs, row / H, (row % H) * DH + d, v);
   }
 }
 
-int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, cudaStream_t st) {
+int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, uint16_t *xs, int ldxs, int H,
+                       cudaStream_t st) {
   HS_REQUIRE(G >= 1 && rows >= 1, HS_ERR_VALUE, "shard_merge: empty");
-  shard_merge_kernel<<<rows, DH < 128 ? DH : 128, 0, st>>>(parts, G, rows, DH, out);
+  shard_merge_kernel<<<rows, DH < 128 ? DH : 128, 0, st>>>(parts, G, rows, DH, out, xs, ldxs, H > 0 ? H : 1);
   return check_launch("shard_merge");
 }
 
@@ -310,18 +319,24 @@ static ProfPair *prof_begin(const HsCache *c, const HsStep *st, cudaStream_t str
 }
 
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
-                     float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream);
+                     float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
+                     uint16_t *xs = nullptr, int ldxs = 0);
 
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
-                           float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream) {
+                           float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
+                           uint16_t *xs, int ldxs) {
   ProfPair *p = prof_begin(c, st, stream);
-  const int rc = launch_attention(c, layer, st, H, q, t, out, packed, ws, ws_bytes, stream);
+  const int rc = launch_attention(c, layer, st, H, q, t, out, packed, ws, ws_bytes, stream, xs, ldxs);
   if (p) cudaEventRecord(p->b, stream);
   return rc;
 }
 
+// out: normalised rows [t][H*DH] fp32 (may be null when xs is given);
+// xs: additionally the exact 3-way split operand [24][ldxs] of the next GEMV
+// (t <= 8), so no separate split kernel runs before wo
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
-                     float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream) {
+                     float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
+                     uint16_t *xs, int ldxs) {
   const int DH = c->head_dim, KVH = c->n_kv_heads;
   HS_REQUIRE(H % KVH == 0, HS_ERR_SHAPE, "attention: H %% KVH != 0");
   HS_REQUIRE(st->split > 0 && st->split % ATT_TILE == 0, HS_ERR_VALUE, "attention: split must be a multiple of %d", ATT_TILE);
@@ -346,7 +361,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   dim3 grid(n_splits, KVH, ceil_div(a.g * t, ATT_QROWS));
   if (n_splits == 0) {   // empty shard view: partial state (-inf, 0, 0) for every row
     attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 16, stream>>>(a.part_m, a.part_l, a.part_o, 0, t * H, DH,
-                                                                     nullptr, packed);
+                                                                     nullptr, packed, nullptr, 0, H);
     return check_launch("attention(empty)");
   }
   // head_dim 128 (the Llama-family targets) runs on the tensor cores; the
@@ -366,7 +381,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
     default: return set_error(HS_ERR_SHAPE, "attention: head_dim %d unsupported (8/16/32/64/128)", DH);
   }
   attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 2 * n_splits * sizeof(float), stream>>>(a.part_m, a.part_l, a.part_o,
-                                                                   n_splits, t * H, DH, out, packed);
+                                                                   n_splits, t * H, DH, out, packed, xs, ldxs, H);
   return check_launch("attention", 2);
 }
 
@@ -424,5 +439,5 @@ extern "C" int hs_attention_partial(const HsCache *c, int layer, const HsStep *s
 }
 
 extern "C" int hs_shard_merge(const float *parts, int n_shards, int rows, int head_dim, float *out, void *stream) {
-  return hs::launch_shard_merge(parts, n_shards, rows, head_dim, out, hs::as_stream(stream));
+  return hs::launch_shard_merge(parts, n_shards, rows, head_dim, out, nullptr, 0, 1, hs::as_stream(stream));
 }

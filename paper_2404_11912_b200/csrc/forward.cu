@@ -16,8 +16,9 @@ int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int 
 int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv, int t,
                        float *q_out, float *q_stash, cudaStream_t st);
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
-                           float *packed, void *ws, size_t ws_bytes, cudaStream_t stream);
-int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, cudaStream_t st);
+                           float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs);
+int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, uint16_t *xs, int ldxs, int H,
+                       cudaStream_t st);
 int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
 
@@ -154,6 +155,7 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim, ff = m->d_ff;
   const int nqkv = (H + 2 * KVH) * dh;
   const float eps = m->norm_eps;
+  const bool fused_split = t <= 8;   // one row block: attention writes the wo operand itself
   int rc;
 #define HS_TRY(call) do { if ((rc = (call)) != HS_OK) return rc; } while (0)
   HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
@@ -173,16 +175,19 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
     if (sharded) {
       // this rank's partial softmax state -> all ranks -> rank-ordered merge
       const size_t part = (size_t)t * H * (dh + 2) * 4;
-      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s));
+      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr, 0));
       HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
-      HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, w.attn, s));
+      HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, fused_split ? nullptr : w.attn,
+                                fused_split ? w.xd : nullptr, m->ld_d, H, s));
     } else {
-      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s));
+      // t <= 8: the combine writes wo's split operand directly (no split kernel)
+      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, fused_split ? nullptr : w.attn, nullptr, w.att_ws,
+                                    w.att_bytes, s, fused_split ? w.xd : nullptr, m->ld_d));
     }
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
       float *xr = w.x + (size_t)r0 * d;
-      HS_TRY(launch_split_rows(w.attn + (size_t)r0 * d, d, tp, d, m->ld_d, nullptr, 0.f, w.xd, s));
+      if (!fused_split) HS_TRY(launch_split_rows(w.attn + (size_t)r0 * d, d, tp, d, m->ld_d, nullptr, 0.f, w.xd, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wo, m->ld_d, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
       HS_TRY(launch_split_rows(xr, d, tp, d, m->ld_d, mn, eps, w.xd, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes,

@@ -84,15 +84,6 @@ int get_tmap_bf16(const void *ptr, uint64_t inner, uint64_t rows, uint64_t row_s
 
 // ---------------------------------------------------------------------------
 // activation prep: optional RMSNorm, then exact 3-way bf16 split
-__device__ __forceinline__ void split3(float h, uint16_t &a, uint16_t &b, uint16_t &c) {
-  const __nv_bfloat16 hi = __float2bfloat16_rn(h);
-  const float r1 = h - __bfloat162float(hi);
-  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-  const float r2 = r1 - __bfloat162float(mid);
-  a = __bfloat16_as_ushort(hi);
-  b = __bfloat16_as_ushort(mid);
-  c = f_to_bf16(r2);
-}
 
 // grid (column blocks of SPLIT_COLS, TC_T rows); rows >= t are written as zeros.
 // With a gain, every CTA of a row recomputes the row's sum of squares over

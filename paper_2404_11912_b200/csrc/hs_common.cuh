@@ -28,6 +28,27 @@ __device__ __forceinline__ uint16_t f_to_bf16(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
+// exact 3-way bf16 split h = hi + mid + lo (8+8+8 significand bits: the full
+// fp32 mantissa), the operand format of the tensor-core GEMV
+__device__ __forceinline__ void split3(float h, uint16_t &a, uint16_t &b, uint16_t &c) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(h);
+  const float r1 = h - __bfloat162float(hi);
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  const float r2 = r1 - __bfloat162float(mid);
+  a = __bfloat16_as_ushort(hi);
+  b = __bfloat16_as_ushort(mid);
+  c = f_to_bf16(r2);
+}
+
+// element (row r <= 7, column k) of a split operand [24][ld]
+__device__ __forceinline__ void store_split(uint16_t *xs, int ld, int r, int k, float v) {
+  uint16_t a, b, c;
+  split3(v, a, b, c);
+  xs[(size_t)r * ld + k] = a;
+  xs[(size_t)(8 + r) * ld + k] = b;
+  xs[(size_t)(16 + r) * ld + k] = c;
+}
+
 // 16-byte streaming load that bypasses L1 allocation (weights, KV: read once)
 __device__ __forceinline__ uint4 ld_stream(const void *p) {
   uint4 r;
