@@ -157,6 +157,16 @@ int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsSha
                const int32_t *tokens, int t, float *logits, float *q_stash,
                void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- batched prefill (model.py:334-354) --------------
+ * Same contract as hs_forward for an unsharded cache, for long prompts: the
+ * dense projections run as tensor-core GEMMs (cuBLAS, three bf16 GEMMs over
+ * the exact split of the fp32 activations, fp32 accumulation) in blocks of
+ * 512 rows, attention causally in blocks of 1024 query rows.  fp32-accurate
+ * but not bit-identical to a decode_step sequence (use hs_forward for that). */
+size_t hs_prefill_workspace_bytes(const HsModel *m, int t, int n_view, int split);
+int hs_prefill(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
+               float *logits, float *q_stash, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- building blocks (also used by tests and the per-layer cache API) ---- */
 
 /* y[r][o] (+)= sum_k pro(x)[r][k] * W[o][k]   (tensor.py:26-36 matmul)

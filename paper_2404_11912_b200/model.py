@@ -431,10 +431,16 @@ class ForwardRecorder:
         return []
 
 
+PREFILL_MIN_ROWS = 64   # prompts at least this long take the GEMM prefill (hs_prefill)
+
+
 def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[ForwardRecorder] = None,
-                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                   out: Optional[torch.Tensor] = None, prefill: bool = False) -> torch.Tensor:
     """Causal forward of `tokens` (host list or device int32 tensor) at
-    cache.frontier; returns device logits [t, V] fp32 (model.py:247-331)."""
+    cache.frontier; returns device logits [t, V] fp32 (model.py:247-331).
+    prefill=True lets a long prompt on an unsharded full cache run through
+    the batched GEMM prefill (hs_prefill); otherwise every row is computed
+    exactly as a decode step would compute it."""
     dm = weights.device()
     cfg = dm.config
     tok = to_i32_device(tokens)
@@ -453,6 +459,16 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
     shards = getattr(cache, "shards", None)
     shard_ref = shards.ref if shards is not None else None
     world = shards.world if shards is not None else 0
+    if prefill and t >= PREFILL_MIN_ROWS and cache.kind == _abi.HS_KV_LINEAR and shards is None:
+        step = cache._step(t)
+        nbytes = lib.hs_prefill_workspace_bytes(dm.ref, t, step.n_view, step.split)
+        ws = workspaces.get("prefill", nbytes)
+        check(lib.hs_prefill(dm.ref, cache._ref, C.byref(step), ptr(tok), t, ptr(out), ptr(stash), ptr(ws), nbytes,
+                             stream_ptr()))
+        cache._advance(t)
+        if recorder is not None:
+            recorder.query_position = cache.frontier - 1
+        return out
     for a, b in cache._batches(t):
         step = cache._step(b - a)
         nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split, world)
@@ -483,7 +499,7 @@ def prefill(weights: ModelWeights, tokens: Sequence[int], cache,
     if cache.frontier + len(tokens) > weights.config.max_seq:
         raise CapacityError(f"sequence of {cache.frontier + len(tokens)} exceeds max_seq "
                             f"{weights.config.max_seq}")
-    logits = forward_device(weights, tokens, cache, recorder)
+    logits = forward_device(weights, tokens, cache, recorder, prefill=True)
     cache.commit(cache.frontier)
     return _host_rows(logits)
 

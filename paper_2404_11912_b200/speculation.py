@@ -219,7 +219,11 @@ class Lane:
     def prefill(self, tokens: Sequence[int]) -> None:
         if len(tokens) == 0:
             raise ValueError("prefill needs at least one token")
-        self._forward(list(tokens))
+        t = len(tokens)
+        out = forward_device(self.weights, list(tokens), self.cache, self.recorder, out=self._logits_buf(t),
+                             prefill=True)
+        self._front.copy_(out[t - 1])
+        self._has_front = True
         self.cache.commit(self.cache.frontier)
 
     def advance(self, tokens: Sequence[int]) -> None:

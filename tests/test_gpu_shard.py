@@ -49,8 +49,12 @@ def test_one_rank_sharded_forward_is_bitwise_unsharded(P, one_rank):
     prompt = np.random.default_rng(0).integers(1, 512, 700).tolist()
     a = P.FullCache.from_config(tw.config)
     b = P.FullCache.shard(tw.config, one_rank, len(prompt), 8)
-    la = P.prefill(tw, prompt, a)
-    lb = P.prefill(tw, prompt, b)
+    # the row-exact decode path on both sides (the GEMM prefill is unsharded-only)
+    from paper_2404_11912_b200 import model as M
+    la = M._host_rows(M.forward_device(tw, prompt, a, None, prefill=False))
+    lb = M._host_rows(M.forward_device(tw, prompt, b, None, prefill=False))
+    a.commit(a.frontier)
+    b.commit(b.frontier)
     assert np.array_equal(la, lb)
     for tok in (3, 17, 400):
         assert np.array_equal(P.decode_step(tw, tok, a), P.decode_step(tw, tok, b))
