@@ -67,12 +67,18 @@ def test_one_rank_sharded_session_matches_unsharded(P, one_rank):
     spec = P.SpecConfig(target_len=900 + 80, gamma1=2, gamma2=4, temperature=0.6, seed=3,
                         streaming=P.StreamingConfig(n_sink=4, budget=128),
                         retrieval=P.RetrievalConfig(chunk_size=8, budget=128, rebuild_stride=24))
-    out_a, tr_a = P.HierarchicalSession(tw, dw, prompt, spec).generate()
-    out_b, tr_b = P.HierarchicalSession(tw, dw, prompt, spec, shards=one_rank).generate()
-    assert out_a == out_b
-    assert tr_a.summary() == tr_b.summary()
-    ar = P.autoregressive_generate(tw, prompt, 900 + 20, 0.0, 0, shards=one_rank, chunk=8)
-    assert ar == P.autoregressive_generate(tw, prompt, 900 + 20, 0.0, 0)
+    from paper_2404_11912_b200 import model as M
+    keep = M.PREFILL_MIN_ROWS
+    M.PREFILL_MIN_ROWS = 10 ** 9      # unsharded prompt through the row-exact path too: bitwise comparison
+    try:
+        out_a, tr_a = P.HierarchicalSession(tw, dw, prompt, spec).generate()
+        out_b, tr_b = P.HierarchicalSession(tw, dw, prompt, spec, shards=one_rank).generate()
+        assert out_a == out_b
+        assert tr_a.summary() == tr_b.summary()
+        ar = P.autoregressive_generate(tw, prompt, 900 + 20, 0.0, 0, shards=one_rank, chunk=8)
+        assert ar == P.autoregressive_generate(tw, prompt, 900 + 20, 0.0, 0)
+    finally:
+        M.PREFILL_MIN_ROWS = keep
 
 
 def _fill(cache, K, V, positions):
