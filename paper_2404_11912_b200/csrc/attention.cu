@@ -214,6 +214,8 @@ __global__ void attn_combine_kernel(const float *pm, const float *pl, const floa
                                     int rows, int DH, float *out, float *packed, uint16_t *xs, int ldxs, int H) {
   extern __shared__ float comb_s[];          // [n_splits] weights | [n_splits] l
   float *sw = comb_s, *sl = comb_s + n_splits;
+  // the next GEMV (wo, PDL-launched) may start streaming its weights now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ float red[32];
   const int row = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   float mx = -INFINITY;
