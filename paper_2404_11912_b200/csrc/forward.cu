@@ -6,6 +6,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include "gemv_norm.h"
 #include "hs_common.cuh"
 
 namespace hs {
@@ -57,7 +58,10 @@ int check_launch(const char *what, int n_kernels) {
 int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const float *gain, float eps, uint16_t *xs,
                       cudaStream_t st);
 int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
-                   uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st);
+                   uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st,
+                   const GemvNorm *norm = nullptr);
+int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk, double *ssq,
+                     cudaStream_t st);
 size_t gemv_tc_ws_bytes(int N, int nkb);
 
 // Workspace layout.  The head is position-independent so that the regions
@@ -69,7 +73,8 @@ size_t gemv_tc_ws_bytes(int N, int nkb);
 struct FwdWs {
   void *gemv_ws;
   size_t gemv_bytes;
-  uint16_t *xd, *xf;
+  uint16_t *xd, *xf, *xa;   // split operands: normed input (xd), act (xf), attention output (xa)
+  double *ssq;              // [1024][8] row sums of squares of the residual stream
   float *x, *qkv, *q, *attn;
   void *att_ws;
   size_t att_bytes;
@@ -98,6 +103,8 @@ static size_t carve(const HsModel *m, int t, int n_view, int split, int world, c
   w->gemv_ws = take(w->gemv_bytes);
   w->xd = (uint16_t *)take((size_t)24 * m->ld_d * 2);
   w->xf = (uint16_t *)take((size_t)24 * m->ld_ff * 2);
+  w->xa = (uint16_t *)take((size_t)24 * m->ld_d * 2);
+  w->ssq = (double *)take((size_t)1024 * 8 * 8);
   w->x = (float *)take((size_t)t * d * 4);
   w->qkv = (float *)take((size_t)t * (H + 2 * KVH) * dh * 4);
   w->q = (float *)take((size_t)t * H * dh * 4);
@@ -129,7 +136,8 @@ extern "C" size_t hs_forward_workspace_bytes(const HsModel *m, int t, int n_view
 
 extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
   // bytes at the head of the workspace that must be zero before the first call
-  return hs::gemv_region(m) + hs::align256((size_t)24 * m->ld_d * 2) + hs::align256((size_t)24 * m->ld_ff * 2);
+  return hs::gemv_region(m) + hs::align256((size_t)24 * m->ld_d * 2) + hs::align256((size_t)24 * m->ld_ff * 2) +
+         hs::align256((size_t)24 * m->ld_d * 2);
 }
 
 extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
@@ -155,9 +163,55 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim, ff = m->d_ff;
   const int nqkv = (H + 2 * KVH) * dh;
   const float eps = m->norm_eps;
-  const bool fused_split = t <= 8;   // one row block: attention writes the wo operand itself
+  const bool fused_split = t <= 8;   // one row block: folded norms, no split kernels
+  const int d_tiles = (d + 127) / 128;
   int rc;
 #define HS_TRY(call) do { if ((rc = (call)) != HS_OK) return rc; } while (0)
+  if (fused_split) {
+    // ---- one row block (decode / verify): every RMSNorm is folded into the
+    // GEMVs -- the residual producer (embedding, wo, w_down) writes the next
+    // operand split(x * gain) and per-tile row sums of squares, the consumer
+    // (wqkv, gate|up, lm_head) scales its result by 1 / rms -- so no split /
+    // normalise kernel runs between the weight streams.
+    HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
+    HS_TRY(launch_norm_prep(w.x, d, t, d, m->attn_norm, w.xd, m->ld_d, w.ssq, s));
+    for (int l = 0; l < m->n_layers; ++l) {
+      const uint16_t *wqkv = m->wqkv + (size_t)l * nqkv * m->ld_d;
+      const uint16_t *wo = m->wo + (size_t)l * d * m->ld_d;
+      const uint16_t *wgu = m->wgu + (size_t)l * 2 * ff * m->ld_d;
+      const uint16_t *wdn = m->wdown + (size_t)l * d * m->ld_ff;
+      const bool last = l + 1 == m->n_layers;
+      GemvNorm in_qkv = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+      HS_TRY(launch_gemv_tc(w.xd, t, wqkv, m->ld_d, nqkv, 0, w.qkv, nqkv, nullptr, 0, w.gemv_ws, w.gemv_bytes, s,
+                            &in_qkv));
+      HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
+      if (sharded) {
+        const size_t part = (size_t)t * H * (dh + 2) * 4;
+        HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr, 0));
+        HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
+        HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, nullptr, w.xa, m->ld_d, H, s));
+      } else {
+        HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, nullptr, w.att_ws, w.att_bytes, s, w.xa,
+                                      m->ld_d));
+      }
+      GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq};
+      HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo));
+      GemvNorm in_gu = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+      HS_TRY(launch_gemv_tc(w.xd, t, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes, s,
+                            &in_gu));
+      GemvNorm out_dn = {nullptr, 0, 1, 0.f, last ? m->final_norm : m->attn_norm + (size_t)(l + 1) * d, w.xd, m->ld_d,
+                         w.ssq};
+      HS_TRY(launch_gemv_tc(w.xf, t, wdn, m->ld_ff, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_dn));
+    }
+    GemvNorm in_head = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+    HS_TRY(launch_gemv_tc(w.xd, t, m->head, m->ld_d, m->vocab_size, 0, logits, m->vocab_size, nullptr, 0, w.gemv_ws,
+                          w.gemv_bytes, s, &in_head));
+    return HS_OK;
+  }
+  // ---- several row blocks (prefill-sized batches through the decode path):
+  // the same folded-norm GEMVs per block of 8 rows, the operand and row
+  // statistics prepared by norm_prep (bit-identical to the producing GEMV
+  // epilogue of the single-block path), so every row equals a decode step.
   HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
   for (int l = 0; l < m->n_layers; ++l) {
     const uint16_t *wqkv = m->wqkv + (size_t)l * nqkv * m->ld_d;
@@ -165,11 +219,12 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
     const uint16_t *wgu = m->wgu + (size_t)l * 2 * ff * m->ld_d;
     const uint16_t *wdn = m->wdown + (size_t)l * d * m->ld_ff;
     const float *an = m->attn_norm + (size_t)l * d, *mn = m->mlp_norm + (size_t)l * d;
+    GemvNorm in_n = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
-      HS_TRY(launch_split_rows(w.x + (size_t)r0 * d, d, tp, d, m->ld_d, an, eps, w.xd, s));
+      HS_TRY(launch_norm_prep(w.x + (size_t)r0 * d, d, tp, d, an, w.xd, m->ld_d, w.ssq, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wqkv, m->ld_d, nqkv, 0, w.qkv + (size_t)r0 * nqkv, nqkv, nullptr, 0, w.gemv_ws,
-                            w.gemv_bytes, s));
+                            w.gemv_bytes, s, &in_n));
     }
     HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
     if (sharded) {
@@ -177,29 +232,27 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
       const size_t part = (size_t)t * H * (dh + 2) * 4;
       HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr, 0));
       HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
-      HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, fused_split ? nullptr : w.attn,
-                                fused_split ? w.xd : nullptr, m->ld_d, H, s));
+      HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, w.attn, nullptr, m->ld_d, H, s));
     } else {
-      // t <= 8: the combine writes wo's split operand directly (no split kernel)
-      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, fused_split ? nullptr : w.attn, nullptr, w.att_ws,
-                                    w.att_bytes, s, fused_split ? w.xd : nullptr, m->ld_d));
+      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s, nullptr, 0));
     }
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
       float *xr = w.x + (size_t)r0 * d;
-      if (!fused_split) HS_TRY(launch_split_rows(w.attn + (size_t)r0 * d, d, tp, d, m->ld_d, nullptr, 0.f, w.xd, s));
+      HS_TRY(launch_split_rows(w.attn + (size_t)r0 * d, d, tp, d, m->ld_d, nullptr, 0.f, w.xd, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wo, m->ld_d, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
-      HS_TRY(launch_split_rows(xr, d, tp, d, m->ld_d, mn, eps, w.xd, s));
-      HS_TRY(launch_gemv_tc(w.xd, tp, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes,
-                            s));
+      HS_TRY(launch_norm_prep(xr, d, tp, d, mn, w.xd, m->ld_d, w.ssq, s));
+      HS_TRY(launch_gemv_tc(w.xd, tp, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes, s,
+                            &in_n));
       HS_TRY(launch_gemv_tc(w.xf, tp, wdn, m->ld_ff, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
     }
   }
   for (int r0 = 0; r0 < t; r0 += 8) {
     const int tp = t - r0 < 8 ? t - r0 : 8;
-    HS_TRY(launch_split_rows(w.x + (size_t)r0 * d, d, tp, d, m->ld_d, m->final_norm, eps, w.xd, s));
+    GemvNorm in_n = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+    HS_TRY(launch_norm_prep(w.x + (size_t)r0 * d, d, tp, d, m->final_norm, w.xd, m->ld_d, w.ssq, s));
     HS_TRY(launch_gemv_tc(w.xd, tp, m->head, m->ld_d, m->vocab_size, 0, logits + (size_t)r0 * m->vocab_size,
-                          m->vocab_size, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
+                          m->vocab_size, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &in_n));
   }
 #undef HS_TRY
   return HS_OK;

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <unordered_map>
 
+#include "gemv_norm.h"
 #include "hs_common.cuh"
 #include "tc_util.cuh"
 
@@ -139,8 +140,50 @@ __global__ void __launch_bounds__(SPLIT_THREADS) split_rows_kernel(const float *
   }
 }
 
+// Folded-RMSNorm operand prep for rows [0, t) of x: split(fp32(x * gain))
+// into xs [24][ldk] and per-128-column-tile row sums of squares into
+// ssq [tile][8].  Thread i of a CTA owns column tile * 128 + i and the sums
+// run lanes-then-warps in the same order as the residual GEMV epilogue
+// (finalize), so both producers of an operand give identical bits.
+// grid (tiles, t), 128 threads.
+__global__ void __launch_bounds__(128) norm_prep_kernel(const float *x, int ldx, int K, const float *gain,
+                                                        uint16_t *xs, int ldk, double *ssq) {
+  const int tile = blockIdx.x, r = blockIdx.y, col = tile * 128 + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ double red[4];
+  double sq = 0.0;
+  if (col < K) {
+    const float v = x[(size_t)r * ldx + col];
+    sq = (double)v * (double)v;
+    store_split(xs, ldk, r, col, (float)((double)v * (double)gain[col]));
+  }
+  sq = warp_sum(sq);
+  if (lane == 0) red[w] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) ssq[(size_t)tile * TC_T + r] = (red[0] + red[1]) + (red[2] + red[3]);
+}
+
+int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk, double *ssq,
+                     cudaStream_t st) {
+  HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "norm_prep: t=%d outside [1,%d]", t, TC_T);
+  norm_prep_kernel<<<dim3((K + 127) / 128, t), 128, 0, st>>>(x, ldx, K, gain, xs, ldk, ssq);
+  return check_launch("norm_prep");
+}
+
 struct GemvTcArgs {
   int N, nkb, ks, t, epilogue, n_tiles;
+  // folded RMSNorm (model.py:282-284) of this GEMV's input rows: the operand
+  // is split(x * gain) and the result is scaled by 1 / rms(x) here, with the
+  // row sums of squares given as ssq_parts per-tile partials [parts][8]
+  const double *ssq_in;
+  int ssq_parts, norm_K;
+  float eps;
+  // residual producer (epilogue 1): also write the next GEMV's operand
+  // split(x_new * gnext) and this tile's row sums of squares of x_new
+  const float *gnext;
+  uint16_t *xs_next;
+  int ld_next;
+  double *ssq_out;
   float *y;
   int ldy;
   uint16_t *xs_out;   // swiglu epilogue: split of act written here ([24][ld_xs_out]) if non-null
@@ -149,7 +192,13 @@ struct GemvTcArgs {
   int *counters;      // [n_tiles]
 };
 
-__device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float *v, int lane) {
+// all 128 threads of the CTA call finalize (uniform control flow: the residual
+// producer reduces its tile's row sums of squares across the CTA)
+__device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float *vin, int lane, int tile,
+                                         const double *inv_rms, double (*red)[TC_T]) {
+  float v[TC_T];
+#pragma unroll
+  for (int r = 0; r < TC_T; ++r) v[r] = a.ssq_in ? (float)((double)vin[r] * inv_rms[r]) : vin[r];
   if (a.epilogue == 2) {
     float up[TC_T];
 #pragma unroll
@@ -162,25 +211,38 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
           const double g = (double)v[r];
           const float act = (float)(g * (0.5 * (tanh(0.5 * g) + 1.0))) * up[r];   // model.py:321-322
           if (a.y) a.y[(size_t)r * a.ldy + i] = act;
-          if (a.xs_out) {
-            uint16_t h0, h1, h2;
-            split3(act, h0, h1, h2);
-            a.xs_out[(size_t)r * a.ld_xs_out + i] = h0;
-            a.xs_out[(size_t)(TC_T + r) * a.ld_xs_out + i] = h1;
-            a.xs_out[(size_t)(2 * TC_T + r) * a.ld_xs_out + i] = h2;
-          }
+          if (a.xs_out) store_split(a.xs_out, a.ld_xs_out, r, i, act);
         }
       }
     }
     return;
   }
-  if (o >= a.N) return;
+  double sq[TC_T];
 #pragma unroll
   for (int r = 0; r < TC_T; ++r) {
-    if (r < a.t) {
+    sq[r] = 0.0;
+    if (r < a.t && o < a.N) {
       float *p = a.y + (size_t)r * a.ldy + o;
-      *p = (a.epilogue == 1) ? (*p + v[r]) : v[r];
+      const float nv = (a.epilogue == 1) ? (*p + v[r]) : v[r];
+      *p = nv;
+      if (a.xs_next) {
+        sq[r] = (double)nv * (double)nv;
+        store_split(a.xs_next, a.ld_next, r, o, (float)((double)nv * (double)a.gnext[o]));
+      }
     }
+  }
+  if (a.xs_next == nullptr) return;
+  // this tile's row sums of squares, fixed order: lanes, then the 4 warps
+  const int w = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < TC_T; ++r) {
+    const double sr = warp_sum(sq[r]);
+    if (lane == 0) red[w][r] = sr;
+  }
+  __syncthreads();
+  if (threadIdx.x < TC_T) {
+    const int r = threadIdx.x;
+    a.ssq_out[(size_t)tile * TC_T + r] = (red[0][r] + red[1][r]) + (red[2][r] + red[3][r]);
   }
 }
 
@@ -261,10 +323,18 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   }
   if (warp != 0) tc::grid_dep_wait();   // epilogue reads y written by earlier kernels
   __syncwarp();
+  __shared__ double inv_rms[TC_T];
+  __shared__ double red[4][TC_T];
+  if (a.ssq_in && warp == 2 && lane < TC_T) {   // folded RMSNorm: 1 / sqrt(mean(x^2) + eps) per row
+    double ss = 0.0;
+    for (int k = 0; k < a.ssq_parts; ++k) ss += __ldcg(a.ssq_in + (size_t)k * TC_T + lane);
+    inv_rms[lane] = 1.0 / sqrt(ss / (double)a.norm_K + (double)a.eps);
+  }
 
   // ---- epilogue: TMEM -> registers ---------------------------------------------------
   tc::mbar_wait(accum, 0);
   tc::fence_after();
+  __syncthreads();   // inv_rms visible
   const int row = warp * 32 + lane;
   const uint32_t tl = taddr + ((uint32_t)(warp * 32) << 16);
   float h[8], m[8], l[8], v[TC_T];
@@ -277,7 +347,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   const int o = tile * TC_BM + row;
 
   if (a.ks == 1) {
-    finalize(a, o, v, lane);
+    finalize(a, o, v, lane, tile, inv_rms, red);
   } else {
     float *pp = a.partial + ((size_t)split * a.n_tiles * TC_BM + o) * TC_T;
     *reinterpret_cast<float4 *>(pp) = make_float4(v[0], v[1], v[2], v[3]);
@@ -300,7 +370,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
         v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
         v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
       }
-      finalize(a, o, v, lane);
+      finalize(a, o, v, lane, tile, inv_rms, red);
       if (threadIdx.x == 0) a.counters[tile] = 0;   // self-cleaning for the next launch
     }
   }
@@ -351,7 +421,8 @@ int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const floa
 
 // y (+)= W . x for one pass of <= 8 rows whose split operand is in xs [24][ldw]
 int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
-                   uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st) {
+                   uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st,
+                   const GemvNorm *norm) {
   HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "gemv_tc: t=%d outside [1,%d]", t, TC_T);
   HS_REQUIRE(ldw % TC_BK == 0, HS_ERR_SHAPE, "gemv_tc: ldw %d not a multiple of %d", ldw, TC_BK);
   HS_REQUIRE(((uintptr_t)w % 16) == 0 && ((uintptr_t)xs % 16) == 0, HS_ERR_VALUE, "gemv_tc: operands must be 16B aligned");
@@ -368,6 +439,14 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   GemvTcArgs a;
   a.N = N; a.nkb = nkb; a.ks = gemv_tc_ksplit(N, nkb); a.t = t; a.epilogue = epilogue; a.n_tiles = tiles;
   a.y = y; a.ldy = ldy; a.xs_out = xs_out; a.ld_xs_out = ld_xs_out;
+  a.ssq_in = nullptr; a.ssq_parts = 0; a.norm_K = 1; a.eps = 0.f;
+  a.gnext = nullptr; a.xs_next = nullptr; a.ld_next = 0; a.ssq_out = nullptr;
+  if (norm) {
+    a.ssq_in = norm->ssq_in; a.ssq_parts = norm->ssq_parts; a.norm_K = norm->norm_K; a.eps = norm->eps;
+    a.gnext = norm->gnext; a.xs_next = norm->xs_next; a.ld_next = norm->ld_next; a.ssq_out = norm->ssq_out;
+    HS_REQUIRE(a.xs_next == nullptr || epilogue == 1, HS_ERR_VALUE, "gemv_tc: next-operand output needs epilogue 1");
+    HS_REQUIRE(a.xs_next == nullptr || tiles <= 1024, HS_ERR_SHAPE, "gemv_tc: too many tiles for the norm partials");
+  }
   a.counters = reinterpret_cast<int *>(ws);
   a.partial = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + (size_t)TC_COUNTER_INTS * 4);
   static bool attr_set = false;
@@ -402,5 +481,5 @@ extern "C" int hs_split_rows(const float *x, int ldx, int t, int K, int ldk, con
 extern "C" int hs_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                           uint16_t *xs_out, int ld_xs_out, void *workspace, size_t ws_bytes, void *stream) {
   return hs::launch_gemv_tc(xs, t, w, ldw, N, epilogue, y, ldy, xs_out, ld_xs_out, workspace, ws_bytes,
-                            hs::as_stream(stream));
+                            hs::as_stream(stream), nullptr);
 }

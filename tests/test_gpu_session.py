@@ -63,6 +63,12 @@ def test_chunk_equals_step_sequence_bitwise(P):
     chunk = P.decode_chunk(w, [9, 10, 11], c1)
     steps = np.stack([P.decode_step(w, tk, c2) for tk in (9, 10, 11)])
     assert np.array_equal(chunk, steps)
+    # across the 8-row block boundary (multi-block path vs single-row steps)
+    toks = list(range(12, 32))
+    chunk = P.decode_chunk(w, toks, c1)
+    steps = np.stack([P.decode_step(w, tk, c2) for tk in toks])
+    assert np.array_equal(chunk, steps)
+    assert torch.equal(c1.k, c2.k) and torch.equal(c1.v, c2.v)
 
 
 def test_cfg1_prefill_and_queries(P, golden):
