@@ -34,7 +34,7 @@ import torch
 from ._abi import (HS_APPEND_LINEAR, HS_APPEND_POS, HS_APPEND_RING, HS_KV_LINEAR, HS_KV_SLOTTED, HsCache,
                    HsStep, check, lib)
 from .errors import CapacityError, ContractError, ShapeError
-from .runtime import STATS, as_device_f32, device, ptr, stream_ptr, workspaces
+from .runtime import STATS, as_device_f32, device, ptr, stream_ptr
 
 FULL_SPLIT = 2048     # keys per attention split over the full cache (fixed: t-invariant rows)
 SMALL_SPLIT = 512     # keys per split over the retrieval view

@@ -28,8 +28,7 @@ import torch
 from . import _abi
 from ._abi import HsModel, check, lib
 from .errors import CapacityError, FiniteError, ShapeError
-from .runtime import (STATS, UniformStream, as_device_f32, as_device_f64, device, ptr, stream_ptr,
-                      to_i32_device, workspaces)
+from .runtime import STATS, as_device_f32, as_device_f64, device, ptr, stream_ptr, to_i32_device, workspaces
 
 BOS = 256
 EOS = 257

@@ -8,8 +8,6 @@ through `_abi.lib`.
 
 from __future__ import annotations
 
-import ctypes as C
-
 import numpy as np
 import torch
 

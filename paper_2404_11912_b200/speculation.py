@@ -18,7 +18,9 @@ reference's (speculation.py:9-12), so traces replay the CPU engine.
 
 from __future__ import annotations
 
+import ctypes as C
 import json
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -29,13 +31,8 @@ from ._abi import check, lib, status_error
 from .caches import (FullCache, KVCache, RetrievalCache, RetrievalConfig, RollingAcceptance, StreamingCache,
                      StreamingConfig, should_rebuild)
 from .errors import ContractError
-from .model import (ForwardRecorder, ModelWeights, forward_device, prob_from_logits, sample_from_probs)
+from .model import ForwardRecorder, ModelWeights, forward_device
 from .runtime import STATS, UniformStream, as_device_f64, device, ptr, staging, stream_ptr, to_i32_device
-
-import ctypes as C
-import os
-
-from ._abi import HsModel  # noqa: F401  (ctypes layout shared with model.py)
 
 # CUDA-graph replay of the draft lane's one-token steps (HS_NO_GRAPHS=1 turns
 # it off: every step is then a regular hs_forward call with the same kernels)
