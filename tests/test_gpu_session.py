@@ -476,3 +476,40 @@ def test_gemm_prefill_matches_decode_path(P):
     assert (np.argmax(la, -1) == np.argmax(lb, -1)).mean() > 0.999
     dk = (a.k[:, :, :1500].float() - b.k[:, :, :1500].float()).abs().max().item()
     assert dk <= 0.02 * b.k[:, :, :1500].float().abs().max().item()
+
+
+@pytest.mark.parametrize("prompt_len,chunk,budget,stream,temp", [
+    (1, 8, 64, 16, 0.0),        # one-token prompt: the build's n == 1 special case (speculation.py:305-308)
+    (37, 16, 64, 32, 0.6),      # ragged last chunk, sampled
+    (203, 8, 256, 64, 0.0),     # budget >= context: clamped build (all chunks)
+    (1203, 16, 64, 48, 0.6),    # long, ragged, tiny budget, sampled
+])
+def test_edge_sessions_match_oracle(P, prompt_len, chunk, budget, stream, temp):
+    """Edge geometries of the reference's build/stream rules, with
+    non-degenerate acceptance: token stream, per-level accept counts and the
+    initial build's chunk selection equal the oracle's."""
+    from oracle import hs_oracle as O
+    mk = lambda w: O.OModel(O.OConfig(**{k: getattr(w.config, k) for k in w.config.__dataclass_fields__}),
+                            O.round_weights_bf16(w.tensors), w.tied_head)
+    tc = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=32, d_ff=96, vocab_size=300, max_seq=2048)
+    dc = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=32, d_ff=64, vocab_size=300, max_seq=2048)
+    tw = bf16_weights(P, P.plant_successor(P.generate_weights(tc, 31, tied_head=False), 4, 0.85))
+    dw = bf16_weights(P, P.plant_successor(P.generate_weights(dc, 32, tied_head=False), 4, 0.85))
+    prompt = np.random.default_rng(prompt_len).integers(1, 300, prompt_len).tolist()
+    n_gen = 48
+    spec = P.SpecConfig(target_len=prompt_len + n_gen, gamma1=2, gamma2=4, temperature=temp, seed=7,
+                        streaming=P.StreamingConfig(n_sink=4, budget=stream),
+                        retrieval=P.RetrievalConfig(chunk_size=chunk, budget=budget, rebuild_stride=24))
+    s = P.HierarchicalSession(tw, dw, prompt, spec)
+    imp0 = s.retr_lane.cache.table.selected
+    out, tr = s.generate()
+    os_ = O.OSession(mk(tw), mk(dw), prompt, O.OSpec(target_len=prompt_len + n_gen, gamma1=2, gamma2=4,
+                                                    temperature=temp, seed=7, n_sink=4, stream_budget=stream,
+                                                    chunk=chunk, retr_budget=budget, rebuild_stride=24),
+                     kv_bf16=True)
+    oimp0 = [list(map(int, layer[2])) for layer in os_.builds[0][0]]   # (bounds, scores, importance) per layer
+    oout, otr = os_.generate()
+    assert out == oout
+    assert [tr.inner.proposed, tr.inner.accepted, tr.outer.proposed, tr.outer.accepted] == \
+        [otr.inner[0], otr.inner[1], otr.outer[0], otr.outer[1]]
+    assert imp0 == oimp0
