@@ -18,6 +18,9 @@
 
 namespace hs {
 
+HS_TRACE_TU
+int trace_set_attn(void *p, unsigned cap) { return trace_set_tu(p, cap); }
+
 constexpr int ATT_THREADS = 128;
 constexpr int ATT_TILE = 64;     // keys per smem tile
 constexpr int ATT_QROWS = 16;    // query rows per CTA
@@ -44,6 +47,7 @@ __device__ __forceinline__ bool visible(int kp, int qp, const AttnArgs &a) {
 
 template <int DH>
 __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
+  HS_TRACE_BEGIN
   if (a.dyn) { a.pos0 += a.dyn[0]; a.win_lo = a.dyn[1]; }
   constexpr int KP = DH + 8;                 // padded K row (bf16) -> conflict-free 16B reads
   constexpr int NDP = DH / 2;                // dim pairs
@@ -202,6 +206,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
       }
     }
   }
+  HS_TRACE_END(8)
 }
 
 // out[i][h*DH + d] = sum_s w_s o_s / sum_s w_s l_s,  w_s = exp(m_s - M), splits in order.
@@ -212,6 +217,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
 // otherwise one dependent L2 round trip per split).
 __global__ void attn_combine_kernel(const float *pm, const float *pl, const float *po, int n_splits,
                                     int rows, int DH, float *out, float *packed, uint16_t *xs, int ldxs, int H) {
+  HS_TRACE_BEGIN
   extern __shared__ float comb_s[];          // [n_splits] weights | [n_splits] l
   float *sw = comb_s, *sl = comb_s + n_splits;
   // the next GEMV (wo, PDL-launched) may start streaming its weights now
@@ -260,6 +266,7 @@ __global__ void attn_combine_kernel(const float *pm, const float *pl, const floa
     packed[(size_t)row * (DH + 2)] = M;
     packed[(size_t)row * (DH + 2) + 1] = l;
   }
+  HS_TRACE_END(5)
 }
 
 // rank-ordered merge of packed partial states [G][rows][2 + DH];

@@ -32,6 +32,9 @@
 
 namespace hs {
 
+HS_TRACE_TU
+int trace_set_attntc(void *p, unsigned cap) { return trace_set_tu(p, cap); }
+
 int get_tmap_bf16(const void *ptr, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes, uint32_t box_rows,
                   CUtensorMap *out);
 
@@ -100,6 +103,7 @@ __device__ __forceinline__ void split3_store(unsigned char *buf, int n, int k, f
 
 __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV, AttTcArgs a) {
+  HS_TRACE_BEGIN
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *sK = base;                        // AT_KSTAGES x 32 KB
@@ -384,6 +388,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
   tc::fence_before();
   softmax_sync();
   if (warp == 0) tc::tmem_dealloc<128>(tmem);
+  HS_TRACE_END(4)
 }
 
 }  // namespace

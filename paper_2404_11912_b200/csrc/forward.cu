@@ -119,6 +119,26 @@ static size_t carve(const HsModel *m, int t, int n_view, int split, int world, c
 
 }  // namespace hs
 
+namespace hs {
+int trace_set_gemv(void *p, unsigned cap);
+int trace_set_kv(void *p, unsigned cap);
+int trace_set_attn(void *p, unsigned cap);
+int trace_set_attntc(void *p, unsigned cap);
+}  // namespace hs
+
+/* debugging/profiling aid (not part of hs_abi.h): per-CTA timeline of the
+ * forward's kernels.  buf holds 4 regions of `cap` records of 3 u64 (kernel
+ * id << 32 | SM, globaltimer start, end); NULL turns tracing off.           */
+extern "C" int hs_cta_trace(void *buf, unsigned cap) {
+  unsigned long long *b = reinterpret_cast<unsigned long long *>(buf);
+  const size_t r = (size_t)cap * 3;
+  int (*set[4])(void *, unsigned) = {hs::trace_set_gemv, hs::trace_set_kv, hs::trace_set_attn, hs::trace_set_attntc};
+  for (int i = 0; i < 4; ++i)
+    if (set[i](b ? b + i * r : nullptr, b ? cap : 0) != 0)
+      return hs::set_error(HS_ERR_VALUE, "cta trace unavailable (build with HS_TRACE_BUILD=1)");
+  return HS_OK;
+}
+
 extern "C" const char *hs_last_error(void) { return hs::g_err; }
 extern "C" int hs_abi_version(void) { return HS_ABI_VERSION; }
 extern "C" unsigned long long hs_launch_count(void) { return __atomic_load_n(&hs::g_launches, __ATOMIC_RELAXED); }

@@ -28,6 +28,9 @@
 
 namespace hs {
 
+HS_TRACE_TU
+int trace_set_gemv(void *p, unsigned cap) { return trace_set_tu(p, cap); }
+
 constexpr int TC_BM = 128;        // output rows per tile (MMA M)
 constexpr int TC_BK = 64;         // K per stage (one 128-byte swizzle row)
 constexpr int TC_XN = 24;         // activation columns: 3 splits x 8 rows
@@ -96,6 +99,7 @@ constexpr int SPLIT_COLS = 1024;
 
 __global__ void __launch_bounds__(SPLIT_THREADS) split_rows_kernel(const float *x, int ldx, int t, int K, int ldk,
                                                                    const float *gain, float eps, uint16_t *xs) {
+  HS_TRACE_BEGIN
   tc::grid_dep_launch();
   tc::grid_dep_wait();
   const int r = blockIdx.y;
@@ -138,6 +142,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS) split_rows_kernel(const float *
     xs[(size_t)(TC_T + r) * ldk + k] = b;
     xs[(size_t)(2 * TC_T + r) * ldk + k] = c;
   }
+  HS_TRACE_END(2)
 }
 
 // Folded-RMSNorm operand prep for rows [0, t) of x: split(fp32(x * gain))
@@ -148,6 +153,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS) split_rows_kernel(const float *
 // grid (tiles, t), 128 threads.
 __global__ void __launch_bounds__(128) norm_prep_kernel(const float *x, int ldx, int K, const float *gain,
                                                         uint16_t *xs, int ldk, double *ssq) {
+  HS_TRACE_BEGIN
   const int tile = blockIdx.x, r = blockIdx.y, col = tile * 128 + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   __shared__ double red[4];
@@ -161,6 +167,7 @@ __global__ void __launch_bounds__(128) norm_prep_kernel(const float *x, int ldx,
   if (lane == 0) red[w] = sq;
   __syncthreads();
   if (threadIdx.x == 0) ssq[(size_t)tile * TC_T + r] = (red[0] + red[1]) + (red[2] + red[3]);
+  HS_TRACE_END(3)
 }
 
 int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk, double *ssq,
@@ -248,6 +255,7 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
 
 __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__ CUtensorMap tmW,
                                                          const __grid_constant__ CUtensorMap tmX, GemvTcArgs a) {
+  HS_TRACE_BEGIN
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *sW = base;
@@ -377,6 +385,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<32>(taddr);
+  HS_TRACE_END(1)
 }
 
 // K split: a function of (N, K) only.  Picks the split count that fills

@@ -4,11 +4,16 @@
 
 namespace hs {
 
+HS_TRACE_TU
+int trace_set_kv(void *p, unsigned cap) { return trace_set_tu(p, cap); }
+
 // ---- embedding (model.py:274) ----------------------------------------------
 __global__ void embed_kernel(const uint16_t *emb, int ld, int d, const int32_t *tokens, float *x) {
+  HS_TRACE_BEGIN
   const int r = blockIdx.x;
   const uint16_t *row = emb + (size_t)tokens[r] * ld;
   for (int c = threadIdx.x; c < d; c += blockDim.x) x[(size_t)r * d + c] = bf16_to_f(row[c]);
+  HS_TRACE_END(6)
 }
 
 int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x,
@@ -34,6 +39,7 @@ __device__ __forceinline__ int append_slot(const HsStep &s, int i, int p) {
 // the reference's rounding points plus the bf16 storage.
 __global__ void rope_append_kernel(HsModel m, HsCache c, HsStep s, int layer, const float *qkv,
                                    float *q_out, float *q_stash, int t) {
+  HS_TRACE_BEGIN
   const int i = blockIdx.x, hh = blockIdx.y, pr = threadIdx.x;
   const int H = m.n_heads, KVH = m.n_kv_heads, DH = m.head_dim, half = DH / 2;
   if (pr >= half) return;
@@ -70,6 +76,7 @@ __global__ void rope_append_kernel(HsModel m, HsCache c, HsStep s, int layer, co
     uint16_t *vd = c.v + (((size_t)layer * KVH + kh) * c.cap + slot) * DH + 2 * pr;
     vd[0] = f_to_bf16(row[col]); vd[1] = f_to_bf16(row[col + 1]);
   }
+  HS_TRACE_END(7)
 }
 
 int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv,
