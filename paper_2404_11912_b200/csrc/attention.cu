@@ -48,6 +48,8 @@ __device__ __forceinline__ bool visible(int kp, int qp, const AttnArgs &a) {
 template <int DH>
 __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
   HS_TRACE_BEGIN
+  pdl_trigger();   // the combine kernel is scheduled once every CTA here has started
+  pdl_wait();      // q and the appended K/V rows come from the rope kernel
   if (a.dyn) { a.pos0 += a.dyn[0]; a.win_lo = a.dyn[1]; }
   constexpr int KP = DH + 8;                 // padded K row (bf16) -> conflict-free 16B reads
   constexpr int NDP = DH / 2;                // dim pairs
@@ -221,7 +223,8 @@ __global__ void attn_combine_kernel(const float *pm, const float *pl, const floa
   extern __shared__ float comb_s[];          // [n_splits] weights | [n_splits] l
   float *sw = comb_s, *sl = comb_s + n_splits;
   // the next GEMV (wo, PDL-launched) may start streaming its weights now
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  pdl_trigger();
+  pdl_wait();      // partial states of the attention kernel
   __shared__ float red[32];
   const int row = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   float mx = -INFINITY;
@@ -369,17 +372,20 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   a.part_o = wsf + (size_t)2 * n_splits * t * H;
   dim3 grid(n_splits, KVH, ceil_div(a.g * t, ATT_QROWS));
   if (n_splits == 0) {   // empty shard view: partial state (-inf, 0, 0) for every row
-    attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 16, stream>>>(a.part_m, a.part_l, a.part_o, 0, t * H, DH,
-                                                                     nullptr, packed, nullptr, 0, H);
+    cudaError_t e = launch_pdl(attn_combine_kernel, dim3(t * H), dim3(DH < 128 ? DH : 128), 16, stream,
+                               (const float *)a.part_m, (const float *)a.part_l, (const float *)a.part_o, 0, t * H,
+                               DH, (float *)nullptr, packed, (uint16_t *)nullptr, 0, H);
+    if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "attention(empty) launch: %s", cudaGetErrorString(e));
     return check_launch("attention(empty)");
   }
   // head_dim 128 (the Llama-family targets) runs on the tensor cores; the
   // small-head draft model and the test-size models use the CUDA-core kernel
+  cudaError_t le = cudaSuccess;
   switch (DH) {
-    case 8: attn_partial_kernel<8><<<grid, ATT_THREADS, 0, stream>>>(a); break;
-    case 16: attn_partial_kernel<16><<<grid, ATT_THREADS, 0, stream>>>(a); break;
-    case 32: attn_partial_kernel<32><<<grid, ATT_THREADS, 0, stream>>>(a); break;
-    case 64: attn_partial_kernel<64><<<grid, ATT_THREADS, 0, stream>>>(a); break;
+    case 8: le = launch_pdl(attn_partial_kernel<8>, grid, dim3(ATT_THREADS), 0, stream, a); break;
+    case 16: le = launch_pdl(attn_partial_kernel<16>, grid, dim3(ATT_THREADS), 0, stream, a); break;
+    case 32: le = launch_pdl(attn_partial_kernel<32>, grid, dim3(ATT_THREADS), 0, stream, a); break;
+    case 64: le = launch_pdl(attn_partial_kernel<64>, grid, dim3(ATT_THREADS), 0, stream, a); break;
     case 128: {
       HS_REQUIRE(st->split % 128 == 0, HS_ERR_VALUE, "attention: split must be a multiple of 128 for head_dim 128");
       HS_REQUIRE(st->dyn == nullptr, HS_ERR_VALUE, "attention: run-time positions need head_dim < 128");
@@ -389,8 +395,11 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
     }
     default: return set_error(HS_ERR_SHAPE, "attention: head_dim %d unsupported (8/16/32/64/128)", DH);
   }
-  attn_combine_kernel<<<t * H, DH < 128 ? DH : 128, 2 * n_splits * sizeof(float), stream>>>(a.part_m, a.part_l, a.part_o,
-                                                                   n_splits, t * H, DH, out, packed, xs, ldxs, H);
+  if (le != cudaSuccess) return set_error(HS_ERR_CUDA, "attention launch: %s", cudaGetErrorString(le));
+  le = launch_pdl(attn_combine_kernel, dim3(t * H), dim3(DH < 128 ? DH : 128), 2 * n_splits * sizeof(float), stream,
+                  (const float *)a.part_m, (const float *)a.part_l, (const float *)a.part_o, n_splits, t * H, DH, out,
+                  packed, xs, ldxs, H);
+  if (le != cudaSuccess) return set_error(HS_ERR_CUDA, "attention combine launch: %s", cudaGetErrorString(le));
   return check_launch("attention", 2);
 }
 

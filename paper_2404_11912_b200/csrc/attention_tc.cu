@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
   __shared__ int qp_s[AT_QR];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  tc::grid_dep_launch();             // the combine kernel is scheduled once every CTA here has started
   if (tid == 0) {
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
@@ -420,7 +421,8 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int grid = a.n_items < 2 * sms ? a.n_items : 2 * sms;
-  attn_tc_kernel<<<grid, AT_THREADS, AT_SMEM, stream>>>(mk, mv, a);
+  cudaError_t e = launch_pdl(attn_tc_kernel, dim3(grid), dim3(AT_THREADS), AT_SMEM, stream, mk, mv, a);
+  if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "attention_tc launch: %s", cudaGetErrorString(e));
   return check_launch("attention_tc");
 }
 

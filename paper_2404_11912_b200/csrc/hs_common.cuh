@@ -1,5 +1,6 @@
 // Shared device helpers for the B200 TriForce kernels (sm_100a).
 #pragma once
+#include <utility>
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -122,6 +123,29 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 
 // programmatic dependent launch on/off (HS_NO_PDL=1 disables it: debugging aid)
 int pdl_enabled();
+
+// launch `kern` as a programmatic dependent of the previous kernel on `st`:
+// it may be scheduled once every CTA of that kernel has issued
+// griddepcontrol.launch_dependents (or exited), and must itself execute
+// griddepcontrol.wait before touching anything the predecessor writes
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled();
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 

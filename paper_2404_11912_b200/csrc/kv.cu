@@ -40,6 +40,8 @@ __device__ __forceinline__ int append_slot(const HsStep &s, int i, int p) {
 __global__ void rope_append_kernel(HsModel m, HsCache c, HsStep s, int layer, const float *qkv,
                                    float *q_out, float *q_stash, int t) {
   HS_TRACE_BEGIN
+  pdl_trigger();   // the attention kernel may set up (barriers, TMEM, tensor maps) meanwhile
+  pdl_wait();      // qkv comes from the preceding GEMV
   const int i = blockIdx.x, hh = blockIdx.y, pr = threadIdx.x;
   const int H = m.n_heads, KVH = m.n_kv_heads, DH = m.head_dim, half = DH / 2;
   if (pr >= half) return;
@@ -92,7 +94,9 @@ int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int 
   if (s->append_mode == HS_APPEND_RING)
     HS_REQUIRE(s->ring > 0 && s->n_sink + s->ring <= c->cap, HS_ERR_CAPACITY, "ring exceeds capacity");
   dim3 grid(t, m->n_heads + 2 * m->n_kv_heads);
-  rope_append_kernel<<<grid, m->head_dim / 2, 0, st>>>(*m, *c, *s, layer, qkv, q_out, q_stash, t);
+  cudaError_t e = launch_pdl(rope_append_kernel, grid, dim3(m->head_dim / 2), 0, st, *m, *c, *s, layer, qkv, q_out,
+                             q_stash, t);
+  if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "rope_append launch: %s", cudaGetErrorString(e));
   return check_launch("rope_append");
 }
 
