@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
   HS_TRACE_BEGIN
   pdl_trigger();   // the combine kernel is scheduled once every CTA here has started
   pdl_wait();      // q and the appended K/V rows come from the rope kernel
+  HS_TRACE_RESTART
   if (a.dyn) { a.pos0 += a.dyn[0]; a.win_lo = a.dyn[1]; }
   constexpr int KP = DH + 8;                 // padded K row (bf16) -> conflict-free 16B reads
   constexpr int NDP = DH / 2;                // dim pairs
@@ -214,60 +215,73 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
 // out[i][h*DH + d] = sum_s w_s o_s / sum_s w_s l_s,  w_s = exp(m_s - M), splits in order.
 // packed != nullptr: write the view's partial state (M, l, o unnormalised)
 // as [rows][2 + DH] instead (sequence-shard input, hs_attention_partial).
-// The split weights are computed once into shared memory; the per-dim sums
-// run in split order with the partial-o loads issued 8 at a time (the loop is
-// otherwise one dependent L2 round trip per split).
+// Latency-shaped: every thread loads the (m, l) of a chunk of COMB_CHUNK
+// splits itself (broadcast loads) together with its own o column, all in
+// flight at once, so a view of <= COMB_CHUNK splits costs one L2 round trip;
+// longer views take one max pass and one sum pass per chunk.  The sums run in
+// split order with the same operations as shard_merge_kernel.
+constexpr int COMB_CHUNK = 16;
+
 __global__ void attn_combine_kernel(const float *pm, const float *pl, const float *po, int n_splits,
                                     int rows, int DH, float *out, float *packed, uint16_t *xs, int ldxs, int H) {
   HS_TRACE_BEGIN
-  extern __shared__ float comb_s[];          // [n_splits] weights | [n_splits] l
-  float *sw = comb_s, *sl = comb_s + n_splits;
   // the next GEMV (wo, PDL-launched) may start streaming its weights now
   pdl_trigger();
   pdl_wait();      // partial states of the attention kernel
-  __shared__ float red[32];
-  const int row = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-  float mx = -INFINITY;
-  for (int s = tid; s < n_splits; s += nt) mx = fmaxf(mx, pm[(size_t)s * rows + row]);
-  mx = warp_max(mx);
-  if ((tid & 31) == 0) red[tid >> 5] = mx;
-  __syncthreads();
+  HS_TRACE_RESTART
+  const int row = blockIdx.x, d = threadIdx.x;
+  const size_t ostride = (size_t)rows * DH;
+  const float *pd = po + (size_t)row * DH + d;
+  float mv[COMB_CHUNK], lv[COMB_CHUNK], ov[COMB_CHUNK];
   float M = -INFINITY;
-  for (int w = 0; w < (nt + 31) / 32; ++w) M = fmaxf(M, red[w]);
-  for (int s = tid; s < n_splits; s += nt) {
-    const float m = pm[(size_t)s * rows + row];
-    sw[s] = (m == -INFINITY) ? 0.f : expf(m - M);
-    sl[s] = (m == -INFINITY) ? 0.f : pl[(size_t)s * rows + row];
-  }
-  __syncthreads();
-  float l = 0.f;
-  for (int s = 0; s < n_splits; ++s)
-    if (sw[s] != 0.f) l = fmaf(sw[s], sl[s], l);
-  for (int d = tid; d < DH; d += nt) {
-    float o = 0.f;
-    const float *pd = po + (size_t)row * DH + d;
-    int s = 0;
-    for (; s + 8 <= n_splits; s += 8) {
-      float v[8];
+  const bool one = n_splits <= COMB_CHUNK;
+  if (one) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = pd[(size_t)(s + u) * rows * DH];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (sw[s + u] != 0.f) o = fmaf(sw[s + u], v[u], o);
+    for (int u = 0; u < COMB_CHUNK; ++u) {
+      mv[u] = u < n_splits ? __ldcg(pm + (size_t)u * rows + row) : -INFINITY;
+      lv[u] = u < n_splits ? __ldcg(pl + (size_t)u * rows + row) : 0.f;
+      ov[u] = u < n_splits ? __ldcg(pd + u * ostride) : 0.f;
     }
-    for (; s < n_splits; ++s)
-      if (sw[s] != 0.f) o = fmaf(sw[s], pd[(size_t)s * rows * DH], o);
-    if (packed) {
-      packed[(size_t)row * (DH + 2) + 2 + d] = o;
-    } else {
-      const float v = o / l;
-      if (out) out[(size_t)row * DH + d] = v;
-      if (xs) store_split(xs, ldxs, row / H, (row % H) * DH + d, v);
+#pragma unroll
+    for (int u = 0; u < COMB_CHUNK; ++u) M = fmaxf(M, mv[u]);
+  } else {
+    for (int s0 = 0; s0 < n_splits; s0 += COMB_CHUNK) {
+#pragma unroll
+      for (int u = 0; u < COMB_CHUNK; ++u) mv[u] = s0 + u < n_splits ? __ldcg(pm + (size_t)(s0 + u) * rows + row) : -INFINITY;
+#pragma unroll
+      for (int u = 0; u < COMB_CHUNK; ++u) M = fmaxf(M, mv[u]);
     }
   }
-  if (packed && tid == 0) {
-    packed[(size_t)row * (DH + 2)] = M;
-    packed[(size_t)row * (DH + 2) + 1] = l;
+  float l = 0.f, o = 0.f;
+  for (int s0 = 0; s0 < n_splits; s0 += COMB_CHUNK) {
+    if (!one) {
+#pragma unroll
+      for (int u = 0; u < COMB_CHUNK; ++u) {
+        const int s = s0 + u;
+        mv[u] = s < n_splits ? __ldcg(pm + (size_t)s * rows + row) : -INFINITY;
+        lv[u] = s < n_splits ? __ldcg(pl + (size_t)s * rows + row) : 0.f;
+        ov[u] = s < n_splits ? __ldcg(pd + s * ostride) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < COMB_CHUNK; ++u) {
+      const float w = (mv[u] == -INFINITY) ? 0.f : expf(mv[u] - M);
+      if (w != 0.f) {
+        l = fmaf(w, lv[u], l);
+        o = fmaf(w, ov[u], o);
+      }
+    }
+  }
+  if (packed) {
+    packed[(size_t)row * (DH + 2) + 2 + d] = o;
+    if (d == 0) {
+      packed[(size_t)row * (DH + 2)] = M;
+      packed[(size_t)row * (DH + 2) + 1] = l;
+    }
+  } else {
+    const float v = o / l;
+    if (out) out[(size_t)row * DH + d] = v;
+    if (xs) store_split(xs, ldxs, row / H, (row % H) * DH + d, v);
   }
   HS_TRACE_END(5)
 }
@@ -310,7 +324,7 @@ size_t attention_ws(int t, int H, int DH, int n_view, int split) {
 }
 
 int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *part_m,
-                        float *part_l, float *part_o, int n_splits, cudaStream_t stream);
+                        float *part_l, float *part_o, int n_splits, cudaStream_t stream, int clean_hi);
 
 // ---- live timing of the dominant kernel (bench.py roofline) --------------------
 // When enabled, every attention launch over a view of >= min_view keys is
@@ -332,13 +346,13 @@ static ProfPair *prof_begin(const HsCache *c, const HsStep *st, cudaStream_t str
 
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
                      float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
-                     uint16_t *xs = nullptr, int ldxs = 0);
+                     uint16_t *xs = nullptr, int ldxs = 0, int clean_hi = -1);
 
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
                            float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
-                           uint16_t *xs, int ldxs) {
+                           uint16_t *xs, int ldxs, int clean_hi) {
   ProfPair *p = prof_begin(c, st, stream);
-  const int rc = launch_attention(c, layer, st, H, q, t, out, packed, ws, ws_bytes, stream, xs, ldxs);
+  const int rc = launch_attention(c, layer, st, H, q, t, out, packed, ws, ws_bytes, stream, xs, ldxs, clean_hi);
   if (p) cudaEventRecord(p->b, stream);
   return rc;
 }
@@ -346,9 +360,13 @@ int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H,
 // out: normalised rows [t][H*DH] fp32 (may be null when xs is given);
 // xs: additionally the exact 3-way split operand [24][ldxs] of the next GEMV
 // (t <= 8), so no separate split kernel runs before wo
+// clean_hi: slots below it are not written by any kernel of the current
+// programmatic-dependency chain (>= 0 only from the forward, which knows where
+// its RoPE kernel appends); the tensor-core kernel may load them before its
+// griddepcontrol.wait
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
                      float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
-                     uint16_t *xs, int ldxs) {
+                     uint16_t *xs, int ldxs, int clean_hi) {
   const int DH = c->head_dim, KVH = c->n_kv_heads;
   HS_REQUIRE(H % KVH == 0, HS_ERR_SHAPE, "attention: H %% KVH != 0");
   HS_REQUIRE(st->split > 0 && st->split % ATT_TILE == 0, HS_ERR_VALUE, "attention: split must be a multiple of %d", ATT_TILE);
@@ -372,7 +390,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   a.part_o = wsf + (size_t)2 * n_splits * t * H;
   dim3 grid(n_splits, KVH, ceil_div(a.g * t, ATT_QROWS));
   if (n_splits == 0) {   // empty shard view: partial state (-inf, 0, 0) for every row
-    cudaError_t e = launch_pdl(attn_combine_kernel, dim3(t * H), dim3(DH < 128 ? DH : 128), 16, stream,
+    cudaError_t e = launch_pdl(attn_combine_kernel, dim3(t * H), dim3(DH), 0, stream,
                                (const float *)a.part_m, (const float *)a.part_l, (const float *)a.part_o, 0, t * H,
                                DH, (float *)nullptr, packed, (uint16_t *)nullptr, 0, H);
     if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "attention(empty) launch: %s", cudaGetErrorString(e));
@@ -389,14 +407,15 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
     case 128: {
       HS_REQUIRE(st->split % 128 == 0, HS_ERR_VALUE, "attention: split must be a multiple of 128 for head_dim 128");
       HS_REQUIRE(st->dyn == nullptr, HS_ERR_VALUE, "attention: run-time positions need head_dim < 128");
-      int rc = launch_attention_tc(c, layer, st, H, q, t, a.part_m, a.part_l, a.part_o, n_splits, stream);
+      int rc = launch_attention_tc(c, layer, st, H, q, t, a.part_m, a.part_l, a.part_o, n_splits, stream,
+                                   clean_hi);
       if (rc != HS_OK) return rc;
       break;
     }
     default: return set_error(HS_ERR_SHAPE, "attention: head_dim %d unsupported (8/16/32/64/128)", DH);
   }
   if (le != cudaSuccess) return set_error(HS_ERR_CUDA, "attention launch: %s", cudaGetErrorString(le));
-  le = launch_pdl(attn_combine_kernel, dim3(t * H), dim3(DH < 128 ? DH : 128), 2 * n_splits * sizeof(float), stream,
+  le = launch_pdl(attn_combine_kernel, dim3(t * H), dim3(DH), 0, stream,
                   (const float *)a.part_m, (const float *)a.part_l, (const float *)a.part_o, n_splits, t * H, DH, out,
                   packed, xs, ldxs, H);
   if (le != cudaSuccess) return set_error(HS_ERR_CUDA, "attention combine launch: %s", cudaGetErrorString(le));

@@ -58,6 +58,7 @@ struct AttTcArgs {
   int t, H, KVH, g;
   const int32_t *pos;   // layer [cap] or null
   int cap, layer, n_view, pos0, window, win_lo, n_sink, split, n_splits, n_qb, n_items, pos_base;
+  int clean_hi;         // slots < clean_hi are not written by the preceding kernels (see launch_attention)
   float scale_log2;     // log2(e) / sqrt(dh)
   float *part_m, *part_l, *part_o;
 };
@@ -138,32 +139,48 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  tc::grid_dep_wait();               // K/V rows appended by the previous kernel
 
   // ---------------------------------------------------------------- TMA producer (warp 4)
   if (warp == 4) {
     if (tc::elect_one()) {
+      auto load_kv = [&](uint32_t g, int row) {
+        const int ks = g % AT_KSTAGES, vs = g % AT_VSTAGES;
+        const uint32_t kph = (g / AT_KSTAGES) & 1, vph = (g / AT_VSTAGES) & 1;
+        tc::mbar_wait(&kempty[ks], kph ^ 1);
+        tc::mbar_expect_tx(&kfull[ks], AT_KV);
+        tc::tma_load_2d(sK + ks * AT_KV, &tmK, &kfull[ks], 0, row);
+        tc::tma_load_2d(sK + ks * AT_KV + AT_HALF, &tmK, &kfull[ks], 64, row);
+        tc::mbar_wait(&vempty[vs], vph ^ 1);
+        tc::mbar_expect_tx(&vfull[vs], AT_KV);
+        tc::tma_load_2d(sV + vs * AT_KV, &tmV, &vfull[vs], 0, row);
+        tc::tma_load_2d(sV + vs * AT_KV + AT_HALF, &tmV, &vfull[vs], 64, row);
+      };
+      // Programmatic dependent launch: the first tile of this CTA's first item
+      // streams in while the RoPE kernel (and the GEMV before it) drain, when
+      // none of its slots is one the current step appends
+      bool pre = false;
+      if (blockIdx.x < a.n_items) {
+        const int split = blockIdx.x % a.n_splits, kh = (blockIdx.x / a.n_splits) % a.KVH;
+        const int lo = split * a.split;
+        if (lo + AT_KT <= a.clean_hi) {
+          load_kv(0, (a.layer * a.KVH + kh) * a.cap + lo);
+          pre = true;
+        }
+      }
+      tc::grid_dep_wait();             // K/V rows appended by the previous kernel
       uint32_t g = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
         const int split = item % a.n_splits, kh = (item / a.n_splits) % a.KVH;
         const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
         const int row0 = (a.layer * a.KVH + kh) * a.cap;
-        for (int tile = lo; tile < hi; tile += AT_KT, ++g) {
-          const int ks = g % AT_KSTAGES, vs = g % AT_VSTAGES;
-          const uint32_t kph = (g / AT_KSTAGES) & 1, vph = (g / AT_VSTAGES) & 1;
-          tc::mbar_wait(&kempty[ks], kph ^ 1);
-          tc::mbar_expect_tx(&kfull[ks], AT_KV);
-          tc::tma_load_2d(sK + ks * AT_KV, &tmK, &kfull[ks], 0, row0 + tile);
-          tc::tma_load_2d(sK + ks * AT_KV + AT_HALF, &tmK, &kfull[ks], 64, row0 + tile);
-          tc::mbar_wait(&vempty[vs], vph ^ 1);
-          tc::mbar_expect_tx(&vfull[vs], AT_KV);
-          tc::tma_load_2d(sV + vs * AT_KV, &tmV, &vfull[vs], 0, row0 + tile);
-          tc::tma_load_2d(sV + vs * AT_KV + AT_HALF, &tmV, &vfull[vs], 64, row0 + tile);
-        }
+        for (int tile = lo; tile < hi; tile += AT_KT, ++g)
+          if (g > 0 || !pre) load_kv(g, row0 + tile);
       }
     }
     return;
   }
+  tc::grid_dep_wait();               // q, positions and the appended K/V rows
+  HS_TRACE_RESTART
 
   // ---------------------------------------------------------------- MMA issuer (warp 5)
   if (warp == 5) {
@@ -395,7 +412,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
 }  // namespace
 
 int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *part_m,
-                        float *part_l, float *part_o, int n_splits, cudaStream_t stream) {
+                        float *part_l, float *part_o, int n_splits, cudaStream_t stream, int clean_hi) {
   HS_REQUIRE(c->head_dim == AT_DH, HS_ERR_SHAPE, "attention_tc: head_dim must be 128");
   CUtensorMap mk, mv;
   const uint64_t rows = (uint64_t)c->n_layers * c->n_kv_heads * c->cap;
@@ -413,6 +430,7 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
   a.n_items = n_splits * a.KVH * a.n_qb;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)AT_DH));
   a.part_m = part_m; a.part_l = part_l; a.part_o = part_o;
+  a.clean_hi = clean_hi;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);

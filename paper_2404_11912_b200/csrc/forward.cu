@@ -17,7 +17,8 @@ int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int 
 int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv, int t,
                        float *q_out, float *q_stash, cudaStream_t st);
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
-                           float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs);
+                           float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs,
+                           int clean_hi = -1);
 int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, uint16_t *xs, int ldxs, int H,
                        cudaStream_t st);
 int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
@@ -183,6 +184,12 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim, ff = m->d_ff;
   const int nqkv = (H + 2 * KVH) * dh;
   const float eps = m->norm_eps;
+  // slots below clean_hi are not appended to by this forward's RoPE kernels,
+  // so the attention kernel may stream them before its dependency wait
+  const int clean_hi = st->dyn ? -1
+                       : st->append_mode == HS_APPEND_POS    ? st->pos0 - st->pos_base
+                       : st->append_mode == HS_APPEND_LINEAR ? st->append_base
+                                                             : -1;
   const bool fused_split = t <= 8;   // one row block: folded norms, no split kernels
   const int d_tiles = (d + 127) / 128;
   int rc;
@@ -207,12 +214,12 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
       HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
       if (sharded) {
         const size_t part = (size_t)t * H * (dh + 2) * 4;
-        HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr, 0));
+        HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr, 0, clean_hi));
         HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
         HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, nullptr, w.xa, m->ld_d, H, s));
       } else {
         HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, nullptr, w.att_ws, w.att_bytes, s, w.xa,
-                                      m->ld_d));
+                                      m->ld_d, clean_hi));
       }
       GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq};
       HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo));
@@ -250,11 +257,11 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
     if (sharded) {
       // this rank's partial softmax state -> all ranks -> rank-ordered merge
       const size_t part = (size_t)t * H * (dh + 2) * 4;
-      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr, 0));
+      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr, 0, clean_hi));
       HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
       HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, w.attn, nullptr, m->ld_d, H, s));
     } else {
-      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s, nullptr, 0));
+      HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s, nullptr, 0, clean_hi));
     }
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;

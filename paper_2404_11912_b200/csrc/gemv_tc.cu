@@ -201,8 +201,10 @@ struct GemvTcArgs {
 
 // all 128 threads of the CTA call finalize (uniform control flow: the residual
 // producer reduces its tile's row sums of squares across the CTA)
-__device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float *vin, int lane, int tile,
-                                         const double *inv_rms, double (*red)[TC_T]) {
+// yres: the residual rows y[r][o] (epilogue 1), loaded by the caller ahead of
+// the split-K handshake so they are not one more round trip on the tail
+__device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float *vin, const float *yres, int lane,
+                                         int tile, const double *inv_rms, double (*red)[TC_T]) {
   float v[TC_T];
 #pragma unroll
   for (int r = 0; r < TC_T; ++r) v[r] = a.ssq_in ? (float)((double)vin[r] * inv_rms[r]) : vin[r];
@@ -230,7 +232,7 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
     sq[r] = 0.0;
     if (r < a.t && o < a.N) {
       float *p = a.y + (size_t)r * a.ldy + o;
-      const float nv = (a.epilogue == 1) ? (*p + v[r]) : v[r];
+      const float nv = (a.epilogue == 1) ? (yres[r] + v[r]) : v[r];
       *p = nv;
       if (a.xs_next) {
         sq[r] = (double)nv * (double)nv;
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
         tc::tma_load_2d_hint(sW + i * TC_W_BYTES, &tmW, &full[i], (kb0 + i) * TC_BK, tile * TC_BM, pol);
       }
       tc::grid_dep_wait();
+      HS_TRACE_RESTART
       for (int i = 0; i < npre; ++i) tc::tma_load_2d(sX + i * TC_X_BYTES, &tmX, &full[i], (kb0 + i) * TC_BK, 0);
       for (int i = npre; i < nk; ++i) {
         const int s = i % TC_STAGES;
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
       }
     } else {
       tc::grid_dep_wait();
+      HS_TRACE_RESTART
     }
   } else if (warp == 1) {
     if (tc::elect_one()) {
@@ -353,9 +357,13 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
 #pragma unroll
   for (int r = 0; r < TC_T; ++r) v[r] = nk > 0 ? (h[r] + m[r]) + l[r] : 0.f;
   const int o = tile * TC_BM + row;
+  float yres[TC_T];
+#pragma unroll
+  for (int r = 0; r < TC_T; ++r)
+    yres[r] = (a.epilogue == 1 && r < a.t && o < a.N) ? __ldcg(a.y + (size_t)r * a.ldy + o) : 0.f;
 
   if (a.ks == 1) {
-    finalize(a, o, v, lane, tile, inv_rms, red);
+    finalize(a, o, v, yres, lane, tile, inv_rms, red);
   } else {
     float *pp = a.partial + ((size_t)split * a.n_tiles * TC_BM + o) * TC_T;
     *reinterpret_cast<float4 *>(pp) = make_float4(v[0], v[1], v[2], v[3]);
@@ -371,21 +379,32 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
       __threadfence();
 #pragma unroll
       for (int r = 0; r < TC_T; ++r) v[r] = 0.f;
-      for (int s2 = 0; s2 < a.ks; ++s2) {
-        const float *q = a.partial + ((size_t)s2 * a.n_tiles * TC_BM + o) * TC_T;
-        const float4 x0 = __ldcg(reinterpret_cast<const float4 *>(q));
-        const float4 x1 = __ldcg(reinterpret_cast<const float4 *>(q + 4));
-        v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
-        v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
+      // all split partials in flight at once, then summed in split order
+      constexpr int KS_MAX = 16;
+      float4 x0[KS_MAX], x1[KS_MAX];
+#pragma unroll
+      for (int s2 = 0; s2 < KS_MAX; ++s2) {
+        if (s2 < a.ks) {
+          const float *q = a.partial + ((size_t)s2 * a.n_tiles * TC_BM + o) * TC_T;
+          x0[s2] = __ldcg(reinterpret_cast<const float4 *>(q));
+          x1[s2] = __ldcg(reinterpret_cast<const float4 *>(q + 4));
+        }
       }
-      finalize(a, o, v, lane, tile, inv_rms, red);
+#pragma unroll
+      for (int s2 = 0; s2 < KS_MAX; ++s2) {
+        if (s2 < a.ks) {
+          v[0] += x0[s2].x; v[1] += x0[s2].y; v[2] += x0[s2].z; v[3] += x0[s2].w;
+          v[4] += x1[s2].x; v[5] += x1[s2].y; v[6] += x1[s2].z; v[7] += x1[s2].w;
+        }
+      }
+      finalize(a, o, v, yres, lane, tile, inv_rms, red);
       if (threadIdx.x == 0) a.counters[tile] = 0;   // self-cleaning for the next launch
     }
   }
   tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<32>(taddr);
-  HS_TRACE_END(1)
+  HS_TRACE_END(1 | (a.n_tiles << 8))
 }
 
 // K split: a function of (N, K) only.  Picks the split count that fills

@@ -43,7 +43,9 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define HS_TRACE_BEGIN const unsigned long long hs_t0_ = g_ctrace ? gtime() : 0ull;
+#define HS_TRACE_BEGIN unsigned long long hs_t0_ = g_ctrace ? gtime() : 0ull;
+// restart the CTA's clock (e.g. after griddepcontrol.wait: time from the dependency release)
+#define HS_TRACE_RESTART if (g_ctrace != nullptr) hs_t0_ = gtime();
 #define HS_TRACE_END(kid)                                                                     \
   if (g_ctrace != nullptr && threadIdx.x == 0) {                                              \
     const unsigned i_ = atomicAdd(&g_ctrace_n, 1u);                                           \
@@ -59,6 +61,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define HS_TRACE_TU \
   static int trace_set_tu(void *, unsigned) { return -1; }
 #define HS_TRACE_BEGIN
+#define HS_TRACE_RESTART
 #define HS_TRACE_END(kid)
 #endif
 

@@ -42,6 +42,7 @@ __global__ void rope_append_kernel(HsModel m, HsCache c, HsStep s, int layer, co
   HS_TRACE_BEGIN
   pdl_trigger();   // the attention kernel may set up (barriers, TMEM, tensor maps) meanwhile
   pdl_wait();      // qkv comes from the preceding GEMV
+  HS_TRACE_RESTART
   const int i = blockIdx.x, hh = blockIdx.y, pr = threadIdx.x;
   const int H = m.n_heads, KVH = m.n_kv_heads, DH = m.head_dim, half = DH / 2;
   if (pr >= half) return;

@@ -21,7 +21,8 @@ int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int 
 int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv, int t,
                        float *q_out, float *q_stash, cudaStream_t st);
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
-                           float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs);
+                           float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs,
+                           int clean_hi = -1);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
 
 namespace {

@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--t", type=int, default=3)
     ap.add_argument("--ctx", type=int, default=16384)
     ap.add_argument("--layers", type=int, default=8, help="layers shown in detail")
+    ap.add_argument("--gemv", action="store_true",
+                    help="per-GEMV CTA distributions (start = dependency release, griddepcontrol.wait)")
     a = ap.parse_args()
     import bench
     import paper_2404_11912_b200 as P
@@ -64,7 +66,8 @@ def main():
     lane.rollback_to(f0)
     rec = buf.view(-1, 3).cpu().numpy().astype(np.uint64)
     rec = rec[rec[:, 1] > 0]
-    kid = (rec[:, 0] >> np.uint64(32)).astype(int)
+    kid_full = (rec[:, 0] >> np.uint64(32)).astype(int)
+    kid = kid_full & 0xff
     t0 = rec[:, 1].astype(np.int64)
     t1 = rec[:, 2].astype(np.int64)
     base = t0.min()
@@ -85,6 +88,8 @@ def main():
         else:
             launches.append({"kid": k, "start": t0[i], "end": t1[i], "ctas": 1, "busy": t1[i] - t0[i]})
     span = max(l["end"] for l in launches)
+    if a.gemv:
+        gemv_tails(kid_full, t0, t1, a.layers)
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     prev_end = 0
     gaps = 0.0
@@ -103,6 +108,30 @@ def main():
     for l in launches[:12 * a.layers // 8 + 12]:
         print(f"  {NAMES[l['kid']]:14s} {l['start'] / 1e3:9.2f} {(l['end'] - l['start']) / 1e3:8.2f} {l['ctas']:5d} "
               f"{l['busy'] / l['ctas'] / 1e3:7.2f}")
+
+
+def gemv_tails(kid_full, t0, t1, layers):
+    """Launches (GEMVs carry their tile count in bits 8+ of the id): per launch the CTA
+    release times (after griddepcontrol.wait) and end times, relative to the
+    first release, and the idle time until the next GEMV's first release."""
+    sel = np.arange(len(kid_full))
+    order = sel[np.argsort(t0[sel], kind="stable")]
+    groups, cur = [], None
+    for i in order:
+        if cur is None or kid_full[i] != cur[0]:
+            cur = (kid_full[i], [])
+            groups.append(cur)
+        cur[1].append(i)
+    print("launches: kernel [gemv tiles] ctas | release spread | end p10 p50 p90 max (us from first release) | "
+          "next release")
+    for j, (k, idx) in enumerate(groups[:8 * layers + 4]):
+        idx = np.array(idx)
+        r0 = t0[idx].min()
+        rel = (t0[idx] - r0) / 1e3
+        end = (t1[idx] - r0) / 1e3
+        nxt = (t0[np.array(groups[j + 1][1])].min() - r0) / 1e3 if j + 1 < len(groups) else float("nan")
+        print(f"  {NAMES[k & 0xff]:12s} {k >> 8:4d} {len(idx):5d} | {rel.max():6.2f} | {np.percentile(end, 10):6.2f} {np.median(end):6.2f} "
+              f"{np.percentile(end, 90):6.2f} {end.max():6.2f} | {nxt:7.2f}")
 
 
 if __name__ == "__main__":
