@@ -664,9 +664,87 @@ def _ar_loop(lane: Lane, out: list, target_len: int, temperature: float, rng) ->
 
 
 class SingleLevelSession:
-    """Standard one-level speculative decoding harness (speculation.py:401-477);
-    an acceptance-measurement pairing, outside Algorithm 1's hot path."""
+    """One draft lane speculated against one full-cache verify lane --
+    standard speculative decoding, the acceptance-measurement pairing of
+    speculation.py:401-477.  The draft cache is a StreamingCache (own draft
+    model or self-speculation), a FullCache, or a RetrievalCache, which is
+    built from (and rebuilt against) the verify lane's full cache and so
+    requires the verify weights (self-speculation).  Runs on the same device
+    round machinery as HierarchicalSession: tokens, distributions and
+    uniforms stay resident, one host read-back per round.  H2O / TopK draft
+    caches need per-query attention probabilities and stay out of scope
+    (SURVEY.md §2.1)."""
 
-    def __init__(self, *a, **k):
-        raise NotImplementedError("SingleLevelSession is an analytics pairing outside the decode hot path "
-                                  "(SURVEY.md §2.1, OUT OF SCOPE)")
+    def __init__(self, draft_weights: ModelWeights, draft_cache: KVCache, verify_weights: ModelWeights,
+                 prefix: Sequence[int], gamma: int, temperature: float,
+                 retrieval_config: Optional[RetrievalConfig] = None):
+        if draft_weights.config.vocab_size != verify_weights.config.vocab_size:
+            raise ContractError("draft and verify models must share a vocabulary")
+        if gamma < 1:
+            raise ValueError("gamma must be >= 1")
+        if not isinstance(draft_cache, (FullCache, StreamingCache, RetrievalCache)):
+            raise ContractError(f"draft cache {type(draft_cache).__name__} is not supported on the device path "
+                                "(H2O / TopK pairings are out of scope, SURVEY.md §2.1)")
+        self.gamma = gamma
+        self.temperature = temperature
+        self.committed = list(prefix)
+        self.verify_lane = Lane(verify_weights, FullCache.from_config(verify_weights.config))
+        self.draft_lane = Lane(draft_weights, draft_cache)
+        self.verify_lane.prefill(prefix)
+        self._retrieval = isinstance(draft_cache, RetrievalCache)
+        self._buf = _RoundBuffers(verify_weights.config.vocab_size, gamma, 1)
+        if self._retrieval:
+            if draft_weights is not verify_weights:
+                raise ContractError("retrieval drafting requires shared weights (self-speculation)")
+            n = len(prefix)
+            draft_cache.build(self.verify_lane.cache, self.verify_lane.recorder.stash, upto=max(n - 1, 1))
+            if n < 2:
+                self.draft_lane.frontier_logits = self.verify_lane.frontier_logits
+            self.rolling = RollingAcceptance(draft_cache.config.rolling_window)
+            self.tokens_since_build = 0
+        else:
+            self.draft_lane.prefill(prefix)
+
+    def _maybe_rebuild(self) -> None:
+        cache: RetrievalCache = self.draft_lane.cache
+        if not should_rebuild(cache.config, self.tokens_since_build, self.rolling):
+            return
+        self.draft_lane.catch_up(self.committed)
+        cache.build(self.verify_lane.cache, self.draft_lane.recorder.stash, upto=self.verify_lane.frontier)
+        self.draft_lane.frontier_logits = None
+        self.tokens_since_build = 0
+        self.rolling.rates.clear()
+        COUNTERS["rebuilds"] += 1
+
+    def generate(self, target_len: int, seed: int = 0):
+        """Speculate until target_len tokens are committed; returns
+        (tokens, LevelStats)."""
+        if target_len <= len(self.committed):
+            raise ValueError("target_len must exceed the prefix length")
+        rng = np.random.default_rng(seed)
+        us = UniformStream(rng)
+        buf, g, T = self._buf, self.gamma, self.temperature
+        stats = LevelStats()
+        cursor = 0
+        while len(self.committed) < target_len:
+            if self._retrieval:
+                self._maybe_rebuild()
+            us.ensure(2 * g + 2, cursor)
+            _draft_round_dev(self.draft_lane, self.committed, g, T, us, buf)
+            _score_rows_dev(self.verify_lane, self.committed, buf.dtok, T, buf.p)
+            _chain_dev(buf.dtok, g, buf.q, buf.p, buf.V, us, buf)
+            emitted, accepted, cursor = _readback(buf, g, us)
+            stats.rounds += 1
+            stats.proposed += g
+            stats.accepted += accepted
+            base = len(self.committed)
+            self.committed.extend(emitted)
+            valid = base + len(emitted) - 1
+            for lane in (self.verify_lane, self.draft_lane):
+                lane.rollback_to(min(lane.frontier, valid))
+                lane.commit()
+            if self._retrieval:
+                self.rolling.push(accepted / g)
+                self.tokens_since_build += len(emitted)
+        del self.committed[target_len:]
+        return list(self.committed), stats

@@ -34,6 +34,15 @@ def golden():
     return data, meta
 
 
+@pytest.fixture(scope="session")
+def golden_single():
+    """One-level speculation fixtures (tests/golden/make_golden_single.py)."""
+    data = np.load(os.path.join(GOLDEN_DIR, "ref_single.npz"))
+    with open(os.path.join(GOLDEN_DIR, "ref_single.json")) as f:
+        meta = json.load(f)
+    return data, meta
+
+
 def small_cfg(**kw):
     from oracle.hs_oracle import OConfig
     base = dict(n_layers=2, n_heads=4, n_kv_heads=4, head_dim=8, d_ff=32,

@@ -8,6 +8,7 @@ import os
 import re
 
 import numpy as np
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -71,3 +72,20 @@ def test_streaming_watermark_matches_oracle_eviction():
                 lo = max(lo, committed - W)
             store = np.concatenate([np.arange(min(ns, frontier)), np.arange(max(lo, ns), frontier)])
             assert store.tolist() == oc.rows[0].pos.tolist(), trial
+
+
+def test_measure_acceptance_pairing_errors():
+    """Pairing validation happens before any device work
+    (analytics.py:296-300): unknown names raise ValueError, the
+    attention-feedback pairings are out of scope on the device path."""
+    import paper_2404_11912_b200 as P
+    cfg = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=8, d_ff=16, vocab_size=16, max_seq=32)
+    w = P.generate_weights(cfg, 1)
+    with pytest.raises(ValueError):
+        P.measure_acceptance("self:nope", w, [[1, 2, 3]])
+    with pytest.raises(ValueError):
+        P.measure_acceptance("hierarchical", w, [[1, 2, 3]])
+    for p in ("self:h2o", "self:topk"):
+        with pytest.raises(P.ContractError):
+            P.measure_acceptance(p, w, [[1, 2, 3]])
+    assert P.AcceptanceStats("x").rate == 0.0

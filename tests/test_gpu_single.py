@@ -1,0 +1,132 @@
+"""One-level speculation on the B200 (`-m gpu`): `SingleLevelSession`
+(speculation.py:401-477) and `measure_acceptance` (analytics.py:265-309)
+against fixtures produced by the reference itself
+(tests/golden/make_golden_single.py, bf16 storage model), plus the
+reference's own properties (tests/test_speculation.py:336-362,
+tests/test_acceptance.py:144-162)."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2404_11912_b200 as pkg
+    return pkg
+
+
+def bf16_weights(P, w):
+    from oracle.hs_oracle import bf16_round
+    t = {n: (x.copy() if "norm" in n else bf16_round(x)) for n, x in w.tensors.items()}
+    return P.ModelWeights(w.config, t, w.tied_head).validate()
+
+
+@pytest.fixture(scope="module")
+def needle(P, golden_single):
+    data, meta = golden_single
+    target = bf16_weights(P, P.load_weights(os.path.join(HERE, "golden", "needle.tfwt")))
+    cfg = dict(target.config.__dict__)
+    cfg["n_layers"] = 1
+    draft = bf16_weights(P, P.generate_weights(P.ModelConfig(**cfg), meta["single_sessions"]["draft_seed"]))
+    prompts = [list(map(int, p)) for p in data["needle/prompts"]]
+    return target, draft, prompts
+
+
+def _draft_cache(P, kind, cfg, kw):
+    if kind == "full":
+        return P.FullCache.from_config(cfg)
+    if kind == "stream":
+        return P.StreamingCache.from_config(cfg, P.StreamingConfig(**kw))
+    return P.RetrievalCache.from_config(cfg, P.RetrievalConfig(**kw))
+
+
+def test_single_level_sessions_match_reference(P, golden_single, needle):
+    data, meta = golden_single
+    target, draft, prompts = needle
+    for c in meta["single_sessions"]["cases"]:
+        dw = target if c["self_spec"] else draft
+        cache = _draft_cache(P, c["kind"], dw.config, c["cache"])
+        prefix = prompts[c["prompt_case"]]
+        s = P.SingleLevelSession(dw, cache, target, prefix, c["gamma"], c["temperature"])
+        out, st = s.generate(len(prefix) + c["gen"], seed=c["seed"])
+        tag = f"single/{c['name']}/bf16"
+        assert out == data[tag + "/tokens"].tolist(), c["name"]
+        assert [st.rounds, st.proposed, st.accepted] == data[tag + "/stats"].tolist(), c["name"]
+
+
+def test_needle_acceptance_matches_reference_and_orders_pairings(P, golden_single, needle):
+    """Acceptance criterion 3 on the device path: retrieval drafting recovers
+    the needle, streaming does not (alpha gap >= 0.3), and every case's
+    counts equal the reference's."""
+    data, meta = golden_single
+    target, _, prompts = needle
+    m = meta["needle"]
+    kw = dict(gamma=m["gamma"], temperature=m["temperature"], gen_tokens=m["gen_tokens"], seed=m["seed"],
+              streaming=P.StreamingConfig(n_sink=m["n_sink"], budget=m["budget"]),
+              retrieval=P.RetrievalConfig(chunk_size=m["chunk_size"], budget=m["budget"]), topk_budget=m["budget"])
+    rates = {}
+    for kind in ("retrieval", "streaming"):
+        st = P.measure_acceptance("self:" + kind, target, prompts, **kw)["self"]
+        tag = f"needle/bf16/{kind}"
+        assert [st.rounds, st.proposed, st.accepted] == data[tag + "/stats"].tolist(), kind
+        assert np.array_equal(np.array(st.per_case), data[tag + "/per_case"]), kind
+        rates[kind] = st.rate
+    assert rates["retrieval"] > rates["streaming"]
+    assert rates["retrieval"] - rates["streaming"] >= 0.3
+
+
+def test_full_budget_self_draft_accepts_everything(P):
+    cfg = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=4, head_dim=8, d_ff=32, vocab_size=40, max_seq=128)
+    w = P.generate_weights(cfg, 5)
+    prefix = [1, 2, 3, 4, 5, 6, 7, 8]
+    s = P.SingleLevelSession(w, P.FullCache.from_config(cfg), w, prefix, gamma=3, temperature=0.0)
+    out, stats = s.generate(len(prefix) + 9, seed=0)
+    assert stats.rate == 1.0
+    assert out == P.autoregressive_generate(w, prefix, len(prefix) + 9, 0.0, 0)
+
+
+def test_rerun_same_seed_same_stats(P, needle):
+    target, draft, prompts = needle
+
+    def run():
+        cache = P.StreamingCache.from_config(draft.config, P.StreamingConfig(n_sink=2, budget=6))
+        s = P.SingleLevelSession(draft, cache, target, prompts[9][:40], gamma=3, temperature=0.6)
+        return s.generate(48, seed=3)
+
+    (o1, s1), (o2, s2) = run(), run()
+    assert o1 == o2 and (s1.proposed, s1.accepted, s1.rounds) == (s2.proposed, s2.accepted, s2.rounds)
+
+
+def test_hierarchical_pairing_reports_both_levels(P, needle):
+    target, draft, prompts = needle
+    kw = dict(draft=draft, gamma=2, gamma2=3, gen_tokens=6, temperature=0.7, seed=2,
+              streaming=P.StreamingConfig(n_sink=2, budget=10), retrieval=P.RetrievalConfig(chunk_size=4, budget=8))
+    r1 = P.measure_acceptance("hierarchical", target, prompts[:2], **kw)
+    r2 = P.measure_acceptance("hierarchical", target, prompts[:2], **kw)
+    assert r1["inner"].rate == r2["inner"].rate and r1["outer"].rate == r2["outer"].rate
+    assert r1["outer"].proposed > 0 and len(r1["inner"].per_case) == 2
+
+
+def test_single_level_contract_errors(P, needle):
+    target, draft, prompts = needle
+    with pytest.raises(ValueError):
+        P.SingleLevelSession(target, P.FullCache.from_config(target.config), target, prompts[0], 0, 0.0)
+    with pytest.raises(P.ContractError):   # retrieval drafting needs the verify weights
+        P.SingleLevelSession(draft, P.RetrievalCache.from_config(draft.config, P.RetrievalConfig(chunk_size=8,
+                                                                                                budget=16)),
+                             target, prompts[0], 2, 0.0)
+    s = P.SingleLevelSession(target, P.FullCache.from_config(target.config), target, prompts[0][:10], 2, 0.0)
+    with pytest.raises(ValueError):
+        s.generate(10)
