@@ -292,7 +292,9 @@ def test_gemv_tc_matches_fp64(P, t, K, N):
     y, _ = _gemv_tc(x, W)
     ref = x.astype(np.float64) @ W.astype(np.float64).T
     err = np.abs(y - ref).max() / np.abs(ref).max()
-    assert err < 2e-6, err
+    # exact bf16 products, fp32 accumulation over up to K / ks terms per
+    # accumulator (TMEM): a few 2^-24 relative; a bf16-rounded operand would be ~1e-3
+    assert err < 1e-5, err
 
 
 def test_gemv_tc_epilogues_and_batch_invariance(P):
