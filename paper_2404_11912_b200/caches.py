@@ -24,6 +24,8 @@ reads the caches directly and never materialises `expose()`.
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 from dataclasses import dataclass
 from typing import Optional
@@ -36,8 +38,10 @@ from ._abi import (HS_APPEND_LINEAR, HS_APPEND_POS, HS_APPEND_RING, HS_KV_LINEAR
 from .errors import CapacityError, ContractError, ShapeError
 from .runtime import STATS, as_device_f32, device, ptr, stream_ptr
 
-FULL_SPLIT = 2048     # keys per attention split over the full cache (fixed: t-invariant rows)
-SMALL_SPLIT = 512     # keys per split over the retrieval view
+FULL_SPLIT = int(os.environ.get("HS_FULL_SPLIT", 2048))    # keys per attention split over the full cache
+SMALL_SPLIT = int(os.environ.get("HS_SMALL_SPLIT", 512))   # keys per split over the retrieval view
+# (fixed per cache kind, never a function of t: a row's result is t-invariant;
+# the environment overrides are experiment hooks for tools/fwdbench.py)
 STREAM_SPLIT = 64     # keys per split over the (small) streaming window: one CTA per 64 keys
 
 

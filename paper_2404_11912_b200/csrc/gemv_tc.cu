@@ -179,6 +179,7 @@ int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, u
 
 struct GemvTcArgs {
   int N, nkb, ks, t, epilogue, n_tiles;
+  int cluster;        // 1: the ks split CTAs of a tile are one cluster, partials reduced through DSMEM
   // folded RMSNorm (model.py:282-284) of this GEMV's input rows: the operand
   // is split(x * gain) and the result is scaled by 1 / rms(x) here, with the
   // row sums of squares given as ssq_parts per-tile partials [parts][8]
@@ -364,6 +365,36 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
 
   if (a.ks == 1) {
     finalize(a, o, v, yres, lane, tile, inv_rms, red);
+  } else if (a.cluster) {
+    // split-K through distributed shared memory: every CTA parks its partial
+    // in its (now idle) stage buffers, the split-0 CTA sums them in split
+    // order -- the same additions as the global-memory path below, without
+    // its fence / atomic / L2 round trips
+    float *ps = reinterpret_cast<float *>(sW) + row * TC_T;
+    *reinterpret_cast<float4 *>(ps) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4 *>(ps + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    tc::cluster_sync();
+    if (split == 0) {
+#pragma unroll
+      for (int r = 0; r < TC_T; ++r) v[r] = 0.f;
+      float4 x0[8], x1[8];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        if (s2 < a.ks) {
+          x0[s2] = tc::ld_dsmem_f4(ps, s2);
+          x1[s2] = tc::ld_dsmem_f4(ps + 4, s2);
+        }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        if (s2 < a.ks) {
+          v[0] += x0[s2].x; v[1] += x0[s2].y; v[2] += x0[s2].z; v[3] += x0[s2].w;
+          v[4] += x1[s2].x; v[5] += x1[s2].y; v[6] += x1[s2].z; v[7] += x1[s2].w;
+        }
+      }
+      finalize(a, o, v, yres, lane, tile, inv_rms, red);
+    }
+    tc::cluster_sync();   // partials stay readable until the leader is done
   } else {
     float *pp = a.partial + ((size_t)split * a.n_tiles * TC_BM + o) * TC_T;
     *reinterpret_cast<float4 *>(pp) = make_float4(v[0], v[1], v[2], v[3]);
@@ -413,6 +444,16 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
 // weight streams per CTA beat wave-filling splits -- gate|up as 172 whole-K
 // CTAs runs the retrieval forward 8% faster than as 860 CTAs in 2.9 waves,
 // and more, shorter CTAs lose monotonically.
+// split-K reduction through a thread-block cluster (default; HS_GEMV_NO_CLUSTER=1
+// uses the global-memory partials + arrival counter path for every split)
+static int gemv_use_cluster() {
+  static const int on = [] {
+    const char *e = getenv("HS_GEMV_NO_CLUSTER");
+    return !(e != nullptr && e[0] == '1');
+  }();
+  return on;
+}
+
 int gemv_tc_ksplit(int N, int nkb) {
   const int tiles = (N + TC_BM - 1) / TC_BM;
   if (const char *e = getenv("HS_GEMV_KS")) {   // experiment hook: "N/nkb:ks,..."
@@ -476,6 +517,7 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   if (rc != HS_OK) return rc;
   GemvTcArgs a;
   a.N = N; a.nkb = nkb; a.ks = gemv_tc_ksplit(N, nkb); a.t = t; a.epilogue = epilogue; a.n_tiles = tiles;
+  a.cluster = (a.ks > 1 && a.ks <= 8 && gemv_use_cluster()) ? 1 : 0;
   a.y = y; a.ldy = ldy; a.xs_out = xs_out; a.ld_xs_out = ld_xs_out;
   a.ssq_in = nullptr; a.ssq_parts = 0; a.norm_K = 1; a.eps = 0.f;
   a.gnext = nullptr; a.xs_next = nullptr; a.ld_next = 0; a.ssq_out = nullptr;
@@ -497,11 +539,22 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   cfg.blockDim = dim3(128, 1, 1);
   cfg.dynamicSmemBytes = TC_SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (a.cluster) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = a.ks;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled();
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_tc_kernel, mw, mx, a);
   if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "gemv_tc launch: %s", cudaGetErrorString(e));
   return check_launch("gemv_tc");

@@ -134,6 +134,20 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float *v) {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // programmatic dependent launch: wait until the preceding grid's writes are visible
+// ---- thread-block clusters: barrier + distributed shared memory ----------------
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 16 bytes at the same shared-memory offset in CTA `rank` of this cluster
+__device__ __forceinline__ float4 ld_dsmem_f4(const void *local, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // allow the next (PDL-launched) grid to start its prologue now; it still
 // waits in grid_dep_wait() for this grid's completion before reading results
