@@ -215,14 +215,15 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
 // out[i][h*DH + d] = sum_s w_s o_s / sum_s w_s l_s,  w_s = exp(m_s - M), splits in order.
 // packed != nullptr: write the view's partial state (M, l, o unnormalised)
 // as [rows][2 + DH] instead (sequence-shard input, hs_attention_partial).
-// Latency-shaped: every thread loads the (m, l) of a chunk of COMB_CHUNK
+// Latency-shaped: every thread loads the (m, l) of a chunk of CHUNK
 // splits itself (broadcast loads) together with its own o column, all in
-// flight at once, so a view of <= COMB_CHUNK splits costs one L2 round trip;
+// flight at once, so a view of <= CHUNK splits costs one L2 round trip
+// (CHUNK 16 for the retrieval / streaming views, 64 for the full cache up to
+// 131,072 keys);
 // longer views take one max pass and one sum pass per chunk.  The sums run in
 // split order with the same operations as shard_merge_kernel.
-constexpr int COMB_CHUNK = 16;
-
-__global__ void attn_combine_kernel(const float *pm, const float *pl, const float *po, int n_splits,
+template <int COMB_CHUNK>
+__global__ void __launch_bounds__(128) attn_combine_kernel(const float *pm, const float *pl, const float *po, int n_splits,
                                     int rows, int DH, float *out, float *packed, uint16_t *xs, int ldxs, int H) {
   HS_TRACE_BEGIN
   // the next GEMV (wo, PDL-launched) may start streaming its weights now
@@ -390,7 +391,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   a.part_o = wsf + (size_t)2 * n_splits * t * H;
   dim3 grid(n_splits, KVH, ceil_div(a.g * t, ATT_QROWS));
   if (n_splits == 0) {   // empty shard view: partial state (-inf, 0, 0) for every row
-    cudaError_t e = launch_pdl(attn_combine_kernel, dim3(t * H), dim3(DH), 0, stream,
+    cudaError_t e = launch_pdl(attn_combine_kernel<16>, dim3(t * H), dim3(DH), 0, stream,
                                (const float *)a.part_m, (const float *)a.part_l, (const float *)a.part_o, 0, t * H,
                                DH, (float *)nullptr, packed, (uint16_t *)nullptr, 0, H);
     if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "attention(empty) launch: %s", cudaGetErrorString(e));
@@ -415,7 +416,8 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
     default: return set_error(HS_ERR_SHAPE, "attention: head_dim %d unsupported (8/16/32/64/128)", DH);
   }
   if (le != cudaSuccess) return set_error(HS_ERR_CUDA, "attention launch: %s", cudaGetErrorString(le));
-  le = launch_pdl(attn_combine_kernel, dim3(t * H), dim3(DH), 0, stream,
+  auto comb = (n_splits > 16 && n_splits <= 64) ? attn_combine_kernel<64> : attn_combine_kernel<16>;
+  le = launch_pdl(comb, dim3(t * H), dim3(DH), 0, stream,
                   (const float *)a.part_m, (const float *)a.part_l, (const float *)a.part_o, n_splits, t * H, DH, out,
                   packed, xs, ldxs, H);
   if (le != cudaSuccess) return set_error(HS_ERR_CUDA, "attention combine launch: %s", cudaGetErrorString(le));
