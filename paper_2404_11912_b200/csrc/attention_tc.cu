@@ -236,14 +236,13 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
     return;
   }
 
-  // ------------------------------------------------ softmax warps 0-3 (rows 0-3), 6-9 (rows 4-7)
+  // ------------------------------------------------ softmax warps 0-3 and 6-9 (two row groups)
   // Two groups of four warps split the (up to) 8 query rows of a work item,
   // halving each thread's per-tile softmax work; warp w reads TMEM lane
   // quarter w % 4, so thread ltid = key (S) / head dim (O) index.
   const int grp = warp < 4 ? 0 : 1;
   const int ltid = (warp & 3) * 32 + lane;
   const int stid = grp * 128 + ltid;                 // 0..255 over both groups
-  const int rb = grp * AT_GR;                        // first row of this group
   const uint32_t tl = (uint32_t)((warp & 3) * 32) << 16;   // this warp's TMEM lane quarter
   uint32_t g = 0;
   for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
@@ -251,7 +250,11 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
     const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
     const int r0 = qb * AT_QR;
     const int nrows = min(AT_QR, a.g * a.t - r0);
-    const bool active = rb < nrows;                  // uniform per group
+    // the item's rows split as evenly as possible between the two groups
+    // (t = 5: 3 + 2, not 4 + 1): the softmax of the busier group paces the tile
+    const int half = (nrows + 1) >> 1;
+    const int rb = grp ? half : 0, re = grp ? nrows : half;   // this group's rows [rb, re)
+    const bool active = rb < re;                     // uniform per group
     const int ntiles = (hi - lo + AT_KT - 1) / AT_KT;
     // ---- stage the query split; zero both P buffers (rows >= nrows stay 0) ----------
     // (all S/P.V MMAs of the previous item completed: its tiles were all consumed)
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
           float x[AT_GR];
 #pragma unroll
           for (int r = 0; r < AT_GR; ++r) {
-            if (rb + r < nrows) {
+            if (rb + r < re) {
               const float sc = ((sv[r] + sv[AT_GR + r]) + sv[2 * AT_GR + r]) * a.scale_log2;
               x[r] = (allvis || visible_tc(kp, qp_s[rb + r], a)) ? sc : -INFINITY;
               const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
 #pragma unroll
           for (int r = 0; r < AT_GR; ++r) {
             const int rr = rb + r;
-            if (rr < nrows) {
+            if (rr < re) {
               const int mi = max(max(red[s][0][rr], red[s][1][rr]), max(red[s][2][rr], red[s][3][rr]));
               const float m_new = fmaxf(m_run[r], o2f(mi));
               float p = 0.f;
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
           if (lane == 0) tc::mbar_arrive(&ofree[sp]);
 #pragma unroll
           for (int r = 0; r < AT_GR; ++r)
-            if (rb + r < nrows)
+            if (rb + r < re)
               o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_GR + r]) + ov[2 * AT_GR + r]);
         }
 #pragma unroll
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         if (lane == 0) tc::mbar_arrive(&ofree[sp]);
 #pragma unroll
         for (int r = 0; r < AT_GR; ++r)
-          if (rb + r < nrows)
+          if (rb + r < re)
             o_acc[r] = o_acc[r] * fac_prev[r] + ((ov[r] + ov[AT_GR + r]) + ov[2 * AT_GR + r]);
       }
     }
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
     // ---- l: sum of the per-thread partials (fixed order), then write partial state ----
 #pragma unroll
     for (int r = 0; r < AT_GR; ++r) {
-      if (rb + r < nrows) {
+      if (rb + r < re) {
         float v = l_run[r];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
 #pragma unroll
     for (int r = 0; r < AT_GR; ++r) {
       const int rr = rb + r;
-      if (rr < nrows) {
+      if (rr < re) {
         const int i = (r0 + rr) / a.g, head = kh * a.g + (r0 + rr) % a.g;
         const size_t row = (size_t)i * a.H + head;
         a.part_o[(pbase + row) * AT_DH + ltid] = o_acc[r];
