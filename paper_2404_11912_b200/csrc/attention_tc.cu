@@ -63,6 +63,16 @@ struct AttTcArgs {
   float *part_m, *part_l, *part_o;
 };
 
+// work item -> (split, kv head, query block).  Query blocks vary fastest, so
+// the items sharing one K/V split run side by side and read it through L2
+// (a long prefill block has up to 128 query blocks per split; decode and
+// verify have one).
+__device__ __forceinline__ void item_coords(int item, const AttTcArgs &a, int &split, int &kh, int &qb) {
+  qb = item % a.n_qb;
+  split = (item / a.n_qb) % a.n_splits;
+  kh = item / (a.n_qb * a.n_splits);
+}
+
 __device__ __forceinline__ bool visible_tc(int kp, int qp, const AttTcArgs &a) {
   if (kp < 0 || kp > qp) return false;
   if (a.window == 0 || kp < a.n_sink) return true;
@@ -160,7 +170,8 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
       // none of its slots is one the current step appends
       bool pre = false;
       if (blockIdx.x < a.n_items) {
-        const int split = blockIdx.x % a.n_splits, kh = (blockIdx.x / a.n_splits) % a.KVH;
+        int split, kh, qb;
+        item_coords(blockIdx.x, a, split, kh, qb);
         const int lo = split * a.split;
         if (lo + AT_KT <= a.clean_hi) {
           load_kv(0, (a.layer * a.KVH + kh) * a.cap + lo);
@@ -170,7 +181,8 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
       tc::grid_dep_wait();             // K/V rows appended by the previous kernel
       uint32_t g = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-        const int split = item % a.n_splits, kh = (item / a.n_splits) % a.KVH;
+        int split, kh, qb;
+        item_coords(item, a, split, kh, qb);
         const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
         const int row0 = (a.layer * a.KVH + kh) * a.cap;
         for (int tile = lo; tile < hi; tile += AT_KT, ++g)
@@ -221,7 +233,8 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
       };
       uint32_t g = 0, nitem = 0;
       for (int item = blockIdx.x; item < a.n_items; item += gridDim.x, ++nitem) {
-        const int split = item % a.n_splits;
+        int split, kh, qb;
+        item_coords(item, a, split, kh, qb);
         const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
         const int ntiles = (hi - lo + AT_KT - 1) / AT_KT;
         tc::mbar_wait(&qfull, nitem & 1);          // this item's query split is staged
@@ -246,7 +259,8 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
   const uint32_t tl = (uint32_t)((warp & 3) * 32) << 16;   // this warp's TMEM lane quarter
   uint32_t g = 0;
   for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-    const int split = item % a.n_splits, kh = (item / a.n_splits) % a.KVH, qb = item / (a.n_splits * a.KVH);
+    int split, kh, qb;
+    item_coords(item, a, split, kh, qb);
     const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
     const int r0 = qb * AT_QR;
     const int nrows = min(AT_QR, a.g * a.t - r0);
