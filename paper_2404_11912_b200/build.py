@@ -75,6 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     extra = ["-Xptxas", "-v"] if verbose else []
     if os.environ.get("HS_TRACE_BUILD") == "1":   # per-CTA timeline (tools/cta_timeline.py); slower
         extra.append("-DHS_CTA_TRACE")
+    extra += os.environ.get("HS_NVCC_DEFINES", "").split()   # experiment builds, e.g. "-DHS_TC_STAGES=4"
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(NCCL, "include"),

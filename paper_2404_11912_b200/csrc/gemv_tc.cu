@@ -35,7 +35,10 @@ constexpr int TC_BM = 128;        // output rows per tile (MMA M)
 constexpr int TC_BK = 64;         // K per stage (one 128-byte swizzle row)
 constexpr int TC_XN = 24;         // activation columns: 3 splits x 8 rows
 constexpr int TC_T = 8;           // activation rows per pass
-constexpr int TC_STAGES = 5;
+#ifndef HS_TC_STAGES
+#define HS_TC_STAGES 5
+#endif
+constexpr int TC_STAGES = HS_TC_STAGES;   // 5 x 19 KB: two CTAs per SM (a GEMV + the next one's prefetch)
 constexpr int TC_W_BYTES = TC_BM * TC_BK * 2;    // 16 KB
 constexpr int TC_X_BYTES = TC_XN * TC_BK * 2;    // 3 KB
 constexpr int TC_SMEM = TC_STAGES * (TC_W_BYTES + TC_X_BYTES) + 1024 + 256;
