@@ -24,6 +24,8 @@ int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H,
                            float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs,
                            int clean_hi = -1);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
+int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int n_keys,
+                             float *out, cudaStream_t stream);
 
 namespace {
 
@@ -170,7 +172,14 @@ extern "C" int hs_prefill(const HsModel *m, const HsCache *c, const HsStep *st, 
       HS_TRY(gemm3(h, wqkv, m->ld_d, nqkv, w, R, 0.f, w.qkv + (size_t)r0 * nqkv, nqkv));
     }
     HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
-    // causal attention in blocks of query rows; a block sees keys up to its last row
+    // causal attention: head_dim 128 on the 128-row tensor-core prefill kernel
+    // (prefill_attn.cu); other head sizes in blocks of query rows on the
+    // decode kernels, a block seeing keys up to its last row
+    static const bool tc_prefill = getenv("HS_PREFILL_DECODE_ATTN") == nullptr;   // A/B hook
+    if (tc_prefill && dh == 128 && st->pos_base == 0 && st->window == 0 && c->kind == HS_KV_LINEAR) {
+      HS_TRY(launch_prefill_attention(c, l, H, w.q, t, st->pos0, st->n_view < st->pos0 + t ? st->n_view : st->pos0 + t,
+                                      w.attn, s));
+    } else
     for (int a0 = 0; a0 < t; a0 += PF_QROWS) {
       const int tq = t - a0 < PF_QROWS ? t - a0 : PF_QROWS;
       HsStep sa = *st;

@@ -1,0 +1,360 @@
+// Causal prefill attention for head_dim 128 on the tensor cores (tcgen05 + TMA),
+// 128 query rows per CTA -- the attention core of the batched prefill
+// `_forward` (model.py:290-315 over model.py:348-349) for long prompts.
+//
+// The decode kernel (attention_tc.cu) is built for <= 8 query rows: keys on
+// the MMA's M side, one thread per key, so every query row costs cross-warp
+// reductions per tile.  Here the orientation is flipped:
+//   S[128 q x 128 keys]  = sum_i Q_i . K^T       (Q split exactly into 3 bf16 terms)
+//   softmax per row in registers: thread = query row = TMEM lane
+//   O_tile[128 q x 128 dh] = sum_i P_i . V       (P split into 2 bf16 terms)
+//   o += o * fac + O_tile in registers (online softmax, fp32)
+// Products of the Q splits with the bf16 keys are exact, so the scores are
+// fp32-accurate; P in probability units is carried to 16 significand bits
+// (relative 2^-17), below the fp32 accumulation noise of a long row.
+//
+// Warp roles (192 threads): warps 0-3 softmax (row = 32 w + lane), warp 4 TMA
+// producer (one K and one V stage), warp 5 MMA issuer.  S and O are double
+// buffered in TMEM (4 x 128 columns), so S(j+1) runs on the tensor core while
+// the softmax of tile j and the fold of O(j-1) run in registers.  One CTA
+// per SM (224 KB shared memory); heavy (late) query tiles are scheduled first.
+#include "hs_common.cuh"
+#include "tc_util.cuh"
+
+namespace hs {
+
+int get_tmap_bf16(const void *ptr, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes, uint32_t box_rows,
+                  CUtensorMap *out);
+
+namespace {
+
+constexpr int PA_DH = 128;
+constexpr int PA_QT = 128;                     // query rows per CTA (MMA M)
+constexpr int PA_KT = 128;                     // keys per tile (MMA N of S, K of P.V)
+constexpr int PA_ATOM = 128 * 64 * 2;          // one [128 rows x 64] bf16 SW128 atom = 16 KB
+constexpr int PA_OP = 2 * PA_ATOM;             // one [128 x 128] bf16 operand = 32 KB
+constexpr int PA_THREADS = 192;
+constexpr int PA_SMEM = 3 * PA_OP /*Q*/ + PA_OP /*K*/ + PA_OP /*V*/ + 2 * PA_OP /*P*/ + 1024;
+
+struct PrefillArgs {
+  const float *q;       // [t][H][128] roped queries
+  float *out;           // [t][H*128]
+  int t, H, KVH, g, layer, cap, pos0, n_keys;
+  float scale_log2;
+};
+
+// byte offset of element (row, col) in a K-major SW128 [128 x 128] operand
+__device__ __forceinline__ uint32_t chunk_off(int row, int chunk16) {   // chunk16 = col / 8
+  return (uint32_t)((chunk16 >> 3) * PA_ATOM + row * 128 + ((((chunk16 & 7) ^ (row & 7)) & 7) << 4));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  const uint32_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(a));
+  const uint32_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(b));
+  return lo | (hi << 16);
+}
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 32 lanes x 32 consecutive 32-bit columns
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __grid_constant__ CUtensorMap tmK,
+                                                                    const __grid_constant__ CUtensorMap tmV,
+                                                                    PrefillArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char *sQ = base;                  // 3 splits x 32 KB
+  unsigned char *sK = sQ + 3 * PA_OP;
+  unsigned char *sV = sK + PA_OP;
+  unsigned char *sP = sV + PA_OP;            // 2 splits x 32 KB
+  __shared__ uint64_t kfull, kempty, vfull, vempty, sfull[2], sfree[2], pfull, pfree, ofull[2], ofree[2], qfull;
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = (a.t + PA_QT - 1) / PA_QT;
+  const int qt = n_qt - 1 - (int)blockIdx.x;           // heavy (late) tiles first
+  const int h = blockIdx.y, kh = h / a.g;
+  const int r0 = qt * PA_QT;
+  const int rows = min(PA_QT, a.t - r0);
+  const int kend = min(a.n_keys, a.pos0 + r0 + rows);  // keys [0, kend) are visible to some row
+  const int ntiles = (kend + PA_KT - 1) / PA_KT;
+  const int qmin = a.pos0 + r0;                        // first query position of the tile
+
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch(&tmK);
+    tc::tma_prefetch(&tmV);
+    tc::mbar_init(&kfull, 1); tc::mbar_init(&kempty, 1); tc::mbar_init(&vfull, 1); tc::mbar_init(&vempty, 1);
+    tc::mbar_init(&pfull, 4); tc::mbar_init(&pfree, 1); tc::mbar_init(&qfull, 4);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&sfull[b], 1); tc::mbar_init(&sfree[b], 4); tc::mbar_init(&ofull[b], 1); tc::mbar_init(&ofree[b], 4);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);     // S[b] at 128 b, O[b] at 256 + 128 b
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+
+  // ------------------------------------------------------------------ TMA producer
+  if (warp == 4) {
+    if (tc::elect_one()) {
+      const int row0 = (a.layer * a.KVH + kh) * a.cap;
+      for (int j = 0; j < ntiles; ++j) {
+        const uint32_t ph = j & 1;
+        tc::mbar_wait(&kempty, ph ^ 1);
+        tc::mbar_expect_tx(&kfull, PA_OP);
+        tc::tma_load_2d(sK, &tmK, &kfull, 0, row0 + j * PA_KT);
+        tc::tma_load_2d(sK + PA_ATOM, &tmK, &kfull, 64, row0 + j * PA_KT);
+        tc::mbar_wait(&vempty, ph ^ 1);
+        tc::mbar_expect_tx(&vfull, PA_OP);
+        tc::tma_load_2d(sV, &tmV, &vfull, 0, row0 + j * PA_KT);
+        tc::tma_load_2d(sV + PA_ATOM, &tmV, &vfull, 64, row0 + j * PA_KT);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ MMA issuer
+  if (warp == 5) {
+    if (tc::elect_one()) {
+      constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idO = tc::idesc_bf16(128, 128, 0, 1);
+      auto issue_S = [&](int j) {
+        const int b = j & 1;
+        tc::mbar_wait(&kfull, j & 1);
+        tc::mbar_wait(&sfree[b], ((j >> 1) & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int kk = 0; kk < PA_DH / 16; ++kk) {
+            const uint64_t da = tc::desc_k_sw128(sQ + i * PA_OP + (kk >> 2) * PA_ATOM) + 2 * (kk & 3);
+            const uint64_t db = tc::desc_k_sw128(sK + (kk >> 2) * PA_ATOM) + 2 * (kk & 3);
+            tc::mma_bf16(tmem + b * 128, da, db, idS, (i | kk) != 0);
+          }
+        tc::mma_commit(&kempty);
+        tc::mma_commit(&sfull[b]);
+      };
+      auto issue_PV = [&](int j) {
+        const int b = j & 1;
+        tc::mbar_wait(&pfull, j & 1);
+        tc::mbar_wait(&vfull, j & 1);
+        tc::mbar_wait(&ofree[b], ((j >> 1) & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int kk = 0; kk < PA_KT / 16; ++kk) {
+            const uint64_t da = tc::desc_k_sw128(sP + i * PA_OP + (kk >> 2) * PA_ATOM) + 2 * (kk & 3);
+            // B = V [keys x dh], dh contiguous (MN-major): 64-dh blocks 16 KB apart, 8-key groups 1 KB apart
+            const uint64_t db = tc::desc_mn_sw128(sV + kk * 2048, PA_ATOM, 1024);
+            tc::mma_bf16(tmem + 256 + b * 128, da, db, idO, (i | kk) != 0);
+          }
+        tc::mma_commit(&vempty);
+        tc::mma_commit(&pfree);
+        tc::mma_commit(&ofull[b]);
+      };
+      tc::mbar_wait(&qfull, 0);
+      issue_S(0);
+      for (int j = 0; j < ntiles; ++j) {
+        if (j + 1 < ntiles) issue_S(j + 1);
+        issue_PV(j);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ softmax warps 0-3
+  const int r = warp * 32 + lane;                      // query row of this thread = TMEM lane
+  const uint32_t tl = (uint32_t)(warp * 32) << 16;
+  const int qp = a.pos0 + r0 + r;                      // its position
+  {  // stage Q (3-way exact split), zero rows past t
+    const float *qrow = a.q + ((size_t)(r0 + r) * a.H + h) * PA_DH;
+#pragma unroll 2
+    for (int c = 0; c < PA_DH / 8; ++c) {
+      float v[8];
+      if (r < rows) {
+        const float4 x0 = *reinterpret_cast<const float4 *>(qrow + 8 * c);
+        const float4 x1 = *reinterpret_cast<const float4 *>(qrow + 8 * c + 4);
+        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w; v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = 0.f;
+      }
+      uint32_t p0[4], p1[4], p2[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float h0[2], m0[2], l0[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const float x = v[2 * e + u];
+          h0[u] = __bfloat162float(__float2bfloat16_rn(x));
+          const float rr = x - h0[u];
+          m0[u] = __bfloat162float(__float2bfloat16_rn(rr));
+          l0[u] = rr - m0[u];
+        }
+        p0[e] = pack_bf16(h0[0], h0[1]);
+        p1[e] = pack_bf16(m0[0], m0[1]);
+        p2[e] = pack_bf16(l0[0], l0[1]);
+      }
+      const uint32_t off = chunk_off(r, c);
+      *reinterpret_cast<uint4 *>(sQ + off) = make_uint4(p0[0], p0[1], p0[2], p0[3]);
+      *reinterpret_cast<uint4 *>(sQ + PA_OP + off) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+      *reinterpret_cast<uint4 *>(sQ + 2 * PA_OP + off) = make_uint4(p2[0], p2[1], p2[2], p2[3]);
+    }
+    tc::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&qfull);
+  }
+
+  float o_acc[PA_DH];
+#pragma unroll
+  for (int d = 0; d < PA_DH; ++d) o_acc[d] = 0.f;
+  float m_run = -INFINITY, l_run = 0.f, fac_prev = 1.f;
+
+  auto fold = [&](int j, float fac) {   // o = o * fac + O_tile(j)
+    const int b = j & 1;
+    tc::mbar_wait(&ofull[b], (j >> 1) & 1);
+    tc::fence_after();
+#pragma unroll
+    for (int c = 0; c < PA_DH / 32; ++c) {
+      float ov[32];
+      tmem_ld32(tmem + 256 + b * 128 + c * 32 + tl, ov);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o_acc[32 * c + e] = fmaf(o_acc[32 * c + e], fac, ov[e]);
+    }
+    tc::fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&ofree[b]);
+  };
+
+  for (int j = 0; j < ntiles; ++j) {
+    const int b = j & 1;
+    const int k0 = j * PA_KT;
+    const bool masked = k0 + PA_KT - 1 > qmin || k0 + PA_KT > kend;   // some key of the tile invisible to some row
+    tc::mbar_wait(&sfull[b], (j >> 1) & 1);
+    tc::fence_after();
+    // pass 1: row max
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < PA_KT / 32; ++c) {
+      float sv[32];
+      tmem_ld32(tmem + b * 128 + c * 32 + tl, sv);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int kp = k0 + 32 * c + e;
+        const float s = (!masked || (kp <= qp && kp < a.n_keys)) ? sv[e] * a.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s);
+      }
+    }
+    const float m_new = fmaxf(m_run, mx);
+    const float fac = ex2f(m_run - m_new);              // ex2(-inf) = 0 on the first tile
+    // pass 2: P = exp2(s - m), split into 2 bf16 terms -> smem (the previous P.V must be done with it)
+    tc::mbar_wait(&pfree, (j & 1) ^ 1);
+    float sum = 0.f;
+#pragma unroll
+    for (int c = 0; c < PA_KT / 32; ++c) {
+      float sv[32];
+      tmem_ld32(tmem + b * 128 + c * 32 + tl, sv);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int kp = k0 + 32 * c + e;
+        const bool vis = !masked || (kp <= qp && kp < a.n_keys);
+        sv[e] = vis ? ex2f(sv[e] * a.scale_log2 - m_new) : 0.f;
+      }
+#pragma unroll
+      for (int q8 = 0; q8 < 4; ++q8) {                 // 4 chunks of 8 keys
+        uint32_t h4[4], m4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float x0 = sv[8 * q8 + 2 * e], x1 = sv[8 * q8 + 2 * e + 1];
+          const float h0 = __bfloat162float(__float2bfloat16_rn(x0));
+          const float h1 = __bfloat162float(__float2bfloat16_rn(x1));
+          const float m0 = __bfloat162float(__float2bfloat16_rn(x0 - h0));
+          const float m1 = __bfloat162float(__float2bfloat16_rn(x1 - h1));
+          h4[e] = pack_bf16(h0, h1);
+          m4[e] = pack_bf16(m0, m1);
+          sum += (h0 + m0) + (h1 + m1);   // l from the same (16-bit) weights the tensor core sees
+        }
+        const uint32_t off = chunk_off(r, c * 4 + q8);
+        *reinterpret_cast<uint4 *>(sP + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+        *reinterpret_cast<uint4 *>(sP + PA_OP + off) = make_uint4(m4[0], m4[1], m4[2], m4[3]);
+      }
+    }
+    tc::fence_before();
+    tc::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tc::mbar_arrive(&sfree[b]);
+      tc::mbar_arrive(&pfull);
+    }
+    l_run = l_run * fac + sum;
+    if (j > 0) fold(j - 1, fac_prev);
+    fac_prev = fac;
+    m_run = m_new;
+  }
+  fold(ntiles - 1, fac_prev);
+  if (r < rows) {
+    const float inv = 1.f / l_run;
+    float *orow = a.out + (size_t)(r0 + r) * a.H * PA_DH + (size_t)h * PA_DH;
+#pragma unroll
+    for (int d = 0; d < PA_DH; d += 4)
+      *reinterpret_cast<float4 *>(orow + d) =
+          make_float4(o_acc[d] * inv, o_acc[d + 1] * inv, o_acc[d + 2] * inv, o_acc[d + 3] * inv);
+  }
+  tc::fence_before();
+  asm volatile("bar.sync 1, 128;" ::: "memory");       // the 4 softmax warps: all TMEM reads done
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+// causal attention of t query rows at positions [pos0, pos0 + t) over keys
+// [0, n_keys) of a linear, unsharded, unwindowed cache (slot == position)
+int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int n_keys,
+                             float *out, cudaStream_t stream) {
+  HS_REQUIRE(c->head_dim == PA_DH, HS_ERR_SHAPE, "prefill attention: head_dim must be 128");
+  HS_REQUIRE(H % c->n_kv_heads == 0, HS_ERR_SHAPE, "prefill attention: H %% KVH != 0");
+  HS_REQUIRE(n_keys <= c->cap && n_keys >= pos0 + 1, HS_ERR_CAPACITY, "prefill attention: bad key range");
+  CUtensorMap mk, mv;
+  const uint64_t rows = (uint64_t)c->n_layers * c->n_kv_heads * c->cap;
+  int rc = get_tmap_bf16(c->k, PA_DH, rows, PA_DH * 2, PA_KT, &mk);
+  if (rc != HS_OK) return rc;
+  rc = get_tmap_bf16(c->v, PA_DH, rows, PA_DH * 2, PA_KT, &mv);
+  if (rc != HS_OK) return rc;
+  PrefillArgs a;
+  a.q = q; a.out = out; a.t = t; a.H = H; a.KVH = c->n_kv_heads; a.g = H / c->n_kv_heads; a.layer = layer;
+  a.cap = c->cap; a.pos0 = pos0; a.n_keys = n_keys;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)PA_DH));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PA_SMEM);
+    attr = true;
+  }
+  dim3 grid((t + PA_QT - 1) / PA_QT, H);
+  prefill_attn_kernel<<<grid, PA_THREADS, PA_SMEM, stream>>>(mk, mv, a);
+  return check_launch("prefill_attention");
+}
+
+}  // namespace hs

@@ -461,18 +461,28 @@ def test_draft_step_graphs_match_direct_forwards(P):
     assert torch.equal(res[0][2], res[1][2]) and torch.equal(res[0][3], res[1][3])
 
 
-def test_gemm_prefill_matches_decode_path(P):
+@pytest.mark.parametrize("head_dim,split_at", [(64, 0), (128, 0), (128, 700)])
+def test_gemm_prefill_matches_decode_path(P, head_dim, split_at):
     """Batched GEMM prefill (hs_prefill, >= 64 rows) against the row-exact
     decode path on the same prompt: logits within fp32 accumulation noise,
-    same argmaxes, same cached K/V to bf16 rounding."""
+    same argmaxes, same cached K/V to bf16 rounding.  head_dim 128 runs the
+    128-row tensor-core prefill attention (prefill_attn.cu), also as a second
+    prefill appended to a non-empty cache (queries at positions >= 700)."""
     from paper_2404_11912_b200 import model as M
-    cfg = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=64, d_ff=344, vocab_size=512, max_seq=4096)
+    cfg = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=head_dim, d_ff=344, vocab_size=512,
+                        max_seq=4096)
     w = P.generate_weights(cfg, 21, tied_head=False)
     prompt = np.random.default_rng(2).integers(1, 512, 1500).tolist()
     a, b = P.FullCache.from_config(cfg), P.FullCache.from_config(cfg)
-    la = P.prefill(w, prompt, a)                                              # GEMM prefill
+    if split_at:
+        la = np.concatenate([P.prefill(w, prompt[:split_at], a), P.prefill(w, prompt[split_at:], a)])
+    else:
+        la = P.prefill(w, prompt, a)                                          # GEMM prefill
     lb = M._host_rows(M.forward_device(w, prompt, b, None, prefill=False))    # decode-path rows
-    assert np.allclose(la, lb, rtol=1e-4, atol=1e-4 * np.abs(lb).max())
+    # both paths are fp32-accurate, but K/V are stored in bf16: where the two
+    # fp32 results straddle a rounding boundary the cached element differs by
+    # one bf16 ulp (2^-8), which moves later logits by ~1e-4 relative
+    assert np.allclose(la, lb, rtol=1e-4, atol=3e-4 * np.abs(lb).max())
     assert (np.argmax(la, -1) == np.argmax(lb, -1)).mean() > 0.999
     dk = (a.k[:, :, :1500].float() - b.k[:, :, :1500].float()).abs().max().item()
     assert dk <= 0.02 * b.k[:, :, :1500].float().abs().max().item()
