@@ -5,7 +5,7 @@
 // The decode kernel (attention_tc.cu) is built for <= 8 query rows: keys on
 // the MMA's M side, one thread per key, so every query row costs cross-warp
 // reductions per tile.  Here the orientation is flipped:
-//   S[128 q x 128 keys]  = sum_i Q_i . K^T       (Q split exactly into 3 bf16 terms)
+//   S[128 q x 64 keys]   = sum_i Q_i . K^T       (Q split exactly into 3 bf16 terms)
 //   softmax per row in registers: thread = query row = TMEM lane
 //   O_tile[128 q x 128 dh] = sum_i P_i . V       (P split into 2 bf16 terms)
 //   o += o * fac + O_tile in registers (online softmax, fp32)
@@ -14,10 +14,10 @@
 // (relative 2^-17), below the fp32 accumulation noise of a long row.
 //
 // Warp roles (192 threads): warps 0-3 softmax (row = 32 w + lane), warp 4 TMA
-// producer (one K and one V stage), warp 5 MMA issuer.  S and O are double
-// buffered in TMEM (4 x 128 columns), so S(j+1) runs on the tensor core while
-// the softmax of tile j and the fold of O(j-1) run in registers.  One CTA
-// per SM (224 KB shared memory); heavy (late) query tiles are scheduled first.
+// producer (3-stage K and V rings of 64-key tiles), warp 5 MMA issuer.  S and
+// O are double buffered in TMEM, so S(j+1) runs on the tensor core while the
+// softmax of tile j and the fold of O(j-1) run in registers.  One CTA per SM
+// (225 KB shared memory); heavy (late) query tiles are scheduled first.
 #include "hs_common.cuh"
 #include "tc_util.cuh"
 
@@ -30,11 +30,14 @@ namespace {
 
 constexpr int PA_DH = 128;
 constexpr int PA_QT = 128;                     // query rows per CTA (MMA M)
-constexpr int PA_KT = 128;                     // keys per tile (MMA N of S, K of P.V)
+constexpr int PA_KT = 64;                      // keys per tile (MMA N of S, K of P.V)
+constexpr int PA_NS = 3;                       // K and V ring stages
 constexpr int PA_ATOM = 128 * 64 * 2;          // one [128 rows x 64] bf16 SW128 atom = 16 KB
-constexpr int PA_OP = 2 * PA_ATOM;             // one [128 x 128] bf16 operand = 32 KB
+constexpr int PA_OP = 2 * PA_ATOM;             // one [128 x 128] bf16 operand (a Q split) = 32 KB
+constexpr int PA_KATOM = PA_KT * 64 * 2;       // [64 keys x 64 dh] half of a K or V tile = 8 KB
+constexpr int PA_KV = 2 * PA_KATOM;            // one K or V stage = 16 KB
 constexpr int PA_THREADS = 192;
-constexpr int PA_SMEM = 3 * PA_OP /*Q*/ + PA_OP /*K*/ + PA_OP /*V*/ + 2 * PA_OP /*P*/ + 1024;
+constexpr int PA_SMEM = 3 * PA_OP /*Q*/ + 2 * PA_NS * PA_KV /*K, V*/ + 2 * PA_ATOM /*P*/ + 1024;
 
 struct PrefillArgs {
   const float *q;       // [t][H][128] roped queries
@@ -52,6 +55,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const uint32_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(a));
   const uint32_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(b));
   return lo | (hi << 16);
+}
+
+// {lo, hi} -> packed bf16x2 (round to nearest), one instruction
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
 }
 
 __device__ __forceinline__ float ex2f(float x) {
@@ -81,10 +91,11 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *sQ = base;                  // 3 splits x 32 KB
-  unsigned char *sK = sQ + 3 * PA_OP;
-  unsigned char *sV = sK + PA_OP;
-  unsigned char *sP = sV + PA_OP;            // 2 splits x 32 KB
-  __shared__ uint64_t kfull, kempty, vfull, vempty, sfull[2], sfree[2], pfull, pfree, ofull[2], ofree[2], qfull;
+  unsigned char *sK = sQ + 3 * PA_OP;        // PA_NS x 16 KB
+  unsigned char *sV = sK + PA_NS * PA_KV;    // PA_NS x 16 KB
+  unsigned char *sP = sV + PA_NS * PA_KV;    // 2 splits x [128 rows x 64 keys] = 2 x 16 KB
+  __shared__ uint64_t kfull[PA_NS], kempty[PA_NS], vfull[PA_NS], vempty[PA_NS];
+  __shared__ uint64_t sfull[2], sfree[2], pfull, pfree, ofull[2], ofree[2], qfull;
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -100,14 +111,17 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
-    tc::mbar_init(&kfull, 1); tc::mbar_init(&kempty, 1); tc::mbar_init(&vfull, 1); tc::mbar_init(&vempty, 1);
+    for (int st = 0; st < PA_NS; ++st) {
+      tc::mbar_init(&kfull[st], 1); tc::mbar_init(&kempty[st], 1); tc::mbar_init(&vfull[st], 1);
+      tc::mbar_init(&vempty[st], 1);
+    }
     tc::mbar_init(&pfull, 4); tc::mbar_init(&pfree, 1); tc::mbar_init(&qfull, 4);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&sfull[b], 1); tc::mbar_init(&sfree[b], 4); tc::mbar_init(&ofull[b], 1); tc::mbar_init(&ofree[b], 4);
     }
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);     // S[b] at 128 b, O[b] at 256 + 128 b
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);     // S[b] at 64 b, O[b] at 128 + 128 b
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -118,15 +132,16 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
     if (tc::elect_one()) {
       const int row0 = (a.layer * a.KVH + kh) * a.cap;
       for (int j = 0; j < ntiles; ++j) {
-        const uint32_t ph = j & 1;
-        tc::mbar_wait(&kempty, ph ^ 1);
-        tc::mbar_expect_tx(&kfull, PA_OP);
-        tc::tma_load_2d(sK, &tmK, &kfull, 0, row0 + j * PA_KT);
-        tc::tma_load_2d(sK + PA_ATOM, &tmK, &kfull, 64, row0 + j * PA_KT);
-        tc::mbar_wait(&vempty, ph ^ 1);
-        tc::mbar_expect_tx(&vfull, PA_OP);
-        tc::tma_load_2d(sV, &tmV, &vfull, 0, row0 + j * PA_KT);
-        tc::tma_load_2d(sV + PA_ATOM, &tmV, &vfull, 64, row0 + j * PA_KT);
+        const int st = j % PA_NS;
+        const uint32_t ph = (j / PA_NS) & 1;
+        tc::mbar_wait_sleep(&kempty[st], ph ^ 1);
+        tc::mbar_expect_tx(&kfull[st], PA_KV);
+        tc::tma_load_2d(sK + st * PA_KV, &tmK, &kfull[st], 0, row0 + j * PA_KT);
+        tc::tma_load_2d(sK + st * PA_KV + PA_KATOM, &tmK, &kfull[st], 64, row0 + j * PA_KT);
+        tc::mbar_wait_sleep(&vempty[st], ph ^ 1);
+        tc::mbar_expect_tx(&vfull[st], PA_KV);
+        tc::tma_load_2d(sV + st * PA_KV, &tmV, &vfull[st], 0, row0 + j * PA_KT);
+        tc::tma_load_2d(sV + st * PA_KV + PA_KATOM, &tmV, &vfull[st], 64, row0 + j * PA_KT);
       }
     }
     return;
@@ -135,44 +150,44 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
   // ------------------------------------------------------------------ MMA issuer
   if (warp == 5) {
     if (tc::elect_one()) {
-      constexpr uint32_t idS = tc::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idS = tc::idesc_bf16(128, PA_KT, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16(128, 128, 0, 1);
       auto issue_S = [&](int j) {
-        const int b = j & 1;
-        tc::mbar_wait(&kfull, j & 1);
-        tc::mbar_wait(&sfree[b], ((j >> 1) & 1) ^ 1);
+        const int b = j & 1, st = j % PA_NS;
+        tc::mbar_wait_sleep(&kfull[st], (j / PA_NS) & 1);
+        tc::mbar_wait_sleep(&sfree[b], ((j >> 1) & 1) ^ 1);
         tc::fence_after();
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
           for (int kk = 0; kk < PA_DH / 16; ++kk) {
             const uint64_t da = tc::desc_k_sw128(sQ + i * PA_OP + (kk >> 2) * PA_ATOM) + 2 * (kk & 3);
-            const uint64_t db = tc::desc_k_sw128(sK + (kk >> 2) * PA_ATOM) + 2 * (kk & 3);
-            tc::mma_bf16(tmem + b * 128, da, db, idS, (i | kk) != 0);
+            const uint64_t db = tc::desc_k_sw128(sK + st * PA_KV + (kk >> 2) * PA_KATOM) + 2 * (kk & 3);
+            tc::mma_bf16(tmem + b * PA_KT, da, db, idS, (i | kk) != 0);
           }
-        tc::mma_commit(&kempty);
+        tc::mma_commit(&kempty[st]);
         tc::mma_commit(&sfull[b]);
       };
       auto issue_PV = [&](int j) {
-        const int b = j & 1;
-        tc::mbar_wait(&pfull, j & 1);
-        tc::mbar_wait(&vfull, j & 1);
-        tc::mbar_wait(&ofree[b], ((j >> 1) & 1) ^ 1);
+        const int b = j & 1, st = j % PA_NS;
+        tc::mbar_wait_sleep(&pfull, j & 1);
+        tc::mbar_wait_sleep(&vfull[st], (j / PA_NS) & 1);
+        tc::mbar_wait_sleep(&ofree[b], ((j >> 1) & 1) ^ 1);
         tc::fence_after();
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
           for (int kk = 0; kk < PA_KT / 16; ++kk) {
-            const uint64_t da = tc::desc_k_sw128(sP + i * PA_OP + (kk >> 2) * PA_ATOM) + 2 * (kk & 3);
-            // B = V [keys x dh], dh contiguous (MN-major): 64-dh blocks 16 KB apart, 8-key groups 1 KB apart
-            const uint64_t db = tc::desc_mn_sw128(sV + kk * 2048, PA_ATOM, 1024);
-            tc::mma_bf16(tmem + 256 + b * 128, da, db, idO, (i | kk) != 0);
+            const uint64_t da = tc::desc_k_sw128(sP + i * PA_ATOM) + 2 * kk;
+            // B = V [keys x dh], dh contiguous (MN-major): 64-dh blocks 8 KB apart, 8-key groups 1 KB apart
+            const uint64_t db = tc::desc_mn_sw128(sV + st * PA_KV + kk * 2048, PA_KATOM, 1024);
+            tc::mma_bf16(tmem + 128 + b * 128, da, db, idO, (i | kk) != 0);
           }
-        tc::mma_commit(&vempty);
+        tc::mma_commit(&vempty[st]);
         tc::mma_commit(&pfree);
         tc::mma_commit(&ofull[b]);
       };
-      tc::mbar_wait(&qfull, 0);
+      tc::mbar_wait_sleep(&qfull, 0);
       issue_S(0);
       for (int j = 0; j < ntiles; ++j) {
         if (j + 1 < ntiles) issue_S(j + 1);
@@ -232,12 +247,12 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
 
   auto fold = [&](int j, float fac) {   // o = o * fac + O_tile(j)
     const int b = j & 1;
-    tc::mbar_wait(&ofull[b], (j >> 1) & 1);
+    tc::mbar_wait_sleep(&ofull[b], (j >> 1) & 1);
     tc::fence_after();
 #pragma unroll
     for (int c = 0; c < PA_DH / 32; ++c) {
       float ov[32];
-      tmem_ld32(tmem + 256 + b * 128 + c * 32 + tl, ov);
+      tmem_ld32(tmem + 128 + b * 128 + c * 32 + tl, ov);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int e = 0; e < 32; ++e) o_acc[32 * c + e] = fmaf(o_acc[32 * c + e], fac, ov[e]);
@@ -251,64 +266,54 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
     const int b = j & 1;
     const int k0 = j * PA_KT;
     const bool masked = k0 + PA_KT - 1 > qmin || k0 + PA_KT > kend;   // some key of the tile invisible to some row
-    tc::mbar_wait(&sfull[b], (j >> 1) & 1);
+    tc::mbar_wait_sleep(&sfull[b], (j >> 1) & 1);
     tc::fence_after();
-    // pass 1: row max
-    float mx = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < PA_KT / 32; ++c) {
-      float sv[32];
-      tmem_ld32(tmem + b * 128 + c * 32 + tl, sv);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const int kp = k0 + 32 * c + e;
-        const float s = (!masked || (kp <= qp && kp < a.n_keys)) ? sv[e] * a.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, s);
-      }
-    }
-    const float m_new = fmaxf(m_run, mx);
-    const float fac = ex2f(m_run - m_new);              // ex2(-inf) = 0 on the first tile
-    // pass 2: P = exp2(s - m), split into 2 bf16 terms -> smem (the previous P.V must be done with it)
-    tc::mbar_wait(&pfree, (j & 1) ^ 1);
-    float sum = 0.f;
-#pragma unroll
-    for (int c = 0; c < PA_KT / 32; ++c) {
-      float sv[32];
-      tmem_ld32(tmem + b * 128 + c * 32 + tl, sv);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const int kp = k0 + 32 * c + e;
-        const bool vis = !masked || (kp <= qp && kp < a.n_keys);
-        sv[e] = vis ? ex2f(sv[e] * a.scale_log2 - m_new) : 0.f;
-      }
-#pragma unroll
-      for (int q8 = 0; q8 < 4; ++q8) {                 // 4 chunks of 8 keys
-        uint32_t h4[4], m4[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float x0 = sv[8 * q8 + 2 * e], x1 = sv[8 * q8 + 2 * e + 1];
-          const float h0 = __bfloat162float(__float2bfloat16_rn(x0));
-          const float h1 = __bfloat162float(__float2bfloat16_rn(x1));
-          const float m0 = __bfloat162float(__float2bfloat16_rn(x0 - h0));
-          const float m1 = __bfloat162float(__float2bfloat16_rn(x1 - h1));
-          h4[e] = pack_bf16(h0, h1);
-          m4[e] = pack_bf16(m0, m1);
-          sum += (h0 + m0) + (h1 + m1);   // l from the same (16-bit) weights the tensor core sees
-        }
-        const uint32_t off = chunk_off(r, c * 4 + q8);
-        *reinterpret_cast<uint4 *>(sP + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
-        *reinterpret_cast<uint4 *>(sP + PA_OP + off) = make_uint4(m4[0], m4[1], m4[2], m4[3]);
-      }
-    }
+    float sv[PA_KT];
+    tmem_ld32(tmem + b * PA_KT + tl, sv);
+    tmem_ld32(tmem + b * PA_KT + 32 + tl, sv + 32);
+    tc::tmem_ld_wait();
     tc::fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&sfree[b]);         // S is in registers: the buffer is free
+    // scores in the log2 domain; invisible keys -> -inf (exp2 -> +0)
+    if (masked) {
+#pragma unroll
+      for (int e = 0; e < PA_KT; ++e) {
+        const int kp = k0 + e;
+        sv[e] = (kp <= qp && kp < a.n_keys) ? sv[e] * a.scale_log2 : -INFINITY;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < PA_KT; ++e) sv[e] *= a.scale_log2;
+    }
+    float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // independent chains
+#pragma unroll
+    for (int e = 0; e < PA_KT; ++e) mx4[e & 3] = fmaxf(mx4[e & 3], sv[e]);
+    const float m_new = fmaxf(m_run, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
+    const float fac = ex2f(m_run - m_new);              // ex2(-inf) = 0 on the first tile
+    // P = exp2(s - m), split into 2 bf16 terms -> smem (the previous P.V must be done with it)
+    tc::mbar_wait_sleep(&pfree, (j & 1) ^ 1);
+    float sm4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q8 = 0; q8 < PA_KT / 8; ++q8) {           // 8 chunks of 8 keys
+      uint32_t h4[4], m4[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float p0 = ex2f(sv[8 * q8 + 2 * e] - m_new), p1 = ex2f(sv[8 * q8 + 2 * e + 1] - m_new);
+        sm4[e] += p0 + p1;
+        const uint32_t hp = cvt_bf16x2(p0, p1);
+        const float h0 = __uint_as_float(hp << 16), h1 = __uint_as_float(hp & 0xffff0000u);
+        h4[e] = hp;
+        m4[e] = cvt_bf16x2(p0 - h0, p1 - h1);
+      }
+      const uint32_t off = chunk_off(r, q8);
+      *reinterpret_cast<uint4 *>(sP + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+      *reinterpret_cast<uint4 *>(sP + PA_ATOM + off) = make_uint4(m4[0], m4[1], m4[2], m4[3]);
+    }
+    const float sum = (sm4[0] + sm4[1]) + (sm4[2] + sm4[3]);
     tc::fence_async_smem();
     __syncwarp();
-    if (lane == 0) {
-      tc::mbar_arrive(&sfree[b]);
-      tc::mbar_arrive(&pfull);
-    }
+    if (lane == 0) tc::mbar_arrive(&pfull);
     l_run = l_run * fac + sum;
     if (j > 0) fold(j - 1, fac_prev);
     fac_prev = fac;
