@@ -29,7 +29,10 @@ int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q,
 
 namespace {
 
-constexpr int PF_ROWS = 512;     // rows per dense block (bounded GEMM scratch)
+#ifndef HS_PF_ROWS
+#define HS_PF_ROWS 2048
+#endif
+constexpr int PF_ROWS = HS_PF_ROWS;   // rows per dense block (bounded GEMM scratch)
 constexpr int PF_QROWS = 1024;   // query rows per attention call (bounded partial-state scratch)
 
 // RMSNorm (optional gain) + exact 3-way split of rows [0, R) into three
