@@ -22,7 +22,7 @@ def main():
     import bench
     import paper_2404_11912_b200 as P
     from paper_2404_11912_b200 import model as M
-    tw = P.ModelWeights.on_device(P.DeviceModel.random(P.ModelConfig(**{**bench.TARGET_7B, "max_seq": 32768}), 1))
+    tw = P.ModelWeights.on_device(P.DeviceModel.random(P.ModelConfig(**{**bench.TARGET_7B, "max_seq": max(a.t) + 64}), 1))
     out = {}
     for t in a.t:
         toks = np.random.default_rng(t).integers(1, 32000, t).tolist()
