@@ -161,11 +161,20 @@ int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsSha
  * Same contract as hs_forward for an unsharded cache, for long prompts: the
  * dense projections run as tensor-core GEMMs (cuBLAS, three bf16 GEMMs over
  * the exact split of the fp32 activations, fp32 accumulation) in blocks of
- * 512 rows, attention causally in blocks of 1024 query rows.  fp32-accurate
- * but not bit-identical to a decode_step sequence (use hs_forward for that). */
+ * 2048 rows; causal attention on the 128-query-row tensor-core prefill kernel
+ * (head_dim 128) or the decode kernels in blocks of 1024 query rows.
+ * fp32-accurate but not bit-identical to a decode_step sequence (use
+ * hs_forward for that).                                                     */
 size_t hs_prefill_workspace_bytes(const HsModel *m, int t, int n_view, int split);
 int hs_prefill(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
                float *logits, float *q_stash, void *workspace, size_t workspace_bytes, void *stream);
+/* the same over a sequence-sharded full cache (head_dim 128): dense layers on
+ * every rank, each rank's attention over its own key slots as packed partial
+ * states, exchanged with sh's communicator and merged in rank order         */
+size_t hs_prefill_sharded_workspace_bytes(const HsModel *m, int t, int n_view, int split, int world);
+int hs_prefill_sharded(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
+                       const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
+                       size_t workspace_bytes, void *stream);
 
 /* ---- building blocks (also used by tests and the per-layer cache API) ---- */
 
@@ -219,6 +228,12 @@ int hs_attention(const HsCache *c, int layer, const HsStep *st, int n_heads,
 int hs_attention_partial(const HsCache *c, int layer, const HsStep *st, int n_heads,
                          const float *q, int t, float *packed, void *workspace, size_t ws_bytes,
                          void *stream);
+/* causal prefill attention (head_dim 128, linear cache; model.py:290-315 for
+ * a prompt block): t query rows at positions st->pos0.. over the cache slots
+ * [0, st->n_view), slot s holding position s + st->pos_base.  Exactly one of
+ * out ([t][H*dh] normalised) / packed ([t*H][2 + dh] partial state) is set. */
+int hs_prefill_attention(const HsCache *c, int layer, const HsStep *st, int n_heads, const float *q, int t,
+                         float *out, float *packed, void *stream);
 
 /* live timing of the dominant kernel for bench.py: while enabled, every
  * attention launch of hs_forward over a view of >= min_view keys is

@@ -76,6 +76,8 @@ _SIGS = {
     "hs_forward": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), _P(HsShard), vp, i32, vp, vp, vp, sz, vp]),
     "hs_prefill_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32]),
     "hs_prefill": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), vp, i32, vp, vp, vp, sz, vp]),
+    "hs_prefill_sharded_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32, i32]),
+    "hs_prefill_sharded": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), _P(HsShard), vp, i32, vp, vp, vp, sz, vp]),
     "hs_gemv": (i32, [vp, i32, i32, i32, vp, i32, i32, i32, vp, f32, i32, vp, i32, vp]),
     "hs_embed": (i32, [vp, i32, i32, vp, i32, vp, vp]),
     "hs_rope_append": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), i32, vp, i32, vp, vp, vp]),
@@ -83,6 +85,7 @@ _SIGS = {
     "hs_attention_workspace_bytes": (sz, [i32, i32, i32, i32, i32]),
     "hs_attention": (i32, [_P(HsCache), i32, _P(HsStep), i32, vp, i32, vp, vp, sz, vp]),
     "hs_attention_partial": (i32, [_P(HsCache), i32, _P(HsStep), i32, vp, i32, vp, vp, sz, vp]),
+    "hs_prefill_attention": (i32, [_P(HsCache), i32, _P(HsStep), i32, vp, i32, vp, vp, vp]),
     "hs_chunk_score": (i32, [vp, i32, i64, i64, i64, i32, i32, i32, i32, i32, vp, i32, vp, vp]),
     "hs_chunk_select_workspace_bytes": (sz, [i32, i32]),
     "hs_chunk_select": (i32, [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]),

@@ -24,8 +24,11 @@ int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H,
                            float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs,
                            int clean_hi = -1);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
-int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int n_keys,
-                             float *out, cudaStream_t stream);
+int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int pos_base,
+                             int n_keys, float *out, float *packed, cudaStream_t stream);
+int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, uint16_t *xs, int ldxs, int H,
+                       cudaStream_t st);
+int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
 
 namespace {
 
@@ -88,11 +91,14 @@ struct PfWs {
   uint16_t *s0, *s1, *s2;   // split planes [PF_ROWS][max(ld_d, ld_ff)]
   void *att_ws;
   size_t att_bytes;
+  float *send, *recv;       // sequence shards: packed partial states of PF_SQROWS query rows, own / all ranks
 };
+
+constexpr int PF_SQROWS = 4096;   // query rows per sharded attention exchange
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-size_t carve(const HsModel *m, int t, int n_view, int split, char *base, PfWs *w) {
+size_t carve(const HsModel *m, int t, int n_view, int split, int world, char *base, PfWs *w) {
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim;
   const int R = t < PF_ROWS ? t : PF_ROWS;
   const int ldk = m->ld_d > m->ld_ff ? m->ld_d : m->ld_ff;
@@ -110,6 +116,9 @@ size_t carve(const HsModel *m, int t, int n_view, int split, char *base, PfWs *w
   w->s2 = (uint16_t *)take((size_t)R * ldk * 2);
   w->att_bytes = attention_ws(t < PF_QROWS ? t : PF_QROWS, H, dh, n_view, split);
   w->att_ws = take(w->att_bytes);
+  const size_t part = (size_t)(t < PF_SQROWS ? t : PF_SQROWS) * H * (dh + 2) * 4;
+  w->send = world > 0 ? (float *)take(part) : nullptr;
+  w->recv = world > 0 ? (float *)take(part * world) : nullptr;
   return off;
 }
 
@@ -139,11 +148,36 @@ int split_rows_n(const float *x, int ldx, int R, int K, int ldk, const float *ga
 
 extern "C" size_t hs_prefill_workspace_bytes(const HsModel *m, int t, int n_view, int split) {
   hs::PfWs w;
-  return hs::carve(m, t, n_view, split, nullptr, &w);
+  return hs::carve(m, t, n_view, split, 0, nullptr, &w);
 }
+
+extern "C" size_t hs_prefill_sharded_workspace_bytes(const HsModel *m, int t, int n_view, int split, int world) {
+  hs::PfWs w;
+  return hs::carve(m, t, n_view, split, world, nullptr, &w);
+}
+
+static int prefill_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
+                        const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
+                        size_t workspace_bytes, void *stream);
 
 extern "C" int hs_prefill(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
                           float *logits, float *q_stash, void *workspace, size_t workspace_bytes, void *stream) {
+  return prefill_impl(m, c, st, nullptr, tokens, t, logits, q_stash, workspace, workspace_bytes, stream);
+}
+
+extern "C" int hs_prefill_sharded(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
+                                  const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
+                                  size_t workspace_bytes, void *stream) {
+  HS_REQUIRE(sh != nullptr && sh->comm != nullptr && sh->world >= 1 && sh->rank >= 0 && sh->rank < sh->world,
+             HS_ERR_VALUE, "prefill: bad shard descriptor");
+  HS_REQUIRE(m->head_dim == 128 && c->kind == HS_KV_LINEAR && st->append_mode == HS_APPEND_POS, HS_ERR_VALUE,
+             "prefill: the sharded prefill needs head_dim 128 and a full (linear) cache");
+  return prefill_impl(m, c, st, sh, tokens, t, logits, q_stash, workspace, workspace_bytes, stream);
+}
+
+static int prefill_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
+                        const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
+                        size_t workspace_bytes, void *stream) {
   using namespace hs;
   HS_REQUIRE(t >= 1, HS_ERR_VALUE, "empty token sequence");
   HS_REQUIRE(c->n_layers == m->n_layers && c->n_kv_heads == m->n_kv_heads && c->head_dim == m->head_dim,
@@ -151,7 +185,7 @@ extern "C" int hs_prefill(const HsModel *m, const HsCache *c, const HsStep *st, 
   HS_REQUIRE(st->pos0 + t <= m->max_seq, HS_ERR_CAPACITY, "sequence of %d exceeds max_seq %d", st->pos0 + t,
              m->max_seq);
   PfWs w;
-  const size_t need = carve(m, t, st->n_view, st->split, (char *)workspace, &w);
+  const size_t need = carve(m, t, st->n_view, st->split, sh ? sh->world : 0, (char *)workspace, &w);
   HS_REQUIRE(workspace_bytes >= need, HS_ERR_VALUE, "prefill: workspace %zu < %zu", workspace_bytes, need);
   cublasHandle_t h = pf_handle();
   HS_REQUIRE(h != nullptr, HS_ERR_CUDA, "prefill: cuBLAS unavailable");
@@ -179,9 +213,21 @@ extern "C" int hs_prefill(const HsModel *m, const HsCache *c, const HsStep *st, 
     // (prefill_attn.cu); other head sizes in blocks of query rows on the
     // decode kernels, a block seeing keys up to its last row
     static const bool tc_prefill = getenv("HS_PREFILL_DECODE_ATTN") == nullptr;   // A/B hook
-    if (tc_prefill && dh == 128 && st->pos_base == 0 && st->window == 0 && c->kind == HS_KV_LINEAR) {
-      HS_TRY(launch_prefill_attention(c, l, H, w.q, t, st->pos0, st->n_view < st->pos0 + t ? st->n_view : st->pos0 + t,
-                                      w.attn, s));
+    if (sh) {
+      // sequence shards: every rank attends all query rows over its own key
+      // slots, the packed partial states go to all ranks and are merged in
+      // rank order (the decode path's exchange), PF_SQROWS rows
+      // at a time
+      for (int a0 = 0; a0 < t; a0 += PF_SQROWS) {
+        const int tq = t - a0 < PF_SQROWS ? t - a0 : PF_SQROWS;
+        HS_TRY(launch_prefill_attention(c, l, H, w.q + (size_t)a0 * H * dh, tq, st->pos0 + a0, st->pos_base,
+                                        st->n_view, nullptr, w.send, s));
+        HS_TRY(shard_all_gather(sh, w.send, w.recv, (size_t)tq * H * (dh + 2) * 4, s));
+        HS_TRY(launch_shard_merge(w.recv, sh->world, tq * H, dh, w.attn + (size_t)a0 * d, nullptr, 0, H, s));
+      }
+    } else if (tc_prefill && dh == 128 && st->pos_base == 0 && st->window == 0 && c->kind == HS_KV_LINEAR) {
+      HS_TRY(launch_prefill_attention(c, l, H, w.q, t, st->pos0, 0,
+                                      st->n_view < st->pos0 + t ? st->n_view : st->pos0 + t, w.attn, nullptr, s));
     } else
     for (int a0 = 0; a0 < t; a0 += PF_QROWS) {
       const int tq = t - a0 < PF_QROWS ? t - a0 : PF_QROWS;

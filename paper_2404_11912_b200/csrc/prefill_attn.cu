@@ -41,8 +41,9 @@ constexpr int PA_SMEM = 3 * PA_OP /*Q*/ + 2 * PA_NS * PA_KV /*K, V*/ + 2 * PA_AT
 
 struct PrefillArgs {
   const float *q;       // [t][H][128] roped queries
-  float *out;           // [t][H*128]
-  int t, H, KVH, g, layer, cap, pos0, n_keys;
+  float *out;           // [t][H*128] normalised rows, or null
+  float *packed;        // [t*H][2 + 128] partial state (m, l, o) of this key range, or null
+  int t, H, KVH, g, layer, cap, pos0, n_keys, pos_base;   // key slot s holds position s + pos_base
   float scale_log2;
 };
 
@@ -104,9 +105,11 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
   const int h = blockIdx.y, kh = h / a.g;
   const int r0 = qt * PA_QT;
   const int rows = min(PA_QT, a.t - r0);
-  const int kend = min(a.n_keys, a.pos0 + r0 + rows);  // keys [0, kend) are visible to some row
+  // slots [0, kend) are visible to some row (a sequence shard's slots may all
+  // lie past the tile's queries: ntiles = 0, the rows' partial state is empty)
+  const int kend = max(0, min(a.n_keys, a.pos0 + r0 + rows - a.pos_base));
   const int ntiles = (kend + PA_KT - 1) / PA_KT;
-  const int qmin = a.pos0 + r0;                        // first query position of the tile
+  const int qmin = a.pos0 + r0 - a.pos_base;           // first query position of the tile, in slots
 
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tmK);
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
         tc::mma_commit(&ofull[b]);
       };
       tc::mbar_wait_sleep(&qfull, 0);
-      issue_S(0);
+      if (ntiles > 0) issue_S(0);
       for (int j = 0; j < ntiles; ++j) {
         if (j + 1 < ntiles) issue_S(j + 1);
         issue_PV(j);
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
   // ------------------------------------------------------------------ softmax warps 0-3
   const int r = warp * 32 + lane;                      // query row of this thread = TMEM lane
   const uint32_t tl = (uint32_t)(warp * 32) << 16;
-  const int qp = a.pos0 + r0 + r;                      // its position
+  const int qp = a.pos0 + r0 + r - a.pos_base;         // its position, in slots (may be < 0 on a shard)
   {  // stage Q (3-way exact split), zero rows past t
     const float *qrow = a.q + ((size_t)(r0 + r) * a.H + h) * PA_DH;
 #pragma unroll 2
@@ -290,7 +293,9 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
 #pragma unroll
     for (int e = 0; e < PA_KT; ++e) mx4[e & 3] = fmaxf(mx4[e & 3], sv[e]);
     const float m_new = fmaxf(m_run, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
-    const float fac = ex2f(m_run - m_new);              // ex2(-inf) = 0 on the first tile
+    // a row with nothing visible yet (shard slots past its position) keeps m = -inf: p = 0, fac = 0
+    const float m_ref = m_new == -INFINITY ? 0.f : m_new;
+    const float fac = ex2f(m_run - m_ref);              // ex2(-inf) = 0 on the first tile
     // P = exp2(s - m), split into 2 bf16 terms -> smem (the previous P.V must be done with it)
     tc::mbar_wait_sleep(&pfree, (j & 1) ^ 1);
     float sm4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
       uint32_t h4[4], m4[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float p0 = ex2f(sv[8 * q8 + 2 * e] - m_new), p1 = ex2f(sv[8 * q8 + 2 * e + 1] - m_new);
+        const float p0 = ex2f(sv[8 * q8 + 2 * e] - m_ref), p1 = ex2f(sv[8 * q8 + 2 * e + 1] - m_ref);
         sm4[e] += p0 + p1;
         const uint32_t hp = cvt_bf16x2(p0, p1);
         const float h0 = __uint_as_float(hp << 16), h1 = __uint_as_float(hp & 0xffff0000u);
@@ -319,8 +324,14 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
     fac_prev = fac;
     m_run = m_new;
   }
-  fold(ntiles - 1, fac_prev);
-  if (r < rows) {
+  if (ntiles > 0) fold(ntiles - 1, fac_prev);
+  if (r < rows && a.packed) {
+    float *pk = a.packed + ((size_t)(r0 + r) * a.H + h) * (PA_DH + 2);
+    pk[0] = m_run == -INFINITY ? -INFINITY : m_run * 0.69314718055994530942f;   // natural-log units
+    pk[1] = l_run;
+#pragma unroll
+    for (int d = 0; d < PA_DH; ++d) pk[2 + d] = o_acc[d];
+  } else if (r < rows) {
     const float inv = 1.f / l_run;
     float *orow = a.out + (size_t)(r0 + r) * a.H * PA_DH + (size_t)h * PA_DH;
 #pragma unroll
@@ -335,13 +346,19 @@ __global__ void __launch_bounds__(PA_THREADS, 1) prefill_attn_kernel(const __gri
 
 }  // namespace
 
-// causal attention of t query rows at positions [pos0, pos0 + t) over keys
-// [0, n_keys) of a linear, unsharded, unwindowed cache (slot == position)
-int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int n_keys,
-                             float *out, cudaStream_t stream) {
+// causal attention of t query rows at positions [pos0, pos0 + t) over the
+// slots [0, n_keys) of a linear, unwindowed cache whose slot s holds position
+// s + pos_base (a sequence shard; 0 for a whole cache).  out: normalised rows;
+// packed: this key range's partial state per row, for the rank-ordered merge.
+int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int pos_base,
+                             int n_keys, float *out, float *packed, cudaStream_t stream) {
   HS_REQUIRE(c->head_dim == PA_DH, HS_ERR_SHAPE, "prefill attention: head_dim must be 128");
   HS_REQUIRE(H % c->n_kv_heads == 0, HS_ERR_SHAPE, "prefill attention: H %% KVH != 0");
-  HS_REQUIRE(n_keys <= c->cap && n_keys >= pos0 + 1, HS_ERR_CAPACITY, "prefill attention: bad key range");
+  HS_REQUIRE(c->kind == HS_KV_LINEAR, HS_ERR_VALUE, "prefill attention: needs a linear (full) cache");
+  HS_REQUIRE(n_keys >= 0 && n_keys <= c->cap, HS_ERR_CAPACITY, "prefill attention: bad key range");
+  HS_REQUIRE(packed != nullptr || n_keys + pos_base >= pos0 + 1, HS_ERR_VALUE,
+             "prefill attention: normalised output needs every query's keys");
+  HS_REQUIRE(t >= 1, HS_ERR_VALUE, "prefill attention: empty query block");
   CUtensorMap mk, mv;
   const uint64_t rows = (uint64_t)c->n_layers * c->n_kv_heads * c->cap;
   int rc = get_tmap_bf16(c->k, PA_DH, rows, PA_DH * 2, PA_KT, &mk);
@@ -349,8 +366,8 @@ int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q,
   rc = get_tmap_bf16(c->v, PA_DH, rows, PA_DH * 2, PA_KT, &mv);
   if (rc != HS_OK) return rc;
   PrefillArgs a;
-  a.q = q; a.out = out; a.t = t; a.H = H; a.KVH = c->n_kv_heads; a.g = H / c->n_kv_heads; a.layer = layer;
-  a.cap = c->cap; a.pos0 = pos0; a.n_keys = n_keys;
+  a.q = q; a.out = out; a.packed = packed; a.t = t; a.H = H; a.KVH = c->n_kv_heads; a.g = H / c->n_kv_heads;
+  a.layer = layer; a.cap = c->cap; a.pos0 = pos0; a.n_keys = n_keys; a.pos_base = pos_base;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)PA_DH));
   static bool attr = false;
   if (!attr) {
@@ -363,3 +380,14 @@ int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q,
 }
 
 }  // namespace hs
+
+// per-layer public entry (hs_abi.h): attention of t query rows at positions
+// st->pos0.. over the cache's slots [0, st->n_view) (positions + st->pos_base)
+extern "C" int hs_prefill_attention(const HsCache *c, int layer, const HsStep *st, int n_heads, const float *q,
+                                    int t, float *out, float *packed, void *stream) {
+  HS_REQUIRE(c != nullptr && st != nullptr && q != nullptr, HS_ERR_VALUE, "prefill attention: null argument");
+  HS_REQUIRE((out != nullptr) != (packed != nullptr), HS_ERR_VALUE, "prefill attention: exactly one of out / packed");
+  HS_REQUIRE(layer >= 0 && layer < c->n_layers, HS_ERR_VALUE, "prefill attention: layer %d out of range", layer);
+  return hs::launch_prefill_attention(c, layer, n_heads, q, t, st->pos0, st->pos_base, st->n_view, out, packed,
+                                      hs::as_stream(stream));
+}

@@ -437,9 +437,10 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
                    out: Optional[torch.Tensor] = None, prefill: bool = False) -> torch.Tensor:
     """Causal forward of `tokens` (host list or device int32 tensor) at
     cache.frontier; returns device logits [t, V] fp32 (model.py:247-331).
-    prefill=True lets a long prompt on an unsharded full cache run through
-    the batched GEMM prefill (hs_prefill); otherwise every row is computed
-    exactly as a decode step would compute it."""
+    prefill=True lets a long prompt on a full cache (unsharded, or
+    sequence-sharded at head_dim 128) run through the batched GEMM prefill
+    (hs_prefill / hs_prefill_sharded); otherwise every row is computed exactly
+    as a decode step would compute it."""
     dm = weights.device()
     cfg = dm.config
     tok = to_i32_device(tokens)
@@ -458,12 +459,19 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
     shards = getattr(cache, "shards", None)
     shard_ref = shards.ref if shards is not None else None
     world = shards.world if shards is not None else 0
-    if prefill and t >= PREFILL_MIN_ROWS and cache.kind == _abi.HS_KV_LINEAR and shards is None:
+    if (prefill and t >= PREFILL_MIN_ROWS and cache.kind == _abi.HS_KV_LINEAR
+            and (shards is None or cfg.head_dim == 128)):
         step = cache._step(t)
-        nbytes = lib.hs_prefill_workspace_bytes(dm.ref, t, step.n_view, step.split)
-        ws = workspaces.get("prefill", nbytes)
-        check(lib.hs_prefill(dm.ref, cache._ref, C.byref(step), ptr(tok), t, ptr(out), ptr(stash), ptr(ws), nbytes,
-                             stream_ptr()))
+        if shards is None:
+            nbytes = lib.hs_prefill_workspace_bytes(dm.ref, t, step.n_view, step.split)
+            ws = workspaces.get("prefill", nbytes)
+            check(lib.hs_prefill(dm.ref, cache._ref, C.byref(step), ptr(tok), t, ptr(out), ptr(stash), ptr(ws),
+                                 nbytes, stream_ptr()))
+        else:   # sequence shards: per-rank partial attention, NCCL exchange, rank-ordered merge
+            nbytes = lib.hs_prefill_sharded_workspace_bytes(dm.ref, t, step.n_view, step.split, world)
+            ws = workspaces.get("prefill", nbytes)
+            check(lib.hs_prefill_sharded(dm.ref, cache._ref, C.byref(step), shard_ref, ptr(tok), t, ptr(out),
+                                         ptr(stash), ptr(ws), nbytes, stream_ptr()))
         cache._advance(t)
         if recorder is not None:
             recorder.query_position = cache.frontier - 1

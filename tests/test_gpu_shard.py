@@ -180,3 +180,76 @@ def test_sharded_cache_rejects_misaligned_bounds(P):
     with pytest.raises(ValueError):
         check(lib.hs_retrieval_gather(src._ref, dst._ref, ptr(dst.chosen), dst.quota, 1, 8, 100, 4, 260,
                                       stream_ptr()))
+
+
+def _causal_ref(q, K, V, pos0, positions):
+    """fp64 causal attention: q [t][H][dh] at positions pos0.., keys K/V [n][KVH][dh]
+    at `positions` (model.py:290-315 with the prefix mask)."""
+    t, H, dh = q.shape
+    KVH = K.shape[1]
+    g = H // KVH
+    out = np.zeros((t, H, dh))
+    for i in range(t):
+        vis = positions <= pos0 + i
+        for h in range(H):
+            k, v = K[vis, h // g].astype(np.float64), V[vis, h // g].astype(np.float64)
+            s = k @ q[i, h].astype(np.float64) / np.sqrt(dh)
+            w = np.exp(s - s.max())
+            out[i, h] = w @ v / w.sum()
+    return out
+
+
+def test_prefill_attention_kernel_and_shard_merge(P):
+    """The 128-row tensor-core prefill attention (hs_prefill_attention)
+    against fp64 causal attention, and its per-shard partial states merged in
+    rank order (hs_shard_merge) against the unsharded kernel output."""
+    from paper_2404_11912_b200._abi import HsStep, check, lib
+    from paper_2404_11912_b200.runtime import ptr, stream_ptr
+    from paper_2404_11912_b200.shard import shard_plan
+    rng = np.random.default_rng(21)
+    L, kvh, H, dh = 1, 2, 4, 128
+    for n, t, G in ((700, 300, 3), (1500, 1500, 2), (2100, 129, 4)):
+        pos0 = n - t
+        K = rng.normal(0, 1, (L, n, kvh, dh)).astype(np.float32)
+        V = rng.normal(0, 1, (L, n, kvh, dh)).astype(np.float32)
+        qh = rng.normal(0, 1, (t, H, dh)).astype(np.float32)
+        q = torch.from_numpy(qh).cuda()
+        full = P.FullCache(L, kvh, dh, n + 64)
+        _fill(full, K, V, range(n))
+        st = HsStep()
+        st.pos0, st.n_view = pos0, n
+        out = torch.zeros((t, H * dh), device="cuda")
+        check(lib.hs_prefill_attention(full._ref, 0, C.byref(st), H, ptr(q), t, ptr(out), None, stream_ptr()))
+        Kb = full.k[0, :, :n].float().permute(1, 0, 2).cpu().numpy()    # bf16-stored keys as the kernel sees them
+        Vb = full.v[0, :, :n].float().permute(1, 0, 2).cpu().numpy()
+        ref = _causal_ref(qh, Kb, Vb, pos0, np.arange(n)).reshape(t, H * dh)
+        got = out.cpu().numpy()
+        assert np.abs(got - ref).max() <= 3e-5 * np.abs(ref).max(), (n, t)
+        parts = torch.zeros((G, t * H, dh + 2), device="cuda")
+        for r, (lo, hi) in enumerate(shard_plan(n, G, 8)):
+            sc = P.FullCache(L, kvh, dh, n + 64, None, lo, hi)
+            end = n if hi is None else min(n, hi)
+            if end > lo:
+                sc._write_rows(0, K[0, lo:end], V[0, lo:end], np.arange(end - lo), np.arange(lo, end))
+            s2 = HsStep()
+            s2.pos0, s2.n_view, s2.pos_base = pos0, max(0, end - lo), lo
+            check(lib.hs_prefill_attention(sc._ref, 0, C.byref(s2), H, ptr(q), t, None, ptr(parts[r]), stream_ptr()))
+        merged = torch.zeros((t, H * dh), device="cuda")
+        check(lib.hs_shard_merge(ptr(parts), G, t * H, dh, ptr(merged), stream_ptr()))
+        assert np.abs(merged.cpu().numpy() - got).max() <= 1e-5 * np.abs(got).max(), (n, t, G)
+
+
+def test_one_rank_sharded_prefill_matches_unsharded(P, one_rank):
+    """hs_prefill_sharded through a one-rank NCCL communicator (partial states,
+    all-gather, merge) against the unsharded GEMM prefill, and the decode that
+    follows."""
+    cfg = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=128, d_ff=344, vocab_size=512, max_seq=2048)
+    w = P.generate_weights(cfg, 9, tied_head=False)
+    prompt = np.random.default_rng(4).integers(1, 512, 900).tolist()
+    a = P.FullCache.from_config(cfg)
+    b = P.FullCache.shard(cfg, one_rank, len(prompt), 8)
+    la, lb = P.prefill(w, prompt, a), P.prefill(w, prompt, b)
+    assert np.allclose(la, lb, rtol=1e-5, atol=1e-5 * np.abs(la).max())
+    assert (np.argmax(la, -1) == np.argmax(lb, -1)).mean() > 0.999
+    da, db = P.decode_step(w, 17, a), P.decode_step(w, 17, b)
+    assert np.allclose(da, db, rtol=1e-4, atol=1e-4 * np.abs(da).max())
