@@ -42,7 +42,7 @@ FULL_SPLIT = int(os.environ.get("HS_FULL_SPLIT", 2048))    # keys per attention 
 SMALL_SPLIT = int(os.environ.get("HS_SMALL_SPLIT", 512))   # keys per split over the retrieval view
 # (fixed per cache kind, never a function of t: a row's result is t-invariant;
 # the environment overrides are experiment hooks for tools/fwdbench.py)
-STREAM_SPLIT = 64     # keys per split over the (small) streaming window: one CTA per 64 keys
+STREAM_SPLIT = int(os.environ.get("HS_STREAM_SPLIT", 64))   # keys per split over the streaming window
 
 
 @dataclass(frozen=True)
