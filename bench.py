@@ -37,6 +37,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("NCCL_DEBUG", "WARN")      # keep stdout to the one JSON line
 
+# stdout carries exactly one JSON line: everything native libraries print
+# (the NCCL banner when NCCL_DEBUG is set verbose, driver messages) goes to
+# stderr; the result line is written to the saved original stdout
+_RESULT_FD = os.dup(1)
+os.dup2(2, 1)
+sys.stdout = os.fdopen(os.dup(2), "w", buffering=1)
+
+
+def emit(line: str) -> None:
+    os.write(_RESULT_FD, (line + "\n").encode())
+
 import numpy as np  # noqa: E402
 
 TARGET_7B = dict(n_layers=32, n_heads=32, n_kv_heads=32, head_dim=128, d_ff=11008, vocab_size=32000,
@@ -227,7 +238,7 @@ def run_reference(args):
            "data": "synthetic", "config": workload_config(args),
            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(json.dumps(out))
 
 
 MODEL_NAMES = {"llama2-7b": "Llama2-7B-128K", "llama2-13b": "Llama2-13B-128K", "lwm-7b": "LWM-Text-7B"}
@@ -383,7 +394,7 @@ def main():
                                                easy_frac=args.easy_frac, target=TARGETS[args.model])
             out["cpu_baseline"] = {"value": statistics.median(rates), "unit": "tokens/s", "cores": cores,
                                    "kind": "port", "sample": desc}
-        print(json.dumps(out), flush=True)
+        emit(json.dumps(out))
     if shards is not None:
         shards.destroy()
     if world > 1:
