@@ -157,6 +157,15 @@ int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsSha
                const int32_t *tokens, int t, float *logits, float *q_stash,
                void *workspace, size_t workspace_bytes, void *stream);
 
+/* one decode position over a TopKCache (caches.py:568-652; the oracle
+ * upper-bound pairing of analytics.measure_acceptance): like hs_forward with
+ * t = 1 on an unsharded full cache, but each layer attends only over the
+ * `budget` keys of each kv group with the largest exact group-mean softmax
+ * weight (fp64; ties to the lower position).  st->n_view must exceed budget. */
+size_t hs_forward_topk_workspace_bytes(const HsModel *m, int n_view, int budget);
+int hs_forward_topk(const HsModel *m, const HsCache *c, const HsStep *st, int budget, const int32_t *tokens,
+                    float *logits, float *q_stash, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- batched prefill (model.py:334-354) --------------
  * Same contract as hs_forward for an unsharded cache, for long prompts: the
  * dense projections run as tensor-core GEMMs (cuBLAS, three bf16 GEMMs over

@@ -4,10 +4,11 @@ the GPU counterpart of hierspec/analytics.py:229-309 (`AcceptanceStats`,
 
 Pairings: 'hierarchical' (draft model + StreamingCache speculated against
 the retrieval-cache target, verified on the full cache; both levels are
-reported) and the self-speculation pairings 'self:streaming' and
-'self:retrieval' (SingleLevelSession against the full cache).  'self:h2o' and
-'self:topk' need per-query attention probabilities fed back into the cache
-and are outside this build: they raise ContractError.
+reported) and the self-speculation pairings 'self:streaming',
+'self:retrieval' and 'self:topk' (SingleLevelSession against the full cache;
+TopK selects per layer and query on the device, csrc/topk.cu).  'self:h2o'
+needs per-query attention probabilities fed back into the cache and is
+outside this build: it raises ContractError.
 The rest of the reference's analytics module (attention-mass recovery,
 needle fixtures, the speedup model) is host-side analysis, not decode work.
 """
@@ -17,7 +18,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
-from .caches import H2OConfig, RetrievalCache, RetrievalConfig, StreamingCache, StreamingConfig
+from .caches import H2OConfig, RetrievalCache, RetrievalConfig, StreamingCache, StreamingConfig, TopKCache
 from .errors import ContractError
 from .model import ModelConfig, ModelWeights
 from .speculation import HierarchicalSession, LevelStats, SingleLevelSession, SpecConfig
@@ -53,7 +54,9 @@ def _draft_cache_for(pairing: str, config: ModelConfig, *, streaming: StreamingC
         return StreamingCache.from_config(config, streaming)
     if kind == "retrieval":
         return RetrievalCache.from_config(config, retrieval)
-    if kind in ("h2o", "topk"):
+    if kind == "topk":
+        return TopKCache.from_config(config, topk_budget)
+    if kind == "h2o":
         raise ContractError(f"pairing {pairing!r} needs attention-probability feedback into the cache; "
                             "out of scope for the device path (SURVEY.md §2.1)")
     raise ValueError(f"unknown pairing {pairing!r}")

@@ -275,6 +275,35 @@ class FullCache(KVCache):
         self._n = [self.frontier] * self.n_layers
 
 
+class TopKCache(FullCache):
+    """Oracle upper bound (caches.py:568-652): keeps every position like the
+    full cache and, for each single-query decode, each layer attends only
+    over the `budget` entries per kv group with the highest exact group-mean
+    softmax weight (ties to the lower position); multi-query forwards, and
+    stores of at most `budget` entries, see everything.  The selection runs on
+    the device inside hs_forward_topk (csrc/topk.cu)."""
+
+    policy = "topk"
+
+    def __init__(self, n_layers: int, n_kv_heads: int, head_dim: int, max_entries: int, budget: int):
+        if budget < 1:
+            raise ValueError("budget must be >= 1")
+        super().__init__(n_layers, n_kv_heads, head_dim, max_entries)
+        self.budget = budget
+
+    @classmethod
+    def from_config(cls, model_config, budget: int):
+        return cls(model_config.n_layers, model_config.n_kv_heads, model_config.head_dim, model_config.max_seq,
+                   budget)
+
+    def clone(self):
+        c = TopKCache(self.n_layers, self.n_kv_heads, self.head_dim, self.max_entries, self.budget)
+        check(lib.hs_cache_copy(c._ref, self._ref, max(self._n + [0]), stream_ptr()))
+        c._n = list(self._n)
+        c.frontier, c.committed = self.frontier, self.committed
+        return c
+
+
 class StreamingCache(KVCache):
     """Attention sinks + recent window (caches.py:224-288).
 

@@ -23,6 +23,9 @@ int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, 
                        cudaStream_t st);
 int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
+size_t topk_ws_bytes(const HsModel *m, int n, int budget);
+int launch_topk_attention(const HsModel *m, const HsCache *c, int layer, int n, int pos, int budget, const float *q,
+                          uint16_t *xs, int ldxs, void *ws, size_t ws_bytes, cudaStream_t st);
 
 // ---- error state -------------------------------------------------------------
 static thread_local char g_err[512] = "";
@@ -161,9 +164,33 @@ extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
          hs::align256((size_t)24 * m->ld_d * 2);
 }
 
+static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
+                        const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
+                        size_t workspace_bytes, void *stream, int topk_budget);
+
 extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                           const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
                           size_t workspace_bytes, void *stream) {
+  return forward_impl(m, c, st, sh, tokens, t, logits, q_stash, workspace, workspace_bytes, stream, 0);
+}
+
+extern "C" size_t hs_forward_topk_workspace_bytes(const HsModel *m, int n_view, int budget) {
+  return hs_forward_workspace_bytes(m, 1, n_view, 512, 0) + 256 + hs::topk_ws_bytes(m, n_view, budget);
+}
+
+// one decode position with TopKCache exposure (caches.py:617-634): every
+// layer attends over the `budget` heaviest keys of each kv group
+extern "C" int hs_forward_topk(const HsModel *m, const HsCache *c, const HsStep *st, int budget,
+                               const int32_t *tokens, float *logits, float *q_stash, void *workspace,
+                               size_t workspace_bytes, void *stream) {
+  HS_REQUIRE(c->kind == HS_KV_LINEAR && st->append_mode == HS_APPEND_POS && st->pos_base == 0, HS_ERR_VALUE,
+             "top-k forward: needs an unsharded linear cache");
+  return forward_impl(m, c, st, nullptr, tokens, 1, logits, q_stash, workspace, workspace_bytes, stream, budget);
+}
+
+static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
+                        const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
+                        size_t workspace_bytes, void *stream, int topk_budget) {
   using namespace hs;
   HS_REQUIRE(t >= 1, HS_ERR_VALUE, "empty token sequence");
   HS_REQUIRE(c->n_layers == m->n_layers && c->n_kv_heads == m->n_kv_heads && c->head_dim == m->head_dim,
@@ -180,6 +207,13 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
   FwdWs w;
   const size_t need = carve(m, t, st->n_view, st->split, sharded ? sh->world : 0, (char *)workspace, &w);
   HS_REQUIRE(workspace_bytes >= need, HS_ERR_VALUE, "forward: workspace %zu < %zu", workspace_bytes, need);
+  void *topk_ws = nullptr;
+  size_t topk_bytes = 0;
+  if (topk_budget > 0) {
+    topk_ws = (char *)workspace + align256(need);
+    topk_bytes = topk_ws_bytes(m, st->n_view, topk_budget);
+    HS_REQUIRE(workspace_bytes >= align256(need) + topk_bytes, HS_ERR_VALUE, "forward: top-k workspace too small");
+  }
   cudaStream_t s = as_stream(stream);
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim, ff = m->d_ff;
   const int nqkv = (H + 2 * KVH) * dh;
@@ -217,6 +251,9 @@ extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, 
         HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr, 0, clean_hi));
         HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
         HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, nullptr, w.xa, m->ld_d, H, s));
+      } else if (topk_budget > 0) {
+        HS_TRY(launch_topk_attention(m, c, l, st->n_view, st->pos0, topk_budget, w.q, w.xa, m->ld_d, topk_ws,
+                                     topk_bytes, s));
       } else {
         HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, nullptr, w.att_ws, w.att_bytes, s, w.xa,
                                       m->ld_d, clean_hi));

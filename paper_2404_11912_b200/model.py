@@ -476,6 +476,16 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
         if recorder is not None:
             recorder.query_position = cache.frontier - 1
         return out
+    if t == 1 and getattr(cache, "policy", "") == "topk" and cache.frontier + 1 > cache.budget:
+        step = cache._step(1)                     # TopKCache single-query exposure (caches.py:629-634)
+        nbytes = lib.hs_forward_topk_workspace_bytes(dm.ref, step.n_view, cache.budget)
+        ws = workspaces.get("topk", nbytes)
+        check(lib.hs_forward_topk(dm.ref, cache._ref, C.byref(step), cache.budget, ptr(tok), ptr(out), ptr(stash),
+                                  ptr(ws), nbytes, stream_ptr()))
+        cache._advance(1)
+        if recorder is not None:
+            recorder.query_position = cache.frontier - 1
+        return out
     for a, b in cache._batches(t):
         step = cache._step(b - a)
         nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split, world)

@@ -667,12 +667,12 @@ class SingleLevelSession:
     """One draft lane speculated against one full-cache verify lane --
     standard speculative decoding, the acceptance-measurement pairing of
     speculation.py:401-477.  The draft cache is a StreamingCache (own draft
-    model or self-speculation), a FullCache, or a RetrievalCache, which is
-    built from (and rebuilt against) the verify lane's full cache and so
-    requires the verify weights (self-speculation).  Runs on the same device
-    round machinery as HierarchicalSession: tokens, distributions and
-    uniforms stay resident, one host read-back per round.  H2O / TopK draft
-    caches need per-query attention probabilities and stay out of scope
+    model or self-speculation), a FullCache or TopKCache, or a RetrievalCache,
+    which is built from (and rebuilt against) the verify lane's full cache
+    and so requires the verify weights (self-speculation).  Runs on the same
+    device round machinery as HierarchicalSession: tokens, distributions and
+    uniforms stay resident, one host read-back per round.  H2O draft caches
+    need per-query attention probabilities and stay out of scope
     (SURVEY.md §2.1)."""
 
     def __init__(self, draft_weights: ModelWeights, draft_cache: KVCache, verify_weights: ModelWeights,
@@ -684,7 +684,7 @@ class SingleLevelSession:
             raise ValueError("gamma must be >= 1")
         if not isinstance(draft_cache, (FullCache, StreamingCache, RetrievalCache)):
             raise ContractError(f"draft cache {type(draft_cache).__name__} is not supported on the device path "
-                                "(H2O / TopK pairings are out of scope, SURVEY.md §2.1)")
+                                "(the H2O pairing is out of scope, SURVEY.md §2.1)")
         self.gamma = gamma
         self.temperature = temperature
         self.committed = list(prefix)
