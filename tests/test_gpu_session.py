@@ -523,3 +523,67 @@ def test_edge_sessions_match_oracle(P, prompt_len, chunk, budget, stream, temp):
     assert [tr.inner.proposed, tr.inner.accepted, tr.outer.proposed, tr.outer.accepted] == \
         [otr.inner[0], otr.inner[1], otr.outer[0], otr.outer[1]]
     assert imp0 == oimp0
+
+
+@pytest.mark.parametrize("temp", [0.6, 1.0])
+def test_first_token_distribution_is_lossless(P, temp):
+    """Acceptance criterion 2 on the device (tests/test_acceptance.py:67-138):
+    the first token emitted by the two-level loop is distributed as the
+    target model's own next-token distribution -- whatever the draft and the
+    retrieval lane proposed.  3,000 sampled sessions cloned from one prefill,
+    chi-square against p = softmax(full-lane logits / T) (bins with expected
+    count < 5 pooled)."""
+    from scipy.stats import chi2
+    cfg_t = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=32, d_ff=96, vocab_size=24, max_seq=256)
+    cfg_d = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=32, d_ff=64, vocab_size=24, max_seq=256)
+    tw = P.plant_successor(P.generate_weights(cfg_t, 41, tied_head=False), 6, 0.6)
+    dw = P.generate_weights(cfg_d, 42, tied_head=False)       # an unrelated draft: many rejections
+    prompt = np.random.default_rng(5).integers(1, 24, 80).tolist()
+    spec = P.SpecConfig(target_len=81, gamma1=2, gamma2=4, temperature=temp, seed=0,
+                        streaming=P.StreamingConfig(n_sink=2, budget=16),
+                        retrieval=P.RetrievalConfig(chunk_size=4, budget=16))
+    base = P.HierarchicalSession(tw, dw, prompt, spec)
+    logits = base.full_lane.frontier_logits.double().cpu().numpy()
+    z = logits / temp
+    p = np.exp(z - z.max())
+    p /= p.sum()
+    n = 3000
+    counts = np.zeros(len(p))
+    for i in range(n):
+        s = base.clone()
+        out, _ = s.generate(seed=1000 + i)
+        counts[out[len(prompt)]] += 1
+    exp_ = n * p
+    big = exp_ >= 5
+    obs = np.append(counts[big], counts[~big].sum())
+    ex = np.append(exp_[big], exp_[~big].sum())
+    keep = ex > 0
+    stat = (((obs - ex) ** 2)[keep] / ex[keep]).sum()
+    dof = int(keep.sum()) - 1
+    assert chi2.sf(stat, dof) > 1e-4, (stat, dof, counts, exp_)
+
+
+def test_greedy_equals_autoregressive_many_pairs(P):
+    """Acceptance criterion 1 (tests/test_acceptance.py:36-58) at desk scale:
+    greedy two-level decoding emits exactly the autoregressive tokens for 30
+    (seed, prompt) pairs x retrieval budgets of 25 / 50 / 100 % of the
+    context, with a planted target so the draft is right often but not
+    always."""
+    cfg_t = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=32, d_ff=96, vocab_size=64, max_seq=256)
+    cfg_d = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=32, d_ff=64, vocab_size=64, max_seq=256)
+    mismatches = []
+    for i in range(30):
+        tw = P.plant_successor(P.generate_weights(cfg_t, 100 + i, tied_head=False), 3 + i, 0.8)
+        dw = P.plant_successor(P.generate_weights(cfg_d, 200 + i, tied_head=False), 3 + i, 0.8)
+        plen = 48 + 4 * i
+        prompt = np.random.default_rng(i).integers(1, 64, plen).tolist()
+        ar = P.autoregressive_generate(tw, prompt, plen + 24, 0.0, 0)
+        for frac in (0.25, 0.5, 1.0):
+            budget = max(8, int(frac * plen) // 4 * 4)
+            spec = P.SpecConfig(target_len=plen + 24, gamma1=2, gamma2=4, temperature=0.0, seed=i,
+                                streaming=P.StreamingConfig(n_sink=2, budget=16),
+                                retrieval=P.RetrievalConfig(chunk_size=4, budget=budget))
+            out, _ = P.hierarchical_generate(tw, dw, prompt, spec)
+            if out != ar:
+                mismatches.append((i, frac))
+    assert not mismatches, mismatches
