@@ -166,6 +166,15 @@ size_t hs_forward_topk_workspace_bytes(const HsModel *m, int n_view, int budget)
 int hs_forward_topk(const HsModel *m, const HsCache *c, const HsStep *st, int budget, const int32_t *tokens,
                     float *logits, float *q_stash, void *workspace, size_t workspace_bytes, void *stream);
 
+/* hs_forward on a slotted cache that also reports the attention feedback of
+ * H2OCache.observe_attention (caches.py:335-345, model.py:306-307): probs
+ * [L][t][n_view] fp64 = per query row, the softmax probabilities over the
+ * exposed slots summed over all heads (0 for invisible slots), with the
+ * reference's rounding points; head_scratch [t][H][n_view] fp32.           */
+int hs_forward_attn_probs(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
+                          float *logits, float *q_stash, double *probs, float *head_scratch, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
 /* ---- batched prefill (model.py:334-354) --------------
  * Same contract as hs_forward for an unsharded cache, for long prompts: the
  * dense projections run as tensor-core GEMMs (cuBLAS, three bf16 GEMMs over

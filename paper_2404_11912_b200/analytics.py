@@ -5,10 +5,9 @@ the GPU counterpart of hierspec/analytics.py:229-309 (`AcceptanceStats`,
 Pairings: 'hierarchical' (draft model + StreamingCache speculated against
 the retrieval-cache target, verified on the full cache; both levels are
 reported) and the self-speculation pairings 'self:streaming',
-'self:retrieval' and 'self:topk' (SingleLevelSession against the full cache;
-TopK selects per layer and query on the device, csrc/topk.cu).  'self:h2o'
-needs per-query attention probabilities fed back into the cache and is
-outside this build: it raises ContractError.
+'self:retrieval', 'self:topk' and 'self:h2o' (SingleLevelSession against the
+full cache; TopK selects per layer and query on the device, csrc/topk.cu;
+H2O feeds back the forward's attention probabilities, csrc/h2o.cu).
 The rest of the reference's analytics module (attention-mass recovery,
 needle fixtures, the speedup model) is host-side analysis, not decode work.
 """
@@ -18,8 +17,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
-from .caches import H2OConfig, RetrievalCache, RetrievalConfig, StreamingCache, StreamingConfig, TopKCache
-from .errors import ContractError
+from .caches import H2OCache, H2OConfig, RetrievalCache, RetrievalConfig, StreamingCache, StreamingConfig, TopKCache
 from .model import ModelConfig, ModelWeights
 from .speculation import HierarchicalSession, LevelStats, SingleLevelSession, SpecConfig
 
@@ -57,8 +55,7 @@ def _draft_cache_for(pairing: str, config: ModelConfig, *, streaming: StreamingC
     if kind == "topk":
         return TopKCache.from_config(config, topk_budget)
     if kind == "h2o":
-        raise ContractError(f"pairing {pairing!r} needs attention-probability feedback into the cache; "
-                            "out of scope for the device path (SURVEY.md §2.1)")
+        return H2OCache.from_config(config, h2o)
     raise ValueError(f"unknown pairing {pairing!r}")
 
 

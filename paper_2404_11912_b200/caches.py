@@ -275,6 +275,120 @@ class FullCache(KVCache):
         self._n = [self.frontier] * self.n_layers
 
 
+class H2OCache(KVCache):
+    """Heavy-hitter eviction (caches.py:291-396): per layer, cumulative
+    attention probabilities summed across heads; at commit the lowest-score
+    committed entry outside the recent window is evicted (ties to the oldest
+    position) until the committed set fits the budget.  Scores earned by
+    speculative queries stay pending until the query's position commits.
+
+    Device layout: a slotted cache with slot == position (entries are never
+    moved; an evicted entry's position becomes -1, so the attention kernels
+    skip it).  The probabilities come from hs_forward_attn_probs (csrc/h2o.cu)
+    with the reference's rounding points; the pending / score / eviction
+    bookkeeping is host logic over them, as in the reference."""
+
+    policy = "h2o"
+    wants_attention = True
+    kind = HS_KV_SLOTTED
+
+    def __init__(self, n_layers: int, n_kv_heads: int, head_dim: int, config: H2OConfig, max_entries: int = 4096):
+        super().__init__(n_layers, n_kv_heads, head_dim, max_entries, with_pos=True)
+        self.config = config
+        self.max_entries = max_entries
+        self._alive = np.zeros((n_layers, max_entries), dtype=bool)
+        self._scores = np.zeros((n_layers, max_entries), dtype=np.float64)
+        self._pending = [[] for _ in range(n_layers)]
+
+    @classmethod
+    def from_config(cls, model_config, config: H2OConfig):
+        return cls(model_config.n_layers, model_config.n_kv_heads, model_config.head_dim, config,
+                   model_config.max_seq)
+
+    def _step(self, t):
+        if self.frontier + t > self.max_entries:
+            raise CapacityError(f"h2o cache overflow past {self.max_entries}")
+        s = HsStep()
+        s.pos0 = self.frontier
+        s.append_mode = HS_APPEND_LINEAR
+        s.append_base = self.frontier
+        s.n_view = self.frontier + t
+        s.split = STREAM_SPLIT
+        return s
+
+    def _advance(self, t):
+        a, b = self.frontier, self.frontier + t
+        self._alive[:, a:b] = True
+        self._scores[:, a:b] = 0.0
+        self.frontier = b
+
+    def observe_forward(self, pos0: int, probs: np.ndarray) -> None:
+        """probs [L][t][n_view]: each new query row's head-summed attention
+        probabilities over the exposed slots (H2OCache.observe_attention)."""
+        t = probs.shape[1]
+        for li in range(self.n_layers):
+            slots = np.nonzero(self._alive[li, :probs.shape[2]])[0]
+            for i in range(t):
+                self._pending[li].append((pos0 + i, slots, probs[li, i, slots].copy()))
+
+    def expose(self, layer, queries=None):
+        slots = np.nonzero(self._alive[layer, :self.frontier])[0]
+        K, V = self._gather_host(layer, slots)
+        return K, V, slots.astype(np.int64), None
+
+    def rollback_to(self, n):
+        if n < self.committed:
+            raise ContractError(f"h2o cache cannot roll below committed {self.committed}")
+        if n < self.frontier:
+            self._alive[:, n:self.frontier] = False
+            self.pos[:, n:self.frontier] = -1
+        for li in range(self.n_layers):
+            self._pending[li] = [p for p in self._pending[li] if p[0] < n]
+        self.frontier = min(self.frontier, n)
+
+    def commit(self, n):
+        self._check_commit(n)
+        self.committed = n
+        cfg = self.config
+        dead = []
+        for li in range(self.n_layers):
+            alive, scores = self._alive[li], self._scores[li]
+            keep = []
+            for qpos, slots, w in self._pending[li]:
+                if qpos >= n:
+                    keep.append((qpos, slots, w))
+                    continue
+                ok = alive[slots]
+                scores[slots[ok]] += w[ok]
+            self._pending[li] = keep
+            while True:   # caches.py:374-388
+                pos = np.nonzero(alive[:self.frontier])[0]
+                comm = pos[pos < n]
+                if comm.size <= cfg.budget:
+                    break
+                recent_cut = comm[-cfg.recent_window] if cfg.recent_window else n
+                cand = comm[comm < recent_cut]
+                victim = cand[np.lexsort((cand, scores[cand]))[0]]
+                alive[victim] = False
+                dead.append((li, victim))
+        if dead:
+            idx = torch.as_tensor(np.asarray(dead, dtype=np.int64).T, device=self.pos.device)
+            self.pos[idx[0], idx[1]] = -1
+
+    def cumulative_scores(self, layer: int) -> dict:
+        slots = np.nonzero(self._alive[layer, :self.frontier])[0]
+        return {int(p): float(self._scores[layer, p]) for p in slots}
+
+    def clone(self):
+        c = H2OCache(self.n_layers, self.n_kv_heads, self.head_dim, self.config, self.max_entries)
+        check(lib.hs_cache_copy(c._ref, self._ref, self.frontier, stream_ptr()))
+        c._alive = self._alive.copy()
+        c._scores = self._scores.copy()
+        c._pending = [[(q, s.copy(), w.copy()) for q, s, w in pl] for pl in self._pending]
+        c.frontier, c.committed = self.frontier, self.committed
+        return c
+
+
 class TopKCache(FullCache):
     """Oracle upper bound (caches.py:568-652): keeps every position like the
     full cache and, for each single-query decode, each layer attends only

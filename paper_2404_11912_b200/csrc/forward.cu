@@ -26,6 +26,8 @@ size_t attention_ws(int t, int H, int DH, int n_view, int split);
 size_t topk_ws_bytes(const HsModel *m, int n, int budget);
 int launch_topk_attention(const HsModel *m, const HsCache *c, int layer, int n, int pos, int budget, const float *q,
                           uint16_t *xs, int ldxs, void *ws, size_t ws_bytes, cudaStream_t st);
+int launch_h2o_probs(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int n, double *probs,
+                     float *hp, cudaStream_t st);
 
 // ---- error state -------------------------------------------------------------
 static thread_local char g_err[512] = "";
@@ -166,7 +168,8 @@ extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
 
 static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                         const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
-                        size_t workspace_bytes, void *stream, int topk_budget);
+                        size_t workspace_bytes, void *stream, int topk_budget, double *probs = nullptr,
+                        float *hprobs = nullptr);
 
 extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                           const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
@@ -188,9 +191,22 @@ extern "C" int hs_forward_topk(const HsModel *m, const HsCache *c, const HsStep 
   return forward_impl(m, c, st, nullptr, tokens, 1, logits, q_stash, workspace, workspace_bytes, stream, budget);
 }
 
+// one forward that also reports, per layer, every query row's attention
+// probabilities over the exposed slots summed over heads (model.py:306-307,
+// H2OCache.observe_attention): probs [L][t][n_view] fp64, head_scratch
+// [t][H][n_view] fp32
+extern "C" int hs_forward_attn_probs(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens,
+                                     int t, float *logits, float *q_stash, double *probs, float *head_scratch,
+                                     void *workspace, size_t workspace_bytes, void *stream) {
+  HS_REQUIRE(probs != nullptr && head_scratch != nullptr, HS_ERR_VALUE, "forward: null probability buffers");
+  HS_REQUIRE(c->kind == HS_KV_SLOTTED, HS_ERR_VALUE, "forward: attention probabilities need a slotted cache");
+  return forward_impl(m, c, st, nullptr, tokens, t, logits, q_stash, workspace, workspace_bytes, stream, 0, probs,
+                      head_scratch);
+}
+
 static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                         const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
-                        size_t workspace_bytes, void *stream, int topk_budget) {
+                        size_t workspace_bytes, void *stream, int topk_budget, double *probs, float *hprobs) {
   using namespace hs;
   HS_REQUIRE(t >= 1, HS_ERR_VALUE, "empty token sequence");
   HS_REQUIRE(c->n_layers == m->n_layers && c->n_kv_heads == m->n_kv_heads && c->head_dim == m->head_dim,
@@ -258,6 +274,9 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
         HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, nullptr, nullptr, w.att_ws, w.att_bytes, s, w.xa,
                                       m->ld_d, clean_hi));
       }
+      if (probs)
+        HS_TRY(launch_h2o_probs(c, l, H, w.q, t, st->pos0, st->n_view, probs + (size_t)l * t * st->n_view, hprobs,
+                                s));
       GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq};
       HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo));
       GemvNorm in_gu = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
@@ -300,6 +319,8 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     } else {
       HS_TRY(launch_attention_timed(c, l, st, H, w.q, t, w.attn, nullptr, w.att_ws, w.att_bytes, s, nullptr, 0, clean_hi));
     }
+    if (probs)
+      HS_TRY(launch_h2o_probs(c, l, H, w.q, t, st->pos0, st->n_view, probs + (size_t)l * t * st->n_view, hprobs, s));
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
       float *xr = w.x + (size_t)r0 * d;

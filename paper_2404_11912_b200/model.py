@@ -486,6 +486,24 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
         if recorder is not None:
             recorder.query_position = cache.frontier - 1
         return out
+    if getattr(cache, "wants_attention", False):
+        # H2OCache: the forward also reports each query row's head-summed
+        # attention probabilities (model.py:306-307), fed to the eviction policy
+        for a, b in cache._batches(t):
+            step = cache._step(b - a)
+            nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split, 0)
+            ws = dm.workspace(nbytes)
+            probs = torch.zeros((cfg.n_layers, b - a, step.n_view), dtype=torch.float64, device=tok.device)
+            hp = torch.empty((b - a, cfg.n_heads, step.n_view), dtype=torch.float32, device=tok.device)
+            check(lib.hs_forward_attn_probs(dm.ref, cache._ref, C.byref(step), ptr(tok) + 4 * a, b - a,
+                                            ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(probs), ptr(hp),
+                                            ptr(ws), nbytes, stream_ptr()))
+            pos0 = cache.frontier
+            cache._advance(b - a)
+            cache.observe_forward(pos0, probs.cpu().numpy())
+        if recorder is not None:
+            recorder.query_position = cache.frontier - 1
+        return out
     for a, b in cache._batches(t):
         step = cache._step(b - a)
         nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split, world)

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from ._abi import check, lib, status_error
-from .caches import (FullCache, KVCache, RetrievalCache, RetrievalConfig, RollingAcceptance, StreamingCache,
+from .caches import (FullCache, H2OCache, KVCache, RetrievalCache, RetrievalConfig, RollingAcceptance, StreamingCache,
                      StreamingConfig, should_rebuild)
 from .errors import ContractError
 from .model import ForwardRecorder, ModelWeights, forward_device
@@ -667,13 +667,12 @@ class SingleLevelSession:
     """One draft lane speculated against one full-cache verify lane --
     standard speculative decoding, the acceptance-measurement pairing of
     speculation.py:401-477.  The draft cache is a StreamingCache (own draft
-    model or self-speculation), a FullCache or TopKCache, or a RetrievalCache,
-    which is built from (and rebuilt against) the verify lane's full cache
-    and so requires the verify weights (self-speculation).  Runs on the same
-    device round machinery as HierarchicalSession: tokens, distributions and
-    uniforms stay resident, one host read-back per round.  H2O draft caches
-    need per-query attention probabilities and stay out of scope
-    (SURVEY.md §2.1)."""
+    model or self-speculation), a FullCache, TopKCache or H2OCache, or a
+    RetrievalCache, which is built from (and rebuilt against) the verify
+    lane's full cache and so requires the verify weights (self-speculation).
+    Runs on the same device round machinery as HierarchicalSession: tokens,
+    distributions and uniforms stay resident, one host read-back per round
+    (an H2O draft also reads back its attention probabilities)."""
 
     def __init__(self, draft_weights: ModelWeights, draft_cache: KVCache, verify_weights: ModelWeights,
                  prefix: Sequence[int], gamma: int, temperature: float,
@@ -682,9 +681,9 @@ class SingleLevelSession:
             raise ContractError("draft and verify models must share a vocabulary")
         if gamma < 1:
             raise ValueError("gamma must be >= 1")
-        if not isinstance(draft_cache, (FullCache, StreamingCache, RetrievalCache)):
+        if not isinstance(draft_cache, (FullCache, StreamingCache, RetrievalCache, H2OCache)):
             raise ContractError(f"draft cache {type(draft_cache).__name__} is not supported on the device path "
-                                "(the H2O pairing is out of scope, SURVEY.md §2.1)")
+                                "(full, streaming, retrieval, top-k or H2O caches)")
         self.gamma = gamma
         self.temperature = temperature
         self.committed = list(prefix)

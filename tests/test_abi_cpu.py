@@ -76,8 +76,7 @@ def test_streaming_watermark_matches_oracle_eviction():
 
 def test_measure_acceptance_pairing_errors():
     """Pairing validation happens before any device work
-    (analytics.py:296-300): unknown names raise ValueError, the
-    attention-feedback pairing (H2O) is out of scope on the device path."""
+    (analytics.py:296-300): unknown names raise ValueError."""
     import paper_2404_11912_b200 as P
     cfg = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=8, d_ff=16, vocab_size=16, max_seq=32)
     w = P.generate_weights(cfg, 1)
@@ -85,6 +84,4 @@ def test_measure_acceptance_pairing_errors():
         P.measure_acceptance("self:nope", w, [[1, 2, 3]])
     with pytest.raises(ValueError):
         P.measure_acceptance("hierarchical", w, [[1, 2, 3]])
-    with pytest.raises(P.ContractError):
-        P.measure_acceptance("self:h2o", w, [[1, 2, 3]])
     assert P.AcceptanceStats("x").rate == 0.0

@@ -49,6 +49,8 @@ def _draft_cache(P, kind, cfg, kw):
         return P.FullCache.from_config(cfg)
     if kind == "topk":
         return P.TopKCache.from_config(cfg, kw["budget"])
+    if kind == "h2o":
+        return P.H2OCache.from_config(cfg, P.H2OConfig(**kw))
     if kind == "stream":
         return P.StreamingCache.from_config(cfg, P.StreamingConfig(**kw))
     return P.RetrievalCache.from_config(cfg, P.RetrievalConfig(**kw))
@@ -66,6 +68,13 @@ def test_single_level_sessions_match_reference(P, golden_single, needle):
         tag = f"single/{c['name']}/bf16"
         assert out == data[tag + "/tokens"].tolist(), c["name"]
         assert [st.rounds, st.proposed, st.accepted] == data[tag + "/stats"].tolist(), c["name"]
+        if c["kind"] == "h2o":   # the surviving entries (exact) and their heavy-hitter scores (the
+            # probabilities come from our forward's fp32 q, so they agree to ~1e-6 relative), per layer
+            for li in range(dw.config.n_layers):
+                assert cache.exposed_positions(li).tolist() == data[tag + f"/exposed{li}"].tolist(), (c["name"], li)
+                sc = cache.cumulative_scores(li)
+                got = np.array([sc[p] for p in sorted(sc)])
+                assert np.allclose(got, data[tag + f"/scores{li}"], rtol=1e-5, atol=1e-9), (c["name"], li)
 
 
 def test_needle_acceptance_matches_reference_and_orders_pairings(P, golden_single, needle):
@@ -78,9 +87,10 @@ def test_needle_acceptance_matches_reference_and_orders_pairings(P, golden_singl
     m = meta["needle"]
     kw = dict(gamma=m["gamma"], temperature=m["temperature"], gen_tokens=m["gen_tokens"], seed=m["seed"],
               streaming=P.StreamingConfig(n_sink=m["n_sink"], budget=m["budget"]),
-              retrieval=P.RetrievalConfig(chunk_size=m["chunk_size"], budget=m["budget"]), topk_budget=m["budget"])
+              retrieval=P.RetrievalConfig(chunk_size=m["chunk_size"], budget=m["budget"]), topk_budget=m["budget"],
+              h2o=P.H2OConfig(budget=m["budget"], recent_window=m["h2o_recent_window"]))
     rates = {}
-    for kind in ("retrieval", "streaming", "topk"):
+    for kind in ("retrieval", "streaming", "topk", "h2o"):
         st = P.measure_acceptance("self:" + kind, target, prompts, **kw)["self"]
         tag = f"needle/bf16/{kind}"
         assert [st.rounds, st.proposed, st.accepted] == data[tag + "/stats"].tolist(), kind
