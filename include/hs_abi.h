@@ -175,6 +175,14 @@ int hs_forward_attn_probs(const HsModel *m, const HsCache *c, const HsStep *st, 
                           float *logits, float *q_stash, double *probs, float *head_scratch, void *workspace,
                           size_t workspace_bytes, void *stream);
 
+/* hs_forward (unsharded) that also records the attention probe of
+ * ForwardRecorder(record_probs=True) (model.py:308-312): probe
+ * [L][H][n_view] fp32 = per layer and head, the last query row's softmax
+ * probabilities over the view's slots (0 where a slot is not visible).     */
+int hs_forward_probe(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
+                     float *logits, float *q_stash, float *probe, void *workspace, size_t workspace_bytes,
+                     void *stream);
+
 /* ---- batched prefill (model.py:334-354) --------------
  * Same contract as hs_forward for an unsharded cache, for long prompts: the
  * dense projections run as tensor-core GEMMs (cuBLAS, three bf16 GEMMs over

@@ -28,6 +28,8 @@ int launch_topk_attention(const HsModel *m, const HsCache *c, int layer, int n, 
                           uint16_t *xs, int ldxs, void *ws, size_t ws_bytes, cudaStream_t st);
 int launch_h2o_probs(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int n, double *probs,
                      float *hp, cudaStream_t st);
+int launch_probe_probs(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *probe,
+                       cudaStream_t s);
 
 // ---- error state -------------------------------------------------------------
 static thread_local char g_err[512] = "";
@@ -169,7 +171,7 @@ extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
 static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                         const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
                         size_t workspace_bytes, void *stream, int topk_budget, double *probs = nullptr,
-                        float *hprobs = nullptr);
+                        float *hprobs = nullptr, float *probe = nullptr);
 
 extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                           const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
@@ -204,9 +206,21 @@ extern "C" int hs_forward_attn_probs(const HsModel *m, const HsCache *c, const H
                       head_scratch);
 }
 
+// hs_forward that also records, per layer and head, the last query row's
+// attention probabilities over the view (ForwardRecorder(record_probs=True),
+// model.py:308-312): probe [L][H][n_view] fp32, 0 for invisible slots
+extern "C" int hs_forward_probe(const HsModel *m, const HsCache *c, const HsStep *st, const int32_t *tokens, int t,
+                                float *logits, float *q_stash, float *probe, void *workspace, size_t workspace_bytes,
+                                void *stream) {
+  HS_REQUIRE(probe != nullptr, HS_ERR_VALUE, "forward: null probe buffer");
+  return forward_impl(m, c, st, nullptr, tokens, t, logits, q_stash, workspace, workspace_bytes, stream, 0, nullptr,
+                      nullptr, probe);
+}
+
 static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                         const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
-                        size_t workspace_bytes, void *stream, int topk_budget, double *probs, float *hprobs) {
+                        size_t workspace_bytes, void *stream, int topk_budget, double *probs, float *hprobs,
+                        float *probe) {
   using namespace hs;
   HS_REQUIRE(t >= 1, HS_ERR_VALUE, "empty token sequence");
   HS_REQUIRE(c->n_layers == m->n_layers && c->n_kv_heads == m->n_kv_heads && c->head_dim == m->head_dim,
@@ -277,6 +291,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       if (probs)
         HS_TRY(launch_h2o_probs(c, l, H, w.q, t, st->pos0, st->n_view, probs + (size_t)l * t * st->n_view, hprobs,
                                 s));
+      if (probe) HS_TRY(launch_probe_probs(c, l, st, H, w.q, t, probe + (size_t)l * H * st->n_view, s));
       GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq};
       HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo));
       GemvNorm in_gu = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
@@ -321,6 +336,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     }
     if (probs)
       HS_TRY(launch_h2o_probs(c, l, H, w.q, t, st->pos0, st->n_view, probs + (size_t)l * t * st->n_view, hprobs, s));
+    if (probe) HS_TRY(launch_probe_probs(c, l, st, H, w.q, t, probe + (size_t)l * H * st->n_view, s));
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
       float *xr = w.x + (size_t)r0 * d;

@@ -27,7 +27,7 @@ import torch
 
 from . import _abi
 from ._abi import HsModel, check, lib
-from .errors import CapacityError, FiniteError, ShapeError
+from .errors import CapacityError, ContractError, FiniteError, ShapeError
 from .runtime import STATS, as_device_f32, as_device_f64, device, ptr, stream_ptr, to_i32_device, workspaces
 
 BOS = 256
@@ -402,15 +402,17 @@ class AttentionProbe:
 class ForwardRecorder:
     """Last-row post-RoPE queries of the most recent forward, per layer
     (model.py:222-233).  Kept on the device ([L, H, dh] fp32) so the
-    retrieval builder reads it without a host round trip."""
+    retrieval builder reads it without a host round trip.  record_probs=True
+    also records each head's post-softmax attention row of the last query and
+    the positions it spans (hs_forward_probe, csrc/h2o.cu) for
+    attention_probe and the recovery analytics."""
 
     def __init__(self, record_probs: bool = False):
-        if record_probs:
-            raise NotImplementedError("attention-probe recording belongs to the analytics harness "
-                                      "(out of scope for the decode hot path)")
-        self.record_probs = False
+        self.record_probs = record_probs
         self.stash: Optional[torch.Tensor] = None
         self.query_position = -1
+        self._probs: list = []
+        self.positions: list = []
 
     def _buffer(self, cfg: ModelConfig) -> torch.Tensor:
         shape = (cfg.n_layers, cfg.n_heads, cfg.head_dim)
@@ -427,7 +429,24 @@ class ForwardRecorder:
 
     @property
     def last_probs(self) -> list:
-        return []
+        return self._probs
+
+    def _record(self, cache, step, probe: torch.Tensor) -> None:
+        """probe [L][H][n_view] over the view's slots -> per layer the
+        visible entries' positions and [H][n] weights (slot order)."""
+        host = probe.cpu().numpy()
+        n = step.n_view
+        qp = step.pos0 + self.query_t - 1
+        self._probs, self.positions = [], []
+        pos_all = cache.pos[:, :n].cpu().numpy() if cache.pos is not None else None
+        for li in range(host.shape[0]):
+            kp = pos_all[li] if pos_all is not None else np.arange(n) + step.pos_base
+            vis = (kp >= 0) & (kp <= qp)
+            if step.window:
+                lo = max(qp - step.window + 1, step.win_lo)
+                vis &= (kp < step.n_sink) | (kp >= lo)
+            self.positions.append(kp[vis].astype(np.int64))
+            self._probs.append(host[li][:, vis].astype(np.float32))
 
 
 PREFILL_MIN_ROWS = 64   # prompts at least this long take the GEMM prefill (hs_prefill)
@@ -459,6 +478,8 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
     shards = getattr(cache, "shards", None)
     shard_ref = shards.ref if shards is not None else None
     world = shards.world if shards is not None else 0
+    if recorder is not None and recorder.record_probs:
+        return _forward_probe(weights, dm, tok, t, cache, recorder, out, stash, prefill)
     if (prefill and t >= PREFILL_MIN_ROWS and cache.kind == _abi.HS_KV_LINEAR
             and (shards is None or cfg.head_dim == 128)):
         step = cache._step(t)
@@ -517,6 +538,31 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
     return out
 
 
+def _forward_probe(weights, dm, tok, t, cache, recorder, out, stash, prefill):
+    """forward_device with an attention probe of the last row: the rows before
+    it take the usual path (GEMM prefill when long), the last one
+    hs_forward_probe (model.py:308-312)."""
+    if getattr(cache, "shards", None) is not None or getattr(cache, "policy", "") in ("topk", "h2o"):
+        raise ContractError("attention probes need an unsharded full, streaming or retrieval cache")
+    cfg = dm.config
+    if t > 1:
+        plain = ForwardRecorder()
+        plain.stash = recorder.stash
+        forward_device(weights, tok[:t - 1], cache, plain, out=out[:t - 1], prefill=prefill)
+    step = cache._step(1)
+    nbytes = lib.hs_forward_workspace_bytes(dm.ref, 1, step.n_view, step.split, 0)
+    ws = dm.workspace(nbytes)
+    probe = torch.zeros((cfg.n_layers, cfg.n_heads, step.n_view), dtype=torch.float32, device=tok.device)
+    check(lib.hs_forward_probe(dm.ref, cache._ref, C.byref(step), ptr(tok) + 4 * (t - 1), 1,
+                               ptr(out) + 4 * (t - 1) * cfg.vocab_size, ptr(stash), ptr(probe), ptr(ws), nbytes,
+                               stream_ptr()))
+    recorder.query_t = 1
+    recorder._record(cache, step, probe)
+    cache._advance(1)
+    recorder.query_position = cache.frontier - 1
+    return out
+
+
 def _host_rows(logits: torch.Tensor) -> np.ndarray:
     host = logits.cpu().numpy()
     if not np.isfinite(host).all():
@@ -559,4 +605,13 @@ def decode_chunk(weights: ModelWeights, tokens: Sequence[int], cache,
 
 
 def attention_probe(recorder: ForwardRecorder, layer: int, head: int) -> AttentionProbe:
-    raise ValueError("recorder has no recorded attention (probes are an analytics feature, out of scope)")
+    """One head's attention row from a recorded forward (model.py:381-393)."""
+    if not recorder.record_probs or not recorder.last_probs:
+        raise ValueError("recorder has no recorded attention (pass record_probs=True)")
+    if not 0 <= layer < len(recorder.last_probs):
+        raise IndexError(f"layer {layer} out of range")
+    row = recorder.last_probs[layer]
+    if not 0 <= head < row.shape[0]:
+        raise IndexError(f"head {head} out of range")
+    return AttentionProbe(layer=layer, head=head, query_position=recorder.query_position,
+                          positions=recorder.positions[layer], weights=row[head])

@@ -143,3 +143,51 @@ def test_single_level_contract_errors(P, needle):
     s = P.SingleLevelSession(target, P.FullCache.from_config(target.config), target, prompts[0][:10], 2, 0.0)
     with pytest.raises(ValueError):
         s.generate(10)
+
+
+def test_attention_probe_matches_bruteforce(P):
+    """ForwardRecorder(record_probs=True) / attention_probe (model.py:208-243,
+    381-393) against an fp64 softmax recomputed from the recorded post-RoPE
+    query and the cached bf16 keys; full and StreamingLLM caches."""
+    cfg = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=32, d_ff=96, vocab_size=64, max_seq=256)
+    w = P.generate_weights(cfg, 17)
+    prompt = np.random.default_rng(3).integers(1, 64, 90).tolist()
+    for cache in (P.FullCache.from_config(cfg), P.StreamingCache.from_config(cfg, P.StreamingConfig(n_sink=4,
+                                                                                                     budget=24))):
+        rec = P.ForwardRecorder(record_probs=True)
+        P.prefill(w, prompt, cache, rec)
+        qs = rec.last_queries
+        for li in range(cfg.n_layers):
+            for h in range(cfg.n_heads):
+                pr = P.attention_probe(rec, li, h)
+                assert pr.query_position == len(prompt) - 1
+                assert abs(float(pr.weights.sum()) - 1.0) < 1e-5
+                kv = h // (cfg.n_heads // cfg.n_kv_heads)
+                if cache.kind == 0:
+                    slots = pr.positions
+                else:
+                    pos = cache.pos[li].cpu().numpy()
+                    slots = np.array([int(np.nonzero(pos == p)[0][0]) for p in pr.positions])
+                K = cache.k[li, kv, torch.as_tensor(slots, device="cuda")].float().cpu().numpy().astype(np.float64)
+                s = K @ qs[li][h].astype(np.float64) / np.sqrt(cfg.head_dim)
+                ref = np.exp(s - s.max())
+                ref /= ref.sum()
+                assert np.abs(pr.weights - ref).max() < 1e-6, (type(cache).__name__, li, h)
+            if cache.kind == 1:   # StreamingLLM exposure: the 4 sinks + the last budget - sinks = 20 positions
+                assert sorted(rec.positions[li].tolist()) == list(range(4)) + list(range(len(prompt) - 20,
+                                                                                         len(prompt)))
+    with pytest.raises(ValueError):
+        P.attention_probe(P.ForwardRecorder(), 0, 0)
+
+
+def test_recovery_analytics_match_reference(P, golden_single, needle):
+    """sparsity_recovery / locality_recovery (analytics.py:36-106) on the
+    planted-needle model against the reference's own values."""
+    data, meta = golden_single
+    target, _, prompts = needle
+    m = meta["recovery"]
+    sp = P.sparsity_recovery(target, prompts[m["sparsity_prompt"]], m["sparsity_budget"])
+    assert np.allclose(sp, data["recovery/bf16/sparsity"], rtol=1e-4, atol=1e-5)
+    lc = P.locality_recovery(target, prompts[m["locality_prompt"]], m["locality_budget"], horizon=m["horizon"])
+    assert np.allclose(lc.frozen, data["recovery/bf16/frozen"], rtol=1e-4, atol=1e-5)
+    assert np.allclose(lc.fresh, data["recovery/bf16/fresh"], rtol=1e-4, atol=1e-5)
