@@ -473,7 +473,7 @@ int gemv_tc_ksplit(int N, int nkb) {
   }
   constexpr int SMS = 148;
   int ks = (SMS + tiles - 1) / tiles;
-  const int cap = nkb / 4 < 16 ? nkb / 4 : 16;
+  const int cap = nkb / 4 < 8 ? nkb / 4 : 8;   // <= 8: the split CTAs of a tile fit one (portable) cluster
   if (ks > cap) ks = cap;
   return ks < 1 ? 1 : ks;
 }
