@@ -325,7 +325,8 @@ size_t attention_ws(int t, int H, int DH, int n_view, int split) {
 }
 
 int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *part_m,
-                        float *part_l, float *part_o, int n_splits, cudaStream_t stream, int clean_hi);
+                        float *part_l, float *part_o, int n_splits, cudaStream_t stream, int clean_hi,
+                        const FusedRope *fr);
 
 // ---- live timing of the dominant kernel (bench.py roofline) --------------------
 // When enabled, every attention launch over a view of >= min_view keys is
@@ -347,13 +348,13 @@ static ProfPair *prof_begin(const HsCache *c, const HsStep *st, cudaStream_t str
 
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
                      float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
-                     uint16_t *xs = nullptr, int ldxs = 0, int clean_hi = -1);
+                     uint16_t *xs = nullptr, int ldxs = 0, int clean_hi = -1, const FusedRope *fr = nullptr);
 
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
                            float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
-                           uint16_t *xs, int ldxs, int clean_hi) {
+                           uint16_t *xs, int ldxs, int clean_hi, const FusedRope *fr) {
   ProfPair *p = prof_begin(c, st, stream);
-  const int rc = launch_attention(c, layer, st, H, q, t, out, packed, ws, ws_bytes, stream, xs, ldxs, clean_hi);
+  const int rc = launch_attention(c, layer, st, H, q, t, out, packed, ws, ws_bytes, stream, xs, ldxs, clean_hi, fr);
   if (p) cudaEventRecord(p->b, stream);
   return rc;
 }
@@ -367,7 +368,7 @@ int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H,
 // griddepcontrol.wait
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t,
                      float *out, float *packed, void *ws, size_t ws_bytes, cudaStream_t stream,
-                     uint16_t *xs, int ldxs, int clean_hi) {
+                     uint16_t *xs, int ldxs, int clean_hi, const FusedRope *fr) {
   const int DH = c->head_dim, KVH = c->n_kv_heads;
   HS_REQUIRE(H % KVH == 0, HS_ERR_SHAPE, "attention: H %% KVH != 0");
   HS_REQUIRE(st->split > 0 && st->split % ATT_TILE == 0, HS_ERR_VALUE, "attention: split must be a multiple of %d", ATT_TILE);
@@ -399,6 +400,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
   }
   // head_dim 128 (the Llama-family targets) runs on the tensor cores; the
   // small-head draft model and the test-size models use the CUDA-core kernel
+  HS_REQUIRE(fr == nullptr || DH == 128, HS_ERR_VALUE, "attention: fused RoPE needs head_dim 128");
   cudaError_t le = cudaSuccess;
   switch (DH) {
     case 8: le = launch_pdl(attn_partial_kernel<8>, grid, dim3(ATT_THREADS), 0, stream, a); break;
@@ -409,7 +411,7 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
       HS_REQUIRE(st->split % 128 == 0, HS_ERR_VALUE, "attention: split must be a multiple of 128 for head_dim 128");
       HS_REQUIRE(st->dyn == nullptr, HS_ERR_VALUE, "attention: run-time positions need head_dim < 128");
       int rc = launch_attention_tc(c, layer, st, H, q, t, a.part_m, a.part_l, a.part_o, n_splits, stream,
-                                   clean_hi);
+                                   clean_hi, fr);
       if (rc != HS_OK) return rc;
       break;
     }

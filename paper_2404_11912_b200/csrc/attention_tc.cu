@@ -59,6 +59,16 @@ struct AttTcArgs {
   const int32_t *pos;   // layer [cap] or null
   int cap, layer, n_view, pos0, window, win_lo, n_sink, split, n_splits, n_qb, n_items, pos_base;
   int clean_hi;         // slots < clean_hi are not written by the preceding kernels (see launch_attention)
+  // fused RoPE + append (forward path, FusedRope): q and this step's K/V rows
+  // come straight from the qkv GEMV output; qkv == null: q given, rows appended
+  const float *qkv;
+  int ncols;
+  const float *rope_cos, *rope_sin;   // [max_seq][64] fp32
+  float *q_stash;                     // this layer's [H][128], or null
+  uint16_t *k_app, *v_app;            // this layer's cache rows [KVH][cap][128]
+  int32_t *pos_app;                   // slotted: this layer's pos [cap], else null
+  int app_mode, app_base, own_hi;     // HsStep append rule (positions or linear tail)
+  int dirty_lo, dirty_hi;             // slots this step appends
   float scale_log2;     // log2(e) / sqrt(dh)
   float *part_m, *part_l, *part_o;
 };
@@ -125,7 +135,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
   // pfull, ofull/ofree, qfull (per item).  Per-tile barriers alternate on
   // buffer b = g & 1 with phase (g >> 1) & 1.
   __shared__ uint64_t kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], sfree[2], pfull[2], ofull[2], ofree[2];
-  __shared__ uint64_t qfull;
+  __shared__ uint64_t qfull, dready;
   __shared__ uint32_t tmem_base;
   __shared__ int red[2][4][AT_QR];
   __shared__ float redl[4][AT_QR];
@@ -142,6 +152,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
       tc::mbar_init(&pfull[s], 8); tc::mbar_init(&ofull[s], 1); tc::mbar_init(&ofree[s], 8);
     }
     tc::mbar_init(&qfull, 8);
+    tc::mbar_init(&dready, 8);
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<128>(&tmem_base);   // S[b] at b*32, O[b] at 64 + b*32
@@ -179,14 +190,21 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         }
       }
       tc::grid_dep_wait();             // K/V rows appended by the previous kernel
-      uint32_t g = 0;
-      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+      uint32_t g = 0, nitem = 0;
+      for (int item = blockIdx.x; item < a.n_items; item += gridDim.x, ++nitem) {
         int split, kh, qb;
         item_coords(item, a, split, kh, qb);
         const int lo = split * a.split, hi = min(a.n_view, lo + a.split);
         const int row0 = (a.layer * a.KVH + kh) * a.cap;
-        for (int tile = lo; tile < hi; tile += AT_KT, ++g)
+        bool waited = false;
+        for (int tile = lo; tile < hi; tile += AT_KT, ++g) {
+          // fused append: the softmax warps write this step's rows first
+          if (a.qkv && !waited && tile < a.dirty_hi && tile + AT_KT > a.dirty_lo) {
+            tc::mbar_wait(&dready, nitem & 1);
+            waited = true;
+          }
           if (g > 0 || !pre) load_kv(g, row0 + tile);
+        }
       }
     }
     return;
@@ -273,14 +291,67 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
     // ---- stage the query split; zero both P buffers (rows >= nrows stay 0) ----------
     // (all S/P.V MMAs of the previous item completed: its tiles were all consumed)
     if (stid < AT_QR) qp_s[stid] = stid < nrows ? a.pos0 + (r0 + stid) / a.g : -1;
-    for (int e = stid; e < AT_QR * AT_DH; e += 256) {
-      const int rr = e >> 7, d = e & 127;
-      float v = 0.f;
-      if (rr < nrows) {
-        const int i = (r0 + rr) / a.g, head = kh * a.g + (r0 + rr) % a.g;
-        v = a.q[((size_t)i * a.H + head) * AT_DH + d];
+    if (a.qkv == nullptr) {
+      for (int e = stid; e < AT_QR * AT_DH; e += 256) {
+        const int rr = e >> 7, d = e & 127;
+        float v = 0.f;
+        if (rr < nrows) {
+          const int i = (r0 + rr) / a.g, head = kh * a.g + (r0 + rr) % a.g;
+          v = a.q[((size_t)i * a.H + head) * AT_DH + d];
+        }
+        split3_store(sQ, rr, d, v);
       }
-      split3_store(sQ, rr, d, v);
+    } else {
+      // RoPE of the query pairs (rope_append_kernel's fp64 rotation, model.py:235-244)
+      for (int e = stid; e < AT_QR * (AT_DH / 2); e += 256) {
+        const int rr = e >> 6, pr = e & 63;
+        float y0 = 0.f, y1 = 0.f;
+        if (rr < nrows) {
+          const int i = (r0 + rr) / a.g, head = kh * a.g + (r0 + rr) % a.g;
+          const int p = a.pos0 + i;
+          const float *row = a.qkv + (size_t)i * a.ncols + head * AT_DH + 2 * pr;
+          const double ev = (double)row[0], ov = (double)row[1];
+          const double cs = (double)a.rope_cos[(size_t)p * (AT_DH / 2) + pr];
+          const double sn = (double)a.rope_sin[(size_t)p * (AT_DH / 2) + pr];
+          y0 = (float)(ev * cs - ov * sn);
+          y1 = (float)(ev * sn + ov * cs);
+          if (a.q_stash && split == 0 && i == a.t - 1) {
+            a.q_stash[head * AT_DH + 2 * pr] = y0;
+            a.q_stash[head * AT_DH + 2 * pr + 1] = y1;
+          }
+        }
+        split3_store(sQ, rr, 2 * pr, y0);
+        split3_store(sQ, rr, 2 * pr + 1, y1);
+      }
+      // this step's K (rotated) and V rows of kv head kh that fall in the item's slots
+      if (lo < a.dirty_hi && hi > a.dirty_lo) {
+        for (int e = stid; e < a.t * (AT_DH / 2); e += 256) {
+          const int i = e >> 6, pr = e & 63;
+          const int p = a.pos0 + i;
+          int slot;
+          if (a.app_mode == HS_APPEND_POS)
+            slot = (p < a.pos_base || (a.own_hi > 0 && p >= a.own_hi)) ? -1 : p - a.pos_base;
+          else
+            slot = a.app_base + i;
+          if (slot < lo || slot >= hi) continue;
+          const float *row = a.qkv + (size_t)i * a.ncols;
+          const float *kr = row + (a.H + kh) * AT_DH + 2 * pr;
+          const double ev = (double)kr[0], ov = (double)kr[1];
+          const double cs = (double)a.rope_cos[(size_t)p * (AT_DH / 2) + pr];
+          const double sn = (double)a.rope_sin[(size_t)p * (AT_DH / 2) + pr];
+          uint16_t *kd = a.k_app + ((size_t)kh * a.cap + slot) * AT_DH + 2 * pr;
+          kd[0] = f_to_bf16((float)(ev * cs - ov * sn));
+          kd[1] = f_to_bf16((float)(ev * sn + ov * cs));
+          const float *vr = row + (a.H + a.KVH + kh) * AT_DH + 2 * pr;
+          uint16_t *vd = a.v_app + ((size_t)kh * a.cap + slot) * AT_DH + 2 * pr;
+          vd[0] = f_to_bf16(vr[0]);
+          vd[1] = f_to_bf16(vr[1]);
+          if (a.pos_app && pr == 0) a.pos_app[slot] = p;   // every reader of the slot writes it (same value)
+        }
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // the TMA reads these rows next
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&dready);
     }
     for (int e = stid; e < 2 * AT_OPND / 16; e += 256) reinterpret_cast<uint4 *>(sP)[e] = make_uint4(0, 0, 0, 0);
     tc::fence_async_smem();
@@ -429,7 +500,8 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
 }  // namespace
 
 int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *part_m,
-                        float *part_l, float *part_o, int n_splits, cudaStream_t stream, int clean_hi) {
+                        float *part_l, float *part_o, int n_splits, cudaStream_t stream, int clean_hi,
+                        const FusedRope *fr) {
   HS_REQUIRE(c->head_dim == AT_DH, HS_ERR_SHAPE, "attention_tc: head_dim must be 128");
   CUtensorMap mk, mv;
   const uint64_t rows = (uint64_t)c->n_layers * c->n_kv_heads * c->cap;
@@ -448,6 +520,26 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)AT_DH));
   a.part_m = part_m; a.part_l = part_l; a.part_o = part_o;
   a.clean_hi = clean_hi;
+  a.qkv = nullptr;
+  a.dirty_lo = a.dirty_hi = 0;
+  if (fr) {
+    HS_REQUIRE(st->append_mode == HS_APPEND_POS || st->append_mode == HS_APPEND_LINEAR, HS_ERR_VALUE,
+               "attention: fused RoPE needs a position or linear-tail append");
+    HS_REQUIRE(st->dyn == nullptr, HS_ERR_VALUE, "attention: fused RoPE needs host positions");
+    const size_t lay = (size_t)layer * c->n_kv_heads * c->cap * AT_DH;
+    a.qkv = fr->qkv; a.ncols = fr->ncols; a.rope_cos = fr->rope_cos; a.rope_sin = fr->rope_sin;
+    a.q_stash = fr->q_stash;
+    a.k_app = c->k + lay; a.v_app = c->v + lay;
+    a.pos_app = c->kind == HS_KV_SLOTTED ? c->pos + (size_t)layer * c->cap : nullptr;
+    a.app_mode = st->append_mode; a.app_base = st->append_base; a.own_hi = st->own_hi;
+    if (st->append_mode == HS_APPEND_POS) {
+      a.dirty_lo = st->pos0 - st->pos_base;
+      a.dirty_hi = a.dirty_lo + t;
+    } else {
+      a.dirty_lo = st->append_base;
+      a.dirty_hi = st->append_base + t;
+    }
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM);

@@ -18,7 +18,7 @@ int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int 
                        float *q_out, float *q_stash, cudaStream_t st);
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
                            float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs,
-                           int clean_hi = -1);
+                           int clean_hi = -1, const FusedRope *fr = nullptr);
 int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, uint16_t *xs, int ldxs, int H,
                        cudaStream_t st);
 int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
@@ -264,6 +264,10 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     // operand split(x * gain) and per-tile row sums of squares, the consumer
     // (wqkv, gate|up, lm_head) scales its result by 1 / rms -- so no split /
     // normalise kernel runs between the weight streams.
+    static const bool fused_rope_ok = getenv("HS_NO_FUSED_ROPE") == nullptr;   // A/B hook
+    const bool fuse_rope = fused_rope_ok && !sharded && topk_budget == 0 && probs == nullptr && probe == nullptr &&
+                           dh == 128 && st->dyn == nullptr &&
+                           (st->append_mode == HS_APPEND_POS || st->append_mode == HS_APPEND_LINEAR);
     HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
     HS_TRY(launch_norm_prep(w.x, d, t, d, m->attn_norm, w.xd, m->ld_d, w.ssq, s));
     for (int l = 0; l < m->n_layers; ++l) {
@@ -275,6 +279,14 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       GemvNorm in_qkv = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
       HS_TRY(launch_gemv_tc(w.xd, t, wqkv, m->ld_d, nqkv, 0, w.qkv, nqkv, nullptr, 0, w.gemv_ws, w.gemv_bytes, s,
                             &in_qkv));
+      if (fuse_rope) {
+        // RoPE + K/V append inside the tensor-core attention (its q staging
+        // reads the qkv rows; the CTA covering the appended slots writes them)
+        const FusedRope fr = {w.qkv, nqkv, m->rope_cos, m->rope_sin,
+                              q_stash ? q_stash + (size_t)l * H * dh : nullptr};
+        HS_TRY(launch_attention_timed(c, l, st, H, nullptr, t, nullptr, nullptr, w.att_ws, w.att_bytes, s, w.xa,
+                                      m->ld_d, clean_hi, &fr));
+      } else {
       HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
       if (sharded) {
         const size_t part = (size_t)t * H * (dh + 2) * 4;
@@ -292,6 +304,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
         HS_TRY(launch_h2o_probs(c, l, H, w.q, t, st->pos0, st->n_view, probs + (size_t)l * t * st->n_view, hprobs,
                                 s));
       if (probe) HS_TRY(launch_probe_probs(c, l, st, H, w.q, t, probe + (size_t)l * H * st->n_view, s));
+      }
       GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq};
       HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo));
       GemvNorm in_gu = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};

@@ -124,6 +124,15 @@ __device__ __forceinline__ float warp_max(float v) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// RoPE + append fused into the tensor-core attention (forward path): the
+// qkv GEMV output [t][ncols] and the model's fp32 rotation tables
+struct FusedRope {
+  const float *qkv;
+  int ncols;
+  const float *rope_cos, *rope_sin;
+  float *q_stash;   // this layer's [H][dh] slice of the recorder stash, or null
+};
+
 // programmatic dependent launch on/off (HS_NO_PDL=1 disables it: debugging aid)
 int pdl_enabled();
 

@@ -22,7 +22,7 @@ int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int 
                        float *q_out, float *q_stash, cudaStream_t st);
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
                            float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs,
-                           int clean_hi = -1);
+                           int clean_hi = -1, const FusedRope *fr = nullptr);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
 int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q, int t, int pos0, int pos_base,
                              int n_keys, float *out, float *packed, cudaStream_t stream);

@@ -18,7 +18,7 @@ namespace hs {
 
 int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
                      float *packed, void *ws, size_t ws_bytes, cudaStream_t stream, uint16_t *xs, int ldxs,
-                     int clean_hi);
+                     int clean_hi, const FusedRope *fr);
 size_t attention_ws(int t, int H, int DH, int n_view, int split);
 
 namespace {
@@ -197,7 +197,7 @@ int launch_topk_attention(const HsModel *m, const HsCache *c, int layer, int n, 
   sv.pos0 = pos;
   sv.n_view = budget;
   sv.split = 512;
-  return launch_attention(&cc, 0, &sv, H, q, 1, nullptr, nullptr, att_ws, att_bytes, st, xs, ldxs, -1);
+  return launch_attention(&cc, 0, &sv, H, q, 1, nullptr, nullptr, att_ws, att_bytes, st, xs, ldxs, -1, nullptr);
 }
 
 }  // namespace hs
