@@ -265,8 +265,9 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     // (wqkv, gate|up, lm_head) scales its result by 1 / rms -- so no split /
     // normalise kernel runs between the weight streams.
     static const bool fused_rope_ok = getenv("HS_NO_FUSED_ROPE") == nullptr;   // A/B hook
-    const bool fuse_rope = fused_rope_ok && !sharded && topk_budget == 0 && probs == nullptr && probe == nullptr &&
-                           dh == 128 && st->dyn == nullptr &&
+    const bool fuse_rope = fused_rope_ok && topk_budget == 0 && probs == nullptr && probe == nullptr &&
+                           dh == 128 && st->dyn == nullptr && st->n_view > 0 &&   // (an empty shard view launches no
+                           // attention kernel, so it could not write q_stash / the rows)
                            (st->append_mode == HS_APPEND_POS || st->append_mode == HS_APPEND_LINEAR);
     HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
     HS_TRY(launch_norm_prep(w.x, d, t, d, m->attn_norm, w.xd, m->ld_d, w.ssq, s));
@@ -284,8 +285,16 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
         // reads the qkv rows; the CTA covering the appended slots writes them)
         const FusedRope fr = {w.qkv, nqkv, m->rope_cos, m->rope_sin,
                               q_stash ? q_stash + (size_t)l * H * dh : nullptr};
-        HS_TRY(launch_attention_timed(c, l, st, H, nullptr, t, nullptr, nullptr, w.att_ws, w.att_bytes, s, w.xa,
-                                      m->ld_d, clean_hi, &fr));
+        if (sharded) {
+          const size_t part = (size_t)t * H * (dh + 2) * 4;
+          HS_TRY(launch_attention_timed(c, l, st, H, nullptr, t, nullptr, w.send, w.att_ws, w.att_bytes, s, nullptr,
+                                        0, clean_hi, &fr));
+          HS_TRY(shard_all_gather(sh, w.send, w.recv, part, s));
+          HS_TRY(launch_shard_merge(w.recv, sh->world, t * H, dh, nullptr, w.xa, m->ld_d, H, s));
+        } else {
+          HS_TRY(launch_attention_timed(c, l, st, H, nullptr, t, nullptr, nullptr, w.att_ws, w.att_bytes, s, w.xa,
+                                        m->ld_d, clean_hi, &fr));
+        }
       } else {
       HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
       if (sharded) {
