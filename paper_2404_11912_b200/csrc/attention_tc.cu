@@ -7,26 +7,29 @@
 // CUDA-core kernel in attention.cu (see there), so attn_combine_kernel merges
 // either.
 //
-// Per CTA work item (split of 2048/512 slots, kv head, block of <= 16 query
-// rows), per 128-key tile:
-//   S^T[128 keys x 48] = K_tile[128 x 128] . Qsplit^T        (8 x tcgen05.mma K16)
+// Per CTA work item (split of 2048/512 slots, kv head, block of <= 8 query
+// rows -- query blocks vary fastest so items sharing a split run together),
+// per 128-key tile:
+//   S^T[128 keys x 24] = K_tile[128 x 128] . Qsplit^T        (8 x tcgen05.mma K16)
 //   softmax in registers (thread = key = TMEM lane), tile max across the 4
-//   warps (redux + one named barrier), P split exactly into 3 bf16 terms ->
-//   smem (K-major, SW128)
-//   O^T[128 dh x 48]   = V_tile^T (MN-major) . Psplit^T      (8 x tcgen05.mma K16)
+//   warps of a group (redux + one named barrier), P split exactly into 3 bf16
+//   terms -> smem (K-major, SW128)
+//   O^T[128 dh x 24]   = V_tile^T (MN-major) . Psplit^T      (8 x tcgen05.mma K16)
 //   thread = dh lane accumulates o = o*fac + (hi + mid + lo) in registers.
 // q and p enter the tensor core as exact 3-way bf16 splits, so every product
 // is exact and accumulation is fp32: numerics match the fp32 CUDA-core path.
 // Each query row is its own MMA column: a row's result does not depend on
 // the other rows in the launch (t-invariance of the verify forward).
 //
-// Software pipeline (double-buffered S, P, O in TMEM/smem; 2 K + 2 V stages):
-//   iteration i issues S(i+1), runs softmax(i), issues PV(i), then folds
-//   O(i-1) into the register accumulator -- the tensor core and the TMA
-//   stream run underneath the softmax of the current tile.
-// Warp roles: warps 0-3 own the TMEM lane quarters, thread 0 issues MMAs at
-// the points where the four warps are synchronised; warp 4 is the TMA
-// producer.  One CTA per SM, persistent over work items.
+// Software pipeline (S, P, O double-buffered in TMEM/smem; one K and one V
+// stage per CTA, two CTAs per SM): S runs one tile ahead of P.V, O(i-1) is
+// folded into the register accumulator while the tensor core and the TMA
+// stream work on tile i.  Warp roles (10 warps): two softmax groups of four
+// warps (the item's rows split evenly between them), warp 4 the TMA producer
+// (first tile issued before griddepcontrol.wait when it holds no appended
+// slot), warp 5 the MMA issuer.  Persistent over work items.  With FusedRope
+// the q staging also applies RoPE to the qkv rows and the CTA covering this
+// step's slots appends the new K/V rows before its producer loads them.
 #include "hs_common.cuh"
 #include "tc_util.cuh"
 
