@@ -11,12 +11,14 @@
 // epilogue sums the three column groups in a fixed order.
 //
 // Pipeline per CTA (128 threads): warp 0 issues TMA loads of [128 x 64]
-// weight tiles + [24 x 64] activation tiles into a 5-stage ring, warp 1 issues
+// weight tiles + [24 x 64] activation tiles into a 5-stage ring (the weight
+// tiles of the first stages before griddepcontrol.wait), warp 1 issues
 // tcgen05.mma (4 x K16 per stage) and tcgen05.commit frees the stage, all four
 // warps drain TMEM (tcgen05.ld) in the epilogue.  K is split over gridDim.y
-// CTAs; partial tiles are reduced by the last-arriving CTA in split order
-// (deterministic; the split depends only on N and K, never on t, so a row's
-// result does not depend on the batch size).
+// CTAs (about one CTA per SM, gemv_tc_ksplit); the split CTAs of a tile form a
+// thread-block cluster and the split-0 CTA sums their partials over DSMEM in
+// split order (deterministic; the split depends only on N and K, never on t,
+// so a row's result does not depend on the batch size).
 #include <cudaTypedefs.h>
 
 #include <mutex>
