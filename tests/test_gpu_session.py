@@ -388,15 +388,18 @@ def test_sampled_acceptance_rates(P):
     assert abs(g[2] / g[3] - o[2] / o[3]) <= 0.01, (g, o)
 
 
-def test_planted_greedy_stream_and_acceptance_match_oracle(P):
+@pytest.mark.parametrize("head_dim", [64, 128])
+def test_planted_greedy_stream_and_acceptance_match_oracle(P, head_dim):
     """Non-degenerate acceptance (random-init greedy is vacuous):
     models with a planted successor channel accept most speculations, and the
     GPU loop's greedy stream and per-level accept counts equal the oracle's
-    exactly, rebuilds included."""
+    exactly, rebuilds included.  head_dim 128 runs the target on the
+    tensor-core attention with RoPE + append fused into it."""
     from oracle import hs_oracle as O
     mk = lambda w: O.OModel(O.OConfig(**{k: getattr(w.config, k) for k in w.config.__dataclass_fields__}),
                             O.round_weights_bf16(w.tensors), w.tied_head)
-    tc = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=64, d_ff=344, vocab_size=512, max_seq=2048)
+    tc = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=head_dim, d_ff=344, vocab_size=512,
+                       max_seq=2048)
     dc = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=64, d_ff=172, vocab_size=512, max_seq=2048)
     tw = bf16_weights(P, P.plant_successor(P.generate_weights(tc, 5, tied_head=False), 9, 0.9))
     dw = bf16_weights(P, P.plant_successor(P.generate_weights(dc, 6, tied_head=False), 9, 0.9))
@@ -587,3 +590,25 @@ def test_greedy_equals_autoregressive_many_pairs(P):
             if out != ar:
                 mismatches.append((i, frac))
     assert not mismatches, mismatches
+
+
+def test_tensor_core_chunk_equals_steps_across_split_boundary(P):
+    """head_dim 128 (tensor-core attention, fused RoPE + append): a 5-row
+    decode_chunk whose appended slots straddle the 2,048-key split boundary
+    is bit-identical to five decode_steps, and both match a prefill of the
+    same tokens on the row-exact path."""
+    from paper_2404_11912_b200 import model as M
+    cfg = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=128, d_ff=344, vocab_size=512, max_seq=2304)
+    w = P.generate_weights(cfg, 23, tied_head=False)
+    prompt = np.random.default_rng(8).integers(1, 512, 2046).tolist()
+    tail = [5, 77, 301, 12, 450]
+    a, b = P.FullCache.from_config(cfg), P.FullCache.from_config(cfg)
+    P.prefill(w, prompt, a)
+    P.prefill(w, prompt, b)
+    rows = P.decode_chunk(w, tail, a)
+    steps = np.stack([P.decode_step(w, tk, b) for tk in tail])
+    assert np.array_equal(rows, steps)
+    assert torch.equal(a.k[:, :, :2051], b.k[:, :, :2051]) and torch.equal(a.v[:, :, :2051], b.v[:, :, :2051])
+    c = P.FullCache.from_config(cfg)
+    ref = M._host_rows(M.forward_device(w, prompt + tail, c, None, prefill=False))[-5:]
+    assert np.allclose(rows, ref, rtol=1e-4, atol=3e-4 * np.abs(ref).max())
