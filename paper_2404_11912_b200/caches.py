@@ -299,6 +299,7 @@ class H2OCache(KVCache):
         self._alive = np.zeros((n_layers, max_entries), dtype=bool)
         self._scores = np.zeros((n_layers, max_entries), dtype=np.float64)
         self._pending = [[] for _ in range(n_layers)]
+        self._nl = [0] * n_layers   # entries appended per layer (slot == position)
 
     @classmethod
     def from_config(cls, model_config, config: H2OConfig):
@@ -321,6 +322,32 @@ class H2OCache(KVCache):
         self._alive[:, a:b] = True
         self._scores[:, a:b] = 0.0
         self.frontier = b
+        self._nl = [b] * self.n_layers
+
+    # -- per-layer protocol (KVCache.append / observe_attention, caches.py:311-345) --
+    def append(self, layer, k, v):
+        self._check_kv(k, v)
+        t = k.shape[0]
+        n = self._nl[layer]
+        if n + t > self.max_entries:
+            raise CapacityError(f"h2o cache overflow past {self.max_entries}")
+        pos = np.arange(n, n + t)
+        self._write_rows(layer, k, v, pos, pos)
+        self._alive[layer, n:n + t] = True
+        self._scores[layer, n:n + t] = 0.0
+        self._nl[layer] = n + t
+        if layer == self.n_layers - 1:
+            self.frontier = n + t
+
+    def observe_attention(self, layer, probs, query_positions):
+        """probs [KVH, g, t, L] over this layer's exposed entries (position order)."""
+        slots = np.nonzero(self._alive[layer, :self._nl[layer]])[0]
+        p = np.asarray(probs)
+        if p.shape[-1] != slots.size:
+            raise ShapeError(f"attention row spans {p.shape[-1]} entries, layer exposes {slots.size}")
+        rows = p.astype(np.float64).sum(axis=(0, 1))
+        for i, qpos in enumerate(np.asarray(query_positions)):
+            self._pending[layer].append((int(qpos), slots, rows[i].copy()))
 
     def observe_forward(self, pos0: int, probs: np.ndarray) -> None:
         """probs [L][t][n_view]: each new query row's head-summed attention
@@ -332,7 +359,7 @@ class H2OCache(KVCache):
                 self._pending[li].append((pos0 + i, slots, probs[li, i, slots].copy()))
 
     def expose(self, layer, queries=None):
-        slots = np.nonzero(self._alive[layer, :self.frontier])[0]
+        slots = np.nonzero(self._alive[layer, :self._nl[layer]])[0]
         K, V = self._gather_host(layer, slots)
         return K, V, slots.astype(np.int64), None
 
@@ -345,6 +372,7 @@ class H2OCache(KVCache):
         for li in range(self.n_layers):
             self._pending[li] = [p for p in self._pending[li] if p[0] < n]
         self.frontier = min(self.frontier, n)
+        self._nl = [min(x, n) for x in self._nl]
 
     def commit(self, n):
         self._check_commit(n)
@@ -385,6 +413,7 @@ class H2OCache(KVCache):
         c._alive = self._alive.copy()
         c._scores = self._scores.copy()
         c._pending = [[(q, s.copy(), w.copy()) for q, s, w in pl] for pl in self._pending]
+        c._nl = list(self._nl)
         c.frontier, c.committed = self.frontier, self.committed
         return c
 

@@ -191,3 +191,69 @@ def test_recovery_analytics_match_reference(P, golden_single, needle):
     lc = P.locality_recovery(target, prompts[m["locality_prompt"]], m["locality_budget"], horizon=m["horizon"])
     assert np.allclose(lc.frozen, data["recovery/bf16/frozen"], rtol=1e-4, atol=1e-5)
     assert np.allclose(lc.fresh, data["recovery/bf16/fresh"], rtol=1e-4, atol=1e-5)
+
+
+def _h2o_row(qpos, positions):
+    """deterministic unnormalised attention mass per exposed position (independent
+    of which other entries are exposed), as in the reference's replay harness"""
+    p = positions.astype(np.float64)
+    return 1.0 / (1.0 + np.abs(qpos - p)) + 0.05 * ((positions * 40503) % 89) / 89.0
+
+
+@pytest.mark.parametrize("policy", ["h2o", "topk"])
+def test_rollback_replay_h2o_topk(P, policy):
+    """Rollback soundness (tests/test_caches.py:416-435, acceptance criterion
+    C6) for the two analytics policies: a cache driven through random
+    speculate / commit / rollback rounds exposes exactly what a fresh cache fed
+    only the committed history (same commit batching) exposes."""
+    L, KVH, DH = 2, 2, 8
+
+    def make():
+        if policy == "h2o":
+            return P.H2OCache(L, KVH, DH, P.H2OConfig(budget=9, recent_window=3), 512)
+        return P.TopKCache(L, KVH, DH, 512, budget=7)
+
+    def append_one(c, pos):
+        for layer in range(L):
+            base = np.arange(KVH * DH, dtype=np.float32).reshape(KVH, DH)
+            k = (np.float32(0.001) * base + np.float32(pos + 0.01 * layer))[None]
+            c.append(layer, k, -k)
+            if c.wants_attention:
+                pe = c.exposed_positions(layer)
+                c.observe_attention(layer, _h2o_row(pos, pe).reshape(1, 1, 1, -1), np.array([pos]))
+
+    def state(c):
+        out = []
+        for layer in range(L):
+            K, V, pos, _ = c.expose(layer)
+            out.append((K, V, pos))
+        return out
+
+    for trial in range(25):
+        rng = np.random.default_rng(1000 + trial)
+        live, oracle = make(), make()
+        for c in (live, oracle):
+            for p_ in range(12):
+                append_one(c, p_)
+            c.commit(12)
+        committed, marks = 12, []
+        for _ in range(8):
+            n_spec = int(rng.integers(1, 5))
+            for i in range(n_spec):
+                append_one(live, committed + i)
+            keep = int(rng.integers(0, n_spec + 1))
+            live.rollback_to(committed + keep)
+            live.commit(committed + keep)
+            committed += keep
+            marks.append(committed)
+        pos = 12
+        for mark in marks:
+            while pos < mark:
+                append_one(oracle, pos)
+                pos += 1
+            oracle.commit(mark)
+        for (K1, V1, p1), (K2, V2, p2) in zip(state(live), state(oracle)):
+            assert np.array_equal(p1, p2) and np.array_equal(K1, K2) and np.array_equal(V1, V2), (policy, trial)
+        if policy == "h2o":
+            for layer in range(L):
+                assert len(live.exposed_positions(layer)) <= 9
