@@ -58,7 +58,7 @@ class StreamingConfig:
 
 @dataclass(frozen=True)
 class H2OConfig:
-    """caches.py:42-49 (policy itself is out of scope for the hot path)."""
+    """caches.py:42-49 (H2OCache below)."""
     budget: int = 64
     recent_window: int = 32
 
