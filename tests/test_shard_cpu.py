@@ -89,3 +89,28 @@ def test_shard_plan_is_chunk_aligned_and_covers_the_context():
 def test_world2_gloo_protocol_matches_unsharded():
     port = _free_port()
     mp.spawn(_worker, args=(2, port), nprocs=2, join=True)
+
+
+def test_shard_plan_properties():
+    """Property check over random geometries (hypothesis): every position has
+    exactly one owner, boundaries are chunk-aligned, no retrieval chunk
+    straddles two ranks, and the per-rank chunk counts add up."""
+    hyp = pytest.importorskip("hypothesis")
+    st = hyp.strategies
+    from paper_2404_11912_b200.shard import shard_chunk_counts, shard_plan
+
+    @hyp.settings(max_examples=200, deadline=None)
+    @hyp.given(n=st.integers(1, 1 << 21), world=st.integers(1, 8), chunk=st.sampled_from([1, 4, 8, 16, 32]),
+               probe=st.integers(0, (1 << 21) + 4096))
+    def check(n, world, chunk, probe):
+        plan = shard_plan(n, world, chunk)
+        owners = [r for r, (lo, hi) in enumerate(plan) if lo <= probe and (hi is None or probe < hi)]
+        assert len(owners) == 1
+        r = owners[0]
+        lo, hi = plan[r]
+        c0 = probe // chunk * chunk                       # the probe's chunk lies on the same rank
+        assert lo <= c0 and (hi is None or c0 + chunk <= hi)
+        assert all(b % chunk == 0 for lo_, hi_ in plan for b in (lo_, hi_) if b is not None)
+        assert sum(shard_chunk_counts(plan, n, chunk)) == -(-n // chunk)
+
+    check()
