@@ -407,3 +407,30 @@ def test_attention_full_context_122880_keys(P):
             ref = p @ V[h // (H // kvh), :vis]
             rel = ((got[i, h] - ref).abs().max() / ref.abs().max()).item()
             assert rel <= 1e-4, (i, h, rel)
+
+
+def test_verify_chain_randomized_against_oracle(P):
+    """The fused verify chain (verify_chain_kernel via speculation._verify_chain)
+    against the oracle's sequential restatement of speculation.py:187-208 on
+    300 random (q, p, drafted tokens, seed) cases -- vocabularies up to 300,
+    peaked and flat distributions, near-equal q/p (residual mass near the
+    1e-12 fallback): identical emitted tokens, labels, accepted count and
+    uniforms consumed."""
+    from oracle import hs_oracle as O
+    from paper_2404_11912_b200 import speculation as S
+    rng = np.random.default_rng(2024)
+    for case in range(300):
+        V = int(rng.integers(2, 300))
+        n = int(rng.integers(0, 7))
+        alpha = float(rng.choice([0.05, 0.5, 5.0]))
+        qd = [rng.dirichlet(np.full(V, alpha)) for _ in range(n)]
+        pd = [rng.dirichlet(np.full(V, alpha)) for _ in range(n + 1)]
+        if case % 5 == 0 and n:                       # p == q: the residual falls back to p
+            pd = [q.copy() for q in qd] + [pd[-1]]
+        toks = [int(rng.choice(V, p=q)) for q in qd]
+        seed = int(rng.integers(0, 1 << 30))
+        r1, r2 = np.random.default_rng(seed), np.random.default_rng(seed)
+        got = S._verify_chain(toks, qd, pd, r1)
+        want = O.verify_chain(toks, qd, pd, r2)
+        assert got == want, case
+        assert r1.random() == r2.random(), case      # same number of uniforms consumed
