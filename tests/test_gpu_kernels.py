@@ -434,3 +434,24 @@ def test_verify_chain_randomized_against_oracle(P):
         want = O.verify_chain(toks, qd, pd, r2)
         assert got == want, case
         assert r1.random() == r2.random(), case      # same number of uniforms consumed
+
+
+def test_sampling_randomized_against_oracle(P):
+    """prob_from_logits + sample_from_probs (probs_kernel / sample_kernel)
+    against the oracle's fp64 softmax and inverse-CDF draw
+    (model.py:182-202) on 400 random cases: vocabularies 2..40,000,
+    temperatures 0 .. 1.7, tied maxima at T = 0 (lowest index wins):
+    same token, probabilities within 1e-12."""
+    from oracle import hs_oracle as O
+    rng = np.random.default_rng(99)
+    for case in range(400):
+        V = int(rng.choice([2, 7, 40, 260, 4096, 32000, 40000]))
+        T = float(rng.choice([0.0, 0.3, 0.6, 1.0, 1.7]))
+        logits = (rng.normal(0, float(rng.choice([0.5, 3.0, 12.0])), V)).astype(np.float32)
+        if case % 7 == 0:                                  # exact ties at the maximum
+            logits[int(rng.integers(0, V))] = logits.max()
+        p = P.prob_from_logits(logits, T)
+        ref = O.probs_of(logits, T)
+        assert np.abs(p - ref).max() <= 1e-12, case
+        seed = int(rng.integers(0, 1 << 30))
+        assert P.sample_from_probs(p, np.random.default_rng(seed)) == O.draw(ref, np.random.default_rng(seed)), case
