@@ -612,3 +612,34 @@ def test_tensor_core_chunk_equals_steps_across_split_boundary(P):
     c = P.FullCache.from_config(cfg)
     ref = M._host_rows(M.forward_device(w, prompt + tail, c, None, prefill=False))[-5:]
     assert np.allclose(rows, ref, rtol=1e-4, atol=3e-4 * np.abs(ref).max())
+
+
+def test_forward_randomized_configs_match_oracle(P):
+    """Whole forwards on random geometries against the oracle (bf16 storage
+    model): head_dim 64 / 128 (CUDA-core and tensor-core attention, fused
+    RoPE), GQA ratios 1 / 2 / 4, prompts long enough for the GEMM prefill or
+    not, then decode chunks crossing the 8-row block and single steps."""
+    from oracle import hs_oracle as O
+    rng = np.random.default_rng(77)
+    for case in range(6):
+        dh = int(rng.choice([64, 128]))
+        kvh = int(rng.choice([1, 2, 4]))
+        H = kvh * int(rng.choice([1, 2, 4]))
+        cfg = P.ModelConfig(n_layers=2, n_heads=H, n_kv_heads=kvh, head_dim=dh, d_ff=int(rng.integers(3, 12)) * 32,
+                            vocab_size=300, max_seq=1024)
+        w = bf16_weights(P, P.generate_weights(cfg, 500 + case, tied_head=bool(case % 2)))
+        om = O.OModel(O.OConfig(**{k: getattr(cfg, k) for k in cfg.__dataclass_fields__}),
+                      O.round_weights_bf16(w.tensors), w.tied_head)
+        plen = int(rng.integers(20, 400))
+        prompt = rng.integers(1, 300, plen).tolist()
+        chunk = rng.integers(1, 300, int(rng.integers(2, 12))).tolist()
+        steps = rng.integers(1, 300, 3).tolist()
+        dc, oc = P.FullCache.from_config(cfg), O.OFullCache(2, kvh, dh, 1024, kv_bf16=True)
+        got = [P.prefill(w, prompt, dc), P.decode_chunk(w, chunk, dc)]
+        got += [P.decode_step(w, tk, dc)[None] for tk in steps]
+        want = [O.prefill(om, prompt, oc), O.forward(om, chunk, oc)]
+        oc.commit(oc.frontier)
+        want += [O.decode_step(om, tk, oc)[None] for tk in steps]
+        g, r = np.concatenate(got), np.concatenate(want)
+        assert np.allclose(g, r, rtol=1e-4, atol=3e-4 * np.abs(r).max()), (case, dh, H, kvh, plen)
+        assert (np.argmax(g, -1) == np.argmax(r, -1)).mean() > 0.99, case
