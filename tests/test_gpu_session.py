@@ -643,3 +643,40 @@ def test_forward_randomized_configs_match_oracle(P):
         g, r = np.concatenate(got), np.concatenate(want)
         assert np.allclose(g, r, rtol=1e-4, atol=3e-4 * np.abs(r).max()), (case, dh, H, kvh, plen)
         assert (np.argmax(g, -1) == np.argmax(r, -1)).mean() > 0.99, case
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_randomized_sessions_match_oracle(P, case):
+    """Random session geometries (target head_dim 64 / 128 -- the latter on
+    the tensor-core attention with fused RoPE --, GQA, chunk / budget /
+    stream sizes, gamma1 / gamma2, greedy and sampled) with planted models:
+    token stream and per-level accept counts equal the oracle's exactly."""
+    from oracle import hs_oracle as O
+    rng = np.random.default_rng(300 + case)
+    mk = lambda w: O.OModel(O.OConfig(**{k: getattr(w.config, k) for k in w.config.__dataclass_fields__}),
+                            O.round_weights_bf16(w.tensors), w.tied_head)
+    dh = [64, 128, 128, 64][case]
+    kvh = int(rng.choice([1, 2]))
+    tc = P.ModelConfig(n_layers=2, n_heads=kvh * 2, n_kv_heads=kvh, head_dim=dh, d_ff=192, vocab_size=400,
+                       max_seq=1536)
+    dc = P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=32, d_ff=64, vocab_size=400, max_seq=1536)
+    tw = bf16_weights(P, P.plant_successor(P.generate_weights(tc, 40 + case, tied_head=False), case, 0.85))
+    dw = bf16_weights(P, P.plant_successor(P.generate_weights(dc, 50 + case, tied_head=False), case, 0.85))
+    plen = int(rng.integers(100, 900))
+    prompt = rng.integers(1, 400, plen).tolist()
+    chunk = int(rng.choice([4, 8, 16]))
+    budget = chunk * int(rng.integers(4, 24))
+    stream = int(rng.choice([24, 48, 96]))
+    g1, g2 = int(rng.integers(1, 4)), int(rng.integers(3, 7))
+    temp = float([0.0, 0.6, 1.0, 0.6][case])
+    spec = P.SpecConfig(target_len=plen + 40, gamma1=g1, gamma2=g2, temperature=temp, seed=case,
+                        streaming=P.StreamingConfig(n_sink=4, budget=stream),
+                        retrieval=P.RetrievalConfig(chunk_size=chunk, budget=budget, rebuild_stride=16))
+    out, tr = P.HierarchicalSession(tw, dw, prompt, spec).generate()
+    os_ = O.OSession(mk(tw), mk(dw), prompt, O.OSpec(target_len=plen + 40, gamma1=g1, gamma2=g2, temperature=temp,
+                                                    seed=case, n_sink=4, stream_budget=stream, chunk=chunk,
+                                                    retr_budget=budget, rebuild_stride=16), kv_bf16=True)
+    oout, otr = os_.generate()
+    assert out == oout, (case, dh, kvh, plen, chunk, budget, stream, g1, g2, temp)
+    assert [tr.inner.proposed, tr.inner.accepted, tr.outer.proposed, tr.outer.accepted] == \
+        [otr.inner[0], otr.inner[1], otr.outer[0], otr.outer[1]]
