@@ -257,3 +257,21 @@ def test_rollback_replay_h2o_topk(P, policy):
         if policy == "h2o":
             for layer in range(L):
                 assert len(live.exposed_positions(layer)) <= 9
+
+
+def test_needle_criterion_with_own_fixtures(P):
+    """Acceptance criterion 3 end to end with this package's own fixtures
+    (host_analysis.needle_corpus / planted_attention_weights) instead of the
+    reference-generated ones: top-k >= retrieval > streaming, gap >= 0.3."""
+    cfg = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=8, d_ff=32, vocab_size=260, max_seq=512,
+                        rope_theta=1e8)
+    corpus = P.needle_corpus(96, 30, seed=11)
+    w = P.planted_attention_weights(cfg, 96, len(corpus[0].needle_positions), strength=0.8, answer_token=ord("A"),
+                                    seed=11)
+    prompts = [c.tokens for c in corpus]
+    kw = dict(gamma=3, temperature=0.0, gen_tokens=8, seed=3, streaming=P.StreamingConfig(n_sink=4, budget=32),
+              retrieval=P.RetrievalConfig(chunk_size=16, budget=32), topk_budget=32)
+    rate = {k: P.measure_acceptance("self:" + k, w, prompts, **kw)["self"].rate
+            for k in ("topk", "retrieval", "streaming")}
+    assert rate["topk"] >= rate["retrieval"] > rate["streaming"], rate
+    assert rate["retrieval"] - rate["streaming"] >= 0.3, rate
