@@ -35,7 +35,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")      # keep stdout to the one JSON line
+# NCCL's INFO lines (communicator size, NVLS) go to stderr like every native
+# print (stdout is redirected below), so they stay visible to the driver
+if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
 
 # stdout carries exactly one JSON line: everything native libraries print
 # (the NCCL banner when NCCL_DEBUG is set verbose, driver messages) goes to

@@ -204,14 +204,6 @@ int hs_prefill_sharded(const HsModel *m, const HsCache *c, const HsStep *st, con
 
 /* ---- building blocks (also used by tests and the per-layer cache API) ---- */
 
-/* y[r][o] (+)= sum_k pro(x)[r][k] * W[o][k]   (tensor.py:26-36 matmul)
- * prologue: 0 none, 1 rmsnorm with gain (tensor.py:57-63)
- * epilogue: 0 store, 1 accumulate into y, 2 SwiGLU pairs (y has N/2 cols,
- *           model.py:320-322)                                              */
-int hs_gemv(const float *x, int ldx, int t, int K, const uint16_t *w, int ldw, int N,
-            int prologue, const float *gain, float eps, int epilogue, float *y, int ldy,
-            void *stream);
-
 /* Tensor-core GEMV (tcgen05 + TMA, swap-AB): y (+)= W . x for one pass of
  * t <= 8 activation rows held as an exact 3-way bf16 split xs [24][ldw]
  * (rows split*8 + r; see hs_split_rows).  epilogue 0 store, 1 accumulate,

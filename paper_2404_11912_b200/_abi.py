@@ -82,7 +82,6 @@ _SIGS = {
     "hs_prefill": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), vp, i32, vp, vp, vp, sz, vp]),
     "hs_prefill_sharded_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32, i32]),
     "hs_prefill_sharded": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), _P(HsShard), vp, i32, vp, vp, vp, sz, vp]),
-    "hs_gemv": (i32, [vp, i32, i32, i32, vp, i32, i32, i32, vp, f32, i32, vp, i32, vp]),
     "hs_embed": (i32, [vp, i32, i32, vp, i32, vp, vp]),
     "hs_rope_append": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), i32, vp, i32, vp, vp, vp]),
     "hs_kv_write": (i32, [_P(HsCache), i32, vp, vp, i32, vp, vp, vp]),

@@ -9,8 +9,8 @@ reported) and the self-speculation pairings 'self:streaming',
 full cache; TopK selects per layer and query on the device, csrc/topk.cu;
 H2O feeds back the forward's attention probabilities, csrc/h2o.cu).
 Attention-mass recovery (`sparsity_recovery`, `locality_recovery`) runs on
-the device attention probes.  The needle fixtures and the speedup model are
-host-side analysis, not decode work, and are not part of this build.
+the device attention probes.  The needle fixtures and the host-side speedup
+model live in host_analysis.py.
 """
 
 from __future__ import annotations

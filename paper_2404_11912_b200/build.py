@@ -76,12 +76,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if os.environ.get("HS_TRACE_BUILD") == "1":   # per-CTA timeline (tools/cta_timeline.py); slower
         extra.append("-DHS_CTA_TRACE")
     extra += os.environ.get("HS_NVCC_DEFINES", "").split()   # experiment builds, e.g. "-DHS_TC_STAGES=4"
+    cmds = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(NCCL, "include"),
-               "-c", src, "-o", obj]
-        subprocess.run(cmd, check=True)
+        cmds.append([NVCC, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(NCCL, "include"),
+                     "-c", src, "-o", obj])
         objs.append(obj)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as pool:
+        for r in pool.map(lambda c: subprocess.run(c, check=True), cmds):
+            pass
     tmp = LIB + ".tmp"
     nccl_lib = os.path.join(NCCL, "lib")
     subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-L", nccl_lib, "-l:libnccl.so.2",

@@ -45,6 +45,12 @@ SMALL_SPLIT = int(os.environ.get("HS_SMALL_SPLIT", 512))   # keys per split over
 STREAM_SPLIT = int(os.environ.get("HS_STREAM_SPLIT", 64))   # keys per split over the streaming window
 
 
+def stream_split(head_dim: int) -> int:
+    """Split for streaming / H2O views: the tensor-core kernel (head_dim 128)
+    walks 128-key tiles, so its splits are whole tiles."""
+    return STREAM_SPLIT if head_dim < 128 else max(128, STREAM_SPLIT // 128 * 128)
+
+
 @dataclass(frozen=True)
 class StreamingConfig:
     """caches.py:32-39"""
@@ -314,7 +320,7 @@ class H2OCache(KVCache):
         s.append_mode = HS_APPEND_LINEAR
         s.append_base = self.frontier
         s.n_view = self.frontier + t
-        s.split = STREAM_SPLIT
+        s.split = stream_split(self.head_dim)
         return s
 
     def _advance(self, t):
@@ -566,7 +572,7 @@ class StreamingCache(KVCache):
         s.n_view = self.cap
         s.window = self.window
         s.win_lo = self.lo
-        s.split = STREAM_SPLIT
+        s.split = stream_split(self.head_dim)
         return s
 
     def _advance(self, t):

@@ -409,7 +409,6 @@ int launch_attention(const HsCache *c, int layer, const HsStep *st, int H, const
     case 64: le = launch_pdl(attn_partial_kernel<64>, grid, dim3(ATT_THREADS), 0, stream, a); break;
     case 128: {
       HS_REQUIRE(st->split % 128 == 0, HS_ERR_VALUE, "attention: split must be a multiple of 128 for head_dim 128");
-      HS_REQUIRE(st->dyn == nullptr, HS_ERR_VALUE, "attention: run-time positions need head_dim < 128");
       int rc = launch_attention_tc(c, layer, st, H, q, t, a.part_m, a.part_l, a.part_o, n_splits, stream,
                                    clean_hi, fr);
       if (rc != HS_OK) return rc;

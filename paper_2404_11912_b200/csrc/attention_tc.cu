@@ -72,6 +72,7 @@ struct AttTcArgs {
   int32_t *pos_app;                   // slotted: this layer's pos [cap], else null
   int app_mode, app_base, own_hi;     // HsStep append rule (positions or linear tail)
   int dirty_lo, dirty_hi;             // slots this step appends
+  const int32_t *dyn;   // HsStep.dyn: run-time frontier offset / win_lo (graph replay), or null
   float scale_log2;     // log2(e) / sqrt(dh)
   float *part_m, *part_l, *part_o;
 };
@@ -86,11 +87,11 @@ __device__ __forceinline__ void item_coords(int item, const AttTcArgs &a, int &s
   kh = item / (a.n_qb * a.n_splits);
 }
 
-__device__ __forceinline__ bool visible_tc(int kp, int qp, const AttTcArgs &a) {
+__device__ __forceinline__ bool visible_tc(int kp, int qp, const AttTcArgs &a, int win_lo) {
   if (kp < 0 || kp > qp) return false;
   if (a.window == 0 || kp < a.n_sink) return true;
   int lo = qp - a.window + 1;
-  if (a.win_lo > lo) lo = a.win_lo;
+  if (win_lo > lo) lo = win_lo;
   return kp >= lo;
 }
 
@@ -214,6 +215,9 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
   }
   tc::grid_dep_wait();               // q, positions and the appended K/V rows
   HS_TRACE_RESTART
+  // query positions: host values, or (graph replay) offset by the device frontier
+  const int pos0 = a.dyn ? a.pos0 + a.dyn[0] : a.pos0;
+  const int win_lo = a.dyn ? a.dyn[1] : a.win_lo;
 
   // ---------------------------------------------------------------- MMA issuer (warp 5)
   if (warp == 5) {
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
     const int ntiles = (hi - lo + AT_KT - 1) / AT_KT;
     // ---- stage the query split; zero both P buffers (rows >= nrows stay 0) ----------
     // (all S/P.V MMAs of the previous item completed: its tiles were all consumed)
-    if (stid < AT_QR) qp_s[stid] = stid < nrows ? a.pos0 + (r0 + stid) / a.g : -1;
+    if (stid < AT_QR) qp_s[stid] = stid < nrows ? pos0 + (r0 + stid) / a.g : -1;
     if (a.qkv == nullptr) {
       for (int e = stid; e < AT_QR * AT_DH; e += 256) {
         const int rr = e >> 7, d = e & 127;
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         float y0 = 0.f, y1 = 0.f;
         if (rr < nrows) {
           const int i = (r0 + rr) / a.g, head = kh * a.g + (r0 + rr) % a.g;
-          const int p = a.pos0 + i;
+          const int p = pos0 + i;
           const float *row = a.qkv + (size_t)i * a.ncols + head * AT_DH + 2 * pr;
           const double ev = (double)row[0], ov = (double)row[1];
           const double cs = (double)a.rope_cos[(size_t)p * (AT_DH / 2) + pr];
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
       if (lo < a.dirty_hi && hi > a.dirty_lo) {
         for (int e = stid; e < a.t * (AT_DH / 2); e += 256) {
           const int i = e >> 6, pr = e & 63;
-          const int p = a.pos0 + i;
+          const int p = pos0 + i;
           int slot;
           if (a.app_mode == HS_APPEND_POS)
             slot = (p < a.pos_base || (a.own_hi > 0 && p >= a.own_hi)) ? -1 : p - a.pos_base;
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
 #pragma unroll
     for (int r = 0; r < AT_GR; ++r) { m_run[r] = -INFINITY; l_run[r] = 0.f; o_acc[r] = 0.f; fac_prev[r] = 1.f; }
 
-    const int qmin = a.pos0 + r0 / a.g;   // smallest query position of this block
+    const int qmin = pos0 + r0 / a.g;   // smallest query position of this block
     for (int it = 0; it <= ntiles; ++it) {
       if (it < ntiles) {
         const uint32_t gi = g + it;
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
           for (int r = 0; r < AT_GR; ++r) {
             if (rb + r < re) {
               const float sc = ((sv[r] + sv[AT_GR + r]) + sv[2 * AT_GR + r]) * a.scale_log2;
-              x[r] = (allvis || visible_tc(kp, qp_s[rb + r], a)) ? sc : -INFINITY;
+              x[r] = (allvis || visible_tc(kp, qp_s[rb + r], a, win_lo)) ? sc : -INFINITY;
               const int mx = __reduce_max_sync(0xffffffffu, f2o(x[r]));
               if (lane == 0) red[s][warp & 3][rb + r] = mx;
             }
@@ -522,7 +526,8 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
   a.n_items = n_splits * a.KVH * a.n_qb;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)AT_DH));
   a.part_m = part_m; a.part_l = part_l; a.part_o = part_o;
-  a.clean_hi = clean_hi;
+  a.clean_hi = st->dyn ? -1 : clean_hi;
+  a.dyn = st->dyn;
   a.qkv = nullptr;
   a.dirty_lo = a.dirty_hi = 0;
   if (fr) {

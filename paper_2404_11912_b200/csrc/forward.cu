@@ -11,8 +11,6 @@
 
 namespace hs {
 
-int launch_gemv(const float *x, int ldx, int t, int K, const uint16_t *w, int ldw, int N, int prologue,
-                const float *gain, float eps, int epilogue, float *y, int ldy, cudaStream_t st);
 int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x, cudaStream_t st);
 int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv, int t,
                        float *q_out, float *q_stash, cudaStream_t st);

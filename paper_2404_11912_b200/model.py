@@ -10,7 +10,8 @@ Same names, signatures and error behaviour as the reference
   call per lane step; `decode_chunk` is a single batched forward whose rows
   are bit-identical to a `decode_step` loop (the kernels' reductions do not
   depend on the batch size), which is the reference's own contract
-  (model.py:366-378);
+  (model.py:366-378) -- except over a TopKCache, whose per-query selection
+  makes the chunk a loop of single-token forwards, as in the reference;
 * sampling (`prob_from_logits`, `sample_from_probs`) runs in fp64 kernels
   consuming exactly one uniform per draw from the caller's Generator.
 """
@@ -478,6 +479,13 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
     shards = getattr(cache, "shards", None)
     shard_ref = shards.ref if shards is not None else None
     world = shards.world if shards is not None else 0
+    if getattr(cache, "policy", "") == "topk" and t > 1 and not (prefill and cache.frontier == 0):
+        # TopKCache selects per single query (caches.py:629-634): a batch is
+        # decoded position by position, as the reference's decode_chunk /
+        # Lane.advance / token-by-token prefill do (model.py:350-378)
+        for i in range(t):
+            forward_device(weights, tok[i:i + 1], cache, recorder, out=out[i:i + 1])
+        return out
     if recorder is not None and recorder.record_probs:
         return _forward_probe(weights, dm, tok, t, cache, recorder, out, stash, prefill)
     if (prefill and t >= PREFILL_MIN_ROWS and cache.kind == _abi.HS_KV_LINEAR

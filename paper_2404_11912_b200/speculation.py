@@ -172,15 +172,18 @@ class Lane:
         self._front = torch.zeros(V, dtype=torch.float32, device=device())
         self._has_front = False
         self._scratch = None
-        self._graphs = {}
+        self._graph = None
+        self._gtok = None
 
-    def step_graph(self, tok: torch.Tensor) -> "_StepGraph":
-        """Captured one-token step reading its token from `tok` (a fixed
-        device slot)."""
-        g = self._graphs.get(tok.data_ptr())
-        if g is None:
-            g = self._graphs[tok.data_ptr()] = _StepGraph(self, tok)
-        return g
+    def step_graph_run(self, tok: torch.Tensor) -> None:
+        """One-token step through the lane's captured graph.  The graph reads
+        its token from a lane-owned device slot (one capture per lane, never
+        per caller buffer); `tok` is copied into it on the stream."""
+        if self._graph is None:
+            self._gtok = torch.zeros(1, dtype=torch.int32, device=device())
+            self._graph = _StepGraph(self, self._gtok)
+        self._gtok.copy_(tok)
+        self._graph.run()
 
     @property
     def frontier(self) -> int:
@@ -348,7 +351,7 @@ def _draft_round_dev(lane: Lane, seq: Sequence[int], gamma1: int, T: float, us: 
         check(lib.hs_draft_sample(ptr(lane._front), V, float(T), ptr(buf.q[g]), ptr(us.buf), ptr(us.cursor),
                                   ptr(buf.dtok[g:g + 1]), s))
         if graphs:
-            lane.step_graph(buf.dtok[g:g + 1]).run()
+            lane.step_graph_run(buf.dtok[g:g + 1])
         else:
             lane._forward(buf.dtok[g:g + 1])
 

@@ -24,66 +24,6 @@ def _bf16(a):
     return bf16_round(a)
 
 
-def _gemv(P, x, W, prologue=0, gain=None, epilogue=0, y0=None, eps=1e-5):
-    from paper_2404_11912_b200._abi import check, lib
-    from paper_2404_11912_b200.runtime import ptr, stream_ptr
-    t, K = x.shape
-    N = W.shape[0]
-    ld = (K + 63) // 64 * 64
-    Wd = torch.zeros((N, ld), dtype=torch.bfloat16, device="cuda")
-    Wd[:, :K] = torch.from_numpy(W).to("cuda").to(torch.bfloat16)
-    xd = torch.from_numpy(x.astype(np.float32)).cuda()
-    ncol = N // 2 if epilogue == 2 else N
-    y = torch.from_numpy(y0.astype(np.float32)).cuda() if y0 is not None else torch.zeros((t, ncol), device="cuda")
-    g = torch.from_numpy(gain.astype(np.float32)).cuda() if gain is not None else None
-    check(lib.hs_gemv(ptr(xd), K, t, K, ptr(Wd), ld, N, prologue, ptr(g), eps, epilogue, ptr(y), ncol, stream_ptr()))
-    return y.cpu().numpy()
-
-
-@pytest.mark.parametrize("t,K,N", [(1, 4096, 4096), (7, 4096, 12288), (5, 11008, 4096), (3, 256, 260),
-                                   (8, 688, 256), (13, 64, 40), (2, 40, 33)])
-def test_gemv_matches_fp64(P, t, K, N):
-    rng = np.random.default_rng(K + N + t)
-    W = _bf16(rng.normal(0, 0.02, (N, K)).astype(np.float32))
-    x = rng.normal(0, 1, (t, K)).astype(np.float32)
-    y = _gemv(P, x, W)
-    ref = (x.astype(np.float64) @ W.astype(np.float64).T)
-    assert np.allclose(y, ref, rtol=1e-5, atol=1e-5 * np.abs(ref).max())
-
-
-def test_gemv_prologue_epilogues(P):
-    rng = np.random.default_rng(0)
-    t, K, N = 4, 512, 320
-    W = _bf16(rng.normal(0, 0.05, (N, K)).astype(np.float32))
-    x = rng.normal(0, 1, (t, K)).astype(np.float32)
-    gain = (1 + rng.normal(0, 0.02, K)).astype(np.float32)
-    x64 = x.astype(np.float64)
-    h = (x64 / np.sqrt(np.square(x64).mean(axis=-1, keepdims=True) + np.float64(np.float32(1e-5)))
-         * gain.astype(np.float64)).astype(np.float32)
-    ref = h.astype(np.float64) @ W.astype(np.float64).T
-    y = _gemv(P, x, W, prologue=1, gain=gain, eps=float(np.float32(1e-5)))
-    assert np.allclose(y, ref, rtol=1e-5, atol=1e-6)
-    y0 = rng.normal(0, 1, (t, N)).astype(np.float32)
-    y = _gemv(P, x, W, epilogue=1, y0=y0)
-    assert np.allclose(y, y0 + x64 @ W.astype(np.float64).T, rtol=1e-5, atol=1e-6)
-    y = _gemv(P, x, W, epilogue=2)
-    gu = (x64 @ W.astype(np.float64).T).astype(np.float32)
-    g64 = gu[:, 0::2].astype(np.float64)
-    act = (g64 * (0.5 * (np.tanh(0.5 * g64) + 1.0))).astype(np.float32) * gu[:, 1::2]
-    assert np.allclose(y, act, rtol=1e-5, atol=1e-6)
-
-
-def test_gemv_rows_independent_of_batch(P):
-    """Bitwise: a row's result does not depend on how many rows share the launch."""
-    rng = np.random.default_rng(1)
-    K, N = 4096, 4096
-    W = _bf16(rng.normal(0, 0.02, (N, K)).astype(np.float32))
-    x = rng.normal(0, 1, (8, K)).astype(np.float32)
-    full = _gemv(P, x, W)
-    for r in range(8):
-        assert np.array_equal(_gemv(P, x[r:r + 1], W)[0], full[r])
-
-
 def test_score_chunks_ranking_bruteforce(P):
     """Criterion 4 of the reference (tests/test_acceptance.py:170-204): chunk
     ranking equals brute-force mean-key scoring, ties by chunk id."""

@@ -275,3 +275,44 @@ def test_needle_criterion_with_own_fixtures(P):
             for k in ("topk", "retrieval", "streaming")}
     assert rate["topk"] >= rate["retrieval"] > rate["streaming"], rate
     assert rate["retrieval"] - rate["streaming"] >= 0.3, rate
+
+
+def test_self_speculation_head_dim_128(P):
+    """StreamingLLM and H2O self-speculation on a head_dim-128 model: the
+    streaming / H2O views run on the tensor-core attention (128-key splits),
+    the streaming draft's captured one-token step with run-time positions
+    (HsStep.dyn) included.  Checks: StreamingCache decode logits vs the CPU
+    oracle's StreamingCache; greedy sessions == autoregressive (lossless);
+    graph replay bit-identical to direct forwards."""
+    from oracle import hs_oracle as O
+    from paper_2404_11912_b200 import speculation as S
+    cfg = P.ModelConfig(n_layers=2, n_heads=4, n_kv_heads=2, head_dim=128, d_ff=344, vocab_size=512, max_seq=1024)
+    w = P.plant_successor(P.generate_weights(cfg, 21, tied_head=False), 4, 0.8)
+    prompt = np.random.default_rng(5).integers(1, 512, 300).tolist()
+    # decode over a sink + window view vs the oracle (bf16 storage model)
+    om = O.OModel(O.OConfig(**{k: getattr(cfg, k) for k in cfg.__dataclass_fields__}),
+                  O.round_weights_bf16(w.tensors), False)
+    sc = P.StreamingCache.from_config(cfg, P.StreamingConfig(n_sink=4, budget=64))
+    oc = O.OStreamingCache(2, 2, 128, 4, 64, kv_bf16=True)
+    P.prefill(w, prompt[:200], sc)
+    O.prefill(om, prompt[:200], oc)
+    for tk in prompt[200:206]:
+        got = P.decode_step(w, tk, sc)
+        ref = O.decode_step(om, tk, oc)
+        assert np.allclose(got, ref, rtol=1e-4, atol=1e-4 * np.abs(ref).max())
+    ar = P.autoregressive_generate(w, prompt, 360, 0.0, 0)
+    res = {}
+    for kind in ("streaming", "h2o"):
+        for graphs in ((False, True) if kind == "streaming" else (True,)):
+            S.USE_GRAPHS = graphs
+            try:
+                cache = (P.StreamingCache.from_config(cfg, P.StreamingConfig(n_sink=4, budget=64)) if kind == "streaming"
+                         else P.H2OCache.from_config(cfg, P.H2OConfig(budget=64, recent_window=16)))
+                s = P.SingleLevelSession(w, cache, w, prompt, gamma=3, temperature=0.0)
+                out, st = s.generate(360, seed=0)
+            finally:
+                S.USE_GRAPHS = True
+            assert out == ar, (kind, graphs)
+            assert st.accepted > 0
+            res[(kind, graphs)] = (out, st.proposed, st.accepted, st.rounds)
+    assert res[("streaming", False)] == res[("streaming", True)]
