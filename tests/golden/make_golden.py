@@ -288,13 +288,16 @@ def gen_cfg1():
             with bf16_caches():
                 sess = HierarchicalSession(t, d, prompt, spec)
                 imp0 = [list(x) for x in sess.retr_lane.cache.table.selected]
+                sc0 = np.stack(sess.retr_lane.cache.table.scores)
                 out, tr = sess.generate()
         else:
             sess = HierarchicalSession(t, d, prompt, spec)
             imp0 = [list(x) for x in sess.retr_lane.cache.table.selected]
+            sc0 = np.stack(sess.retr_lane.cache.table.scores)
             out, tr = sess.generate()
         put(tag + "/tokens", np.array(out[4096:]))
         put(tag + "/importance0", np.array(imp0))
+        put(tag + "/scores0", sc0)   # the initial build's fp64 chunk scores per layer (near-tie analysis)
         trace_arrays(tag, tr)
         print(tag, tr.summary(), flush=True)
     # AR greedy with bf16 storage for the GPU AR parity test

@@ -82,8 +82,8 @@ def test_cfg1_prefill_and_queries(P, golden):
     cache = P.FullCache.from_config(cfg)
     rec = P.ForwardRecorder()
     lg = P.prefill(w, prompt, cache, rec)
-    assert np.allclose(lg[-1], data["cfg1/bf16/prefill_last"], rtol=1e-3, atol=1e-4)
-    assert np.allclose(np.stack(rec.last_queries), data["cfg1/bf16/q_last"], rtol=1e-3, atol=1e-4)
+    assert np.allclose(lg[-1], data["cfg1/bf16/prefill_last"], rtol=1e-4, atol=1e-5)
+    assert np.allclose(np.stack(rec.last_queries), data["cfg1/bf16/q_last"], rtol=1e-4, atol=1e-5)
 
 
 def test_errors(P):
@@ -321,10 +321,40 @@ def test_single_round_api_matches_oracle(P):
     assert ox == x_hat
 
 
+def _delta_consistent(gpu_imp, ref_imp, ref_scores, delta):
+    """True iff the GPU's importance list can be the reference's selection
+    under score perturbations of at most `delta` per chunk: every chunk only
+    one side chose sits within 2*delta of the reference's selection threshold,
+    and the GPU's order never ranks a chunk above one whose reference score
+    is higher by more than 2*delta (caches.py:474-486, ties to the lower id)."""
+    tol = 2.0 * delta
+    thr = min(ref_scores[c] for c in ref_imp[1:])
+    for c in set(gpu_imp) ^ set(ref_imp):
+        if abs(ref_scores[c] - thr) > tol:
+            return False
+    rest = [ref_scores[c] for c in gpu_imp[1:]]
+    suffix = -np.inf
+    for v in reversed(rest):
+        if v < suffix - tol:
+            return False
+        suffix = max(suffix, v)
+    return gpu_imp[0] == ref_imp[0]   # the pinned last chunk
+
+
 @pytest.mark.slow
 def test_cfg1_greedy_and_sampled(P, golden):
-    """BASELINE config 1: greedy stream bit-exact with the reference; at
-    T=0.6 the acceptance rates agree within +-1% at the fixed seed."""
+    """BASELINE config 1 (the reference's own CPU-runnable configuration).
+
+    * initial build: the GPU's top-k ids, importance order and victim FIFO
+      are bit-exact against the oracle's selection on the GPU's own keys and
+      query; against the reference's ids (whose keys/query differ from the
+      GPU's by fp32 accumulation and bf16 rounding of the cached keys) they
+      are identical, or every difference is a near-tie within twice the
+      measured score perturbation (reference scores from make_golden.py);
+    * T = 0: the 64-token stream and per-level counts equal the reference's;
+    * T = 0.6: inner and outer acceptance rates within +-1% of the
+      reference's at the fixed seed."""
+    from oracle import hs_oracle as O
     data, meta = golden
     c = meta["cfg1"]
     tw = bf16_weights(P, P.generate_weights(P.ModelConfig(**c["target"]), 1, tied_head=False))
@@ -336,22 +366,40 @@ def test_cfg1_greedy_and_sampled(P, golden):
                             retrieval=P.RetrievalConfig(chunk_size=8, budget=256))
         sess = P.HierarchicalSession(tw, dw, prompt, spec)
         tag = f"cfg1/bf16/T{temp}"
-        imp0 = sess.retr_lane.cache.table.selected
+        tab = sess.retr_lane.cache.table
+        imp0 = tab.selected
+        rc = sess.retr_lane.cache
+        q = sess.full_lane.recorder.stash.cpu().numpy()
+        ref_imp = data[tag + "/importance0"].tolist()
+        ref_sc = data[tag + "/scores0"]
+        for li in range(2):
+            # exact: the oracle's selection on the GPU's inputs
+            K = sess.full_lane.cache.k[li, :, :4095].permute(1, 0, 2).float().cpu().numpy()
+            bounds, osc = O.chunk_scores(K, q[li], 8, 4)
+            _, oimp = O.select_chunks(osc, 32, False)
+            assert imp0[li] == oimp, li
+            assert np.array_equal(tab.scores[li], osc), li
+            pos = rc.pos[li, :rc.n_sel].cpu().numpy()
+            vict = [p for ci in reversed(oimp) for p in range(int(bounds[ci]), int(bounds[ci + 1]))]
+            assert pos[rc.ring[li, :rc.n_sel].cpu().numpy()].tolist() == vict, li
+            # vs the reference's own build
+            delta = float(np.abs(tab.scores[li] - ref_sc[li]).max())
+            same = imp0[li] == ref_imp[li]
+            print(f"cfg1 T={temp} layer {li}: ids {'identical' if same else 'differ'} to the reference; "
+                  f"max |score - ref score| = {delta:.3g}")
+            assert same or _delta_consistent(imp0[li], ref_imp[li], ref_sc[li], delta), li
         out, tr = sess.generate()
         st = data[tag + "/stats"].tolist()
         s = tr.summary()
+        ref_rates = (st[1] / st[0], st[4] / st[3])
+        agree = next((i for i, (a, b) in enumerate(zip(out[4096:], data[tag + "/tokens"].tolist())) if a != b), 64)
+        print(f"cfg1 T={temp}: GPU {s}; reference stats {st}; streams agree on {agree}/64 tokens")
         if temp == 0.0:
             assert out[4096:] == data[tag + "/tokens"].tolist()
-            # top-k ids of the initial build: near-ties may differ only through q rounding
-            same = sum(a == b for a, b in zip(imp0, data[tag + "/importance0"].tolist()))
-            assert same >= 1
-        else:
-            # same uniforms, same protocol: the sampled stream replays the
-            # reference until the first sub-1e-5 probability difference flips a
-            # draw (statistical agreement is test_sampled_acceptance_rates)
-            ref = data[tag + "/tokens"].tolist()
-            agree = next((i for i, (a, b) in enumerate(zip(out[4096:], ref)) if a != b), len(ref))
-            assert agree >= 32, agree
+            assert [s["inner"]["proposed"], s["inner"]["accepted"], s["inner"]["rounds"],
+                    s["outer"]["proposed"], s["outer"]["accepted"], s["outer"]["rounds"]] == st[:6]
+        assert abs(s["inner"]["rate"] - ref_rates[0]) <= 0.01, (s, st)
+        assert abs(s["outer"]["rate"] - ref_rates[1]) <= 0.01, (s, st)
 
 
 def _desk(P, seed):
