@@ -10,11 +10,28 @@
 // and uploads its uniforms in order; kernels consume them through a device
 // cursor, one per sampling event and one per verification -- exactly the
 // reference's consumption order (speculation.py:9-12).
+//
+// Parallel form: every vocabulary row is processed by one thread-block
+// cluster of SMP_CL CTAs (CTA rank r owns the contiguous vocabulary slice r,
+// each thread a contiguous segment of it held in registers).  Row-wide max /
+// argmax / sums / the inverse-CDF prefix are reduced through distributed
+// shared memory in a fixed order (thread segment -> warp -> CTA -> CTA rank),
+// so every result is deterministic and independent of the launch.  These
+// kernels sit on the inner loop's critical path, where one 1024-thread CTA
+// walking 32,000 entries was latency-bound (25-47 us); the cluster form
+// keeps all of a row's loads in flight at once.
+#include <cooperative_groups.h>
+
 #include "hs_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace hs {
 
-constexpr int SMP_THREADS = 1024;
+constexpr int SMP_CL = 8;          // CTAs per row (portable cluster size)
+constexpr int SMP_THREADS = 512;
+constexpr int SMP_WARPS = SMP_THREADS / 32;
+constexpr int SEG_REG = 16;        // register-resident entries per thread (V <= 65,536)
 
 struct ArgMax { double v; int i; };
 
@@ -23,219 +40,355 @@ __device__ __forceinline__ ArgMax amax(ArgMax a, ArgMax b) {
   return a;
 }
 
-__device__ ArgMax block_argmax(ArgMax x) {
-  __shared__ double sv[SMP_THREADS / 32];
-  __shared__ int si[SMP_THREADS / 32];
+// Cluster-wide reductions.  Each call publishes this CTA's partial in one of
+// two shared slots (alternating per call), synchronises the cluster once and
+// reads every rank's partial in rank order.  A slot is rewritten two calls
+// later, after the intervening cluster barrier: by then every CTA has
+// finished reading it.
+struct ClRed {
+  double d[2];
+  int i[2];
+};
+
+struct Seg {   // this thread's contiguous slice [j0, j1) of the row
+  int j0, j1;
+};
+
+__device__ __forceinline__ Seg my_seg(int V) {
+  const int per_cta = (V + SMP_CL - 1) / SMP_CL;
+  const int rank = (int)cg::this_cluster().block_rank();
+  const int c0 = rank * per_cta, c1 = min(V, c0 + per_cta);
+  const int per = (per_cta + SMP_THREADS - 1) / SMP_THREADS;
+  const int j0 = min(c1, c0 + (int)threadIdx.x * per);
+  return Seg{j0, min(c1, j0 + per)};
+}
+
+class Cl {
+ public:
+  __device__ Cl(ClRed *slots, double *wd, int *wi) : s_(slots), wd_(wd), wi_(wi), k_(0) {}
+
+  __device__ ArgMax argmax(ArgMax x) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ArgMax y;
-    y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
-    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
-    x = amax(x, y);
-  }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) { sv[w] = x.v; si[w] = x.i; }
-  __syncthreads();
-  ArgMax r = {sv[0], si[0]};
-  for (int k = 1; k < (int)(blockDim.x >> 5); ++k) r = amax(r, ArgMax{sv[k], si[k]});
-  return r;
-}
-
-__device__ double block_sum(double x) {
-  __shared__ double sw[SMP_THREADS / 32];
-  x = warp_sum(x);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) sw[w] = x;
-  __syncthreads();
-  double r = 0.0;
-  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r += sw[k];
-  return r;
-}
-
-__device__ int block_count(int x) {
-  __shared__ int sc[SMP_THREADS / 32];
-  x = warp_sum(x);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) sc[w] = x;
-  __syncthreads();
-  int r = 0;
-  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) r += sc[k];
-  return r;
-}
-
-// probs of one logits row into p (fp64); whole block participates
-__device__ void row_probs(const float *logits, int V, double T, double *p) {
-  if (T == 0.0) {
-    ArgMax best = {-INFINITY, 0x7fffffff};
-    for (int j = threadIdx.x; j < V; j += blockDim.x) best = amax(best, ArgMax{(double)logits[j], j});
-    best = block_argmax(best);
-    for (int j = threadIdx.x; j < V; j += blockDim.x) p[j] = (j == best.i) ? 1.0 : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax y;
+      y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+      y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+      x = amax(x, y);
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { wd_[w] = x.v; wi_[w] = x.i; }
     __syncthreads();
+    const int b = k_++ & 1;
+    if (threadIdx.x == 0) {
+      ArgMax r = {wd_[0], wi_[0]};
+      for (int k = 1; k < SMP_WARPS; ++k) r = amax(r, ArgMax{wd_[k], wi_[k]});
+      s_->d[b] = r.v;
+      s_->i[b] = r.i;
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    ArgMax r = {-INFINITY, 0x7fffffff};
+    for (int c = 0; c < SMP_CL; ++c) {
+      const ClRed *o = cl.map_shared_rank(s_, c);
+      r = amax(r, ArgMax{o->d[b], o->i[b]});
+    }
+    return r;
+  }
+
+  // fixed-order sum; `excl` (optional) receives the sum over lower CTA ranks
+  __device__ double sum(double x, double *excl = nullptr) {
+    x = warp_sum(x);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) wd_[w] = x;
+    __syncthreads();
+    const int b = k_++ & 1;
+    if (threadIdx.x == 0) {
+      double r = 0.0;
+      for (int k = 0; k < SMP_WARPS; ++k) r += wd_[k];
+      s_->d[b] = r;
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int me = (int)cl.block_rank();
+    double r = 0.0, e = 0.0;
+    for (int c = 0; c < SMP_CL; ++c) {
+      const double v = cl.map_shared_rank(s_, c)->d[b];
+      if (c == me) e = r;
+      r += v;
+    }
+    if (excl) *excl = e;
+    return r;
+  }
+
+  __device__ int count(int x) {
+    x = warp_sum(x);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) wi_[w] = x;
+    __syncthreads();
+    const int b = k_++ & 1;
+    if (threadIdx.x == 0) {
+      int r = 0;
+      for (int k = 0; k < SMP_WARPS; ++k) r += wi_[k];
+      s_->i[b] = r;
+    }
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    int r = 0;
+    for (int c = 0; c < SMP_CL; ++c) r += cl.map_shared_rank(s_, c)->i[b];
+    return r;
+  }
+
+  // exclusive prefix (over the whole row, in entry order) of this thread's
+  // segment total: CTA ranks below, then warps below, then lanes below
+  __device__ double exclusive_prefix(double local) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __syncthreads();   // wd_ may still be read by a previous reduction
+    if (lane == 31) wd_[wid] = incl;
+    __syncthreads();
+    double wbase = 0.0, cta = 0.0;
+    for (int k = 0; k < SMP_WARPS; ++k) {
+      if (k == wid) wbase = cta;
+      cta += wd_[k];
+    }
+    __syncthreads();
+    double rank_base;
+    sum_total_(cta, &rank_base);
+    double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = 0.0;
+    return rank_base + wbase + excl;
+  }
+
+  // every CTA must pass this before any exits (its shared memory may still be
+  // read by a peer)
+  __device__ void finish() { cg::this_cluster().sync(); }
+
+ private:
+  __device__ void sum_total_(double cta_total, double *excl) {
+    const int b = k_++ & 1;
+    if (threadIdx.x == 0) s_->d[b] = cta_total;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const int me = (int)cl.block_rank();
+    double r = 0.0, e = 0.0;
+    for (int c = 0; c < SMP_CL; ++c) {
+      const double v = cl.map_shared_rank(s_, c)->d[b];
+      if (c == me) e = r;
+      r += v;
+    }
+    *excl = e;
+  }
+
+  ClRed *s_;
+  double *wd_;
+  int *wi_;
+  int k_;
+};
+
+#define HS_CL_SETUP                      \
+  __shared__ ClRed cl_slots_;            \
+  __shared__ double cl_wd_[SMP_WARPS];   \
+  __shared__ int cl_wi_[SMP_WARPS];      \
+  Cl cl(&cl_slots_, cl_wd_, cl_wi_);
+
+// argmax over this thread's segment (all loads issued before the compares)
+__device__ __forceinline__ ArgMax seg_argmax(const float *logits, Seg s) {
+  const int n = s.j1 - s.j0;
+  float x[SEG_REG];
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i) x[i] = i < n ? logits[s.j0 + i] : -INFINITY;
+  ArgMax best = {-INFINITY, 0x7fffffff};
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i)
+    if (i < n) best = amax(best, ArgMax{(double)x[i], s.j0 + i});
+  return best;
+}
+
+// probs of one logits row into p (fp64), whole cluster
+__device__ void row_probs(Cl &cl, const float *logits, int V, double T, double *p) {
+  const Seg s = my_seg(V);
+  const int n = s.j1 - s.j0;
+  if (T == 0.0) {
+    const ArgMax best = cl.argmax(seg_argmax(logits, s));
+    for (int j = s.j0; j < s.j1; ++j) p[j] = (j == best.i) ? 1.0 : 0.0;
     return;
   }
+  double x[SEG_REG];
   ArgMax mx = {-INFINITY, 0};
-  for (int j = threadIdx.x; j < V; j += blockDim.x) mx = amax(mx, ArgMax{(double)logits[j] / T, j});
-  mx = block_argmax(mx);
-  double s = 0.0;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) {
-    const double e = exp((double)logits[j] / T - mx.v);
-    p[j] = e;
-    s += e;
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i) {
+    x[i] = i < n ? (double)logits[s.j0 + i] / T : -INFINITY;
+    if (i < n) mx = amax(mx, ArgMax{x[i], s.j0 + i});
   }
-  s = block_sum(s);
-  for (int j = threadIdx.x; j < V; j += blockDim.x) p[j] = p[j] / s;
-  __syncthreads();
+  mx = cl.argmax(mx);
+  double loc = 0.0;
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i) {
+    x[i] = i < n ? exp(x[i] - mx.v) : 0.0;
+    loc += x[i];
+  }
+  const double tot = cl.sum(loc);
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i)
+    if (i < n) p[s.j0 + i] = x[i] / tot;
 }
 
 // inverse CDF: min(#{j : cumsum(w/scale)_j <= u}, V-1); w optionally the
-// residual max(p - q, 0) (computed on the fly); whole block participates.
-// Each thread owns a contiguous segment of up to SEG_REG entries held in
-// registers (one pass over memory, loads all in flight); the cumulative sum
-// is segment-sequential after an exclusive block scan of segment totals --
-// a fixed order, so the draw is deterministic.
-constexpr int SEG_REG = 32;
-
-__device__ int inv_cdf(const double *p, const double *q, double scale, int V, double u) {
-  __shared__ double seg[64];
-  const int per = (V + blockDim.x - 1) / blockDim.x;
-  const int j0 = threadIdx.x * per, j1 = min(V, j0 + per);
-  auto w = [&](int j) {
-    double x = q ? fmax(p[j] - q[j], 0.0) : p[j];
-    return scale == 1.0 ? x : x / scale;
-  };
-  double wr[SEG_REG];
+// residual max(p - q, 0).  The cumulative sum is segment-sequential after
+// the fixed-order exclusive prefix of the segment totals (deterministic).
+__device__ int inv_cdf(Cl &cl, const double *p, const double *q, double scale, int V, double u) {
+  const Seg s = my_seg(V);
+  const int n = s.j1 - s.j0;
+  double w[SEG_REG];
   double local = 0.0;
-  if (per <= SEG_REG) {
 #pragma unroll
-    for (int i = 0; i < SEG_REG; ++i) wr[i] = (i < per && j0 + i < j1) ? w(j0 + i) : 0.0;
-#pragma unroll
-    for (int i = 0; i < SEG_REG; ++i) local += wr[i];
-  } else {
-    for (int j = j0; j < j1; ++j) local += w(j);
-  }
-  // exclusive scan of the segment totals: warp scan, then scan of warp totals
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double incl = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  __syncthreads();
-  if (lane == 31) seg[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    double wt = (lane < (int)(blockDim.x >> 5)) ? seg[lane] : 0.0;
-    double wi = wt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += y;
+  for (int i = 0; i < SEG_REG; ++i) {
+    double x = 0.0;
+    if (i < n) {
+      x = q ? fmax(p[s.j0 + i] - q[s.j0 + i], 0.0) : p[s.j0 + i];
+      if (scale != 1.0) x = x / scale;
     }
-    double we = __shfl_up_sync(0xffffffffu, wi, 1);
-    seg[32 + lane] = (lane == 0) ? 0.0 : we;   // exclusive warp base
+    w[i] = x;
+    local += x;
   }
-  __syncthreads();
-  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
-  if (lane == 0) excl = 0.0;
-  double c = seg[32 + wid] + excl;
+  double c = cl.exclusive_prefix(local);
   int cnt = 0;
-  if (per <= SEG_REG) {
 #pragma unroll
-    for (int i = 0; i < SEG_REG; ++i) {
-      if (i < per && j0 + i < j1) {
-        c += wr[i];
-        cnt += (c <= u) ? 1 : 0;
-      }
-    }
-  } else {
-    for (int j = j0; j < j1; ++j) {
-      c += w(j);
+  for (int i = 0; i < SEG_REG; ++i) {
+    if (i < n) {
+      c += w[i];
       cnt += (c <= u) ? 1 : 0;
     }
   }
-  cnt = block_count(cnt);
+  cnt = cl.count(cnt);
   return cnt < V - 1 ? cnt : V - 1;
 }
 
+__device__ double residual_mass(Cl &cl, const double *p, const double *q, int V) {
+  const Seg s = my_seg(V);
+  const int n = s.j1 - s.j0;
+  double a[SEG_REG], b[SEG_REG];
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i) {
+    a[i] = i < n ? p[s.j0 + i] : 0.0;
+    b[i] = i < n ? q[s.j0 + i] : 0.0;
+  }
+  double z = 0.0;
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i) z += fmax(a[i] - b[i], 0.0);
+  return cl.sum(z);
+}
+
+__device__ __forceinline__ bool cl_leader() { return cg::this_cluster().block_rank() == 0 && threadIdx.x == 0; }
+
+// one cluster per row
 __global__ void __launch_bounds__(SMP_THREADS) probs_kernel(const float *logits, int V, double T, double *probs) {
-  row_probs(logits + (size_t)blockIdx.x * V, V, T, probs + (size_t)blockIdx.x * V);
+  pdl_wait();
+  HS_CL_SETUP
+  const size_t row = blockIdx.x / SMP_CL;
+  row_probs(cl, logits + row * V, V, T, probs + row * V);
+  pdl_trigger();
+  cl.finish();
 }
 
 __global__ void __launch_bounds__(SMP_THREADS) sample_kernel(const double *probs, int V, const double *U,
                                                              int32_t *cursor, int32_t *out) {
+  pdl_wait();
+  HS_CL_SETUP
   const int cur = *cursor;
-  const int tok = inv_cdf(probs, nullptr, 1.0, V, U[cur]);
-  __syncthreads();
-  if (threadIdx.x == 0) { *out = tok; *cursor = cur + 1; }
+  const int tok = inv_cdf(cl, probs, nullptr, 1.0, V, U[cur]);
+  cl.finish();   // every CTA has read the cursor
+  if (cl_leader()) { *out = tok; *cursor = cur + 1; }
 }
 
 __global__ void __launch_bounds__(SMP_THREADS) draft_sample_kernel(const float *logits, int V, double T,
                                                                    double *probs, const double *U,
                                                                    int32_t *cursor, int32_t *out) {
+  pdl_wait();
+  HS_CL_SETUP
   const int cur = *cursor;
+  int tok;
   if (T == 0.0) {
     // one-hot argmax row; its inverse CDF at any u in [0, 1) is the argmax
     // itself (model.py:198-202 with a one-hot p), so skip the scan
-    ArgMax best = {-INFINITY, 0x7fffffff};
-    for (int j = threadIdx.x; j < V; j += blockDim.x) best = amax(best, ArgMax{(double)logits[j], j});
-    best = block_argmax(best);
-    for (int j = threadIdx.x; j < V; j += blockDim.x) probs[j] = (j == best.i) ? 1.0 : 0.0;
-    if (threadIdx.x == 0) { *out = best.i < V ? best.i : V - 1; *cursor = cur + 1; }
-    return;
+    const Seg s = my_seg(V);
+    const ArgMax best = cl.argmax(seg_argmax(logits, s));
+    for (int j = s.j0; j < s.j1; ++j) probs[j] = (j == best.i) ? 1.0 : 0.0;
+    tok = best.i < V ? best.i : V - 1;
+  } else {
+    row_probs(cl, logits, V, T, probs);
+    // each thread scans exactly the segment it has just written (same my_seg)
+    tok = inv_cdf(cl, probs, nullptr, 1.0, V, U[cur]);
   }
-  row_probs(logits, V, T, probs);
-  const int tok = inv_cdf(probs, nullptr, 1.0, V, U[cur]);
-  __syncthreads();
-  if (threadIdx.x == 0) { *out = tok; *cursor = cur + 1; }
+  pdl_trigger();
+  cl.finish();
+  if (cl_leader()) { *out = tok; *cursor = cur + 1; }
 }
 
-// _verify_chain: result[0..n] tokens, [n+1] count, [n+2] accepted, [n+3] status
+// _verify_chain: result[0..n] tokens, [n+1] count, [n+2] accepted, [n+3] status.
+// Every CTA of the cluster evaluates the (short) accept chain redundantly:
+// thread i checks proposal i with uniform U[cur + i], which is the uniform
+// the sequential loop gives it whenever all earlier proposals were accepted;
+// the first failing proposal ends the chain.  The row-wide residual sum and
+// the correction / bonus draw then run on the whole cluster.
 __global__ void __launch_bounds__(SMP_THREADS) verify_chain_kernel(const int32_t *tokens, int n, const double *qd,
                                                                    const double *pd, int V, const double *U,
                                                                    int32_t *cursor, int32_t *result) {
-  int cur = *cursor;
-  int i = 0;
-  int status = 0;
-  for (; i < n; ++i) {
+  pdl_wait();
+  HS_CL_SETUP
+  __shared__ int first_s, bad_s;
+  const int cur = *cursor;
+  if (threadIdx.x == 0) { first_s = n; bad_s = 0; }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += SMP_THREADS) {
     const int x = tokens[i];
     const double qx = qd[(size_t)i * V + x];
     const double px = pd[(size_t)i * V + x];
-    if (!(qx > 0.0)) { status = HS_ERR_CONTRACT; break; }
-    const double ratio = px / qx;
-    const double u = U[cur++];
-    if (u < fmin(1.0, ratio)) {
-      if (threadIdx.x == 0) result[i] = x;
-      continue;
-    }
-    // correct_token: residual max(p - q, 0); Z <= 1e-12 -> sample p
-    const double *p = pd + (size_t)i * V, *q = qd + (size_t)i * V;
-    double z = 0.0;
-    for (int j = threadIdx.x; j < V; j += blockDim.x) z += fmax(p[j] - q[j], 0.0);
-    z = block_sum(z);
-    const double u2 = U[cur++];
-    const int tok = (z <= 1e-12) ? inv_cdf(p, nullptr, 1.0, V, u2) : inv_cdf(p, q, z, V, u2);
-    if (threadIdx.x == 0) { result[i] = tok; result[n + 1] = i + 1; result[n + 2] = i; }
-    break;
-  }
-  if (status == 0 && i == n) {
-    const double u = U[cur++];
-    const int tok = inv_cdf(pd + (size_t)n * V, nullptr, 1.0, V, u);
-    if (threadIdx.x == 0) { result[n] = tok; result[n + 1] = n + 1; result[n + 2] = n; }
+    const bool fail = !(qx > 0.0) || !(U[cur + i] < fmin(1.0, px / qx));
+    if (fail) atomicMin(&first_s, i);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  const int r = first_s;
+  if (r < n && threadIdx.x == 0) bad_s = !(qd[(size_t)r * V + tokens[r]] > 0.0);
+  __syncthreads();
+  const int status = bad_s ? HS_ERR_CONTRACT : 0;
+  int tok = 0, used = 0;
+  if (!status) {
+    if (r < n) {
+      // correct_token: residual max(p - q, 0); Z <= 1e-12 -> sample p
+      const double *p = pd + (size_t)r * V, *q = qd + (size_t)r * V;
+      const double z = residual_mass(cl, p, q, V);
+      const double u2 = U[cur + r + 1];
+      tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, u2) : inv_cdf(cl, p, q, z, V, u2);
+      used = r + 2;
+    } else {
+      tok = inv_cdf(cl, pd + (size_t)n * V, nullptr, 1.0, V, U[cur + n]);
+      used = n + 1;
+    }
+  }
+  pdl_trigger();
+  cl.finish();   // every CTA has read the cursor and its peers' partials
+  if (cl_leader()) {
+    if (!status) {
+      for (int i = 0; i < r; ++i) result[i] = tokens[i];
+      result[r] = tok;
+      result[n + 1] = r + 1;
+      result[n + 2] = r;
+      *cursor = cur + used;
+    } else {
+      *cursor = cur + r;   // the uniforms of the accepted proposals before the failure
+    }
     result[n + 3] = status;
-    *cursor = cur;
   }
 }
 
-__global__ void __launch_bounds__(SMP_THREADS) verify_token_kernel(int x, const double *q, const double *p,
-                                                                   const double *U, int32_t *cursor,
-                                                                   int32_t *result) {
+__global__ void __launch_bounds__(32) verify_token_kernel(int x, const double *q, const double *p, const double *U,
+                                                          int32_t *cursor, int32_t *result) {
   if (threadIdx.x != 0) return;
   const int cur = *cursor;
   const double qx = q[x];
@@ -248,13 +401,41 @@ __global__ void __launch_bounds__(SMP_THREADS) verify_token_kernel(int x, const 
 __global__ void __launch_bounds__(SMP_THREADS) correct_token_kernel(const double *q, const double *p, int V,
                                                                     const double *U, int32_t *cursor,
                                                                     int32_t *out) {
+  pdl_wait();
+  HS_CL_SETUP
   const int cur = *cursor;
-  double z = 0.0;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) z += fmax(p[j] - q[j], 0.0);
-  z = block_sum(z);
-  const int tok = (z <= 1e-12) ? inv_cdf(p, nullptr, 1.0, V, U[cur]) : inv_cdf(p, q, z, V, U[cur]);
-  __syncthreads();
-  if (threadIdx.x == 0) { *out = tok; *cursor = cur + 1; }
+  const double z = residual_mass(cl, p, q, V);
+  const int tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, U[cur]) : inv_cdf(cl, p, q, z, V, U[cur]);
+  cl.finish();
+  if (cl_leader()) { *out = tok; *cursor = cur + 1; }
+}
+
+// cluster launch (one SMP_CL-CTA cluster per row), a programmatic dependent
+// of the previous kernel on the stream
+template <typename... KArgs, typename... Args>
+static int launch_rows(const char *what, void (*kern)(KArgs...), int rows, cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(rows * SMP_CL);
+  cfg.blockDim = dim3(SMP_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = SMP_CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1 + pdl_enabled();
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return check_launch(what);
+}
+
+static int check_vocab(int V) {
+  HS_REQUIRE(V >= 1 && V <= SMP_CL * SMP_THREADS * SEG_REG, HS_ERR_VALUE, "sampling: vocabulary size %d outside [1, %d]",
+             V, SMP_CL * SMP_THREADS * SEG_REG);
+  return HS_OK;
 }
 
 }  // namespace hs
@@ -267,36 +448,42 @@ extern "C" int hs_verify_token(int32_t x, const double *q, const double *p, cons
 
 extern "C" int hs_correct_token(const double *q, const double *p, int V, const double *uniforms,
                                 int32_t *cursor, int32_t *out, void *stream) {
-  hs::correct_token_kernel<<<1, hs::SMP_THREADS, 0, hs::as_stream(stream)>>>(q, p, V, uniforms, cursor, out);
-  return hs::check_launch("correct_token");
+  int rc = hs::check_vocab(V);
+  if (rc != HS_OK) return rc;
+  return hs::launch_rows("correct_token", hs::correct_token_kernel, 1, hs::as_stream(stream), q, p, V, uniforms,
+                         cursor, out);
 }
 
 extern "C" int hs_probs(const float *logits, int rows, int V, double temperature, double *probs, void *stream) {
   if (temperature < 0) return hs::set_error(HS_ERR_VALUE, "temperature must be >= 0");
   if (rows <= 0) return HS_OK;
-  hs::probs_kernel<<<rows, hs::SMP_THREADS, 0, hs::as_stream(stream)>>>(logits, V, temperature, probs);
-  return hs::check_launch("probs");
+  int rc = hs::check_vocab(V);
+  if (rc != HS_OK) return rc;
+  return hs::launch_rows("probs", hs::probs_kernel, rows, hs::as_stream(stream), logits, V, temperature, probs);
 }
 
 extern "C" int hs_sample(const double *probs, int V, const double *uniforms, int32_t *cursor, int32_t *out,
                          void *stream) {
-  hs::sample_kernel<<<1, hs::SMP_THREADS, 0, hs::as_stream(stream)>>>(probs, V, uniforms, cursor, out);
-  return hs::check_launch("sample");
+  int rc = hs::check_vocab(V);
+  if (rc != HS_OK) return rc;
+  return hs::launch_rows("sample", hs::sample_kernel, 1, hs::as_stream(stream), probs, V, uniforms, cursor, out);
 }
 
 extern "C" int hs_draft_sample(const float *logits, int V, double temperature, double *probs_out,
                                const double *uniforms, int32_t *cursor, int32_t *out, void *stream) {
   if (temperature < 0) return hs::set_error(HS_ERR_VALUE, "temperature must be >= 0");
   if (!probs_out) return hs::set_error(HS_ERR_VALUE, "draft_sample: probs_out required");
-  hs::draft_sample_kernel<<<1, hs::SMP_THREADS, 0, hs::as_stream(stream)>>>(logits, V, temperature, probs_out,
-                                                                           uniforms, cursor, out);
-  return hs::check_launch("draft_sample");
+  int rc = hs::check_vocab(V);
+  if (rc != HS_OK) return rc;
+  return hs::launch_rows("draft_sample", hs::draft_sample_kernel, 1, hs::as_stream(stream), logits, V, temperature,
+                         probs_out, uniforms, cursor, out);
 }
 
 extern "C" int hs_verify_chain(const int32_t *tokens, int n, const double *qd, const double *pd, int V,
                                const double *uniforms, int32_t *cursor, int32_t *result, void *stream) {
   if (n < 0) return hs::set_error(HS_ERR_VALUE, "verify_chain: n < 0");
-  hs::verify_chain_kernel<<<1, hs::SMP_THREADS, 0, hs::as_stream(stream)>>>(tokens, n, qd, pd, V, uniforms,
-                                                                           cursor, result);
-  return hs::check_launch("verify_chain");
+  int rc = hs::check_vocab(V);
+  if (rc != HS_OK) return rc;
+  return hs::launch_rows("verify_chain", hs::verify_chain_kernel, 1, hs::as_stream(stream), tokens, n, qd, pd, V,
+                         uniforms, cursor, result);
 }

@@ -82,8 +82,14 @@ def test_cfg1_prefill_and_queries(P, golden):
     cache = P.FullCache.from_config(cfg)
     rec = P.ForwardRecorder()
     lg = P.prefill(w, prompt, cache, rec)
-    assert np.allclose(lg[-1], data["cfg1/bf16/prefill_last"], rtol=1e-4, atol=1e-5)
-    assert np.allclose(np.stack(rec.last_queries), data["cfg1/bf16/q_last"], rtol=1e-4, atol=1e-5)
+    ref_lg, ref_q = data["cfg1/bf16/prefill_last"], data["cfg1/bf16/q_last"]
+    e_lg = np.abs(lg[-1] - ref_lg).max() / np.abs(ref_lg).max()
+    e_q = np.abs(np.stack(rec.last_queries) - ref_q).max() / np.abs(ref_q).max()
+    print(f"cfg1 prefill: logits max err / max |logit| = {e_lg:.3g}, queries {e_q:.3g}")
+    # fp32 accumulation (GPU) vs fp64 accumulation rounded to fp32 (reference)
+    # over 4,096 positions, 2 layers: a few 1e-7 of the largest value
+    assert e_lg < 1e-5 and e_q < 1e-5, (e_lg, e_q)
+    assert lg[-1].argmax() == ref_lg.argmax()
 
 
 def test_errors(P):
@@ -378,7 +384,8 @@ def test_cfg1_greedy_and_sampled(P, golden):
             bounds, osc = O.chunk_scores(K, q[li], 8, 4)
             _, oimp = O.select_chunks(osc, 32, False)
             assert imp0[li] == oimp, li
-            assert np.array_equal(tab.scores[li], osc), li
+            # same fp64 arithmetic up to the order of the 8-key chunk sums
+            assert np.allclose(tab.scores[li], osc, rtol=1e-12, atol=1e-15 * np.abs(osc).max()), li
             pos = rc.pos[li, :rc.n_sel].cpu().numpy()
             vict = [p for ci in reversed(oimp) for p in range(int(bounds[ci]), int(bounds[ci + 1]))]
             assert pos[rc.ring[li, :rc.n_sel].cpu().numpy()].tolist() == vict, li
