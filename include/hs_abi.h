@@ -138,6 +138,28 @@ int hs_comm_destroy(void *comm);
 int hs_all_gather(void *comm, const void *send, void *recv, size_t bytes, void *stream);
 /* in-place sum; dtype 0 bf16, 1 f32, 2 f64, 3 i32                          */
 int hs_all_reduce_sum(void *comm, void *buf, size_t count, int dtype, void *stream);
+/* recv = every rank's send block of bytes_per_rank[r] bytes, concatenated in
+ * rank order (variable-size all-gather: grouped NCCL broadcasts)           */
+int hs_all_gather_v(void *comm, int rank, int world, const void *send, void *recv,
+                    const size_t *bytes_per_rank, void *stream);
+/* HS_OK, or the communicator's asynchronous error (NCCL) / a broken
+ * loopback group.  NCCL communicators are created non-blocking and every
+ * call is bounded by HS_NCCL_TIMEOUT_S seconds (default 300): a peer that
+ * never arrives aborts the communicator and returns HS_ERR_CUDA.          */
+int hs_comm_check(void *comm);
+/* In-process loopback group of `world` ranks on one device: comms[r] is rank
+ * r's communicator (use it in HsShard.comm from rank r's host thread and
+ * stream).  Collectives are device-to-device copies with the NCCL calls'
+ * semantics, so G-shard sessions run (and are tested) on one GPU.         */
+int hs_loopback_create(int world, void **comms);
+int hs_loopback_destroy(void *any_comm_of_the_group);
+/* Replicated retrieval cache after a sharded build (caches.py:458-502 over
+ * a sequence-sharded source): ranges [layer][rank][2] (host int32) are the
+ * slot ranges each rank filled from its own shard; per layer every rank's
+ * K/V block is all-gathered (variable sizes) and unpacked into its slots.  */
+size_t hs_retrieval_exchange_workspace_bytes(const HsCache *c);
+int hs_retrieval_exchange(const HsShard *sh, const HsCache *c, const int32_t *ranges, void *workspace,
+                          size_t ws_bytes, void *stream);
 
 /* ---- fused forward (model.py:247-331) -----------------------------------
  * t tokens (device int32) at st->pos0 through all layers: RMSNorm+QKV GEMV,
@@ -280,8 +302,9 @@ int hs_chunk_select(const double *scores, int n_layers, int n_chunks, int upto, 
 /* gather of the chosen chunks into the retrieval cache slots, position order
  * (st.push(K[sel_idx], ...) caches.py:490-493).  src is a LINEAR cache
  * holding positions [src_lo, src_hi) (a sequence shard; 0, 0 = unsharded);
- * chunks outside it are written as zeros (a sum all-reduce then assembles
- * the selection across shards).                                             */
+ * the K/V slots of chunks outside it are left untouched (positions are
+ * written for every chunk); hs_retrieval_exchange then fills them from their
+ * owner ranks.                                                              */
 int hs_retrieval_gather(const HsCache *src, const HsCache *dst, const int32_t *chosen,
                         int chosen_stride, int n_chosen, int chunk, int upto, int src_lo, int src_hi,
                         void *stream);

@@ -110,6 +110,12 @@ _SIGS = {
     "hs_comm_destroy": (i32, [vp]),
     "hs_all_gather": (i32, [vp, vp, vp, sz, vp]),
     "hs_all_reduce_sum": (i32, [vp, vp, sz, i32, vp]),
+    "hs_all_gather_v": (i32, [vp, i32, i32, vp, vp, vp, vp]),
+    "hs_comm_check": (i32, [vp]),
+    "hs_loopback_create": (i32, [i32, vp]),
+    "hs_loopback_destroy": (i32, [vp]),
+    "hs_retrieval_exchange_workspace_bytes": (sz, [_P(HsCache)]),
+    "hs_retrieval_exchange": (i32, [_P(HsShard), _P(HsCache), vp, vp, sz, vp]),
 }
 
 

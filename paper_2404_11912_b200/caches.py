@@ -686,10 +686,7 @@ class RetrievalCache(KVCache):
         check(lib.hs_retrieval_gather(source._ref, self._ref, ptr(self.chosen), self.quota, n_chosen,
                                       cfg.chunk_size, upto, source.lo, source.hi or 0, stream_ptr()))
         if source.sharded:
-            # every rank wrote the chunks it owns and zeros elsewhere: x + 0 is
-            # exact in bf16, so the sum assembles the selection on every rank
-            source.shards.all_reduce_sum_(self.k)
-            source.shards.all_reduce_sum_(self.v)
+            self._exchange(source, n_chosen, upto)
         self.ring_head = 0
         self.n_spec = [0] * self.n_layers
         self.frontier = self.committed = upto
@@ -699,6 +696,27 @@ class RetrievalCache(KVCache):
         self.table = ChunkScoreTable(cfg.chunk_size, upto, self.n_layers, scores, self.importance, n_chosen,
                                      clamped)
         return self.table
+
+    def _exchange(self, source: FullCache, n_chosen: int, upto: int) -> None:
+        """Sharded build: every rank has gathered the chosen chunks it stores
+        (chunks never straddle shards, and the chosen list is ascending, so
+        each rank's chunks are one contiguous slot range per layer).  The
+        ranges are exchanged so every rank holds the whole selection -- each
+        byte crosses the fabric once (hs_retrieval_exchange)."""
+        cfg, sh = self.config, source.shards
+        ch = self.chosen[:, :n_chosen].cpu().numpy().astype(np.int64)      # replicated selection
+        los = np.array([lo for lo, _ in source.bounds], dtype=np.int64)
+        owner = np.searchsorted(los, ch * cfg.chunk_size, side="right") - 1  # [L, n_chosen]
+        ranges = np.zeros((self.n_layers, sh.world, 2), dtype=np.int32)
+        for l in range(self.n_layers):
+            first = np.searchsorted(owner[l], np.arange(sh.world), side="left")
+            last = np.searchsorted(owner[l], np.arange(sh.world), side="right")
+            ranges[l, :, 0] = np.minimum(first * cfg.chunk_size, self.n_sel)
+            ranges[l, :, 1] = np.minimum(last * cfg.chunk_size, self.n_sel)
+        nb = lib.hs_retrieval_exchange_workspace_bytes(self._ref)
+        from .runtime import workspaces
+        ws = workspaces.get("retrieval_exchange", nb)
+        check(lib.hs_retrieval_exchange(sh.ref, self._ref, ranges.ctypes.data, ptr(ws), nb, stream_ptr()))
 
     def _score(self, source: FullCache, q: torch.Tensor, upto: int, n: int) -> torch.Tensor:
         """fp64 chunk scores [L, n] of source positions [0, upto).  Sharded:

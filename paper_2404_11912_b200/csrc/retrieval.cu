@@ -230,8 +230,8 @@ __global__ void __launch_bounds__(SEL_THREADS) chunk_select_kernel(
 
 // grid (n_chosen, KVH, L): copy chunk tokens (position order) into slots j*chunk..
 // src holds positions [src_lo, src_hi) (a sequence shard; src_hi 0 = no bound);
-// chosen chunks outside it are written as zeros so that a sum all-reduce over
-// the shards assembles the full selection (chunks never straddle shards).
+// the K/V slots of chosen chunks outside it are left untouched (their owner
+// rank ships them, hs_retrieval_exchange); positions are written for all.
 __global__ void retrieval_gather_kernel(HsCache src, HsCache dst, const int32_t *chosen, int quota,
                                         int chunk, int upto, int src_lo, int src_hi) {
   const int j = blockIdx.x, kh = blockIdx.y, l = blockIdx.z, DH = src.head_dim;
@@ -248,11 +248,6 @@ __global__ void retrieval_gather_kernel(HsCache src, HsCache dst, const int32_t 
     for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
       reinterpret_cast<uint4 *>(kd)[e] = ld_stream(reinterpret_cast<const uint4 *>(ks) + e);
       reinterpret_cast<uint4 *>(vd)[e] = ld_stream(reinterpret_cast<const uint4 *>(vs) + e);
-    }
-  } else {
-    for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
-      reinterpret_cast<uint4 *>(kd)[e] = make_uint4(0, 0, 0, 0);
-      reinterpret_cast<uint4 *>(vd)[e] = make_uint4(0, 0, 0, 0);
     }
   }
   if (kh == 0)

@@ -12,8 +12,9 @@
 // reference's consumption order (speculation.py:9-12).
 //
 // Parallel form: every vocabulary row is processed by one thread-block
-// cluster of SMP_CL CTAs (CTA rank r owns the contiguous vocabulary slice r,
-// each thread a contiguous segment of it held in registers).  Row-wide max /
+// cluster of SMP_CL CTAs (CTA rank r owns the contiguous vocabulary slice r;
+// element-wise passes stride over it, the inverse CDF gives each thread a
+// contiguous segment staged in shared memory).  Row-wide max /
 // argmax / sums / the inverse-CDF prefix are reduced through distributed
 // shared memory in a fixed order (thread segment -> warp -> CTA -> CTA rank),
 // so every result is deterministic and independent of the launch.  These
@@ -196,65 +197,86 @@ class Cl {
   __shared__ int cl_wi_[SMP_WARPS];      \
   Cl cl(&cl_slots_, cl_wd_, cl_wi_);
 
-// argmax over this thread's segment (all loads issued before the compares)
-__device__ __forceinline__ ArgMax seg_argmax(const float *logits, Seg s) {
-  const int n = s.j1 - s.j0;
+// this CTA's contiguous slice [c0, c1) of the row
+__device__ __forceinline__ void cta_range(int V, int &c0, int &c1) {
+  const int per_cta = (V + SMP_CL - 1) / SMP_CL;
+  c0 = (int)cg::this_cluster().block_rank() * per_cta;
+  c1 = min(V, c0 + per_cta);
+  c0 = min(c0, V);
+}
+
+// Element-wise passes walk the CTA slice with a block stride (coalesced):
+// entry k of thread t is c0 + t + k * SMP_THREADS.  Argmax (ties to the
+// lower index) and the exp / divide passes do not depend on the order; the
+// sums are reduced in a fixed order (thread -> warp -> CTA -> rank).
+__device__ __forceinline__ ArgMax strided_argmax(const float *logits, int c0, int c1, double inv_t) {
   float x[SEG_REG];
 #pragma unroll
-  for (int i = 0; i < SEG_REG; ++i) x[i] = i < n ? logits[s.j0 + i] : -INFINITY;
+  for (int k = 0; k < SEG_REG; ++k) {
+    const int j = c0 + (int)threadIdx.x + k * SMP_THREADS;
+    x[k] = j < c1 ? logits[j] : -INFINITY;
+  }
   ArgMax best = {-INFINITY, 0x7fffffff};
 #pragma unroll
-  for (int i = 0; i < SEG_REG; ++i)
-    if (i < n) best = amax(best, ArgMax{(double)x[i], s.j0 + i});
+  for (int k = 0; k < SEG_REG; ++k) {
+    const int j = c0 + (int)threadIdx.x + k * SMP_THREADS;
+    if (j < c1) best = amax(best, ArgMax{inv_t == 1.0 ? (double)x[k] : (double)x[k] / inv_t, j});
+  }
   return best;
+}
+
+__device__ __forceinline__ void one_hot(double *p, int c0, int c1, int hot) {
+  for (int j = c0 + (int)threadIdx.x; j < c1; j += SMP_THREADS) p[j] = (j == hot) ? 1.0 : 0.0;
 }
 
 // probs of one logits row into p (fp64), whole cluster
 __device__ void row_probs(Cl &cl, const float *logits, int V, double T, double *p) {
-  const Seg s = my_seg(V);
-  const int n = s.j1 - s.j0;
+  int c0, c1;
+  cta_range(V, c0, c1);
   if (T == 0.0) {
-    const ArgMax best = cl.argmax(seg_argmax(logits, s));
-    for (int j = s.j0; j < s.j1; ++j) p[j] = (j == best.i) ? 1.0 : 0.0;
+    one_hot(p, c0, c1, cl.argmax(strided_argmax(logits, c0, c1, 1.0)).i);
     return;
   }
-  double x[SEG_REG];
-  ArgMax mx = {-INFINITY, 0};
-#pragma unroll
-  for (int i = 0; i < SEG_REG; ++i) {
-    x[i] = i < n ? (double)logits[s.j0 + i] / T : -INFINITY;
-    if (i < n) mx = amax(mx, ArgMax{x[i], s.j0 + i});
-  }
-  mx = cl.argmax(mx);
+  // max of logits / T (model.py:190-195), then exp(x / T - max) and its sum
+  const double mx = cl.argmax(strided_argmax(logits, c0, c1, T)).v;
+  double e[SEG_REG];
   double loc = 0.0;
 #pragma unroll
-  for (int i = 0; i < SEG_REG; ++i) {
-    x[i] = i < n ? exp(x[i] - mx.v) : 0.0;
-    loc += x[i];
+  for (int k = 0; k < SEG_REG; ++k) {
+    const int j = c0 + (int)threadIdx.x + k * SMP_THREADS;
+    e[k] = j < c1 ? exp((double)logits[j] / T - mx) : 0.0;
+    loc += e[k];
   }
   const double tot = cl.sum(loc);
 #pragma unroll
-  for (int i = 0; i < SEG_REG; ++i)
-    if (i < n) p[s.j0 + i] = x[i] / tot;
+  for (int k = 0; k < SEG_REG; ++k) {
+    const int j = c0 + (int)threadIdx.x + k * SMP_THREADS;
+    if (j < c1) p[j] = e[k] / tot;
+  }
 }
 
 // inverse CDF: min(#{j : cumsum(w/scale)_j <= u}, V-1); w optionally the
-// residual max(p - q, 0).  The cumulative sum is segment-sequential after
-// the fixed-order exclusive prefix of the segment totals (deterministic).
-__device__ int inv_cdf(Cl &cl, const double *p, const double *q, double scale, int V, double u) {
+// residual max(p - q, 0).  The CTA slice of w is staged in shared memory
+// with coalesced loads; the cumulative sum is then segment-sequential per
+// thread (contiguous segments) after the fixed-order exclusive prefix of the
+// segment totals (deterministic).
+__device__ int inv_cdf(Cl &cl, const double *p, const double *q, double scale, int V, double u, double *sw) {
+  int c0, c1;
+  cta_range(V, c0, c1);
+  for (int j = c0 + (int)threadIdx.x; j < c1; j += SMP_THREADS) {
+    double x = q ? fmax(p[j] - q[j], 0.0) : p[j];
+    if (scale != 1.0) x = x / scale;
+    sw[j - c0] = x;
+  }
+  __syncthreads();
   const Seg s = my_seg(V);
   const int n = s.j1 - s.j0;
   double w[SEG_REG];
   double local = 0.0;
 #pragma unroll
   for (int i = 0; i < SEG_REG; ++i) {
-    double x = 0.0;
-    if (i < n) {
-      x = q ? fmax(p[s.j0 + i] - q[s.j0 + i], 0.0) : p[s.j0 + i];
-      if (scale != 1.0) x = x / scale;
-    }
-    w[i] = x;
-    local += x;
+    w[i] = i < n ? sw[s.j0 - c0 + i] : 0.0;
+    local += w[i];
   }
   double c = cl.exclusive_prefix(local);
   int cnt = 0;
@@ -266,21 +288,19 @@ __device__ int inv_cdf(Cl &cl, const double *p, const double *q, double scale, i
     }
   }
   cnt = cl.count(cnt);
+  __syncthreads();   // sw may be restaged by a later call
   return cnt < V - 1 ? cnt : V - 1;
 }
 
 __device__ double residual_mass(Cl &cl, const double *p, const double *q, int V) {
-  const Seg s = my_seg(V);
-  const int n = s.j1 - s.j0;
-  double a[SEG_REG], b[SEG_REG];
-#pragma unroll
-  for (int i = 0; i < SEG_REG; ++i) {
-    a[i] = i < n ? p[s.j0 + i] : 0.0;
-    b[i] = i < n ? q[s.j0 + i] : 0.0;
-  }
+  int c0, c1;
+  cta_range(V, c0, c1);
   double z = 0.0;
 #pragma unroll
-  for (int i = 0; i < SEG_REG; ++i) z += fmax(a[i] - b[i], 0.0);
+  for (int k = 0; k < SEG_REG; ++k) {
+    const int j = c0 + (int)threadIdx.x + k * SMP_THREADS;
+    if (j < c1) z += fmax(p[j] - q[j], 0.0);
+  }
   return cl.sum(z);
 }
 
@@ -301,7 +321,8 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_kernel(const double *probs
   pdl_wait();
   HS_CL_SETUP
   const int cur = *cursor;
-  const int tok = inv_cdf(cl, probs, nullptr, 1.0, V, U[cur]);
+  extern __shared__ double sw[];
+  const int tok = inv_cdf(cl, probs, nullptr, 1.0, V, U[cur], sw);
   cl.finish();   // every CTA has read the cursor
   if (cl_leader()) { *out = tok; *cursor = cur + 1; }
 }
@@ -311,19 +332,21 @@ __global__ void __launch_bounds__(SMP_THREADS) draft_sample_kernel(const float *
                                                                    int32_t *cursor, int32_t *out) {
   pdl_wait();
   HS_CL_SETUP
+  extern __shared__ double sw[];
   const int cur = *cursor;
   int tok;
   if (T == 0.0) {
     // one-hot argmax row; its inverse CDF at any u in [0, 1) is the argmax
     // itself (model.py:198-202 with a one-hot p), so skip the scan
-    const Seg s = my_seg(V);
-    const ArgMax best = cl.argmax(seg_argmax(logits, s));
-    for (int j = s.j0; j < s.j1; ++j) probs[j] = (j == best.i) ? 1.0 : 0.0;
+    int c0, c1;
+    cta_range(V, c0, c1);
+    const ArgMax best = cl.argmax(strided_argmax(logits, c0, c1, 1.0));
+    one_hot(probs, c0, c1, best.i);
     tok = best.i < V ? best.i : V - 1;
   } else {
     row_probs(cl, logits, V, T, probs);
-    // each thread scans exactly the segment it has just written (same my_seg)
-    tok = inv_cdf(cl, probs, nullptr, 1.0, V, U[cur]);
+    __syncthreads();   // the CTA's slice of the row is written (it restages only its own slice)
+    tok = inv_cdf(cl, probs, nullptr, 1.0, V, U[cur], sw);
   }
   pdl_trigger();
   cl.finish();
@@ -341,6 +364,7 @@ __global__ void __launch_bounds__(SMP_THREADS) verify_chain_kernel(const int32_t
                                                                    int32_t *cursor, int32_t *result) {
   pdl_wait();
   HS_CL_SETUP
+  extern __shared__ double sw[];
   __shared__ int first_s, bad_s;
   const int cur = *cursor;
   if (threadIdx.x == 0) { first_s = n; bad_s = 0; }
@@ -364,10 +388,10 @@ __global__ void __launch_bounds__(SMP_THREADS) verify_chain_kernel(const int32_t
       const double *p = pd + (size_t)r * V, *q = qd + (size_t)r * V;
       const double z = residual_mass(cl, p, q, V);
       const double u2 = U[cur + r + 1];
-      tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, u2) : inv_cdf(cl, p, q, z, V, u2);
+      tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, u2, sw) : inv_cdf(cl, p, q, z, V, u2, sw);
       used = r + 2;
     } else {
-      tok = inv_cdf(cl, pd + (size_t)n * V, nullptr, 1.0, V, U[cur + n]);
+      tok = inv_cdf(cl, pd + (size_t)n * V, nullptr, 1.0, V, U[cur + n], sw);
       used = n + 1;
     }
   }
@@ -404,8 +428,9 @@ __global__ void __launch_bounds__(SMP_THREADS) correct_token_kernel(const double
   pdl_wait();
   HS_CL_SETUP
   const int cur = *cursor;
+  extern __shared__ double sw[];
   const double z = residual_mass(cl, p, q, V);
-  const int tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, U[cur]) : inv_cdf(cl, p, q, z, V, U[cur]);
+  const int tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, U[cur], sw) : inv_cdf(cl, p, q, z, V, U[cur], sw);
   cl.finish();
   if (cl_leader()) { *out = tok; *cursor = cur + 1; }
 }
@@ -413,10 +438,14 @@ __global__ void __launch_bounds__(SMP_THREADS) correct_token_kernel(const double
 // cluster launch (one SMP_CL-CTA cluster per row), a programmatic dependent
 // of the previous kernel on the stream
 template <typename... KArgs, typename... Args>
-static int launch_rows(const char *what, void (*kern)(KArgs...), int rows, cudaStream_t st, Args &&...args) {
+static int launch_rows(const char *what, void (*kern)(KArgs...), int rows, int V, cudaStream_t st,
+                       Args &&...args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(rows * SMP_CL);
   cfg.blockDim = dim3(SMP_THREADS);
+  cfg.dynamicSmemBytes = (size_t)((V + SMP_CL - 1) / SMP_CL) * sizeof(double);   // inverse-CDF staging
+  if (cfg.dynamicSmemBytes > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -450,7 +479,7 @@ extern "C" int hs_correct_token(const double *q, const double *p, int V, const d
                                 int32_t *cursor, int32_t *out, void *stream) {
   int rc = hs::check_vocab(V);
   if (rc != HS_OK) return rc;
-  return hs::launch_rows("correct_token", hs::correct_token_kernel, 1, hs::as_stream(stream), q, p, V, uniforms,
+  return hs::launch_rows("correct_token", hs::correct_token_kernel, 1, V, hs::as_stream(stream), q, p, V, uniforms,
                          cursor, out);
 }
 
@@ -459,14 +488,14 @@ extern "C" int hs_probs(const float *logits, int rows, int V, double temperature
   if (rows <= 0) return HS_OK;
   int rc = hs::check_vocab(V);
   if (rc != HS_OK) return rc;
-  return hs::launch_rows("probs", hs::probs_kernel, rows, hs::as_stream(stream), logits, V, temperature, probs);
+  return hs::launch_rows("probs", hs::probs_kernel, rows, V, hs::as_stream(stream), logits, V, temperature, probs);
 }
 
 extern "C" int hs_sample(const double *probs, int V, const double *uniforms, int32_t *cursor, int32_t *out,
                          void *stream) {
   int rc = hs::check_vocab(V);
   if (rc != HS_OK) return rc;
-  return hs::launch_rows("sample", hs::sample_kernel, 1, hs::as_stream(stream), probs, V, uniforms, cursor, out);
+  return hs::launch_rows("sample", hs::sample_kernel, 1, V, hs::as_stream(stream), probs, V, uniforms, cursor, out);
 }
 
 extern "C" int hs_draft_sample(const float *logits, int V, double temperature, double *probs_out,
@@ -475,7 +504,7 @@ extern "C" int hs_draft_sample(const float *logits, int V, double temperature, d
   if (!probs_out) return hs::set_error(HS_ERR_VALUE, "draft_sample: probs_out required");
   int rc = hs::check_vocab(V);
   if (rc != HS_OK) return rc;
-  return hs::launch_rows("draft_sample", hs::draft_sample_kernel, 1, hs::as_stream(stream), logits, V, temperature,
+  return hs::launch_rows("draft_sample", hs::draft_sample_kernel, 1, V, hs::as_stream(stream), logits, V, temperature,
                          probs_out, uniforms, cursor, out);
 }
 
@@ -484,6 +513,6 @@ extern "C" int hs_verify_chain(const int32_t *tokens, int n, const double *qd, c
   if (n < 0) return hs::set_error(HS_ERR_VALUE, "verify_chain: n < 0");
   int rc = hs::check_vocab(V);
   if (rc != HS_OK) return rc;
-  return hs::launch_rows("verify_chain", hs::verify_chain_kernel, 1, hs::as_stream(stream), tokens, n, qd, pd, V,
+  return hs::launch_rows("verify_chain", hs::verify_chain_kernel, 1, V, hs::as_stream(stream), tokens, n, qd, pd, V,
                          uniforms, cursor, result);
 }

@@ -218,15 +218,20 @@ class DeviceModel:
         self.ref = C.byref(s)
 
     def workspace(self, nbytes: int) -> torch.Tensor:
-        """This model's forward workspace.  Its head (GEMV arrival counters and
-        K-split partials, hs_forward_workspace_clean_bytes) must be zero
-        before first use and is left zero by every call; the layout of that
-        head depends on the model's matrix shapes, so the buffer is owned by
-        the model and never shared with another one."""
-        ws = getattr(self, "_ws", None)
+        """This model's forward workspace on the current stream.  Its head
+        (GEMV arrival counters and K-split partials,
+        hs_forward_workspace_clean_bytes) must be zero before first use and is
+        left zero by every call; the layout of that head depends on the
+        model's matrix shapes, so the buffer is owned by the model and never
+        shared with another one -- nor between streams (the ranks of a
+        loopback shard group run one model concurrently)."""
+        if not hasattr(self, "_ws"):
+            self._ws = {}
+        key = stream_ptr()
+        ws = self._ws.get(key)
         if ws is None or ws.numel() < nbytes:
             ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=self.emb.device)
-            self._ws = ws
+            self._ws[key] = ws
         return ws
 
     @property

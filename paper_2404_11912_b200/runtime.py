@@ -8,6 +8,8 @@ through `_abi.lib`.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -33,16 +35,19 @@ def ptr(t) -> int:
 
 
 class _Workspaces:
-    """Grow-only scratch buffers keyed by purpose (one stream => reuse is safe)."""
+    """Grow-only scratch buffers keyed by purpose and by the current stream:
+    work on one stream is ordered, so reuse is safe; concurrent streams (the
+    host threads of a loopback shard group) never share one."""
 
     def __init__(self):
         self.bufs = {}
 
     def get(self, key: str, nbytes: int) -> torch.Tensor:
-        b = self.bufs.get(key)
+        k = (key, stream_ptr())
+        b = self.bufs.get(k)
         if b is None or b.numel() < nbytes:
             b = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device())
-            self.bufs[key] = b
+            self.bufs[k] = b
         return b
 
 
@@ -107,7 +112,27 @@ class _PinnedStaging:
         return out
 
 
-staging = _PinnedStaging()
+class _ThreadStaging:
+    """One staging ring per host thread (its events are recorded on that
+    thread's current stream)."""
+
+    def __init__(self):
+        self._tl = threading.local()
+
+    def _ring(self) -> _PinnedStaging:
+        r = getattr(self._tl, "ring", None)
+        if r is None:
+            r = self._tl.ring = _PinnedStaging()
+        return r
+
+    def copy_into(self, dst: torch.Tensor, arr) -> None:
+        self._ring().copy_into(dst, arr)
+
+    def to_device(self, arr: np.ndarray) -> torch.Tensor:
+        return self._ring().to_device(arr)
+
+
+staging = _ThreadStaging()
 
 
 def to_i32_device(tokens) -> torch.Tensor:

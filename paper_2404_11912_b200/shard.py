@@ -12,11 +12,16 @@ the exchange steps run inside the native code over NCCL:
 * per layer of every full-cache forward, the per-rank partial softmax
   states are all-gathered and merged in rank order (hs_forward, HsShard);
 * per retrieval build, per-rank fp64 chunk scores are all-gathered (the
-  replicated selection is then bit-identical to the unsharded one) and the
-  gathered chunks are assembled with a sum all-reduce (caches.py).
+  replicated selection is then bit-identical to the unsharded one); each
+  rank gathers the chosen chunks it stores and the per-rank slot ranges are
+  exchanged with a variable-size all-gather (hs_retrieval_exchange).
 
-The communicator is NCCL's own (hs_comm_init); torch.distributed only ships
-its unique id from rank 0 to the others.
+The communicator is NCCL's own (hs_comm_init, non-blocking, every call
+bounded by a deadline); torch.distributed only ships its unique id from rank
+0 to the others.  `SequenceShards.loopback(G)` instead makes G ranks inside
+one process on one GPU (one host thread and CUDA stream per rank, exchanges
+by device-to-device copies with the same semantics): the G-shard session is
+then checked bit for bit against the unsharded one without G GPUs.
 """
 
 from __future__ import annotations
@@ -57,8 +62,9 @@ class SequenceShards:
     """This rank's place in the sequence-sharded full cache plus the NCCL
     communicator used by the native exchange steps."""
 
-    def __init__(self, rank: int, world: int, comm: int):
+    def __init__(self, rank: int, world: int, comm: int, loopback: bool = False):
         self.rank, self.world, self._comm = rank, world, comm
+        self.is_loopback = loopback
         d = HsShard()
         d.comm, d.rank, d.world = comm, rank, world
         self.desc = d
@@ -88,15 +94,30 @@ class SequenceShards:
         return cls._join(bytes(buf), 1, 0)
 
     @classmethod
+    def loopback(cls, world: int) -> List["SequenceShards"]:
+        """G ranks in this process (hs_loopback_create): rank r's object must
+        be used from one host thread with its own current CUDA stream."""
+        comms = (C.c_void_p * world)()
+        check(lib.hs_loopback_create(world, comms))
+        return [cls(r, world, comms[r], loopback=True) for r in range(world)]
+
+    @classmethod
     def _join(cls, uid: bytes, world: int, rank: int) -> "SequenceShards":
         comm = C.c_void_p()
         check(lib.hs_comm_init(C.byref(comm), uid, world, rank))
         return cls(rank, world, comm.value)
 
     def destroy(self) -> None:
+        """NCCL: finalize and destroy this rank's communicator.  Loopback:
+        call on any one rank after every rank is done (frees the group)."""
         if self._comm:
-            check(lib.hs_comm_destroy(self._comm))
+            check(lib.hs_loopback_destroy(self._comm) if self.is_loopback else lib.hs_comm_destroy(self._comm))
             self._comm = None
+
+    def check(self) -> None:
+        """Raise if the communicator carries an asynchronous error (a peer
+        failed or timed out)."""
+        check(lib.hs_comm_check(self._comm))
 
     # -- plan ------------------------------------------------------------------------
     def plan(self, n_positions: int, chunk: int):
@@ -109,6 +130,16 @@ class SequenceShards:
         recv = torch.empty((self.world, *send.shape), dtype=send.dtype, device=send.device)
         check(lib.hs_all_gather(self._comm, ptr(send), ptr(recv), send.numel() * send.element_size(),
                                 stream_ptr()))
+        return recv
+
+    def all_gather_v(self, send: torch.Tensor, counts: List[int]) -> torch.Tensor:
+        """1-D concat in rank order of each rank's first counts[r] elements
+        (this rank sends send[:counts[rank]])."""
+        send = send.contiguous()
+        es = send.element_size()
+        recv = torch.empty(sum(counts), dtype=send.dtype, device=send.device)
+        nb = (C.c_size_t * self.world)(*[c * es for c in counts])
+        check(lib.hs_all_gather_v(self._comm, self.rank, self.world, ptr(send), ptr(recv), nb, stream_ptr()))
         return recv
 
     def all_reduce_sum_(self, buf: torch.Tensor) -> torch.Tensor:

@@ -68,7 +68,9 @@ class _StepGraph:
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         n0 = lib.hs_launch_count()
-        with torch.cuda.graph(self.graph, stream=side):
+        # thread_local: other host threads (loopback shard ranks) keep
+        # launching on their own streams while this one captures
+        with torch.cuda.graph(self.graph, stream=side, capture_error_mode="thread_local"):
             check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), None, ptr(tok), 1, ptr(self.out), ptr(self.stash),
                                  ptr(self.ws), self.nbytes, stream_ptr()))
             lane._front.copy_(self.out[0])

@@ -128,8 +128,8 @@ def test_shard_partials_merge_equals_unsharded_attention(P):
 
 def test_shard_scores_and_gathers_assemble_the_unsharded_build(P):
     """Per-shard chunk scores concatenated in rank order are bit-identical to
-    the unsharded scores; per-shard gathers (zeros for foreign chunks) sum to
-    the unsharded retrieval buffer."""
+    the unsharded scores; per-shard gathers (foreign chunks left untouched,
+    here zero-initialised) sum to the unsharded retrieval buffer."""
     from paper_2404_11912_b200._abi import check, lib
     from paper_2404_11912_b200.runtime import ptr, stream_ptr
     from paper_2404_11912_b200.shard import shard_chunk_counts, shard_plan
@@ -253,3 +253,105 @@ def test_one_rank_sharded_prefill_matches_unsharded(P, one_rank):
     assert (np.argmax(la, -1) == np.argmax(lb, -1)).mean() > 0.999
     da, db = P.decode_step(w, 17, a), P.decode_step(w, 17, b)
     assert np.allclose(da, db, rtol=1e-4, atol=1e-4 * np.abs(da).max())
+
+
+def _run_ranks(fn, world):
+    """Run fn(rank) on `world` host threads, each with its own CUDA stream
+    (the loopback group's execution model); re-raise the first failure."""
+    import threading
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[r] = fn(r)
+                torch.cuda.current_stream().synchronize()
+        except BaseException as e:   # noqa: BLE001 - re-raised below
+            errs.append((r, e))
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0][1]
+    return out
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_loopback_shards_session_matches_unsharded(P, G):
+    """G sequence shards on ONE GPU through the loopback group (G host
+    threads and streams; all-gather / all-gather-v as device copies with the
+    NCCL calls' semantics) run the whole sharded product path: sharded GEMM
+    prefill, per-layer partial-state exchange in every full-cache forward,
+    sharded rebuilds (per-shard scores + the chunk exchange) and the decoded
+    tail appended to the last shard.  Every rank's session equals the
+    unsharded one: token stream, per-level counts, rebuilds and the
+    retrieval cache's positions exactly; logits and the cached K/V to fp32
+    accumulation noise (the G per-shard partial softmax states merge in a
+    different order than one GPU's splits)."""
+    from paper_2404_11912_b200.shard import SequenceShards
+    tw, dw = _planted(P, seed=7)
+    tw.device(), dw.device()                 # pack once, before the threads share them
+    prompt = np.random.default_rng(2).integers(1, 512, 900).tolist()
+    spec = P.SpecConfig(target_len=900 + 96, gamma1=2, gamma2=4, temperature=0.6, seed=5,
+                        streaming=P.StreamingConfig(n_sink=4, budget=128),
+                        retrieval=P.RetrievalConfig(chunk_size=8, budget=128, rebuild_stride=24))
+    ref = P.HierarchicalSession(tw, dw, prompt, spec)
+    ref_out, ref_tr = ref.generate()
+    shards = SequenceShards.loopback(G)
+
+    def rank(r):
+        s = P.HierarchicalSession(tw, dw, prompt, spec, shards=shards[r])
+        out, tr = s.generate()
+        fc = s.full_lane.cache
+        lo, n = fc.lo, fc._local(fc.frontier)
+        return (out, tr.summary(), s.rebuilds, s.retr_lane.cache.pos.clone(), lo, n,
+                fc.k[:, :, :n].clone(), s.full_lane._front.clone())
+
+    try:
+        res = _run_ranks(rank, G)
+    finally:
+        shards[0].destroy()
+    for r, (out, summ, rebuilds, rpos, lo, n, k, front) in enumerate(res):
+        assert out == ref_out, r
+        assert summ == ref_tr.summary(), r
+        assert rebuilds == ref.rebuilds and rebuilds >= 2, (r, rebuilds)
+        assert torch.equal(rpos, ref.retr_lane.cache.pos), r
+        # this rank's slice of the full cache (the last rank holds the decoded tail)
+        want = ref.full_lane.cache.k[:, :, lo:lo + n].float()
+        assert torch.allclose(k.float(), want, rtol=2 ** -7, atol=1e-6), r
+        f0 = ref.full_lane._front
+        assert (front - f0).abs().max().item() <= 1e-5 * f0.abs().max().item(), r
+    assert res[-1][5] > 0 and res[-1][4] + res[-1][5] == ref.full_lane.cache.frontier
+
+
+def test_loopback_collectives(P):
+    """all_gather / all_gather_v / sum all_reduce over a 3-rank loopback group
+    equal their definitions (rank order)."""
+    from paper_2404_11912_b200.shard import SequenceShards
+    G = 3
+    shards = SequenceShards.loopback(G)
+    try:
+        def rank(r):
+            sh = shards[r]
+            x = torch.arange(5, dtype=torch.float64, device="cuda") + 10 * r
+            g = sh.all_gather(x)
+            v = sh.all_gather_v(torch.full((r + 1,), float(r), device="cuda"), [1, 2, 3])
+            y = torch.full((7,), 0.5 * (r + 1), dtype=torch.float32, device="cuda")
+            sh.all_reduce_sum_(y)
+            b = torch.full((4,), 1.0 + r, dtype=torch.bfloat16, device="cuda")
+            sh.all_reduce_sum_(b)
+            sh.check()
+            return g.cpu(), v.cpu(), y.cpu(), b.float().cpu()
+
+        for g, v, y, b in _run_ranks(rank, G):
+            assert torch.equal(g, torch.stack([torch.arange(5, dtype=torch.float64) + 10 * r for r in range(G)]))
+            assert torch.equal(v, torch.tensor([0.0, 1, 1, 2, 2, 2]))
+            assert torch.equal(y, torch.full((7,), 3.0))
+            assert torch.equal(b, torch.full((4,), 6.0))
+    finally:
+        shards[0].destroy()
