@@ -35,6 +35,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the CPU arms (reference arm, cpu_baseline) use every host core for numpy's BLAS
+os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")   # the unmodified reference package (pip --target)
 # NCCL's INFO lines (communicator size, NVLS) go to stderr like every native
 # print (stdout is redirected below), so they stay visible to the driver
 if int(os.environ.get("WORLD_SIZE", "1")) > 1:
@@ -226,20 +229,175 @@ def oracle_sample(context: int, temperature: float, rounds: int, time_budget_s: 
     return [1.0 / x for x in per_token], desc, cores
 
 
+def _bf16_host(a: np.ndarray) -> np.ndarray:
+    """Round fp32 to the nearest bf16 value (ties to even), kept as fp32."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + np.uint64(0x7FFF) + ((u >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)) << np.uint64(16)
+    return r.astype(np.uint32).view(np.float32).reshape(a.shape)
+
+
+def host_cpu() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), model)
+    except OSError:
+        pass
+    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0)),
+            "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+def reference_sample(context: int, temperature: float, rounds: int, time_budget_s: float = 150.0,
+                     easy_frac: float = EASY_FRAC, target: dict = TARGET_7B):
+    """TriForce outer rounds through the UNMODIFIED reference package
+    (`hierspec`, installed into baseline/_ref; its public Lane /
+    inner_speculate / outer_verify / RetrievalCache API, i.e. the body of
+    HierarchicalSession.generate, speculation.py:338-368) on this host's
+    cores.  The 7B shape does not fit the reference's fp32 + fp64 layout in
+    host memory, so the target is a 1-layer slice at the real layer shape
+    over the full 122,880-position context plus the full
+    2-layer draft; target-forward time is scaled x n_layers and the measured
+    per-layer build is amortised over the rebuild stride.  The full and draft
+    caches are filled directly with bf16-representable random K/V (the
+    reference's O(N^2) prefill is infeasible at this length).  Falls back to
+    the numpy port (oracle/) when baseline/_ref is absent.  Returns
+    (tokens/s per round, description, kind)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "hierspec")):
+        rates, desc, _ = oracle_sample(context, temperature, rounds, time_budget_s, easy_frac, target)
+        return rates, desc, "port"
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import hierspec as H
+    from hierspec import caches as HC, model as HM, speculation as HS
+    max_seq = max(target["max_seq"], context + 1024)
+    tcfg = H.ModelConfig(**{**target, "n_layers": 1, "max_seq": max_seq})
+    dcfg = H.ModelConfig(**{**DRAFT_68M, "max_seq": max_seq})
+    t0 = time.perf_counter()
+    tw = H.generate_weights(tcfg, 1, tied_head=False)
+    dw = H.generate_weights(dcfg, 2, tied_head=False)
+    if easy_frac > 0:
+        plant_host(tw.tensors, tcfg.d_model, tcfg.vocab_size, PLANT_SEED, easy_frac)
+        plant_host(dw.tensors, dcfg.d_model, dcfg.vocab_size, PLANT_SEED, easy_frac)
+    ctx = np.random.default_rng(0).integers(1, 32000, context).tolist()
+    n = context
+    spec = H.SpecConfig(target_len=context + 10 ** 6, gamma1=GAMMA1, gamma2=GAMMA2, temperature=temperature,
+                        seed=0, streaming=H.StreamingConfig(n_sink=SINK, budget=STREAM),
+                        retrieval=H.RetrievalConfig(chunk_size=CHUNK, budget=BUDGET))
+    rng = np.random.default_rng(0)
+
+    def fill(store, positions, kvh, dh):
+        cap = len(positions) + 1024
+        store.k = np.empty((cap, kvh, dh), np.float32)
+        store.v = np.empty((cap, kvh, dh), np.float32)
+        store.pos = np.empty(cap, np.int64)
+        m = len(positions)
+        store.k[:m] = _bf16_host(rng.standard_normal((m, kvh, dh), dtype=np.float32))
+        store.v[:m] = _bf16_host(rng.standard_normal((m, kvh, dh), dtype=np.float32))
+        store.pos[:m] = positions
+        store.n = m
+
+    full = HC.FullCache.from_config(tcfg)
+    for st in full._layers:
+        fill(st, np.arange(n - 1), tcfg.n_kv_heads, tcfg.head_dim)
+    full.frontier = full.committed = n - 1
+    stream = HC.StreamingCache.from_config(dcfg, spec.streaming)
+    w = STREAM - SINK
+    keep = np.r_[np.arange(min(SINK, n - 1)), np.arange(max(SINK, n - 1 - w), n - 1)]
+    for st in stream._layers:
+        fill(st, keep, dcfg.n_kv_heads, dcfg.head_dim)
+    stream.frontier = stream.committed = n - 1
+    sess = object.__new__(HS.HierarchicalSession)
+    sess.config, sess.committed = spec, list(ctx)
+    sess.full_lane, sess.draft_lane = HS.Lane(tw, full), HS.Lane(dw, stream)
+    retr = HC.RetrievalCache.from_config(tcfg, spec.retrieval)
+    sess.retr_lane = HS.Lane(tw, retr)
+    for lane in (sess.full_lane, sess.draft_lane):
+        lane.advance([ctx[-1]])
+        lane.commit()
+    tb = time.perf_counter()
+    retr.build(full, sess.full_lane.last_queries(), upto=n - 1)
+    build_s = time.perf_counter() - tb
+    sess.rolling = HC.RollingAcceptance(spec.retrieval.rolling_window)
+    sess.tokens_since_build = 0
+    setup = time.perf_counter() - t0
+
+    spent = {"target": 0.0, "draft": 0.0}
+    real_forward = HM._forward
+
+    def timed_forward(weights, *a, **k):
+        t = time.perf_counter()
+        try:
+            return real_forward(weights, *a, **k)
+        finally:
+            spent["target" if weights is tw else "draft"] += time.perf_counter() - t
+
+    def outer_round(grng, trace):
+        # HierarchicalSession.generate's loop body (speculation.py:338-368), the reference's own calls
+        cfg = sess.config
+        sess._maybe_rebuild()
+        x_hat, p_hats, inner_labels = HS.inner_speculate(sess.retr_lane, sess.draft_lane, sess.committed, cfg,
+                                                         grng, trace)
+        emitted, outer_labels, accepted, _ = HS.outer_verify(sess.full_lane, sess.committed, x_hat, p_hats,
+                                                             cfg.temperature, grng)
+        base = len(sess.committed)
+        sess.committed.extend(emitted)
+        valid = base + min(accepted, len(emitted))
+        sess.full_lane.rollback_to(valid)
+        sess.full_lane.commit()
+        for lane in (sess.draft_lane, sess.retr_lane):
+            lane.rollback_to(min(lane.frontier, valid))
+            lane.commit()
+        sess.rolling.push(accepted / len(x_hat))
+        sess.tokens_since_build += len(emitted)
+        return len(emitted)
+
+    HM._forward = timed_forward
+    per_token = []
+    grng = np.random.default_rng(0)
+    trace = HS.StepTrace()
+    start = time.perf_counter()
+    try:
+        for _ in range(rounds):
+            spent["target"] = spent["draft"] = 0.0
+            t = time.perf_counter()
+            got = outer_round(grng, trace)
+            wall = time.perf_counter() - t
+            rest = wall - spent["target"] - spent["draft"]
+            est = spent["target"] * target["n_layers"] + spent["draft"] + rest
+            est += build_s * target["n_layers"] * got / spec.retrieval.rebuild_stride
+            per_token.append(est / got)
+            if time.perf_counter() - start > time_budget_s:
+                break
+    finally:
+        HM._forward = real_forward
+    desc = (f"reference hierspec {H.__version__} (baseline/_ref, unmodified, numpy/OpenBLAS): TriForce outer "
+            f"rounds on a 1-layer slice of the target shape over a {context}-token synthetic bf16 context + the "
+            f"full JF68M-shaped draft; target forwards x{target['n_layers']} layers, build ({build_s:.1f} s/layer) "
+            f"amortised over the {spec.retrieval.rebuild_stride}-token stride; {len(per_token)} round(s), "
+            f"setup {setup:.0f} s")
+    return [1.0 / x for x in per_token], desc, "reference"
+
+
+CPU_ROUNDS = 4   # outer rounds of the CPU sample (both arms run the same ones: same seeds)
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port; the Python
-    reference cannot travel to the GPU box) on this host's cores."""
+    """--impl reference: the reference's own CPU path (the unmodified hierspec
+    package from baseline/_ref; the numpy port if it is absent) on this
+    host's cores.  Under torchrun only rank 0 runs it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=max(1, args.steps),
-                                       easy_frac=args.easy_frac, target=TARGETS[args.model])
+    rates, desc, kind = reference_sample(args.context, args.temperature, rounds=min(max(1, args.steps), CPU_ROUNDS),
+                                         easy_frac=args.easy_frac, target=TARGETS[args.model])
     val = statistics.median(rates)
+    cpu = host_cpu()
     out = {"metric": metric_name(args), "value": val,
            "unit": "tokens/s", "n_gpus": 0, "steps": len(rates), "warmup": 0, "ms_per_step": 1000.0 / val,
            "higher_is_better": True, "impl": "reference", "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": workload_config(args),
-           "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
+           "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cpu["cores"], "kind": kind, "sample": desc,
+                            **cpu},
            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(json.dumps(out))
 
@@ -393,10 +551,13 @@ def main():
                               "rebuilds": stats.get("rebuilds", 0)},
                **extra}
         if world == 1 and not args.no_cpu_baseline:
-            rates, desc, cores = oracle_sample(args.context, args.temperature, rounds=1, time_budget_s=60,
-                                               easy_frac=args.easy_frac, target=TARGETS[args.model])
-            out["cpu_baseline"] = {"value": statistics.median(rates), "unit": "tokens/s", "cores": cores,
-                                   "kind": "port", "sample": desc}
+            # the reference arm's sample (same rounds, same seeds)
+            rates, desc, kind = reference_sample(args.context, args.temperature,
+                                                 rounds=min(max(1, args.steps), CPU_ROUNDS),
+                                                 easy_frac=args.easy_frac, target=TARGETS[args.model])
+            cpu = host_cpu()
+            out["cpu_baseline"] = {"value": statistics.median(rates), "unit": "tokens/s", "cores": cpu["cores"],
+                                   "kind": kind, "sample": desc, **cpu}
         emit(json.dumps(out))
     if shards is not None:
         shards.destroy()
