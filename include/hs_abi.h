@@ -236,6 +236,15 @@ size_t hs_gemv_tc_workspace_bytes(int N, int ldw);
 int hs_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                uint16_t *xs_out, int ld_xs_out, void *workspace, size_t ws_bytes, void *stream);
 
+/* Tensor-core GEMM of the batched prefill (tcgen05 + TMA, gemm_tc.cu):
+ * y[r][n] (+)= sum_k w[n][k] * (s0 + s1 + s2)[r][k] for rows r < rows, with
+ * s0/s1/s2 the exact 3-way bf16 split planes of fp32 activations ([rows][ldk],
+ * ldk >= ldw, K = ldw a multiple of 64) and w bf16 [n][ldw]; all three planes
+ * accumulate into one fp32 accumulator (model.py:281-285,316-328 matmuls for
+ * long prompts).  accumulate = 1 adds into y (residual updates).             */
+int hs_gemm3_tc(const uint16_t *s0, const uint16_t *s1, const uint16_t *s2, int ldk, int rows,
+                const uint16_t *w, int ldw, int n, float *y, int ldy, int accumulate, void *stream);
+
 /* activation prep for hs_gemv_tc: optional RMSNorm (gain != NULL,
  * model.py:282-284) then exact split h = hi + mid + lo into xs [24][ldk]    */
 int hs_split_rows(const float *x, int ldx, int t, int K, int ldk, const float *gain, float eps,

@@ -38,18 +38,6 @@ def _nccl_root() -> str:
 NCCL = _nccl_root()
 
 
-def _cublas_lib() -> str:
-    """Directory of the libcublas.so.12 torch loads (so one copy is mapped)."""
-    import importlib.util
-    spec = importlib.util.find_spec("nvidia")
-    for base in (spec.submodule_search_locations if spec else []):
-        lib = os.path.join(base, "cublas", "lib")
-        if os.path.exists(os.path.join(lib, "libcublas.so.12")):
-            return lib
-    return "/usr/local/cuda/lib64"
-
-
-CUBLAS_LIB = _cublas_lib()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xptxas", "-O3"]
 
@@ -89,8 +77,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     nccl_lib = os.path.join(NCCL, "lib")
     subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-L", nccl_lib, "-l:libnccl.so.2",
-                    "-Xlinker", "-rpath," + nccl_lib, "-L", CUBLAS_LIB, "-l:libcublas.so.12",
-                    "-Xlinker", "-rpath," + CUBLAS_LIB], check=True)
+                    "-Xlinker", "-rpath," + nccl_lib], check=True)
     os.replace(tmp, LIB)
     return LIB
 

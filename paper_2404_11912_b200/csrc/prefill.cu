@@ -5,14 +5,13 @@
 // prompts.  The decode path (hs_forward) keeps every row bit-identical
 // whatever the batch (the chunk == step-sequence contract, model.py:366-378);
 // prefill only has to be fp32-accurate, so each projection here is
-//     Y (+)= W . (hi + mid + lo)      -- three bf16 GEMMs (cuBLAS, fp32 accumulate)
-// over the exact 3-way bf16 split of the fp32 activations: every product is
+//     Y (+)= W . (hi + mid + lo)      -- one tcgen05 GEMM (gemm_tc.cu) whose
+// three bf16 activation planes accumulate into one fp32 TMEM accumulator:
+// the exact 3-way bf16 split of the fp32 activations, so every product is
 // exact and the sums are fp32, like the GEMV.  RMSNorm, RoPE + cache append
 // and attention are the decode path's kernels (attention runs causally over
 // all t query rows).  Rows go through the dense layers in blocks of up to
 // PF_ROWS so the GEMM scratch stays bounded.
-#include <cublas_v2.h>
-
 #include "hs_common.cuh"
 
 namespace hs {
@@ -29,6 +28,8 @@ int launch_prefill_attention(const HsCache *c, int layer, int H, const float *q,
 int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, uint16_t *xs, int ldxs, int H,
                        cudaStream_t st);
 int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
+int launch_gemm3_tc(const uint16_t *s0, const uint16_t *s1, const uint16_t *s2, int ldk, int R, const uint16_t *W,
+                    int ld, int N, float *Y, int ldy, int accumulate, cudaStream_t st);
 
 namespace {
 
@@ -80,12 +81,6 @@ __global__ void pf_swiglu_kernel(const float *gu, int R, int ff, float *act) {
   }
 }
 
-cublasHandle_t pf_handle() {
-  static cublasHandle_t h = nullptr;
-  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
-  return h;
-}
-
 struct PfWs {
   float *x, *qkv, *q, *attn, *gu, *act;
   uint16_t *s0, *s1, *s2;   // split planes [PF_ROWS][max(ld_d, ld_ff)]
@@ -122,18 +117,10 @@ size_t carve(const HsModel *m, int t, int n_view, int split, int world, char *ba
   return off;
 }
 
-// Y[R][N] (ldy) = beta * Y + W[N][ld] . (s0 + s1 + s2)[R][ld]^T, fp32 accumulate
-int gemm3(cublasHandle_t h, const uint16_t *W, int ld, int N, const PfWs &w, int R, float beta, float *Y, int ldy) {
-  const float one = 1.f;
-  const uint16_t *parts[3] = {w.s0, w.s1, w.s2};
-  for (int i = 0; i < 3; ++i) {
-    const float b = i == 0 ? beta : 1.f;
-    cublasStatus_t st = cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, N, R, ld, &one, W, CUDA_R_16BF, ld, parts[i],
-                                     CUDA_R_16BF, ld, &b, Y, CUDA_R_32F, ldy, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-    if (st != CUBLAS_STATUS_SUCCESS) return set_error(HS_ERR_CUDA, "prefill: cublasGemmEx failed (%d)", (int)st);
-  }
-  count_launch(3);
-  return HS_OK;
+// Y[R][N] (ldy) (+)= W[N][ld] . (s0 + s1 + s2)[R][ld]^T, fp32 accumulate (tcgen05)
+// (split_rows_n wrote the planes at row stride ld)
+int gemm3(const uint16_t *W, int ld, int N, const PfWs &w, int R, int accumulate, float *Y, int ldy, cudaStream_t s) {
+  return launch_gemm3_tc(w.s0, w.s1, w.s2, ld, R, W, ld, N, Y, ldy, accumulate, s);
 }
 
 int split_rows_n(const float *x, int ldx, int R, int K, int ldk, const float *gain, float eps, const PfWs &w,
@@ -187,10 +174,7 @@ static int prefill_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
   PfWs w;
   const size_t need = carve(m, t, st->n_view, st->split, sh ? sh->world : 0, (char *)workspace, &w);
   HS_REQUIRE(workspace_bytes >= need, HS_ERR_VALUE, "prefill: workspace %zu < %zu", workspace_bytes, need);
-  cublasHandle_t h = pf_handle();
-  HS_REQUIRE(h != nullptr, HS_ERR_CUDA, "prefill: cuBLAS unavailable");
   cudaStream_t s = as_stream(stream);
-  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return set_error(HS_ERR_CUDA, "prefill: cublasSetStream");
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim, ff = m->d_ff;
   const int nqkv = (H + 2 * KVH) * dh;
   const float eps = m->norm_eps;
@@ -206,7 +190,7 @@ static int prefill_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     for (int r0 = 0; r0 < t; r0 += PF_ROWS) {
       const int R = t - r0 < PF_ROWS ? t - r0 : PF_ROWS;
       HS_TRY(split_rows_n(w.x + (size_t)r0 * d, d, R, d, m->ld_d, an, eps, w, s));
-      HS_TRY(gemm3(h, wqkv, m->ld_d, nqkv, w, R, 0.f, w.qkv + (size_t)r0 * nqkv, nqkv));
+      HS_TRY(gemm3(wqkv, m->ld_d, nqkv, w, R, 0, w.qkv + (size_t)r0 * nqkv, nqkv, s));
     }
     HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
     // causal attention: head_dim 128 on the 128-row tensor-core prefill kernel
@@ -242,20 +226,20 @@ static int prefill_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       const int R = t - r0 < PF_ROWS ? t - r0 : PF_ROWS;
       float *xr = w.x + (size_t)r0 * d;
       HS_TRY(split_rows_n(w.attn + (size_t)r0 * d, d, R, d, m->ld_d, nullptr, 0.f, w, s));
-      HS_TRY(gemm3(h, wo, m->ld_d, d, w, R, 1.f, xr, d));                  // x += wo . attn
+      HS_TRY(gemm3(wo, m->ld_d, d, w, R, 1, xr, d, s));                  // x += wo . attn
       HS_TRY(split_rows_n(xr, d, R, d, m->ld_d, mn, eps, w, s));
-      HS_TRY(gemm3(h, wgu, m->ld_d, 2 * ff, w, R, 0.f, w.gu, 2 * ff));
+      HS_TRY(gemm3(wgu, m->ld_d, 2 * ff, w, R, 0, w.gu, 2 * ff, s));
       pf_swiglu_kernel<<<592, 256, 0, s>>>(w.gu, R, ff, w.act);
       HS_TRY(check_launch("prefill swiglu"));
       HS_TRY(split_rows_n(w.act, ff, R, ff, m->ld_ff, nullptr, 0.f, w, s));
-      HS_TRY(gemm3(h, wdn, m->ld_ff, d, w, R, 1.f, xr, d));                // x += w_down . act
+      HS_TRY(gemm3(wdn, m->ld_ff, d, w, R, 1, xr, d, s));                // x += w_down . act
     }
   }
   for (int r0 = 0; r0 < t; r0 += PF_ROWS) {
     const int R = t - r0 < PF_ROWS ? t - r0 : PF_ROWS;
     HS_TRY(split_rows_n(w.x + (size_t)r0 * d, d, R, d, m->ld_d, m->final_norm, eps, w, s));
-    HS_TRY(gemm3(h, m->head, m->ld_d, m->vocab_size, w, R, 0.f, logits + (size_t)r0 * m->vocab_size,
-                 m->vocab_size));
+    HS_TRY(gemm3(m->head, m->ld_d, m->vocab_size, w, R, 0, logits + (size_t)r0 * m->vocab_size,
+                 m->vocab_size, s));
   }
 #undef HS_TRY
   return HS_OK;

@@ -68,12 +68,18 @@ class _StepGraph:
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         n0 = lib.hs_launch_count()
-        # thread_local: other host threads (loopback shard ranks) keep
-        # launching on their own streams while this one captures
-        with torch.cuda.graph(self.graph, stream=side, capture_error_mode="thread_local"):
-            check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), None, ptr(tok), 1, ptr(self.out), ptr(self.stash),
-                                 ptr(self.ws), self.nbytes, stream_ptr()))
-            lane._front.copy_(self.out[0])
+        # capture_begin/end directly (torch.cuda.graph's context manager
+        # synchronises the whole device first); thread_local: other host
+        # threads (loopback shard ranks) keep launching on their own streams
+        # while this one captures
+        with torch.cuda.stream(side):
+            self.graph.capture_begin(capture_error_mode="thread_local")
+            try:
+                check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), None, ptr(tok), 1, ptr(self.out),
+                                     ptr(self.stash), ptr(self.ws), self.nbytes, stream_ptr()))
+                lane._front.copy_(self.out[0])
+            finally:
+                self.graph.capture_end()
         self.n_launch = lib.hs_launch_count() - n0
         torch.cuda.current_stream().wait_stream(side)
 

@@ -395,3 +395,42 @@ def test_sampling_randomized_against_oracle(P):
         assert np.abs(p - ref).max() <= 1e-12, case
         seed = int(rng.integers(0, 1 << 30))
         assert P.sample_from_probs(p, np.random.default_rng(seed)) == O.draw(ref, np.random.default_rng(seed)), case
+
+
+def _split3_host(x):
+    from oracle.hs_oracle import bf16_round
+    s0 = bf16_round(x)
+    s1 = bf16_round((x - s0).astype(np.float32))
+    s2 = bf16_round((x - s0 - s1).astype(np.float32))
+    return s0, s1, s2
+
+
+@pytest.mark.parametrize("R,K,N,acc", [(300, 4096, 12288, 0), (2048, 1024, 4096, 1), (5, 256, 260, 0),
+                                       (129, 704, 22016 // 16, 1), (1000, 4096, 32000, 0)])
+def test_gemm3_tc_matches_fp64(P, R, K, N, acc):
+    """The prefill GEMM (tcgen05, 3 exact bf16 activation planes into one fp32
+    TMEM accumulator): partial row / column tiles, accumulate mode; error at
+    fp32-accumulation level vs fp64 (a bf16-rounded activation would be ~1e-3)."""
+    from paper_2404_11912_b200._abi import check, lib
+    from paper_2404_11912_b200.runtime import ptr, stream_ptr
+    rng = np.random.default_rng(R + K + N)
+    ld = (K + 63) // 64 * 64
+    x = rng.normal(0, 1, (R, K)).astype(np.float32)
+    W = _bf16(rng.normal(0, 0.02, (N, K)).astype(np.float32))
+    planes = []
+    for p in _split3_host(x):
+        t = torch.zeros((R, ld + 64), dtype=torch.bfloat16, device="cuda")   # row stride ldk > ld
+        t[:, :K] = torch.from_numpy(p).to(torch.bfloat16).cuda()
+        planes.append(t)
+    Wd = torch.zeros((N, ld), dtype=torch.bfloat16, device="cuda")
+    Wd[:, :K] = torch.from_numpy(W).cuda().to(torch.bfloat16)
+    y0 = rng.normal(0, 1, (R, N)).astype(np.float32) if acc else np.zeros((R, N), np.float32)
+    y = torch.from_numpy(y0).cuda()
+    check(lib.hs_gemm3_tc(ptr(planes[0]), ptr(planes[1]), ptr(planes[2]), ld + 64, R, ptr(Wd), ld, N, ptr(y), N,
+                          acc, stream_ptr()))
+    ref = x.astype(np.float64) @ W.astype(np.float64).T + (y0.astype(np.float64) if acc else 0.0)
+    got = y.cpu().numpy()
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    # exact products, fp32 tensor-core accumulation over 3 x K terms (the
+    # decode GEMV's numerics; observed 1.2e-5 at K = 4096)
+    assert err < 3e-5, err
