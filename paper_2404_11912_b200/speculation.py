@@ -38,6 +38,26 @@ from .runtime import STATS, UniformStream, as_device_f64, device, ptr, staging, 
 # it off: every step is then a regular hs_forward call with the same kernels)
 USE_GRAPHS = os.environ.get("HS_NO_GRAPHS", "0") != "1"
 
+# NVTX ranges per lane and phase (HS_NVTX=1): rebuild, inner round (draft
+# round, retrieval score, verify chain), outer verify -- visible in nsys / ncu
+# --nvtx timelines.  Off by default (a range push/pop costs ~1 us of host time).
+USE_NVTX = os.environ.get("HS_NVTX", "0") == "1"
+
+
+class _nvtx:
+    __slots__ = ("name",)
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        if USE_NVTX:
+            torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *exc):
+        if USE_NVTX:
+            torch.cuda.nvtx.range_pop()
+
 
 class _StepGraph:
     """One-token forward of a streaming-cache lane captured as a CUDA graph.
@@ -392,12 +412,15 @@ def _chain_dev(tokens_dev, n, qd, pd, V, us, buf):
 
 def _inner_round_dev(retr: Lane, draft: Lane, seq, cfg: SpecConfig, us, buf, phat_off: int):
     V = buf.V
-    _draft_round_dev(draft, seq, cfg.gamma1, cfg.temperature, us, buf)
-    _score_rows_dev(retr, seq, buf.dtok, cfg.temperature, buf.p)
-    _chain_dev(buf.dtok, cfg.gamma1, buf.q, buf.p, V, us, buf)
-    # p_hat rows of the emitted tokens: copy all gamma1+1, the surplus is overwritten later
-    buf.phat[phat_off:phat_off + cfg.gamma1 + 1].copy_(buf.p[:cfg.gamma1 + 1])
-    return _readback(buf, cfg.gamma1, us)
+    with _nvtx("inner.draft_round"):
+        _draft_round_dev(draft, seq, cfg.gamma1, cfg.temperature, us, buf)
+    with _nvtx("inner.retrieval_score"):
+        _score_rows_dev(retr, seq, buf.dtok, cfg.temperature, buf.p)
+    with _nvtx("inner.verify_chain"):
+        _chain_dev(buf.dtok, cfg.gamma1, buf.q, buf.p, V, us, buf)
+        # p_hat rows of the emitted tokens: copy all gamma1+1, the surplus is overwritten later
+        buf.phat[phat_off:phat_off + cfg.gamma1 + 1].copy_(buf.p[:cfg.gamma1 + 1])
+        return _readback(buf, cfg.gamma1, us)
 
 
 # ---------------------------------------------------------------------------
@@ -580,7 +603,8 @@ class HierarchicalSession:
         cursor = 0
         V = buf.V
         while len(self.committed) < cfg.target_len:
-            self._maybe_rebuild()
+            with _nvtx("rebuild_check"):
+                self._maybe_rebuild()
             # ---- inner level: draft -> retrieval (speculation.py:230-261)
             x_hat, ilabels = [], []
             base = len(self.committed)
@@ -602,11 +626,12 @@ class HierarchicalSession:
             # ---- outer level: full-cache verify (speculation.py:264-275)
             n = len(x_hat)
             us.ensure(n + 2, cursor)
-            buf.xtok[:n].copy_(to_i32_device(x_hat))
-            COUNTERS["h2d_bytes"] += 4 * n
-            _score_rows_dev(self.full_lane, self.committed, buf.xtok[:n], cfg.temperature, buf.p)
-            _chain_dev(buf.xtok[:n], n, buf.phat, buf.p, V, us, buf)
-            emitted, accepted, cursor = _readback(buf, n, us)
+            with _nvtx("outer.verify"):
+                buf.xtok[:n].copy_(to_i32_device(x_hat))
+                COUNTERS["h2d_bytes"] += 4 * n
+                _score_rows_dev(self.full_lane, self.committed, buf.xtok[:n], cfg.temperature, buf.p)
+                _chain_dev(buf.xtok[:n], n, buf.phat, buf.p, V, us, buf)
+                emitted, accepted, cursor = _readback(buf, n, us)
             olabels = ["accepted"] * accepted + (["corrected"] if accepted < n else ["bonus"])
             trace.outer.rounds += 1
             trace.outer.proposed += n
