@@ -147,6 +147,9 @@ int hs_all_gather_v(void *comm, int rank, int world, const void *send, void *rec
  * call is bounded by HS_NCCL_TIMEOUT_S seconds (default 300): a peer that
  * never arrives aborts the communicator and returns HS_ERR_CUDA.          */
 int hs_comm_check(void *comm);
+/* abort: a failing rank releases its peers (NCCL: ncclCommAbort; loopback:
+ * every pending and later collective of the group fails at once)            */
+int hs_comm_abort(void *comm);
 /* In-process loopback group of `world` ranks on one device: comms[r] is rank
  * r's communicator (use it in HsShard.comm from rank r's host thread and
  * stream).  Collectives are device-to-device copies with the NCCL calls'

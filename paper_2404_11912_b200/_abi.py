@@ -112,6 +112,7 @@ _SIGS = {
     "hs_all_reduce_sum": (i32, [vp, vp, sz, i32, vp]),
     "hs_all_gather_v": (i32, [vp, i32, i32, vp, vp, vp, vp]),
     "hs_comm_check": (i32, [vp]),
+    "hs_comm_abort": (i32, [vp]),
     "hs_gemm3_tc": (i32, [vp, vp, vp, i32, i32, vp, i32, i32, vp, i32, i32, vp]),
     "hs_loopback_create": (i32, [i32, vp]),
     "hs_loopback_destroy": (i32, [vp]),

@@ -30,6 +30,8 @@
 // slot), warp 5 the MMA issuer.  Persistent over work items.  With FusedRope
 // the q staging also applies RoPE to the qkv rows and the CTA covering this
 // step's slots appends the new K/V rows before its producer loads them.
+#include <stdlib.h>
+
 #include "hs_common.cuh"
 #include "tc_util.cuh"
 
@@ -62,6 +64,7 @@ struct AttTcArgs {
   const int32_t *pos;   // layer [cap] or null
   int cap, layer, n_view, pos0, window, win_lo, n_sink, split, n_splits, n_qb, n_items, pos_base;
   int clean_hi;         // slots < clean_hi are not written by the preceding kernels (see launch_attention)
+  int l2_prefetch;      // prefetch the first item's clean tiles to L2 before the dependency wait
   // fused RoPE + append (forward path, FusedRope): q and this step's K/V rows
   // come straight from the qkv GEMV output; qkv == null: q given, rows appended
   const float *qkv;
@@ -188,9 +191,22 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
         int split, kh, qb;
         item_coords(blockIdx.x, a, split, kh, qb);
         const int lo = split * a.split;
+        const int row0 = (a.layer * a.KVH + kh) * a.cap;
         if (lo + AT_KT <= a.clean_hi) {
-          load_kv(0, (a.layer * a.KVH + kh) * a.cap + lo);
+          load_kv(0, row0 + lo);
           pre = true;
+        }
+        // small views (the retrieval lane): the rest of the first item's
+        // clean tiles go to L2 at once, so the single-stage ring refills
+        // from L2 instead of paying an HBM round trip per tile
+        if (a.l2_prefetch) {
+          const int hi = min(a.n_view, lo + a.split);
+          for (int tile = lo + AT_KT; tile < hi && tile + AT_KT <= a.clean_hi; tile += AT_KT) {
+            tc::tma_prefetch_l2_2d(&tmK, 0, row0 + tile);
+            tc::tma_prefetch_l2_2d(&tmK, 64, row0 + tile);
+            tc::tma_prefetch_l2_2d(&tmV, 0, row0 + tile);
+            tc::tma_prefetch_l2_2d(&tmV, 64, row0 + tile);
+          }
         }
       }
       tc::grid_dep_wait();             // K/V rows appended by the previous kernel
@@ -527,6 +543,8 @@ int launch_attention_tc(const HsCache *c, int layer, const HsStep *st, int H, co
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)AT_DH));
   a.part_m = part_m; a.part_l = part_l; a.part_o = part_o;
   a.clean_hi = st->dyn ? -1 : clean_hi;
+  static const int l2pf = getenv("HS_ATT_L2PF") ? atoi(getenv("HS_ATT_L2PF")) : 1;   // A/B hook
+  a.l2_prefetch = l2pf && st->split <= 512;   // one item per CTA: its whole split fits the prefetch
   a.dyn = st->dyn;
   a.qkv = nullptr;
   a.dirty_lo = a.dirty_hi = 0;

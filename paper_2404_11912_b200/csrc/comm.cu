@@ -275,6 +275,19 @@ extern "C" int hs_comm_check(void *comm) {
   return HS_OK;
 }
 
+extern "C" int hs_comm_abort(void *comm) {
+  HS_REQUIRE(comm != nullptr, HS_ERR_VALUE, "comm_abort: no communicator");
+  if (hs::is_loopback(comm)) {
+    hs::LbGroup *g = ((hs::LbComm *)comm)->g;
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->broken = true;   // every rank waiting in (or entering) a collective fails at once
+    g->cv.notify_all();
+    return HS_OK;
+  }
+  ncclResult_t r = ncclCommAbort(reinterpret_cast<ncclComm_t>(comm));
+  return r == ncclSuccess ? HS_OK : hs::nccl_error("ncclCommAbort", r);
+}
+
 extern "C" int hs_comm_destroy(void *comm) {
   if (!comm) return HS_OK;
   if (hs::is_loopback(comm)) return HS_OK;   // owned by its group (hs_loopback_destroy)

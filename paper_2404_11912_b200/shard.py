@@ -114,6 +114,11 @@ class SequenceShards:
             check(lib.hs_loopback_destroy(self._comm) if self.is_loopback else lib.hs_comm_destroy(self._comm))
             self._comm = None
 
+    def abort(self) -> None:
+        """Release the peers of a failing rank (their collectives raise)."""
+        if self._comm:
+            check(lib.hs_comm_abort(self._comm))
+
     def check(self) -> None:
         """Raise if the communicator carries an asynchronous error (a peer
         failed or timed out)."""

@@ -19,6 +19,7 @@ reference's (speculation.py:9-12), so traces replay the CPU engine.
 from __future__ import annotations
 
 import ctypes as C
+import gc
 import json
 import os
 from dataclasses import dataclass, field
@@ -92,14 +93,24 @@ class _StepGraph:
         # synchronises the whole device first); thread_local: other host
         # threads (loopback shard ranks) keep launching on their own streams
         # while this one captures
-        with torch.cuda.stream(side):
-            self.graph.capture_begin(capture_error_mode="thread_local")
-            try:
-                check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), None, ptr(tok), 1, ptr(self.out),
-                                     ptr(self.stash), ptr(self.ws), self.nbytes, stream_ptr()))
-                lane._front.copy_(self.out[0])
-            finally:
-                self.graph.capture_end()
+        # (a graph object freed by the garbage collector during the capture
+        # would destroy its executable mid-capture and invalidate it: collect
+        # first and keep the collector off until the capture ends)
+        gc.collect()
+        was_enabled = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.stream(side):
+                self.graph.capture_begin(capture_error_mode="thread_local")
+                try:
+                    check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), None, ptr(tok), 1, ptr(self.out),
+                                         ptr(self.stash), ptr(self.ws), self.nbytes, stream_ptr()))
+                    lane._front.copy_(self.out[0])
+                finally:
+                    self.graph.capture_end()
+        finally:
+            if was_enabled:
+                gc.enable()
         self.n_launch = lib.hs_launch_count() - n0
         torch.cuda.current_stream().wait_stream(side)
 

@@ -255,9 +255,10 @@ def test_one_rank_sharded_prefill_matches_unsharded(P, one_rank):
     assert np.allclose(da, db, rtol=1e-4, atol=1e-4 * np.abs(da).max())
 
 
-def _run_ranks(fn, world):
+def _run_ranks(fn, world, shards=None):
     """Run fn(rank) on `world` host threads, each with its own CUDA stream
-    (the loopback group's execution model); re-raise the first failure."""
+    (the loopback group's execution model); a failing rank aborts the group
+    so its peers fail fast; re-raise the first failure."""
     import threading
     out, errs = [None] * world, []
 
@@ -270,6 +271,8 @@ def _run_ranks(fn, world):
                 torch.cuda.current_stream().synchronize()
         except BaseException as e:   # noqa: BLE001 - re-raised below
             errs.append((r, e))
+            if shards is not None:
+                shards[r].abort()
 
     th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
     for t in th:
@@ -313,7 +316,7 @@ def test_loopback_shards_session_matches_unsharded(P, G):
                 fc.k[:, :, :n].clone(), s.full_lane._front.clone())
 
     try:
-        res = _run_ranks(rank, G)
+        res = _run_ranks(rank, G, shards)
     finally:
         shards[0].destroy()
     for r, (out, summ, rebuilds, rpos, lo, n, k, front) in enumerate(res):
@@ -348,7 +351,7 @@ def test_loopback_collectives(P):
             sh.check()
             return g.cpu(), v.cpu(), y.cpu(), b.float().cpu()
 
-        for g, v, y, b in _run_ranks(rank, G):
+        for g, v, y, b in _run_ranks(rank, G, shards):
             assert torch.equal(g, torch.stack([torch.arange(5, dtype=torch.float64) + 10 * r for r in range(G)]))
             assert torch.equal(v, torch.tensor([0.0, 1, 1, 2, 2, 2]))
             assert torch.equal(y, torch.full((7,), 3.0))
