@@ -15,7 +15,12 @@ constexpr int SCORE_THREADS = 256;
 constexpr int SEL_THREADS = 1024;
 constexpr int SEL_MAX = 8192;   // max chunks kept per layer (quota)
 
-// grid (n_chunks, n_layers); thread = VW consecutive head dims of one kv head
+// grid (n_chunks, n_layers); thread = VW consecutive head dims of one kv head.
+// Keys are read in batches of SB rows per (head, dims) group with every load
+// of the batch -- for all of the thread's groups -- issued before any is
+// consumed: a 64 KB chunk (8 keys x 32 heads x 128 dims bf16) is in flight at
+// once instead of one 16-byte load per dependent step.
+constexpr int SB = 8;
 template <typename KT, int VW>
 __global__ void __launch_bounds__(SCORE_THREADS) chunk_score_kernel(
     const KT *keys, long long ls, long long hs_, long long ts, int KVH, int DH, int upto, int chunk,
@@ -24,34 +29,59 @@ __global__ void __launch_bounds__(SCORE_THREADS) chunk_score_kernel(
   const int b0 = c * chunk, b1 = min(upto, b0 + chunk);
   const int g = H / KVH;
   const int groups = KVH * (DH / VW);
+  constexpr int GPT = 2;   // groups per thread per pass (KVH 32 x 16 vectors = 512 = 2 x 256 threads)
   double part = 0.0;
-  for (int e = threadIdx.x; e < groups; e += SCORE_THREADS) {
-    const int kh = e / (DH / VW), d0 = (e % (DH / VW)) * VW;
-    const KT *kp = keys + l * ls + kh * hs_ + d0;
-    double sum[VW];
+  for (int e0 = threadIdx.x; e0 < groups; e0 += GPT * SCORE_THREADS) {
+    double sum[GPT][VW];
 #pragma unroll
-    for (int u = 0; u < VW; ++u) sum[u] = 0.0;
-    for (int i = b0; i < b1; ++i) {
-      float f[VW];
-      if constexpr (VW == 8 && sizeof(KT) == 2) {
-        unpack8(*reinterpret_cast<const uint4 *>(kp + (size_t)i * ts), f);
-      } else if constexpr (VW == 8) {
-        const float4 a = *reinterpret_cast<const float4 *>(kp + (size_t)i * ts);
-        const float4 b = *reinterpret_cast<const float4 *>(kp + (size_t)i * ts + 4);
-        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-      } else if constexpr (sizeof(KT) == 2) {
-        f[0] = bf16_to_f(kp[(size_t)i * ts]);
-      } else {
-        f[0] = kp[(size_t)i * ts];
+    for (int j = 0; j < GPT; ++j)
+#pragma unroll
+      for (int u = 0; u < VW; ++u) sum[j][u] = 0.0;
+    for (int i0 = b0; i0 < b1; i0 += SB) {
+      float f[GPT][SB][VW];
+#pragma unroll
+      for (int j = 0; j < GPT; ++j) {
+        const int e = e0 + j * SCORE_THREADS;
+        const int kh = e / (DH / VW), d0 = (e % (DH / VW)) * VW;
+        const KT *kp = keys + l * ls + kh * hs_ + d0;
+#pragma unroll
+        for (int s = 0; s < SB; ++s) {
+          const int i = i0 + s;
+          const bool ok = e < groups && i < b1;
+          if constexpr (VW == 8 && sizeof(KT) == 2) {
+            const uint4 w = ok ? *reinterpret_cast<const uint4 *>(kp + (size_t)i * ts) : make_uint4(0, 0, 0, 0);
+            unpack8(w, f[j][s]);
+          } else if constexpr (VW == 8) {
+            const float4 a = ok ? *reinterpret_cast<const float4 *>(kp + (size_t)i * ts) : make_float4(0, 0, 0, 0);
+            const float4 b = ok ? *reinterpret_cast<const float4 *>(kp + (size_t)i * ts + 4) : make_float4(0, 0, 0, 0);
+            f[j][s][0] = a.x; f[j][s][1] = a.y; f[j][s][2] = a.z; f[j][s][3] = a.w;
+            f[j][s][4] = b.x; f[j][s][5] = b.y; f[j][s][6] = b.z; f[j][s][7] = b.w;
+          } else if constexpr (sizeof(KT) == 2) {
+            f[j][s][0] = ok ? bf16_to_f(kp[(size_t)i * ts]) : 0.f;
+          } else {
+            f[j][s][0] = ok ? kp[(size_t)i * ts] : 0.f;
+          }
+        }
       }
+      // the reference's per-chunk key sum, in key order (caches.py:431)
 #pragma unroll
-      for (int u = 0; u < VW; ++u) sum[u] += (double)f[u];
+      for (int j = 0; j < GPT; ++j)
+#pragma unroll
+        for (int s = 0; s < SB; ++s)
+#pragma unroll
+          for (int u = 0; u < VW; ++u) sum[j][u] += (double)f[j][s][u];
     }
     const double cnt = (double)(b1 - b0);
-    for (int gi = 0; gi < g; ++gi) {
-      const float *qh = queries + ((size_t)l * H + kh * g + gi) * DH + d0;
 #pragma unroll
-      for (int u = 0; u < VW; ++u) part += (double)qh[u] * (sum[u] / cnt);
+    for (int j = 0; j < GPT; ++j) {
+      const int e = e0 + j * SCORE_THREADS;
+      if (e >= groups) continue;
+      const int kh = e / (DH / VW), d0 = (e % (DH / VW)) * VW;
+      for (int gi = 0; gi < g; ++gi) {
+        const float *qh = queries + ((size_t)l * H + kh * g + gi) * DH + d0;
+#pragma unroll
+        for (int u = 0; u < VW; ++u) part += (double)qh[u] * (sum[j][u] / cnt);
+      }
     }
   }
   __shared__ double red[SCORE_THREADS / 32];

@@ -153,40 +153,56 @@ def hierarchical_speedup_coarse(alpha1: float, alpha2: float, gamma1: int, gamma
                            inner_rounds_per_outer=rounds)
 
 
+def _accepted_run(u: np.ndarray, alpha: float, cap) -> np.ndarray:
+    """Length of the accepted run before the first rejection, capped at `cap`,
+    for i.i.d. acceptances of probability alpha: P(run >= k) = alpha^k, so
+    the inverse CDF of one uniform is floor(log u / log alpha)
+    (analytics.py:446-457 draws it this way: one uniform per chain)."""
+    cap_arr = np.broadcast_to(np.asarray(cap, dtype=np.int64), u.shape)
+    if alpha <= 0.0:
+        return np.zeros(u.shape, dtype=np.int64)
+    if alpha >= 1.0:
+        return cap_arr.copy()
+    with np.errstate(divide="ignore"):
+        run = np.floor(np.log(u) / np.log(alpha))
+    run = np.where(np.isfinite(run), run, cap_arr)   # u == 0: the whole cap
+    return np.minimum(run.astype(np.int64), cap_arr)
+
+
 def simulate_speedup(alpha1: float, alpha2: float, gamma1: int, gamma2: int, latency: LatencyModel,
                      context: int, budget: int, rounds: int, seed: int,
                      draft_budget: Optional[int] = None) -> SpeedupEstimate:
-    """Monte-Carlo counterpart of hierarchical_speedup: independent Bernoulli
-    accept / reject draws through the two-level round structure; the speedup
-    carries a 95% confidence half-width from 20 batch means."""
+    """Monte-Carlo counterpart of hierarchical_speedup (analytics.py:460-499):
+    all `rounds` outer rounds advance together, vectorised -- each inner pass
+    draws one uniform per round (the accepted draft run, capped at gamma1)
+    until every round has staged gamma2 tokens, then one uniform per round
+    for the outer run (capped at the staged count).  Same draw order and the
+    same 100 batch means for the 95% half-width as the reference, so a seed
+    reproduces its estimate."""
     if rounds < 100:
         raise ValueError("need at least 100 simulated rounds")
     _check_rates(alpha1, alpha2, gamma1, gamma2)
     t_d, t_r, t_f = _latencies(latency, context, budget, draft_budget)
     rng = np.random.default_rng(seed)
-    tok = np.zeros(rounds)
-    wall = np.zeros(rounds)
-    inner = np.zeros(rounds)
-    for r in range(rounds):
-        staged, n_inner = 0, 0
-        while staged < gamma2:
-            acc = 0
-            while acc < gamma1 and rng.random() < alpha1:
-                acc += 1
-            staged += acc + 1
-            n_inner += 1
-        acc = 0
-        while acc < staged and rng.random() < alpha2:
-            acc += 1
-        tok[r] = acc + 1
-        inner[r] = n_inner
-        wall[r] = n_inner * (gamma1 * t_d + t_r) + t_f
+    staged = np.zeros(rounds, dtype=np.int64)
+    inner = np.zeros(rounds, dtype=np.int64)
+    pending = np.ones(rounds, dtype=bool)
+    while pending.any():
+        run = _accepted_run(rng.random(rounds), alpha1, gamma1)   # every round draws, as in the reference
+        staged[pending] += run[pending] + 1
+        inner[pending] += 1
+        pending = staged < gamma2
+    tok = _accepted_run(rng.random(rounds), alpha2, staged) + 1
+    wall = inner * (gamma1 * t_d + t_r) + t_f
     speed = tok.sum() * t_f / wall.sum()
-    batches = np.array_split(np.arange(rounds), 20)
-    bs = np.array([tok[b].sum() * t_f / wall[b].sum() for b in batches])
-    half = 1.96 * bs.std(ddof=1) / np.sqrt(len(bs))
+    nb = 100
+    per = rounds // nb
+    bt = tok[:nb * per].reshape(nb, per).sum(axis=1).astype(np.float64)
+    bw = wall[:nb * per].reshape(nb, per).sum(axis=1)
+    bs = bt * t_f / bw
+    half = 1.96 * float(bs.std(ddof=1)) / np.sqrt(nb)
     return SpeedupEstimate(tokens_per_round=float(tok.mean()), wall_ms_per_round=float(wall.mean()),
-                           speedup=float(speed), ci_halfwidth=float(half), inner_rounds_per_outer=float(inner.mean()))
+                           speedup=float(speed), ci_halfwidth=half, inner_rounds_per_outer=float(inner.mean()))
 
 
 # ---------------------------------------------------------------------------

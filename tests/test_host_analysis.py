@@ -76,3 +76,17 @@ def test_planted_attention_weights_construction(P):
     with pytest.raises(ValueError):
         P.planted_attention_weights(P.ModelConfig(n_layers=1, n_heads=2, n_kv_heads=2, head_dim=8, d_ff=16,
                                                   vocab_size=260, max_seq=512), 96, 6, 0.8, ord("A"))
+
+
+def test_monte_carlo_reproduces_reference_seeds(P):
+    """Same draw order and batch means as the reference: a seed gives the
+    reference's estimate (tests/golden/make_golden_mc.py)."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ref_mc.json")) as f:
+        cases = json.load(f)
+    for c in cases:
+        a1, a2, g1, g2, ctx, b, rounds, seed = c["args"]
+        r = P.simulate_speedup(a1, a2, g1, g2, P.LatencyModel(), ctx, b, rounds=rounds, seed=seed)
+        got = [r.tokens_per_round, r.wall_ms_per_round, r.speedup, r.ci_halfwidth, r.inner_rounds_per_outer]
+        assert np.allclose(got, c["result"], rtol=1e-12, atol=1e-12), c["args"]
