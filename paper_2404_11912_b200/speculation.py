@@ -93,10 +93,10 @@ class _StepGraph:
         # synchronises the whole device first); thread_local: other host
         # threads (loopback shard ranks) keep launching on their own streams
         # while this one captures
-        # (a graph object freed by the garbage collector during the capture
-        # would destroy its executable mid-capture and invalidate it: collect
-        # first and keep the collector off until the capture ends)
-        gc.collect()
+        # (a graph object freed by the cycle collector during the capture
+        # would destroy its executable mid-capture and invalidate it: keep the
+        # collector off until the capture ends; nothing in the captured region
+        # drops a reference to a graph)
         was_enabled = gc.isenabled()
         gc.disable()
         try:
