@@ -108,9 +108,14 @@ class DeviceModel:
     the rope table stay fp32.
     """
 
-    def __init__(self, config: ModelConfig, tensors: dict, tied_head: bool):
+    def __init__(self, config: ModelConfig, tensors, tied_head: bool, rope_scaling=None):
+        """tensors: name -> numpy [in, out] fp32 (the reference layout), as a
+        dict or a callable fetching one tensor at a time (checkpoint import:
+        only one matrix is on the host at once)."""
         self.config = config
         self.tied_head = tied_head
+        self.rope_scaling = rope_scaling
+        get = tensors if callable(tensors) else tensors.__getitem__
         dev = device()
         L, d, dff, V = config.n_layers, config.d_model, config.d_ff, config.vocab_size
         kv = config.n_kv_heads * config.head_dim
@@ -123,7 +128,7 @@ class DeviceModel:
             out[:, :t.shape[1]] = t.to(torch.bfloat16)
             return out
 
-        g = lambda i, n: tensors[f"layers.{i}.{n}"]
+        g = lambda i, n: get(f"layers.{i}.{n}")
         self.wqkv = torch.empty((L, nqkv, self.ld_d), dtype=torch.bfloat16, device=dev)
         self.wo = torch.empty((L, d, self.ld_d), dtype=torch.bfloat16, device=dev)
         self.wgu = torch.empty((L, 2 * dff, self.ld_d), dtype=torch.bfloat16, device=dev)
@@ -140,10 +145,15 @@ class DeviceModel:
             self.wdown[i] = mat(g(i, "w_down"), self.ld_ff)
             self.attn_norm[i] = torch.from_numpy(g(i, "attn_norm").astype(np.float32))
             self.mlp_norm[i] = torch.from_numpy(g(i, "mlp_norm").astype(np.float32))
-        self.emb = mat(tensors["embedding"].T, self.ld_d)
-        self.head = self.emb if tied_head else mat(tensors["lm_head"], self.ld_d)
-        self.final_norm = torch.from_numpy(tensors["final_norm"].astype(np.float32)).to(dev)
+        self.emb = mat(get("embedding").T, self.ld_d)
+        self.head = self.emb if tied_head else mat(get("lm_head"), self.ld_d)
+        self.final_norm = torch.from_numpy(get("final_norm").astype(np.float32)).to(dev)
         self._finish()
+
+    @classmethod
+    def from_tensor_source(cls, config: ModelConfig, tied_head: bool, get, rope_scaling=None) -> "DeviceModel":
+        """Pack from a per-tensor getter (checkpoint.load_hf_llama)."""
+        return cls(config, get, tied_head, rope_scaling)
 
     @classmethod
     def random(cls, config: ModelConfig, seed: int, tied_head: bool = False, std: float = 0.02):
@@ -151,7 +161,7 @@ class DeviceModel:
         model sizes whose host fp32 copy is impractical (Llama2-7B shape).
         Same distribution as generate_weights, different stream."""
         self = cls.__new__(cls)
-        self.config, self.tied_head = config, tied_head
+        self.config, self.tied_head, self.rope_scaling = config, tied_head, None
         dev = device()
         gen = torch.Generator(device=dev)
         gen.manual_seed(seed)
@@ -203,7 +213,9 @@ class DeviceModel:
 
     def _finish(self):
         cfg = self.config
-        cos, sin = rope_tables(cfg.max_seq, cfg.head_dim, cfg.rope_theta)
+        scaling = getattr(self, "rope_scaling", None)
+        cos, sin = (scaling.tables(cfg.max_seq, cfg.head_dim, cfg.rope_theta) if scaling is not None
+                    else rope_tables(cfg.max_seq, cfg.head_dim, cfg.rope_theta))
         dev = device()
         self.rope_cos = torch.from_numpy(cos).to(dev)
         self.rope_sin = torch.from_numpy(sin).to(dev)
@@ -252,6 +264,9 @@ class ModelWeights:
     tensors: dict
     tied_head: bool = True
     _dev: Optional[DeviceModel] = field(default=None, repr=False, compare=False)
+    # checkpoint.RopeScaling of an imported HF checkpoint (linear / YaRN /
+    # llama3 tables); None = the reference's plain RoPE (tensor.py:66-76)
+    rope_scaling: Optional[object] = field(default=None, compare=False)
 
     def validate(self):
         expected = dict(tensor_order(self.config, self.tied_head))
@@ -276,7 +291,7 @@ class ModelWeights:
 
     def device(self) -> DeviceModel:
         if self._dev is None:
-            self._dev = DeviceModel(self.config, self.tensors, self.tied_head)
+            self._dev = DeviceModel(self.config, self.tensors, self.tied_head, self.rope_scaling)
         return self._dev
 
     def runtime(self) -> DeviceModel:
@@ -297,7 +312,7 @@ class ModelWeights:
     @classmethod
     def on_device(cls, dm: DeviceModel) -> "ModelWeights":
         """Wrap device-only random weights (DeviceModel.random)."""
-        w = cls(dm.config, {}, dm.tied_head)
+        w = cls(dm.config, {}, dm.tied_head, rope_scaling=getattr(dm, "rope_scaling", None))
         w._dev = dm
         return w
 
