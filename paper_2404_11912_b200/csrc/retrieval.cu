@@ -7,7 +7,11 @@
 // positions ascending inside a chunk.  Scores are fp64 like the reference;
 // products of bf16/fp32 keys and fp32 queries are exact in fp64, so rankings
 // agree with the reference except for sub-1e-16 near-ties.
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+
 #include "hs_common.cuh"
+#include "tc_util.cuh"
 
 namespace hs {
 
@@ -95,6 +99,174 @@ __global__ void __launch_bounds__(SCORE_THREADS) chunk_score_kernel(
     if (s == 0.0) s = 0.0;   // fold -0.0 so ties compare like Python floats
     scores[(size_t)l * n_chunks + c] = s;
   }
+}
+
+// ---- TMA-staged chunk scoring (bf16 keys, the build path) -------------------
+// grid (ceil(n_chunks / CS_NB), n_layers), 8 consumer warps + 1 TMA warp, two
+// CTAs per SM.  Each stage is one 3-D tensor-map box {dh, chunk keys, hb kv
+// heads} of one chunk (hb chosen so a stage is <= 32 KB: 16 heads at chunk 8,
+// dh 128), streamed through a CS_STAGES-deep ring; a chunk is KVH / hb
+// stages.  Thread = (head of the stage, 8 consecutive dims): fp64 sum of the
+// chunk's keys in key order (caches.py:431, exact for bf16 inputs), then the
+// fp64 dot with the group's queries, accumulated over the chunk's stages;
+// per chunk the 8 warp partials are summed in warp order (deterministic; the
+// same arithmetic as chunk_score_kernel up to the order of the final sum).
+constexpr int CS_STAGES = 3;
+constexpr int CS_STAGE_BYTES = 32768;
+constexpr int CS_NB = 16;            // chunks per CTA
+constexpr int CS_CONSUMERS = 256;
+constexpr int CS_THREADS = CS_CONSUMERS + 32;
+constexpr int CS_SMEM = CS_STAGES * CS_STAGE_BYTES + 1024;
+
+struct CsArgs {
+  int KVH, DH, H, g, upto, chunk, n_chunks, hb, spc;
+  const float *q;     // [L][H][DH]
+  double *scores;     // [L][n_chunks]
+};
+
+__global__ void __launch_bounds__(CS_THREADS, 2) chunk_score_tma_kernel(const __grid_constant__ CUtensorMap tm,
+                                                                      CsArgs a) {
+  extern __shared__ __align__(128) unsigned char cs_smem[];
+  unsigned char *ring = cs_smem;
+  uint64_t *full = reinterpret_cast<uint64_t *>(cs_smem + CS_STAGES * CS_STAGE_BYTES);
+  uint64_t *empty = full + CS_STAGES;
+  __shared__ double red[CS_NB][CS_CONSUMERS / 32];
+  const int l = blockIdx.y;
+  const int c0 = blockIdx.x * CS_NB;
+  const int nc = min(CS_NB, a.n_chunks - c0);
+  const int n_st = nc * a.spc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < CS_STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], CS_CONSUMERS / 32);
+    }
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t stage_bytes = (uint32_t)a.hb * a.chunk * a.DH * 2;
+  if (warp == CS_CONSUMERS / 32) {
+    // TMA producer
+    if (lane == 0) {
+      tc::tma_prefetch(&tm);
+      const uint64_t pol = tc::policy_evict_first();
+      for (int i = 0; i < n_st; ++i) {
+        const int slot = i % CS_STAGES;
+        if (i >= CS_STAGES) tc::mbar_wait_sleep(&empty[slot], ((i / CS_STAGES) - 1) & 1);
+        const int c = c0 + i / a.spc, j = i % a.spc;
+        tc::mbar_expect_tx(&full[slot], stage_bytes);
+        tc::tma_load_3d_hint(ring + slot * CS_STAGE_BYTES, &tm, &full[slot], 0, c * a.chunk,
+                             l * a.KVH + j * a.hb, pol);
+      }
+    }
+    return;
+  }
+  const int dgs = a.DH / 8;
+  const int hl = threadIdx.x / dgs, dg = threadIdx.x % dgs;
+  const bool active = hl < a.hb;
+  double part = 0.0;
+  for (int i = 0; i < n_st; ++i) {
+    const int slot = i % CS_STAGES;
+    const int ci = i / a.spc, j = i % a.spc;
+    const int c = c0 + ci;
+    const int b0 = c * a.chunk, cnt = min(a.upto, b0 + a.chunk) - b0;
+    tc::mbar_wait(&full[slot], (i / CS_STAGES) & 1);
+    if (active) {
+      const unsigned char *src = ring + slot * CS_STAGE_BYTES + ((size_t)hl * a.chunk * a.DH + dg * 8) * 2;
+      double sum[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum[u] = 0.0;
+      for (int s = 0; s < cnt; ++s) {   // key order (caches.py:431)
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4 *>(src + (size_t)s * a.DH * 2), f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum[u] += (double)f[u];
+      }
+      // the chunk mean sum / cnt: for a power-of-two count the product with
+      // the exact reciprocal is the same correctly rounded value, without
+      // the fp64 division sequence (the partial last chunk divides)
+      const double dcnt = (double)cnt;
+      if ((cnt & (cnt - 1)) == 0) {
+        const double rc = 1.0 / dcnt;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum[u] *= rc;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum[u] /= dcnt;
+      }
+      const int kh = j * a.hb + hl;
+      for (int gi = 0; gi < a.g; ++gi) {
+        const float4 *qh = reinterpret_cast<const float4 *>(a.q + ((size_t)l * a.H + kh * a.g + gi) * a.DH + dg * 8);
+        const float4 x = __ldg(qh), y = __ldg(qh + 1);
+        const float qv[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) part += (double)qv[u] * sum[u];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&empty[slot]);
+    if (j == a.spc - 1) {   // chunk complete: warp partial, then start the next chunk
+      const double w = warp_sum(part);
+      if (lane == 0) red[ci][warp] = w;
+      part = 0.0;
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(CS_CONSUMERS) : "memory");
+  if (threadIdx.x < nc) {
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < CS_CONSUMERS / 32; ++w) tot += red[threadIdx.x][w];
+    double sc = tot / (double)a.H / sqrt((double)a.DH);
+    if (sc == 0.0) sc = 0.0;   // fold -0.0 so ties compare like Python floats
+    a.scores[(size_t)l * a.n_chunks + c0 + threadIdx.x] = sc;
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 cs_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess && p)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// TMA path: bf16 keys laid out [layer][kv head][slot][dh] (layer stride = KVH x
+// head stride), dh a multiple of 8 up to 256, 16-byte aligned strides.
+// Returns 1 when launched, 0 when the geometry needs the generic kernel.
+static int launch_chunk_score_tma(const void *keys, long long ls, long long hs_, long long ts, int L, int KVH,
+                                  int DH, int upto, int chunk, const float *q, int H, double *scores, int n_chunks,
+                                  cudaStream_t st) {
+  if (DH % 8 || DH > 256 || ts != DH || ls != (long long)KVH * hs_ || (hs_ * 2) % 16 || ((uintptr_t)keys % 16) ||
+      ((uintptr_t)q % 16) || chunk > 256 || DH / 8 > CS_CONSUMERS)
+    return 0;
+  int hb = KVH < CS_CONSUMERS / (DH / 8) ? KVH : CS_CONSUMERS / (DH / 8);
+  while (hb > 1 && ((long long)hb * chunk * DH * 2 > CS_STAGE_BYTES || KVH % hb)) --hb;
+  if ((long long)hb * chunk * DH * 2 > CS_STAGE_BYTES || hb > 256) return 0;
+  auto enc = cs_encode();
+  if (!enc) return 0;
+  CUtensorMap m;
+  cuuint64_t dims[3] = {(cuuint64_t)DH, (cuuint64_t)upto, (cuuint64_t)L * KVH};
+  cuuint64_t strides[2] = {(cuuint64_t)ts * 2, (cuuint64_t)hs_ * 2};
+  cuuint32_t box[3] = {(cuuint32_t)DH, (cuuint32_t)chunk, (cuuint32_t)hb};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(keys), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return 0;
+  CsArgs a;
+  a.KVH = KVH; a.DH = DH; a.H = H; a.g = H / KVH; a.upto = upto; a.chunk = chunk; a.n_chunks = n_chunks;
+  a.hb = hb; a.spc = KVH / hb; a.q = q; a.scores = scores;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chunk_score_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CS_SMEM);
+    attr = true;
+  }
+  dim3 grid(ceil_div(n_chunks, CS_NB), L);
+  chunk_score_tma_kernel<<<grid, CS_THREADS, CS_SMEM, st>>>(m, a);
+  return 1;
 }
 
 __device__ __forceinline__ unsigned long long order_key(double s) {
@@ -300,6 +472,11 @@ extern "C" int hs_chunk_score(const void *keys, int key_bf16, long long layer_st
 #define HS_SCORE(KT, VW)                                                                                 \
   hs::chunk_score_kernel<KT, VW><<<grid, hs::SCORE_THREADS, 0, st>>>((const KT *)keys, layer_stride,    \
       head_stride, token_stride, n_kv_heads, head_dim, upto, chunk, queries, n_heads, scores, n_chunks)
+  static const bool no_tma = getenv("HS_SCORE_NO_TMA") != nullptr;   // A/B hook: the generic kernel
+  if (key_bf16 && !no_tma &&
+      hs::launch_chunk_score_tma(keys, layer_stride, head_stride, token_stride, n_layers, n_kv_heads, head_dim, upto,
+                                 chunk, queries, n_heads, scores, n_chunks, st))
+    return hs::check_launch("chunk_score");
   if (key_bf16) { if (vec) HS_SCORE(uint16_t, 8); else HS_SCORE(uint16_t, 1); }
   else { if (vec) HS_SCORE(float, 8); else HS_SCORE(float, 1); }
 #undef HS_SCORE

