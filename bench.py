@@ -85,6 +85,8 @@ def parse():
                     help="planted successor channel (model.plant_successor); 0 = pure random init")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true", help="use the sequence-sharded (NCCL) path even on 1 GPU")
+    ap.add_argument("--tp", action="store_true",
+                    help="also split the target's dense projections over the ranks (tensor parallel, hs_forward_tp)")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no extras)")
     return ap.parse_args()
 
@@ -419,7 +421,8 @@ def workload_config(args, world=1):
                         f"{args.easy_frac} (model.plant_successor; acceptance near the paper's 0.92)"
                         if args.easy_frac > 0 else "pure random-init N(0,0.02) bf16 (acceptance ~0)"),
             "parallelism": ("host CPU (reference arm)" if args.impl == "reference" else
-                            "1 GPU" if world == 1 else f"full KV cache sequence-sharded over {world} GPUs (NCCL)")}
+                            ("1 GPU" if world == 1 else f"full KV cache sequence-sharded over {world} GPUs (NCCL)")
+                            + (f", dense projections tensor-parallel over {world}" if args.tp else ""))}
 
 
 # ---------------------------------------------------------------------------
@@ -449,7 +452,7 @@ def main():
     # one sequence sharded over the ranks: every rank holds the same weights and
     # tokens and runs the same (deterministic) loop; only the full cache is split
     shards = None
-    if world > 1 or args.shard:
+    if world > 1 or args.shard or args.tp:
         from paper_2404_11912_b200.shard import SequenceShards
         shards = SequenceShards.init() if world > 1 else SequenceShards.single()
     tdm, ddm = P.DeviceModel.random(tcfg, seed=1), P.DeviceModel.random(dcfg, seed=1001)
@@ -461,7 +464,8 @@ def main():
     spec = P.SpecConfig(target_len=args.context + 1, gamma1=GAMMA1, gamma2=GAMMA2, temperature=args.temperature,
                         seed=0, streaming=P.StreamingConfig(n_sink=SINK, budget=STREAM),
                         retrieval=P.RetrievalConfig(chunk_size=CHUNK, budget=BUDGET))
-    sess = P.HierarchicalSession.synthetic(target, draft, ctx, spec, seed=0, shards=shards)
+    sess = P.HierarchicalSession.synthetic(target, draft, ctx, spec, seed=0, shards=shards,
+                                           tp=shards if args.tp else None)
     torch.cuda.synchronize()
 
     def step(i):

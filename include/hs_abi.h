@@ -182,6 +182,18 @@ int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsSha
                const int32_t *tokens, int t, float *logits, float *q_stash,
                void *workspace, size_t workspace_bytes, void *stream);
 
+/* hs_forward with tensor-parallel dense layers (the
+ * projections of model.py:285,316,320-323,328 split by output rows in
+ * 128-row tiles over tp->world ranks, each block all-gathered over tp->comm
+ * and the next RMSNorm operand rebuilt replicated).  sh: the sequence
+ * shards of a full cache (may share tp's communicator) or NULL for a
+ * replicated cache (the retrieval lane).  t <= 8 (decode / verify blocks).
+ * Logits and every activation end up identical on all ranks.               */
+size_t hs_forward_tp_workspace_bytes(const HsModel *m, int t, int n_view, int split, int world, int tp_world);
+int hs_forward_tp(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh, const HsShard *tp,
+                  const int32_t *tokens, int t, float *logits, float *q_stash,
+                  void *workspace, size_t workspace_bytes, void *stream);
+
 /* one decode position over a TopKCache (caches.py:568-652; the oracle
  * upper-bound pairing of analytics.measure_acceptance): like hs_forward with
  * t = 1 on an unsharded full cache, but each layer attends only over the

@@ -74,6 +74,9 @@ _SIGS = {
     "hs_gemv_tc": (i32, [vp, i32, vp, i32, i32, i32, vp, i32, vp, i32, vp, sz, vp]),
     "hs_split_rows": (i32, [vp, i32, i32, i32, i32, vp, f32, vp, vp]),
     "hs_forward": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), _P(HsShard), vp, i32, vp, vp, vp, sz, vp]),
+    "hs_forward_tp_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32, i32, i32]),
+    "hs_forward_tp": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), _P(HsShard), _P(HsShard), vp, i32, vp, vp, vp, sz,
+                            vp]),
     "hs_forward_attn_probs": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), vp, i32, vp, vp, vp, vp, vp, sz, vp]),
     "hs_forward_probe": (i32, [_P(HsModel), _P(HsCache), _P(HsStep), vp, i32, vp, vp, vp, vp, sz, vp]),
     "hs_forward_topk_workspace_bytes": (sz, [_P(HsModel), i32, i32]),

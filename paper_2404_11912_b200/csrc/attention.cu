@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
         fac = (m_old == -INFINITY) ? 0.f : expf(m_old - m_new);
       }
       float ps = warp_sum(p0 + p1);
+      __syncwarp();   // every lane's reads of this row (and of m_s / l_s) precede the writes
       S[rr][lane] = p0; S[rr][lane + 32] = p1;
       if (lane == 0) {
         f_s[rr] = fac; m_s[rr] = m_new; l_s[rr] = l_s[rr] * fac + ps;

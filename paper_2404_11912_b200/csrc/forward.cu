@@ -65,10 +65,67 @@ int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const floa
                       cudaStream_t st);
 int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                    uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st,
-                   const GemvNorm *norm = nullptr);
+                   const GemvNorm *norm = nullptr, const float *yin = nullptr, int ldyin = 0);
 int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk, double *ssq,
                      cudaStream_t st);
 size_t gemv_tc_ws_bytes(int N, int nkb);
+
+// ---- tensor-parallel dense layers ("TP-shard the dense
+// weights"): every projection is split by output rows in whole 128-row tiles
+// (rank r of G computes tiles [T*r/G, T*(r+1)/G)); the rank's block goes to a
+// packed send buffer [rows][wmax], an all-gather (NCCL, or the loopback
+// group's device copies) replicates every block, and tp_unpack_kernel
+// scatters them into the replicated activation.  The RMSNorm operand and row
+// statistics of the next projection are rebuilt by norm_prep (bit-identical
+// to the GEMV epilogue that produces them in the replicated forward).  Each
+// rank streams 1/G of the weight bytes; the K split of a block follows its
+// own row count, so results equal the G = 1 forward to fp32 rounding (and
+// are bitwise identical on every rank).
+__host__ __device__ inline void tp_rows(int N, int rank, int world, int &r0, int &n) {
+  const int tiles = (N + 127) / 128;
+  const int t0 = (int)((long long)tiles * rank / world), t1 = (int)((long long)tiles * (rank + 1) / world);
+  r0 = t0 * 128;
+  const int r1 = t1 * 128 < N ? t1 * 128 : N;
+  n = r1 > r0 ? r1 - r0 : 0;
+}
+inline int tp_wmax(int N, int world) { return ((N + 127) / 128 + world - 1) / world * 128; }
+
+// recv [world][rows][wm] elements of es bytes -> dst [rows][ld]: rank g's
+// block lands at its columns (half: SwiGLU output, act column = row / 2)
+__global__ void tp_unpack_kernel(const unsigned char *recv, int world, int rows, int wm, int es, int N, int half,
+                                 unsigned char *dst, int ld) {
+  const int row = blockIdx.x, g = blockIdx.y;
+  int r0, n;
+  tp_rows(N, g, world, r0, n);
+  if (half) { r0 >>= 1; n >>= 1; }
+  const unsigned char *src = recv + ((size_t)g * rows + row) * wm * es;
+  unsigned char *d = dst + ((size_t)row * ld + r0) * es;
+  if (es == 4) {
+    for (int c = threadIdx.x; c < n; c += blockDim.x) reinterpret_cast<float *>(d)[c] = reinterpret_cast<const float *>(src)[c];
+  } else {
+    for (int c = threadIdx.x; c < n; c += blockDim.x)
+      reinterpret_cast<uint16_t *>(d)[c] = reinterpret_cast<const uint16_t *>(src)[c];
+  }
+}
+
+static int tp_exchange(const HsShard *tp, const void *send, void *recv, int rows, int wm, int es, int N, int half,
+                       void *dst, int ld, cudaStream_t s) {
+  int rc = shard_all_gather(tp, send, recv, (size_t)rows * wm * es, s);
+  if (rc != HS_OK) return rc;
+  tp_unpack_kernel<<<dim3(rows, tp->world), 256, 0, s>>>((const unsigned char *)recv, tp->world, rows, wm, es, N,
+                                                         half, (unsigned char *)dst, ld);
+  return check_launch("tp_unpack");
+}
+
+static size_t tp_send_bytes(const HsModel *m, int t, int world) {
+  if (world <= 0) return 0;
+  const int d = m->d_model, nqkv = (m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
+  size_t b = (size_t)t * tp_wmax(nqkv, world) * 4;
+  const size_t cand[3] = {(size_t)t * tp_wmax(d, world) * 4, (size_t)24 * (tp_wmax(2 * m->d_ff, world) / 2) * 2,
+                          (size_t)t * tp_wmax(m->vocab_size, world) * 4};
+  for (size_t c : cand) b = c > b ? c : b;
+  return b;
+}
 
 // Workspace layout.  The head is position-independent so that the regions
 // which must stay zero/clean between calls never move:
@@ -85,6 +142,7 @@ struct FwdWs {
   void *att_ws;
   size_t att_bytes;
   float *send, *recv;
+  void *tsend, *trecv;      // tensor-parallel block exchange
 };
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -95,13 +153,18 @@ static size_t gemv_region(const HsModel *m) {
   const int Ns[5] = {d + 2 * kv, d, 2 * m->d_ff, d, m->vocab_size};
   const int Ks[5] = {m->ld_d, m->ld_d, m->ld_d, m->ld_ff, m->ld_d};
   for (int i = 0; i < 5; ++i) {
-    size_t b = gemv_tc_ws_bytes(Ns[i], Ks[i] / 64);
-    if (b > g) g = b;
+    // the whole matrix and every row block a tensor-parallel rank can own
+    for (int tiles = (Ns[i] + 127) / 128; tiles >= 1; --tiles) {
+      const int n = tiles * 128 < Ns[i] ? tiles * 128 : Ns[i];
+      size_t b = gemv_tc_ws_bytes(n, Ks[i] / 64);
+      if (b > g) g = b;
+    }
   }
   return align256(g);
 }
 
-static size_t carve(const HsModel *m, int t, int n_view, int split, int world, char *base, FwdWs *w) {
+static size_t carve(const HsModel *m, int t, int n_view, int split, int world, char *base, FwdWs *w,
+                    int tp_world = 0) {
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim;
   size_t off = 0;
   auto take = [&](size_t bytes) { char *p = base ? base + off : nullptr; off += align256(bytes); return p; };
@@ -120,6 +183,9 @@ static size_t carve(const HsModel *m, int t, int n_view, int split, int world, c
   const size_t part = (size_t)t * H * (dh + 2) * 4;
   w->send = world > 0 ? (float *)take(part) : nullptr;
   w->recv = world > 0 ? (float *)take(part * world) : nullptr;
+  const size_t tb = tp_send_bytes(m, t, tp_world);
+  w->tsend = tp_world > 0 ? take(tb) : nullptr;
+  w->trecv = tp_world > 0 ? take(tb * tp_world) : nullptr;
   return off;
 }
 
@@ -169,12 +235,31 @@ extern "C" size_t hs_forward_workspace_clean_bytes(const HsModel *m) {
 static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                         const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
                         size_t workspace_bytes, void *stream, int topk_budget, double *probs = nullptr,
-                        float *hprobs = nullptr, float *probe = nullptr);
+                        float *hprobs = nullptr, float *probe = nullptr, const HsShard *tp = nullptr);
 
 extern "C" int hs_forward(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                           const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
                           size_t workspace_bytes, void *stream) {
   return forward_impl(m, c, st, sh, tokens, t, logits, q_stash, workspace, workspace_bytes, stream, 0);
+}
+
+extern "C" size_t hs_forward_tp_workspace_bytes(const HsModel *m, int t, int n_view, int split, int world,
+                                                int tp_world) {
+  hs::FwdWs w;
+  return hs::carve(m, t, n_view, split, world, nullptr, &w, tp_world);
+}
+
+// hs_forward with tensor-parallel dense layers over `tp` (rank / world of
+// its communicator; may be the same communicator as the sequence shards
+// `sh`, or sh == NULL for a replicated cache such as the retrieval lane's)
+extern "C" int hs_forward_tp(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
+                             const HsShard *tp, const int32_t *tokens, int t, float *logits, float *q_stash,
+                             void *workspace, size_t workspace_bytes, void *stream) {
+  HS_REQUIRE(tp != nullptr && tp->comm != nullptr && tp->world >= 1 && tp->rank >= 0 && tp->rank < tp->world,
+             HS_ERR_VALUE, "forward: bad tensor-parallel descriptor");
+  HS_REQUIRE(t <= 8, HS_ERR_VALUE, "forward: tensor-parallel layers run decode / verify blocks of <= 8 rows");
+  return forward_impl(m, c, st, sh, tokens, t, logits, q_stash, workspace, workspace_bytes, stream, 0, nullptr,
+                      nullptr, nullptr, tp);
 }
 
 extern "C" size_t hs_forward_topk_workspace_bytes(const HsModel *m, int n_view, int budget) {
@@ -218,7 +303,7 @@ extern "C" int hs_forward_probe(const HsModel *m, const HsCache *c, const HsStep
 static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, const HsShard *sh,
                         const int32_t *tokens, int t, float *logits, float *q_stash, void *workspace,
                         size_t workspace_bytes, void *stream, int topk_budget, double *probs, float *hprobs,
-                        float *probe) {
+                        float *probe, const HsShard *tp) {
   using namespace hs;
   HS_REQUIRE(t >= 1, HS_ERR_VALUE, "empty token sequence");
   HS_REQUIRE(c->n_layers == m->n_layers && c->n_kv_heads == m->n_kv_heads && c->head_dim == m->head_dim,
@@ -233,7 +318,8 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
                "forward: only a full (linear) cache can be sequence-sharded");
   }
   FwdWs w;
-  const size_t need = carve(m, t, st->n_view, st->split, sharded ? sh->world : 0, (char *)workspace, &w);
+  const size_t need = carve(m, t, st->n_view, st->split, sharded ? sh->world : 0, (char *)workspace, &w,
+                            tp ? tp->world : 0);
   HS_REQUIRE(workspace_bytes >= need, HS_ERR_VALUE, "forward: workspace %zu < %zu", workspace_bytes, need);
   void *topk_ws = nullptr;
   size_t topk_bytes = 0;
@@ -253,6 +339,8 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
                        : st->append_mode == HS_APPEND_LINEAR ? st->append_base
                                                              : -1;
   const bool fused_split = t <= 8;   // one row block: folded norms, no split kernels
+  HS_REQUIRE(tp == nullptr || (fused_split && topk_budget == 0 && probs == nullptr && probe == nullptr), HS_ERR_VALUE,
+             "forward: tensor-parallel layers need a plain forward of <= 8 rows");
   const int d_tiles = (d + 127) / 128;
   int rc;
 #define HS_TRY(call) do { if ((rc = (call)) != HS_OK) return rc; } while (0)
@@ -276,8 +364,18 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       const uint16_t *wdn = m->wdown + (size_t)l * d * m->ld_ff;
       const bool last = l + 1 == m->n_layers;
       GemvNorm in_qkv = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
-      HS_TRY(launch_gemv_tc(w.xd, t, wqkv, m->ld_d, nqkv, 0, w.qkv, nqkv, nullptr, 0, w.gemv_ws, w.gemv_bytes, s,
-                            &in_qkv));
+      if (tp) {
+        int r0, n;
+        tp_rows(nqkv, tp->rank, tp->world, r0, n);
+        const int wm = tp_wmax(nqkv, tp->world);
+        if (n > 0)
+          HS_TRY(launch_gemv_tc(w.xd, t, wqkv + (size_t)r0 * m->ld_d, m->ld_d, n, 0, (float *)w.tsend, wm, nullptr,
+                                0, w.gemv_ws, w.gemv_bytes, s, &in_qkv));
+        HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, nqkv, 0, w.qkv, nqkv, s));
+      } else {
+        HS_TRY(launch_gemv_tc(w.xd, t, wqkv, m->ld_d, nqkv, 0, w.qkv, nqkv, nullptr, 0, w.gemv_ws, w.gemv_bytes, s,
+                              &in_qkv));
+      }
       if (fuse_rope) {
         // RoPE + K/V append inside the tensor-core attention (its q staging
         // reads the qkv rows; the CTA covering the appended slots writes them)
@@ -312,16 +410,53 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
                                 s));
       if (probe) HS_TRY(launch_probe_probs(c, l, st, H, w.q, t, probe + (size_t)l * H * st->n_view, s));
       }
+      const float *gain_next = last ? m->final_norm : m->attn_norm + (size_t)(l + 1) * d;
+      GemvNorm in_gu = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+      if (tp) {
+        int r0, n, wm;
+        // w_o: residual block -> all ranks; the mlp_norm operand is rebuilt replicated
+        tp_rows(d, tp->rank, tp->world, r0, n);
+        wm = tp_wmax(d, tp->world);
+        if (n > 0)
+          HS_TRY(launch_gemv_tc(w.xa, t, wo + (size_t)r0 * m->ld_d, m->ld_d, n, 1, (float *)w.tsend, wm, nullptr, 0,
+                                w.gemv_ws, w.gemv_bytes, s, nullptr, w.x + r0, d));
+        HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, d, 0, w.x, d, s));
+        HS_TRY(launch_norm_prep(w.x, d, t, d, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq, s));
+        // gate|up: SwiGLU act block (split operand rows) -> all ranks
+        tp_rows(2 * ff, tp->rank, tp->world, r0, n);
+        wm = tp_wmax(2 * ff, tp->world);
+        if (n > 0)
+          HS_TRY(launch_gemv_tc(w.xd, t, wgu + (size_t)r0 * m->ld_d, m->ld_d, n, 2, nullptr, 0, (uint16_t *)w.tsend,
+                                wm / 2, w.gemv_ws, w.gemv_bytes, s, &in_gu));
+        HS_TRY(tp_exchange(tp, w.tsend, w.trecv, 3 * 8, wm / 2, 2, 2 * ff, 1, w.xf, m->ld_ff, s));
+        // w_down: residual block -> all ranks; next norm operand rebuilt
+        tp_rows(d, tp->rank, tp->world, r0, n);
+        wm = tp_wmax(d, tp->world);
+        if (n > 0)
+          HS_TRY(launch_gemv_tc(w.xf, t, wdn + (size_t)r0 * m->ld_ff, m->ld_ff, n, 1, (float *)w.tsend, wm, nullptr,
+                                0, w.gemv_ws, w.gemv_bytes, s, nullptr, w.x + r0, d));
+        HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, d, 0, w.x, d, s));
+        HS_TRY(launch_norm_prep(w.x, d, t, d, gain_next, w.xd, m->ld_d, w.ssq, s));
+        continue;
+      }
       GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq};
       HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo));
-      GemvNorm in_gu = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
       HS_TRY(launch_gemv_tc(w.xd, t, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes, s,
                             &in_gu));
-      GemvNorm out_dn = {nullptr, 0, 1, 0.f, last ? m->final_norm : m->attn_norm + (size_t)(l + 1) * d, w.xd, m->ld_d,
-                         w.ssq};
+      GemvNorm out_dn = {nullptr, 0, 1, 0.f, gain_next, w.xd, m->ld_d, w.ssq};
       HS_TRY(launch_gemv_tc(w.xf, t, wdn, m->ld_ff, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_dn));
     }
     GemvNorm in_head = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+    if (tp) {
+      int r0, n;
+      tp_rows(m->vocab_size, tp->rank, tp->world, r0, n);
+      const int wm = tp_wmax(m->vocab_size, tp->world);
+      if (n > 0)
+        HS_TRY(launch_gemv_tc(w.xd, t, m->head + (size_t)r0 * m->ld_d, m->ld_d, n, 0, (float *)w.tsend, wm, nullptr,
+                              0, w.gemv_ws, w.gemv_bytes, s, &in_head));
+      HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, m->vocab_size, 0, logits, m->vocab_size, s));
+      return HS_OK;
+    }
     HS_TRY(launch_gemv_tc(w.xd, t, m->head, m->ld_d, m->vocab_size, 0, logits, m->vocab_size, nullptr, 0, w.gemv_ws,
                           w.gemv_bytes, s, &in_head));
     return HS_OK;

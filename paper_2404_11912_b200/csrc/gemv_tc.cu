@@ -199,6 +199,11 @@ struct GemvTcArgs {
   double *ssq_out;
   float *y;
   int ldy;
+  // residual source of epilogue 1 (null: y itself, updated in place); the
+  // tensor-parallel forward reads x[:, block] and writes the block to a send
+  // buffer
+  const float *yin;
+  int ldyin;
   uint16_t *xs_out;   // swiglu epilogue: split of act written here ([24][ld_xs_out]) if non-null
   int ld_xs_out;
   float *partial;     // [ks][n_tiles*128][8]
@@ -366,7 +371,9 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   float yres[TC_T];
 #pragma unroll
   for (int r = 0; r < TC_T; ++r)
-    yres[r] = (a.epilogue == 1 && r < a.t && o < a.N) ? __ldcg(a.y + (size_t)r * a.ldy + o) : 0.f;
+    yres[r] = (a.epilogue == 1 && r < a.t && o < a.N)
+                  ? __ldcg(a.yin ? a.yin + (size_t)r * a.ldyin + o : a.y + (size_t)r * a.ldy + o)
+                  : 0.f;
 
   if (a.ks == 1) {
     finalize(a, o, v, yres, lane, tile, inv_rms, red);
@@ -506,7 +513,7 @@ int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const floa
 // y (+)= W . x for one pass of <= 8 rows whose split operand is in xs [24][ldw]
 int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                    uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st,
-                   const GemvNorm *norm) {
+                   const GemvNorm *norm, const float *yin, int ldyin) {
   HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "gemv_tc: t=%d outside [1,%d]", t, TC_T);
   HS_REQUIRE(ldw % TC_BK == 0, HS_ERR_SHAPE, "gemv_tc: ldw %d not a multiple of %d", ldw, TC_BK);
   HS_REQUIRE(((uintptr_t)w % 16) == 0 && ((uintptr_t)xs % 16) == 0, HS_ERR_VALUE, "gemv_tc: operands must be 16B aligned");
@@ -524,6 +531,7 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   a.N = N; a.nkb = nkb; a.ks = gemv_tc_ksplit(N, nkb); a.t = t; a.epilogue = epilogue; a.n_tiles = tiles;
   a.cluster = (a.ks > 1 && a.ks <= 8 && gemv_use_cluster()) ? 1 : 0;
   a.y = y; a.ldy = ldy; a.xs_out = xs_out; a.ld_xs_out = ld_xs_out;
+  a.yin = yin; a.ldyin = ldyin;
   a.ssq_in = nullptr; a.ssq_parts = 0; a.norm_K = 1; a.eps = 0.f;
   a.gnext = nullptr; a.xs_next = nullptr; a.ld_next = 0; a.ssq_out = nullptr;
   if (norm) {
@@ -577,5 +585,5 @@ extern "C" int hs_split_rows(const float *x, int ldx, int t, int K, int ldk, con
 extern "C" int hs_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                           uint16_t *xs_out, int ld_xs_out, void *workspace, size_t ws_bytes, void *stream) {
   return hs::launch_gemv_tc(xs, t, w, ldw, N, epilogue, y, ldy, xs_out, ld_xs_out, workspace, ws_bytes,
-                            hs::as_stream(stream), nullptr);
+                            hs::as_stream(stream), nullptr, nullptr, 0);
 }

@@ -474,13 +474,16 @@ PREFILL_MIN_ROWS = 64   # prompts at least this long take the GEMM prefill (hs_p
 
 
 def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[ForwardRecorder] = None,
-                   out: Optional[torch.Tensor] = None, prefill: bool = False) -> torch.Tensor:
+                   out: Optional[torch.Tensor] = None, prefill: bool = False, tp=None) -> torch.Tensor:
     """Causal forward of `tokens` (host list or device int32 tensor) at
     cache.frontier; returns device logits [t, V] fp32 (model.py:247-331).
     prefill=True lets a long prompt on a full cache (unsharded, or
     sequence-sharded at head_dim 128) run through the batched GEMM prefill
     (hs_prefill / hs_prefill_sharded); otherwise every row is computed exactly
-    as a decode step would compute it."""
+    as a decode step would compute it.
+    tp: a shard.SequenceShards whose ranks split the dense projections by
+    output rows (hs_forward_tp) for blocks of <= 8 rows; longer batches and
+    prefill stay replicated."""
     dm = weights.device()
     cfg = dm.config
     tok = to_i32_device(tokens)
@@ -555,11 +558,19 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
         return out
     for a, b in cache._batches(t):
         step = cache._step(b - a)
-        nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split, world)
-        ws = dm.workspace(nbytes)
-        check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), shard_ref, ptr(tok) + 4 * a, b - a,
-                             ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))
-        STATS["alg_bytes"] += dm.weight_bytes + step.n_view * cfg.n_kv_heads * cfg.head_dim * 4 * cfg.n_layers
+        kv_bytes = step.n_view * cfg.n_kv_heads * cfg.head_dim * 4 * cfg.n_layers
+        if tp is not None and b - a <= 8:
+            nbytes = lib.hs_forward_tp_workspace_bytes(dm.ref, b - a, step.n_view, step.split, world, tp.world)
+            ws = dm.workspace(nbytes)
+            check(lib.hs_forward_tp(dm.ref, cache._ref, C.byref(step), shard_ref, tp.ref, ptr(tok) + 4 * a, b - a,
+                                    ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))
+            STATS["alg_bytes"] += dm.weight_bytes // tp.world + kv_bytes
+        else:
+            nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split, world)
+            ws = dm.workspace(nbytes)
+            check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), shard_ref, ptr(tok) + 4 * a, b - a,
+                                 ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))
+            STATS["alg_bytes"] += dm.weight_bytes + kv_bytes
         cache._advance(b - a)
     if recorder is not None:
         recorder.query_position = cache.frontier - 1

@@ -213,6 +213,9 @@ class Lane:
         self._scratch = None
         self._graph = None
         self._gtok = None
+        # shard.SequenceShards splitting this lane's dense projections
+        # (tensor parallel, hs_forward_tp); None = replicated weights
+        self.tp = None
 
     def step_graph_run(self, tok: torch.Tensor) -> None:
         """One-token step through the lane's captured graph.  The graph reads
@@ -250,7 +253,7 @@ class Lane:
         """Forward (host list or device int32 tensor) -> device logits [t, V];
         updates the frontier row."""
         t = tokens.numel() if isinstance(tokens, torch.Tensor) else len(tokens)
-        out = forward_device(self.weights, tokens, self.cache, self.recorder, out=self._logits_buf(t))
+        out = forward_device(self.weights, tokens, self.cache, self.recorder, out=self._logits_buf(t), tp=self.tp)
         self._front.copy_(out[t - 1])
         self._has_front = True
         return out
@@ -297,6 +300,7 @@ class Lane:
 
     def clone(self) -> "Lane":
         c = Lane(self.weights, self.cache.clone())
+        c.tp = self.tp
         c._front.copy_(self._front)
         c._has_front = self._has_front
         if self.recorder.stash is not None:
@@ -520,10 +524,14 @@ class HierarchicalSession:
     (speculation.py:278-368).  Single-threaded; clone() snapshots."""
 
     def __init__(self, target: ModelWeights, draft: ModelWeights, prefix: Sequence[int], config: SpecConfig,
-                 _prefill: bool = True, shards=None):
+                 _prefill: bool = True, shards=None, tp=None):
         """shards: a shard.SequenceShards -- the full cache is then split
         along the sequence over its ranks (every rank runs this session with
-        the same arguments).  None = one GPU."""
+        the same arguments).  None = one GPU.
+        tp: a shard.SequenceShards (typically the same object) over which the
+        target's dense projections of the full and retrieval lanes are split
+        by output rows (tensor parallel); the draft lane
+        stays replicated."""
         if target.config.vocab_size != draft.config.vocab_size:
             raise ContractError("target and draft models must share a vocabulary")
         if len(prefix) < 1:
@@ -537,6 +545,7 @@ class HierarchicalSession:
         self.full_lane = Lane(target, full)
         self.draft_lane = Lane(draft, StreamingCache.from_config(draft.config, config.streaming))
         self.retr_lane = Lane(target, RetrievalCache.from_config(target.config, config.retrieval))
+        self.full_lane.tp = self.retr_lane.tp = tp
         self.rolling = RollingAcceptance(config.retrieval.rolling_window)
         self.tokens_since_build = 0
         self.rebuilds = 0
@@ -558,12 +567,12 @@ class HierarchicalSession:
 
     @classmethod
     def synthetic(cls, target: ModelWeights, draft: ModelWeights, context: Sequence[int], config: SpecConfig,
-                  seed: int = 0, shards=None):
+                  seed: int = 0, shards=None, tp=None):
         """Session over a synthetic long context (throughput configs,
         SURVEY §7.4 item 6): the full and draft caches are filled with random
         bf16 K/V for positions [0, n-1); the last context token is then
         decoded for real on every lane and the initial build uses its queries."""
-        s = cls(target, draft, context, config, _prefill=False, shards=shards)
+        s = cls(target, draft, context, config, _prefill=False, shards=shards, tp=tp)
         n = len(context)
         s.full_lane.cache.fill_random_(n - 1, seed=seed)
         s.draft_lane.cache.fill_random_(n - 1, seed=seed + 1)
@@ -677,7 +686,8 @@ def hierarchical_generate(target: ModelWeights, draft: ModelWeights, prefix: Seq
 
 
 def autoregressive_generate(weights: ModelWeights, prefix: Sequence[int], target_len: int,
-                            temperature: float = 0.0, seed: int = 0, shards=None, chunk: int = 16) -> list:
+                            temperature: float = 0.0, seed: int = 0, shards=None, chunk: int = 16,
+                            tp=None) -> list:
     """Plain decode over the full cache (speculation.py:378-398); the
     sampled token never leaves the device until the end.  shards: sequence-
     shard the full cache (shard.SequenceShards, boundaries aligned to chunk)."""
@@ -689,6 +699,7 @@ def autoregressive_generate(weights: ModelWeights, prefix: Sequence[int], target
     cache = (FullCache.from_config(weights.config) if shards is None else
              FullCache.shard(weights.config, shards, len(prefix), chunk))
     lane = Lane(weights, cache)
+    lane.tp = tp
     lane.prefill(list(prefix))
     return _ar_loop(lane, list(prefix), target_len, temperature, rng)
 

@@ -358,3 +358,82 @@ def test_loopback_collectives(P):
             assert torch.equal(b, torch.full((4,), 6.0))
     finally:
         shards[0].destroy()
+
+
+# ---------------------------------------------------------------------------
+# tensor-parallel dense layers (hs_forward_tp)
+
+def test_one_rank_tensor_parallel_is_bitwise_replicated(P, one_rank):
+    """World 1 through the NCCL code path: the row block is the whole matrix
+    (same K split), the all-gather a copy and norm_prep rebuilds the operand
+    the GEMV epilogue would have written -- logits bitwise equal to hs_forward,
+    for decode steps, verify blocks and a whole session (TP on the full and
+    retrieval lanes)."""
+    from paper_2404_11912_b200 import model as M
+    tw, dw = _planted(P)
+    prompt = np.random.default_rng(0).integers(1, 512, 600).tolist()
+    a = P.FullCache.from_config(tw.config)
+    b = P.FullCache.from_config(tw.config)
+    P.prefill(tw, prompt, a)
+    P.prefill(tw, prompt, b)
+    for toks in ([3], [17, 18, 19, 20, 21], [7] * 8):
+        la = M._host_rows(M.forward_device(tw, toks, a))
+        lb = M._host_rows(M.forward_device(tw, toks, b, tp=one_rank))
+        assert np.array_equal(la, lb), len(toks)
+    spec = P.SpecConfig(target_len=600 + 64, gamma1=2, gamma2=4, temperature=0.6, seed=3,
+                        streaming=P.StreamingConfig(n_sink=4, budget=128),
+                        retrieval=P.RetrievalConfig(chunk_size=8, budget=128, rebuild_stride=24))
+    sa = P.HierarchicalSession(tw, dw, prompt, spec)
+    sb = P.HierarchicalSession(tw, dw, prompt, spec, tp=one_rank)   # (the sharded GEMM prefill is not bitwise)
+    out_a, tr_a = sa.generate()
+    out_b, tr_b = sb.generate()
+    assert out_a == out_b and tr_a.summary() == tr_b.summary()
+    assert torch.equal(sa.full_lane._front, sb.full_lane._front)
+    with pytest.raises(ValueError):    # probes / batches > 8 rows are not tensor-parallel
+        from paper_2404_11912_b200._abi import check, lib
+        from paper_2404_11912_b200.runtime import ptr, stream_ptr
+        dm = tw.device()
+        st = b._step(9)
+        nb = lib.hs_forward_tp_workspace_bytes(dm.ref, 9, st.n_view, st.split, 0, 1)
+        ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        tok = torch.ones(9, dtype=torch.int32, device="cuda")
+        out = torch.empty((9, tw.config.vocab_size), device="cuda")
+        check(lib.hs_forward_tp(dm.ref, b._ref, C.byref(st), None, one_rank.ref, ptr(tok), 9, ptr(out), None,
+                                ptr(ws), nb, stream_ptr()))
+
+
+@pytest.mark.parametrize("G,seq", [(2, True), (4, True), (8, True), (3, False)])
+def test_loopback_tensor_parallel_session(P, G, seq):
+    """G ranks on one GPU (loopback group): every projection of the target's
+    full and retrieval lanes split by output rows over the ranks (rank r
+    streams 1/G of the weight bytes; with 8 ranks several own no tile of the
+    small test matrices), optionally with the full cache also sequence-
+    sharded.  Every rank ends bitwise identical to the others; against one
+    GPU the K splits of the smaller row blocks differ, so logits agree to
+    fp32 accumulation noise and the greedy stream and counts are equal."""
+    from paper_2404_11912_b200.shard import SequenceShards
+    tw, dw = _planted(P, seed=7)
+    tw.device(), dw.device()
+    prompt = np.random.default_rng(2).integers(1, 512, 700).tolist()
+    spec = P.SpecConfig(target_len=700 + 72, gamma1=2, gamma2=4, temperature=0.0, seed=5,
+                        streaming=P.StreamingConfig(n_sink=4, budget=128),
+                        retrieval=P.RetrievalConfig(chunk_size=8, budget=128, rebuild_stride=24))
+    ref = P.HierarchicalSession(tw, dw, prompt, spec)
+    ref_out, ref_tr = ref.generate()
+    shards = SequenceShards.loopback(G)
+
+    def rank(r):
+        s = P.HierarchicalSession(tw, dw, prompt, spec, shards=shards[r] if seq else None, tp=shards[r])
+        out, tr = s.generate()
+        return out, tr.summary(), s.full_lane._front.clone(), s.retr_lane._front.clone()
+
+    try:
+        res = _run_ranks(rank, G, shards)
+    finally:
+        shards[0].destroy()
+    f0 = ref.full_lane._front
+    for r, (out, summ, front, rfront) in enumerate(res):
+        assert out == ref_out, r
+        assert summ == ref_tr.summary(), r
+        assert torch.equal(front, res[0][2]) and torch.equal(rfront, res[0][3]), r
+        assert (front - f0).abs().max().item() <= 1e-5 * f0.abs().max().item(), r
