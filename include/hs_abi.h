@@ -40,6 +40,8 @@ extern "C" {
 
 const char *hs_last_error(void);
 int hs_abi_version(void);
+/* block the host until the stream's work is done (the per-round read-back) */
+int hs_stream_sync(void *stream);
 int hs_device_sm_count(int device);
 /* number of kernels this library has launched since it was loaded */
 unsigned long long hs_launch_count(void);

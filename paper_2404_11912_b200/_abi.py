@@ -68,6 +68,7 @@ _SIGS = {
     "hs_device_sm_count": (i32, [i32]),
     "hs_launch_count": (C.c_ulonglong, []),
     "hs_note_launches": (None, [C.c_ulonglong]),
+    "hs_stream_sync": (i32, [vp]),
     "hs_forward_workspace_bytes": (sz, [_P(HsModel), i32, i32, i32, i32]),
     "hs_forward_workspace_clean_bytes": (sz, [_P(HsModel)]),
     "hs_gemv_tc_workspace_bytes": (sz, [i32, i32]),

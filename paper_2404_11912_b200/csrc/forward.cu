@@ -212,6 +212,10 @@ extern "C" int hs_cta_trace(void *buf, unsigned cap) {
 }
 
 extern "C" const char *hs_last_error(void) { return hs::g_err; }
+extern "C" int hs_stream_sync(void *stream) {
+  const cudaError_t e = cudaStreamSynchronize(hs::as_stream(stream));
+  return e == cudaSuccess ? HS_OK : hs::set_error(HS_ERR_CUDA, "stream sync: %s", cudaGetErrorString(e));
+}
 extern "C" int hs_abi_version(void) { return HS_ABI_VERSION; }
 extern "C" unsigned long long hs_launch_count(void) { return __atomic_load_n(&hs::g_launches, __ATOMIC_RELAXED); }
 extern "C" void hs_note_launches(unsigned long long n) { hs::count_launch((int)n); }

@@ -246,6 +246,17 @@ class DeviceModel:
             self._ws[key] = ws
         return ws
 
+    def forward_ws_bytes(self, t: int, n_view: int, split: int, world: int) -> int:
+        """hs_forward_workspace_bytes, memoised: it depends on n_view only
+        through the number of attention splits."""
+        key = (t, -(-n_view // split), split, world)
+        memo = self.__dict__.setdefault("_ws_memo", {})
+        nb = memo.get(key)
+        if nb is None:
+            nb = memo[key] = max(lib.hs_forward_workspace_bytes(self.ref, t, n_view, split, world),
+                                 lib.hs_forward_workspace_bytes(self.ref, t, key[1] * split, split, world))
+        return nb
+
     @property
     def weight_bytes(self) -> int:
         """Algorithmic weight bytes streamed per forward (embedding row excluded)."""
@@ -566,7 +577,7 @@ def forward_device(weights: ModelWeights, tokens, cache, recorder: Optional[Forw
                                     ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))
             STATS["alg_bytes"] += dm.weight_bytes // tp.world + kv_bytes
         else:
-            nbytes = lib.hs_forward_workspace_bytes(dm.ref, b - a, step.n_view, step.split, world)
+            nbytes = dm.forward_ws_bytes(b - a, step.n_view, step.split, world)
             ws = dm.workspace(nbytes)
             check(lib.hs_forward(dm.ref, cache._ref, C.byref(step), shard_ref, ptr(tok) + 4 * a, b - a,
                                  ptr(out) + 4 * a * cfg.vocab_size, ptr(stash), ptr(ws), nbytes, stream_ptr()))

@@ -20,14 +20,30 @@ import torch
 STATS = {"alg_bytes": 0}
 
 
+_CUDA_OK = False
+# torch's C entry points for the current device / raw stream: torch.cuda.
+# current_stream() re-validates the device through Python helpers (~10 us a
+# call, several calls per decode round on the host's critical path between a
+# round's read-back and its next launch)
+_get_device = torch._C._cuda_getDevice
+_get_raw_stream = torch._C._cuda_getCurrentRawStream
+
+
 def device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2404_11912_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
-    return torch.device("cuda", torch.cuda.current_device())
+    global _CUDA_OK
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2404_11912_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+        torch.cuda.init()
+        _CUDA_OK = True
+    return torch.device("cuda", _get_device())
 
 
 def stream_ptr() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    """cudaStream_t of this thread's current stream on the current device."""
+    if not _CUDA_OK:
+        device()
+    return _get_raw_stream(_get_device())
 
 
 def ptr(t) -> int:
@@ -67,15 +83,24 @@ class _PinnedStaging:
         self.events = [None] * slots
         self.i = 0
 
-    def copy_into(self, dst: torch.Tensor, arr) -> None:
-        """Stream-ordered copy of a small host array into an existing device
-        tensor (fixed address: inputs of captured CUDA graphs)."""
-        arr = np.ascontiguousarray(arr, dtype=torch.empty(0, dtype=dst.dtype).numpy().dtype)
+    _NP = {torch.int32: np.int32, torch.float32: np.float32, torch.float64: np.float64, torch.int64: np.int64}
+
+    def _slot(self) -> int:
+        """Next ring slot, once its previous copy has run (events are reused)."""
         slot = self.i
         self.i = (self.i + 1) % self.slots
         ev = self.events[slot]
-        if ev is not None:
+        if ev is None:
+            self.events[slot] = torch.cuda.Event()
+        else:
             ev.synchronize()
+        return slot
+
+    def copy_into(self, dst: torch.Tensor, arr) -> None:
+        """Stream-ordered copy of a small host array into an existing device
+        tensor (fixed address: inputs of captured CUDA graphs)."""
+        arr = np.ascontiguousarray(arr, dtype=self._NP[dst.dtype])
+        slot = self._slot()
         key = (slot, arr.dtype.str)
         buf = self.bufs.get(key)
         if buf is None:
@@ -84,19 +109,13 @@ class _PinnedStaging:
         host = buf[:arr.size]
         host.numpy()[:] = arr.reshape(-1)
         dst.view(-1)[:arr.size].copy_(host, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        self.events[slot] = ev
+        self.events[slot].record()
 
     def to_device(self, arr: np.ndarray) -> torch.Tensor:
         arr = np.ascontiguousarray(arr)
         if arr.size > self.cap:
             return torch.from_numpy(arr).to(device())
-        slot = self.i
-        self.i = (self.i + 1) % self.slots
-        ev = self.events[slot]
-        if ev is not None:
-            ev.synchronize()
+        slot = self._slot()
         key = (slot, arr.dtype.str)
         buf = self.bufs.get(key)
         if buf is None:
@@ -106,9 +125,7 @@ class _PinnedStaging:
         host.numpy()[:] = arr.reshape(-1)
         out = torch.empty(arr.shape, dtype=host.dtype, device=device())
         out.view(-1).copy_(host, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        self.events[slot] = ev
+        self.events[slot].record()
         return out
 
 
@@ -137,6 +154,8 @@ staging = _ThreadStaging()
 
 def to_i32_device(tokens) -> torch.Tensor:
     if isinstance(tokens, torch.Tensor):
+        if tokens.dtype == torch.int32 and tokens.is_cuda:
+            return tokens
         return tokens.to(device=device(), dtype=torch.int32)
     return staging.to_device(np.asarray(tokens, dtype=np.int32))
 

@@ -71,12 +71,15 @@ class _StepGraph:
     captured with (workspace, logits rows) so later re-allocations elsewhere
     cannot invalidate it."""
 
-    def __init__(self, lane: "Lane", tok: torch.Tensor):
+    def __init__(self, lane: "Lane"):
         cache = lane.cache
         dm = lane.weights.device()
         cfg = dm.config
-        self.lane, self.tok = lane, tok
-        self.dyn = torch.zeros(2, dtype=torch.int32, device=device())
+        self.lane = lane
+        # [frontier, window watermark, token]: one fixed device slot the graph
+        # reads its positions and its input token from
+        self.dyn = torch.zeros(3, dtype=torch.int32, device=device())
+        self.tok = tok = self.dyn[2:3]
         step = cache._step(1)
         step.pos0, step.win_lo, step.dyn = 0, 0, self.dyn.data_ptr()
         self.step = step
@@ -114,10 +117,15 @@ class _StepGraph:
         self.n_launch = lib.hs_launch_count() - n0
         torch.cuda.current_stream().wait_stream(side)
 
-    def run(self) -> None:
+    def run(self, host_token: Optional[int] = None) -> None:
+        """Replay; the token is already in self.tok (device) or is host_token
+        (shipped with the positions in one staging copy)."""
         lane, cache = self.lane, self.lane.cache
         cache._step(1)                                    # guard / capacity checks on the live state
-        staging.copy_into(self.dyn, [cache.frontier, cache.lo])
+        if host_token is None:
+            staging.copy_into(self.dyn, [cache.frontier, cache.lo])
+        else:
+            staging.copy_into(self.dyn, [cache.frontier, cache.lo, host_token])
         self.graph.replay()
         lib.hs_note_launches(self.n_launch)
         STATS["alg_bytes"] += self.alg_bytes
@@ -212,20 +220,22 @@ class Lane:
         self._has_front = False
         self._scratch = None
         self._graph = None
-        self._gtok = None
         # shard.SequenceShards splitting this lane's dense projections
         # (tensor parallel, hs_forward_tp); None = replicated weights
         self.tp = None
 
-    def step_graph_run(self, tok: torch.Tensor) -> None:
+    def step_graph_run(self, tok) -> None:
         """One-token step through the lane's captured graph.  The graph reads
         its token from a lane-owned device slot (one capture per lane, never
-        per caller buffer); `tok` is copied into it on the stream."""
+        per caller buffer); a device `tok` is copied into it on the stream, a
+        host int travels with the step's positions."""
         if self._graph is None:
-            self._gtok = torch.zeros(1, dtype=torch.int32, device=device())
-            self._graph = _StepGraph(self, self._gtok)
-        self._gtok.copy_(tok)
-        self._graph.run()
+            self._graph = _StepGraph(self)
+        if isinstance(tok, torch.Tensor):
+            self._graph.tok.copy_(tok)
+            self._graph.run()
+        else:
+            self._graph.run(host_token=int(tok))
 
     @property
     def frontier(self) -> int:
@@ -372,7 +382,7 @@ def _readback(buf: _RoundBuffers, n: int, us: UniformStream):
     """One device->host sync: chain result for n proposals + RNG cursor."""
     buf.host[:n + 4].copy_(buf.res[:n + 4], non_blocking=True)
     buf.host[n + 4:n + 5].copy_(us.cursor, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    check(lib.hs_stream_sync(stream_ptr()))
     COUNTERS["d2h_bytes"] += 4 * (n + 5)
     h = buf.host.numpy()
     count, accepted, status, cursor = int(h[n + 1]), int(h[n + 2]), int(h[n + 3]), int(h[n + 4])
@@ -384,12 +394,15 @@ def _readback(buf: _RoundBuffers, n: int, us: UniformStream):
 def _draft_round_dev(lane: Lane, seq: Sequence[int], gamma1: int, T: float, us: UniformStream,
                      buf: _RoundBuffers) -> None:
     """draft_round (speculation.py:211-227) with tokens and q rows on device."""
-    lane.catch_up(seq)
+    graphs = USE_GRAPHS and isinstance(lane.cache, StreamingCache)
+    if graphs and lane.frontier + 1 == len(seq):
+        lane.step_graph_run(seq[len(seq) - 1:][0])       # the usual one-token catch-up
+    else:
+        lane.catch_up(seq)
     if not lane._has_front:
         raise ContractError("lane has no frontier logits; advance over committed tokens first")
     V = buf.V
     s = stream_ptr()
-    graphs = USE_GRAPHS and isinstance(lane.cache, StreamingCache)
     for g in range(gamma1):
         check(lib.hs_draft_sample(ptr(lane._front), V, float(T), ptr(buf.q[g]), ptr(us.buf), ptr(us.cursor),
                                   ptr(buf.dtok[g:g + 1]), s))
