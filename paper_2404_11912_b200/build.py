@@ -78,6 +78,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nccl_lib = os.path.join(NCCL, "lib")
     subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-L", nccl_lib, "-l:libnccl.so.2",
                     "-Xlinker", "-rpath," + nccl_lib], check=True)
+    # every hs:: symbol must resolve inside the library (a declaration that
+    # drifted from its definition links as an undefined symbol and only fails
+    # at dlopen on the GPU box)
+    und = subprocess.run(["nm", "-u", "-C", tmp], capture_output=True, text=True).stdout.splitlines()
+    bad = [u.strip() for u in und if "hs::" in u]
+    if bad:
+        os.remove(tmp)
+        raise RuntimeError("unresolved library-internal symbols: " + "; ".join(bad))
     os.replace(tmp, LIB)
     return LIB
 
