@@ -196,6 +196,7 @@ int trace_set_gemv(void *p, unsigned cap);
 int trace_set_kv(void *p, unsigned cap);
 int trace_set_attn(void *p, unsigned cap);
 int trace_set_attntc(void *p, unsigned cap);
+int trace_set_gemv_phases(void *p, unsigned cap);
 }  // namespace hs
 
 /* debugging/profiling aid (not part of hs_abi.h): per-CTA timeline of the
@@ -204,9 +205,11 @@ int trace_set_attntc(void *p, unsigned cap);
 extern "C" int hs_cta_trace(void *buf, unsigned cap) {
   unsigned long long *b = reinterpret_cast<unsigned long long *>(buf);
   const size_t r = (size_t)cap * 3;
-  int (*set[4])(void *, unsigned) = {hs::trace_set_gemv, hs::trace_set_kv, hs::trace_set_attn, hs::trace_set_attntc};
-  for (int i = 0; i < 4; ++i)
-    if (set[i](b ? b + i * r : nullptr, b ? cap : 0) != 0)
+  // regions of cap x 3 u64 each; the fifth holds the GEMV phase records (16 u64 per CTA)
+  int (*set[5])(void *, unsigned) = {hs::trace_set_gemv, hs::trace_set_kv, hs::trace_set_attn, hs::trace_set_attntc,
+                                     hs::trace_set_gemv_phases};
+  for (int i = 0; i < 5; ++i)
+    if (set[i](b ? b + i * r : nullptr, b ? (i == 4 ? cap * 3 / 16 : cap) : 0) != 0)
       return hs::set_error(HS_ERR_VALUE, "cta trace unavailable (build with HS_TRACE_BUILD=1)");
   return HS_OK;
 }

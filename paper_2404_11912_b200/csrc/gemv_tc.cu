@@ -21,6 +21,7 @@
 // so a row's result does not depend on the batch size).
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <mutex>
 #include <unordered_map>
 
@@ -33,6 +34,28 @@ namespace hs {
 HS_TRACE_TU
 int trace_set_gemv(void *p, unsigned cap) { return trace_set_tu(p, cap); }
 
+// per-CTA phase stamps of the GEMV (trace builds only, tools/gemv_phases.py):
+// [id: tile | split << 16 | sm << 32 | n_tiles << 48, start, release, first
+// stage landed, last stage landed, accumulator complete, reduced/finalised,
+// TMEM read, residual loaded, cluster barrier 1, DSMEM partials loaded,
+// finalize done, -, -, -, end]  (16 u64)
+#ifdef HS_CTA_TRACE
+static __device__ unsigned long long *g_gph = nullptr;
+static __device__ unsigned int g_gph_n = 0, g_gph_cap = 0;
+int trace_set_gemv_phases(void *p, unsigned cap) {
+  unsigned long long *q = reinterpret_cast<unsigned long long *>(p);
+  unsigned zero = 0;
+  if (cudaMemcpyToSymbol(g_gph, &q, sizeof(q)) != cudaSuccess) return -1;
+  if (cudaMemcpyToSymbol(g_gph_n, &zero, sizeof(zero)) != cudaSuccess) return -1;
+  if (cudaMemcpyToSymbol(g_gph_cap, &cap, sizeof(cap)) != cudaSuccess) return -1;
+  return 0;
+}
+#define GPH_STAMP(slot) if (g_gph != nullptr) gph[slot] = gtime();
+#else
+int trace_set_gemv_phases(void *, unsigned) { return -1; }
+#define GPH_STAMP(slot)
+#endif
+
 constexpr int TC_BM = 128;        // output rows per tile (MMA M)
 constexpr int TC_BK = 64;         // K per stage (one 128-byte swizzle row)
 constexpr int TC_XN = 24;         // activation columns: 3 splits x 8 rows
@@ -44,6 +67,8 @@ constexpr int TC_STAGES = HS_TC_STAGES;   // 5 x 19 KB: two CTAs per SM (a GEMV 
 constexpr int TC_W_BYTES = TC_BM * TC_BK * 2;    // 16 KB
 constexpr int TC_X_BYTES = TC_XN * TC_BK * 2;    // 3 KB
 constexpr int TC_SMEM = TC_STAGES * (TC_W_BYTES + TC_X_BYTES) + 1024 + 256;
+// + the split-0 CTA's landing area for the partials of splits 1..ks-1 (cluster split-K)
+constexpr int TC_SMEM_MAX = TC_SMEM + 7 * TC_BM * TC_T * 4;
 constexpr int TC_COUNTER_INTS = 16384;           // per-tile arrival counters at the workspace head
 
 // ---------------------------------------------------------------------------
@@ -185,6 +210,8 @@ int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, u
 struct GemvTcArgs {
   int N, nkb, ks, t, epilogue, n_tiles;
   int cluster;        // 1: the ks split CTAs of a tile are one cluster, partials reduced through DSMEM
+  int push;           // cluster reduction by pushes into the split-0 CTA (its landing area fits two CTAs per SM)
+  int nrow;           // pushed floats per row (4 when t <= 4, else 8)
   // folded RMSNorm (model.py:282-284) of this GEMV's input rows: the operand
   // is split(x * gain) and the result is scaled by 1 / rms(x) here, with the
   // row sums of squares given as ssq_parts per-tile partials [parts][8]
@@ -214,12 +241,13 @@ struct GemvTcArgs {
 // producer reduces its tile's row sums of squares across the CTA)
 // yres: the residual rows y[r][o] (epilogue 1), loaded by the caller ahead of
 // the split-K handshake so they are not one more round trip on the tail
-__device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float *vin, const float *yres, int lane,
-                                         int tile, const double *inv_rms, double (*red)[TC_T]) {
+template <int EPI>
+__device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float *vin, const float *yres, float gn,
+                                         int lane, int tile, const double *inv_rms, double (*red)[TC_T]) {
   float v[TC_T];
 #pragma unroll
   for (int r = 0; r < TC_T; ++r) v[r] = a.ssq_in ? (float)((double)vin[r] * inv_rms[r]) : vin[r];
-  if (a.epilogue == 2) {
+  if constexpr (EPI == 2) {
     float up[TC_T];
 #pragma unroll
     for (int r = 0; r < TC_T; ++r) up[r] = __shfl_down_sync(0xffffffffu, v[r], 1);
@@ -235,37 +263,47 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
         }
       }
     }
-    return;
-  }
-  double sq[TC_T];
+  } else {
+    double sq[TC_T];
 #pragma unroll
-  for (int r = 0; r < TC_T; ++r) {
-    sq[r] = 0.0;
-    if (r < a.t && o < a.N) {
-      float *p = a.y + (size_t)r * a.ldy + o;
-      const float nv = (a.epilogue == 1) ? (yres[r] + v[r]) : v[r];
-      *p = nv;
-      if (a.xs_next) {
-        sq[r] = (double)nv * (double)nv;
-        store_split(a.xs_next, a.ld_next, r, o, (float)((double)nv * (double)a.gnext[o]));
+    for (int r = 0; r < TC_T; ++r) {
+      sq[r] = 0.0;
+      if (r < a.t && o < a.N) {
+        float *p = a.y + (size_t)r * a.ldy + o;
+        const float nv = (EPI == 1) ? (yres[r] + v[r]) : v[r];
+        *p = nv;
+        if (a.xs_next) {
+          sq[r] = (double)nv * (double)nv;
+          store_split(a.xs_next, a.ld_next, r, o, (float)((double)nv * (double)gn));
+        }
+      }
+    }
+    if (a.xs_next != nullptr) {
+      // this tile's row sums of squares, fixed order: lanes, then the 4 warps
+      const int w = threadIdx.x >> 5;
+#pragma unroll
+      for (int r = 0; r < TC_T; ++r) {
+        if (r < a.t) {   // rows >= t are zero: no shuffles for them
+          const double sr = warp_sum(sq[r]);
+          if (lane == 0) red[w][r] = sr;
+        } else if (lane == 0) {
+          red[w][r] = 0.0;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < TC_T) {
+        const int r = threadIdx.x;
+        a.ssq_out[(size_t)tile * TC_T + r] = (red[0][r] + red[1][r]) + (red[2][r] + red[3][r]);
       }
     }
   }
-  if (a.xs_next == nullptr) return;
-  // this tile's row sums of squares, fixed order: lanes, then the 4 warps
-  const int w = threadIdx.x >> 5;
-#pragma unroll
-  for (int r = 0; r < TC_T; ++r) {
-    const double sr = warp_sum(sq[r]);
-    if (lane == 0) red[w][r] = sr;
-  }
-  __syncthreads();
-  if (threadIdx.x < TC_T) {
-    const int r = threadIdx.x;
-    a.ssq_out[(size_t)tile * TC_T + r] = (red[0][r] + red[1][r]) + (red[2][r] + red[3][r]);
-  }
 }
 
+// EPI: 0 store (optionally scaled by the folded RMSNorm), 1 residual
+// accumulate (+ next operand and row statistics), 2 SwiGLU -- one
+// instantiation per epilogue keeps each kernel's code (and its instruction
+// cache footprint on the tail) small
+template <int EPI>
 __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__ CUtensorMap tmW,
                                                          const __grid_constant__ CUtensorMap tmX, GemvTcArgs a) {
   HS_TRACE_BEGIN
@@ -276,8 +314,18 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   uint64_t *full = reinterpret_cast<uint64_t *>(sX + TC_STAGES * TC_X_BYTES);
   uint64_t *empty = full + TC_STAGES;
   uint64_t *accum = empty + TC_STAGES;
-  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(accum + 1);
+  uint64_t *redbar = accum + 1;   // split-0 CTA: the other splits' pushed partials have landed
+  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(redbar + 1);
   int *flag = reinterpret_cast<int *>(tmem_base + 1);
+  // split-0 CTA of a cluster: partials pushed by splits 1..ks-1, [ks-1][128][nrow] fp32
+  float *pushed = reinterpret_cast<float *>(base + TC_STAGES * (TC_W_BYTES + TC_X_BYTES) + 256);
+#ifdef HS_CTA_TRACE
+  __shared__ unsigned long long gph[16];
+  if (threadIdx.x == 0 && g_gph != nullptr) {
+    for (int j = 0; j < 16; ++j) gph[j] = 0;
+    gph[1] = gtime();
+  }
+#endif
 
   tc::grid_dep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -291,6 +339,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
     tc::tma_prefetch(&tmX);
     for (int s = 0; s < TC_STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
     tc::mbar_init(accum, 1);
+    tc::mbar_init(redbar, a.ks > 1 ? (a.ks - 1) * 128 : 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc<32>(tmem_base);
@@ -298,6 +347,9 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   __syncthreads();
   tc::fence_after();
   const uint32_t taddr = *tmem_base;
+  // the split CTAs push into the split-0 CTA's shared memory at the end: its
+  // reduction barrier must be initialised cluster-wide first (waited below)
+  if (a.cluster && a.push) tc::cluster_arrive_relaxed();
 
   if (warp == 0) {
     if (tc::elect_one()) {
@@ -312,6 +364,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
       }
       tc::grid_dep_wait();
       HS_TRACE_RESTART
+      GPH_STAMP(2)
       for (int i = 0; i < npre; ++i) tc::tma_load_2d(sX + i * TC_X_BYTES, &tmX, &full[i], (kb0 + i) * TC_BK, 0);
       for (int i = npre; i < nk; ++i) {
         const int s = i % TC_STAGES;
@@ -334,6 +387,10 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
         const uint32_t ph = (i / TC_STAGES) & 1;
         tc::mbar_wait(&full[s], ph);
         tc::fence_after();
+#ifdef HS_CTA_TRACE
+        if (i == 0) GPH_STAMP(3)
+        if (i == nk - 1) GPH_STAMP(4)
+#endif
         const uint64_t da = tc::desc_k_sw128(sW + s * TC_W_BYTES);
         const uint64_t db = tc::desc_k_sw128(sX + s * TC_X_BYTES);
 #pragma unroll
@@ -353,43 +410,102 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
     for (int k = 0; k < a.ssq_parts; ++k) ss += __ldcg(a.ssq_in + (size_t)k * TC_T + lane);
     inv_rms[lane] = 1.0 / sqrt(ss / (double)a.norm_K + (double)a.eps);
   }
+  const int row = warp * 32 + lane;
+  const int o = tile * TC_BM + row;
+  // operands of the epilogue that do not depend on the accumulator (residual
+  // rows, next norm's gain) are loaded while the main loop still runs, so
+  // they are not a memory round trip on the tail; only the finalising CTA
+  // of a cluster needs them
+  const bool fin_cta = a.ks == 1 || !a.cluster || split == 0;
+  float yres[TC_T];
+#pragma unroll
+  for (int r = 0; r < TC_T; ++r)
+    yres[r] = (fin_cta && EPI == 1 && r < a.t && o < a.N)
+                  ? __ldcg(a.yin ? a.yin + (size_t)r * a.ldyin + o : a.y + (size_t)r * a.ldy + o)
+                  : 0.f;
+  const float gn = (fin_cta && EPI == 1 && a.xs_next && o < a.N) ? __ldg(a.gnext + o) : 0.f;
 
   // ---- epilogue: TMEM -> registers ---------------------------------------------------
   tc::mbar_wait(accum, 0);
   tc::fence_after();
+#ifdef HS_CTA_TRACE
+  if (threadIdx.x == 0) GPH_STAMP(5)
+#endif
   __syncthreads();   // inv_rms visible
-  const int row = warp * 32 + lane;
   const uint32_t tl = taddr + ((uint32_t)(warp * 32) << 16);
   float h[8], m[8], l[8], v[TC_T];
   tc::tmem_ld8(tl + 0, h);
   tc::tmem_ld8(tl + 8, m);
   tc::tmem_ld8(tl + 16, l);
   tc::tmem_ld_wait();
+#ifdef HS_CTA_TRACE
+  if (threadIdx.x == 0) GPH_STAMP(7)
+#endif
 #pragma unroll
   for (int r = 0; r < TC_T; ++r) v[r] = nk > 0 ? (h[r] + m[r]) + l[r] : 0.f;
-  const int o = tile * TC_BM + row;
-  float yres[TC_T];
-#pragma unroll
-  for (int r = 0; r < TC_T; ++r)
-    yres[r] = (a.epilogue == 1 && r < a.t && o < a.N)
-                  ? __ldcg(a.yin ? a.yin + (size_t)r * a.ldyin + o : a.y + (size_t)r * a.ldy + o)
-                  : 0.f;
+#ifdef HS_CTA_TRACE
+  if (threadIdx.x == 0 && g_gph != nullptr) {
+    float sy = 0.f;
+    for (int r = 0; r < TC_T; ++r) sy += yres[r];
+    if (sy == -1.2345e-30f) gph[0] = 1;
+    GPH_STAMP(8)
+  }
+#endif
 
+  // split-K reduction into acc (split order, the finalising CTA's own
+  // partial first), then ONE finalize call site for every reduction mode
+  float acc[TC_T];
+  bool do_fin = true;   // CTA-uniform
   if (a.ks == 1) {
-    finalize(a, o, v, yres, lane, tile, inv_rms, red);
+#pragma unroll
+    for (int r = 0; r < TC_T; ++r) acc[r] = v[r];
+  } else if (a.cluster && a.push) {
+    // push style: splits 1..ks-1 store their partial rows straight into the
+    // split-0 CTA's shared memory and arrive (release, cluster scope) on its
+    // reduction barrier, then exit without waiting; the split-0 CTA waits for
+    // the arrivals and sums locally
+    tc::cluster_wait();   // the split-0 CTA's barrier is initialised
+#ifdef HS_CTA_TRACE
+    if (threadIdx.x == 0) GPH_STAMP(9)
+#endif
+    const int nrow = a.nrow;   // rows >= t are zero
+    if (split != 0) {
+      float *dst = pushed + ((size_t)(split - 1) * TC_BM + row) * nrow;
+      const uint32_t ra = tc::mapa_u32(dst, 0);
+      tc::st_dsmem_f4(ra, make_float4(v[0], v[1], v[2], v[3]));
+      if (nrow > 4) tc::st_dsmem_f4(ra + 16, make_float4(v[4], v[5], v[6], v[7]));
+      tc::mbar_arrive_remote(tc::mapa_u32(redbar, 0));
+      do_fin = false;
+    } else {
+      tc::mbar_wait_cluster(redbar, 0);
+#pragma unroll
+      for (int r = 0; r < TC_T; ++r) acc[r] = 0.f + v[r];
+      for (int s2 = 1; s2 < a.ks; ++s2) {
+        const float *src = pushed + ((size_t)(s2 - 1) * TC_BM + row) * nrow;
+        const float4 x0 = *reinterpret_cast<const float4 *>(src);
+        acc[0] += x0.x; acc[1] += x0.y; acc[2] += x0.z; acc[3] += x0.w;
+        if (nrow > 4) {
+          const float4 x1 = *reinterpret_cast<const float4 *>(src + 4);
+          acc[4] += x1.x; acc[5] += x1.y; acc[6] += x1.z; acc[7] += x1.w;
+        }
+      }
+#ifdef HS_CTA_TRACE
+      if (threadIdx.x == 0) GPH_STAMP(10)
+#endif
+    }
   } else if (a.cluster) {
-    // split-K through distributed shared memory: every CTA parks its partial
-    // in its (now idle) stage buffers, the split-0 CTA sums them in split
-    // order -- the same additions as the global-memory path below, without
-    // its fence / atomic / L2 round trips
+    // pull style (the landing area would not fit): every CTA parks its
+    // partial in its idle stage buffers, the split-0 CTA reads them over
+    // DSMEM between two cluster barriers
     float *ps = reinterpret_cast<float *>(sW) + row * TC_T;
     *reinterpret_cast<float4 *>(ps) = make_float4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<float4 *>(ps + 4) = make_float4(v[4], v[5], v[6], v[7]);
     tc::cluster_sync();
-    if (split == 0) {
+    do_fin = split == 0;
+    if (do_fin) {
 #pragma unroll
-      for (int r = 0; r < TC_T; ++r) v[r] = 0.f;
-      float4 x0[8], x1[8];
+      for (int r = 0; r < TC_T; ++r) acc[r] = 0.f;
+      float4 x0[8], x1[8];   // all splits' partials in flight at once
 #pragma unroll
       for (int s2 = 0; s2 < 8; ++s2) {
         if (s2 < a.ks) {
@@ -400,14 +516,13 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
 #pragma unroll
       for (int s2 = 0; s2 < 8; ++s2) {
         if (s2 < a.ks) {
-          v[0] += x0[s2].x; v[1] += x0[s2].y; v[2] += x0[s2].z; v[3] += x0[s2].w;
-          v[4] += x1[s2].x; v[5] += x1[s2].y; v[6] += x1[s2].z; v[7] += x1[s2].w;
+          acc[0] += x0[s2].x; acc[1] += x0[s2].y; acc[2] += x0[s2].z; acc[3] += x0[s2].w;
+          acc[4] += x1[s2].x; acc[5] += x1[s2].y; acc[6] += x1[s2].z; acc[7] += x1[s2].w;
         }
       }
-      finalize(a, o, v, yres, lane, tile, inv_rms, red);
     }
-    tc::cluster_sync();   // partials stay readable until the leader is done
   } else {
+    // global partials + arrival counter (> 8 splits, or clusters disabled)
     float *pp = a.partial + ((size_t)split * a.n_tiles * TC_BM + o) * TC_T;
     *reinterpret_cast<float4 *>(pp) = make_float4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<float4 *>(pp + 4) = make_float4(v[4], v[5], v[6], v[7]);
@@ -418,12 +533,12 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
       *flag = (old == a.ks - 1);
     }
     __syncthreads();
-    if (*flag) {
+    do_fin = *flag != 0;
+    if (do_fin) {
       __threadfence();
 #pragma unroll
-      for (int r = 0; r < TC_T; ++r) v[r] = 0.f;
-      // all split partials in flight at once, then summed in split order
-      constexpr int KS_MAX = 16;
+      for (int r = 0; r < TC_T; ++r) acc[r] = 0.f;
+      constexpr int KS_MAX = 16;   // all split partials in flight at once, then summed in split order
       float4 x0[KS_MAX], x1[KS_MAX];
 #pragma unroll
       for (int s2 = 0; s2 < KS_MAX; ++s2) {
@@ -436,17 +551,40 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
 #pragma unroll
       for (int s2 = 0; s2 < KS_MAX; ++s2) {
         if (s2 < a.ks) {
-          v[0] += x0[s2].x; v[1] += x0[s2].y; v[2] += x0[s2].z; v[3] += x0[s2].w;
-          v[4] += x1[s2].x; v[5] += x1[s2].y; v[6] += x1[s2].z; v[7] += x1[s2].w;
+          acc[0] += x0[s2].x; acc[1] += x0[s2].y; acc[2] += x0[s2].z; acc[3] += x0[s2].w;
+          acc[4] += x1[s2].x; acc[5] += x1[s2].y; acc[6] += x1[s2].z; acc[7] += x1[s2].w;
         }
       }
-      finalize(a, o, v, yres, lane, tile, inv_rms, red);
       if (threadIdx.x == 0) a.counters[tile] = 0;   // self-cleaning for the next launch
     }
   }
+  if (do_fin) {
+    finalize<EPI>(a, o, acc, yres, gn, lane, tile, inv_rms, red);
+#ifdef HS_CTA_TRACE
+    if (threadIdx.x == 0) GPH_STAMP(11)
+#endif
+  }
+  if (a.cluster && !a.push) tc::cluster_sync();   // pull style: partials stay readable until the leader is done
+#ifdef HS_CTA_TRACE
+  if (threadIdx.x == 0) GPH_STAMP(6)
+#endif
   tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<32>(taddr);
+#ifdef HS_CTA_TRACE
+  if (threadIdx.x == 0 && g_gph != nullptr) {
+    const unsigned i_ = atomicAdd(&g_gph_n, 1u);
+    if (i_ < g_gph_cap) {
+      unsigned sm_;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
+      unsigned long long *o = g_gph + (size_t)i_ * 16;
+      o[0] = (unsigned long long)tile | ((unsigned long long)split << 16) | ((unsigned long long)sm_ << 32) |
+             ((unsigned long long)a.n_tiles << 48);
+      for (int j = 1; j < 15; ++j) o[j] = gph[j];
+      o[15] = gtime();
+    }
+  }
+#endif
   HS_TRACE_END(1 | (a.n_tiles << 8))
 }
 
@@ -464,6 +602,23 @@ static int gemv_use_cluster() {
     return !(e != nullptr && e[0] == '1');
   }();
   return on;
+}
+
+// dynamic shared memory one GEMV CTA may use while two fit per SM (a GEMV
+// and its programmatic dependent's prefetching CTA)
+static int gemv_smem_budget() {
+  static const int b = [] {
+    int dev = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, gemv_tc_kernel<1>) != cudaSuccess) return TC_SMEM;
+    const int reserved = 1024;   // per-CTA system reservation
+    const int r = per_sm / 2 - reserved - (int)fa.sharedSizeBytes;
+    if (getenv("HS_GEMV_DEBUG")) fprintf(stderr, "gemv_tc: smem budget %d (per SM %d, static %zu)\n", r, per_sm, fa.sharedSizeBytes);
+    return r;
+  }();
+  return b;
 }
 
 int gemv_tc_ksplit(int N, int nkb) {
@@ -517,6 +672,7 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "gemv_tc: t=%d outside [1,%d]", t, TC_T);
   HS_REQUIRE(ldw % TC_BK == 0, HS_ERR_SHAPE, "gemv_tc: ldw %d not a multiple of %d", ldw, TC_BK);
   HS_REQUIRE(((uintptr_t)w % 16) == 0 && ((uintptr_t)xs % 16) == 0, HS_ERR_VALUE, "gemv_tc: operands must be 16B aligned");
+  HS_REQUIRE(epilogue >= 0 && epilogue <= 2, HS_ERR_VALUE, "gemv_tc: epilogue %d not in {0, 1, 2}", epilogue);
   HS_REQUIRE(epilogue != 2 || N % 2 == 0, HS_ERR_SHAPE, "gemv_tc: swiglu needs an even N");
   const int nkb = ldw / TC_BK;
   const int tiles = (N + TC_BM - 1) / TC_BM;
@@ -530,6 +686,10 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   GemvTcArgs a;
   a.N = N; a.nkb = nkb; a.ks = gemv_tc_ksplit(N, nkb); a.t = t; a.epilogue = epilogue; a.n_tiles = tiles;
   a.cluster = (a.ks > 1 && a.ks <= 8 && gemv_use_cluster()) ? 1 : 0;
+  static const int push_mode = getenv("HS_GEMV_PUSH") ? atoi(getenv("HS_GEMV_PUSH")) : 1;   // A/B hook
+  a.nrow = (t <= 4 && push_mode != 2) ? 4 : TC_T;
+  const int land = a.cluster ? (a.ks - 1) * TC_BM * a.nrow * 4 : 0;
+  a.push = (a.cluster && push_mode && (push_mode == 2 || TC_SMEM + land <= gemv_smem_budget())) ? 1 : 0;
   a.y = y; a.ldy = ldy; a.xs_out = xs_out; a.ld_xs_out = ld_xs_out;
   a.yin = yin; a.ldyin = ldyin;
   a.ssq_in = nullptr; a.ssq_parts = 0; a.norm_K = 1; a.eps = 0.f;
@@ -544,13 +704,15 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   a.partial = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + (size_t)TC_COUNTER_INTS * 4);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaFuncSetAttribute(gemv_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
+    cudaFuncSetAttribute(gemv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
+    cudaFuncSetAttribute(gemv_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles, a.ks, 1);
   cfg.blockDim = dim3(128, 1, 1);
-  cfg.dynamicSmemBytes = TC_SMEM;
+  cfg.dynamicSmemBytes = TC_SMEM + (a.push ? land : 0);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -568,7 +730,8 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_tc_kernel, mw, mx, a);
+  auto kern = epilogue == 2 ? gemv_tc_kernel<2> : epilogue == 1 ? gemv_tc_kernel<1> : gemv_tc_kernel<0>;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mw, mx, a);
   if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "gemv_tc launch: %s", cudaGetErrorString(e));
   return check_launch("gemv_tc");
 }

@@ -57,7 +57,7 @@ def main():
         lane._forward(toks)
         lane.rollback_to(f0)
     cap = 1 << 18
-    buf = torch.zeros(4 * cap * 3, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(5 * cap * 3, dtype=torch.int64, device="cuda")   # 4 TU regions + GEMV phases
     torch.cuda.synchronize()
     lib.hs_cta_trace(buf.data_ptr(), cap)
     lane._forward(toks)
