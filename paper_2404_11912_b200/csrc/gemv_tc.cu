@@ -243,7 +243,8 @@ struct GemvTcArgs {
 // the split-K handshake so they are not one more round trip on the tail
 template <int EPI>
 __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float *vin, const float *yres, float gn,
-                                         int lane, int tile, const double *inv_rms, double (*red)[TC_T]) {
+                                         int lane, int tile, const double *inv_rms, double (*red)[TC_T],
+                                         unsigned long long *gst) {
   float v[TC_T];
 #pragma unroll
   for (int r = 0; r < TC_T; ++r) v[r] = a.ssq_in ? (float)((double)vin[r] * inv_rms[r]) : vin[r];
@@ -278,6 +279,9 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
         }
       }
     }
+#ifdef HS_CTA_TRACE
+    if (gst && threadIdx.x == 0) gst[12] = gtime();
+#endif
     if (a.xs_next != nullptr) {
       // this tile's row sums of squares, fixed order: lanes, then the 4 warps
       const int w = threadIdx.x >> 5;
@@ -290,7 +294,13 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
           red[w][r] = 0.0;
         }
       }
+#ifdef HS_CTA_TRACE
+      if (gst && threadIdx.x == 0) gst[13] = gtime();
+#endif
       __syncthreads();
+#ifdef HS_CTA_TRACE
+      if (gst && threadIdx.x == 0) gst[14] = gtime();
+#endif
       if (threadIdx.x < TC_T) {
         const int r = threadIdx.x;
         a.ssq_out[(size_t)tile * TC_T + r] = (red[0][r] + red[1][r]) + (red[2][r] + red[3][r]);
@@ -339,8 +349,10 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
     tc::tma_prefetch(&tmX);
     for (int s = 0; s < TC_STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
     tc::mbar_init(accum, 1);
-    tc::mbar_init(redbar, a.ks > 1 ? (a.ks - 1) * 128 : 1);
+    tc::mbar_init(redbar, 1);
     tc::fence_mbar_init();
+    // split-0 CTA: the pushed partials arrive as transaction bytes
+    if (a.cluster && a.push && split == 0) tc::mbar_expect_tx(redbar, (a.ks - 1) * TC_BM * a.nrow * 4);
   }
   if (warp == 1) tc::tmem_alloc<32>(tmem_base);
   tc::fence_before();
@@ -461,9 +473,9 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
     for (int r = 0; r < TC_T; ++r) acc[r] = v[r];
   } else if (a.cluster && a.push) {
     // push style: splits 1..ks-1 store their partial rows straight into the
-    // split-0 CTA's shared memory and arrive (release, cluster scope) on its
-    // reduction barrier, then exit without waiting; the split-0 CTA waits for
-    // the arrivals and sums locally
+    // split-0 CTA's shared memory with st.async, each store completing its
+    // transaction bytes on the split-0 CTA's reduction barrier, then exit
+    // without waiting; the split-0 CTA waits for all bytes and sums locally
     tc::cluster_wait();   // the split-0 CTA's barrier is initialised
 #ifdef HS_CTA_TRACE
     if (threadIdx.x == 0) GPH_STAMP(9)
@@ -471,10 +483,9 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
     const int nrow = a.nrow;   // rows >= t are zero
     if (split != 0) {
       float *dst = pushed + ((size_t)(split - 1) * TC_BM + row) * nrow;
-      const uint32_t ra = tc::mapa_u32(dst, 0);
-      tc::st_dsmem_f4(ra, make_float4(v[0], v[1], v[2], v[3]));
-      if (nrow > 4) tc::st_dsmem_f4(ra + 16, make_float4(v[4], v[5], v[6], v[7]));
-      tc::mbar_arrive_remote(tc::mapa_u32(redbar, 0));
+      const uint32_t ra = tc::mapa_u32(dst, 0), rb = tc::mapa_u32(redbar, 0);
+      tc::st_async_f4(ra, make_float4(v[0], v[1], v[2], v[3]), rb);
+      if (nrow > 4) tc::st_async_f4(ra + 16, make_float4(v[4], v[5], v[6], v[7]), rb);
       do_fin = false;
     } else {
       tc::mbar_wait_cluster(redbar, 0);
@@ -559,7 +570,11 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
     }
   }
   if (do_fin) {
-    finalize<EPI>(a, o, acc, yres, gn, lane, tile, inv_rms, red);
+#ifdef HS_CTA_TRACE
+    finalize<EPI>(a, o, acc, yres, gn, lane, tile, inv_rms, red, g_gph ? gph : nullptr);
+#else
+    finalize<EPI>(a, o, acc, yres, gn, lane, tile, inv_rms, red, nullptr);
+#endif
 #ifdef HS_CTA_TRACE
     if (threadIdx.x == 0) GPH_STAMP(11)
 #endif

@@ -179,6 +179,14 @@ __device__ __forceinline__ void st_dsmem_f4(uint32_t ra, float4 v) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ra), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
+// asynchronous 16-byte store into another CTA's shared memory that signals
+// its completion (16 transaction bytes) on that CTA's mbarrier -- no fence
+// on the storing side
+__device__ __forceinline__ void st_async_f4(uint32_t ra, float4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(ra),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+               : "memory");
+}
 // arrive on an mbarrier in another CTA of the cluster, ordering this
 // thread's earlier (distributed) shared-memory stores before it
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t ra) {

@@ -63,7 +63,7 @@ def main():
     # columns: start, release, first, last, accum, (final), tmem, yres, csync1, dsmem, finalize, end
     r = rec.astype(np.int64)
     ts = np.stack([r[:, 1], r[:, 2], r[:, 3], r[:, 4], r[:, 5], r[:, 6], r[:, 7], r[:, 8], r[:, 9], r[:, 10],
-                   r[:, 11], r[:, 15]], axis=1)
+                   r[:, 12], r[:, 13], r[:, 14], r[:, 11], r[:, 15]], axis=1)
     # group into launches: consecutive (by release time) CTAs of the same tile count
     order = np.argsort(ts[:, 1], kind="stable")
     groups, cur = [], None
@@ -73,8 +73,8 @@ def main():
             groups.append(cur)
         cur[1].append(i)
         cur[2] = max(cur[2], ts[i, 1])
-    names = ["start", "release", "first", "last", "accum", "final", "tmem", "yres", "csync1", "dsmem", "fin",
-             "end"]
+    names = ["start", "release", "first", "last", "accum", "final", "tmem", "yres", "csync1", "dsmem", "stores",
+             "wsum", "bar", "fin", "end"]
     kinds = collections.defaultdict(list)
     prev_end = None
     for nt, idx, _ in groups:
@@ -90,7 +90,7 @@ def main():
             row[n + "_p50"] = np.median(v)
             row[n + "_max"] = v.max()
         row["gap_prev_end_to_release"] = (r0 - prev_end) / 1e3 if prev_end is not None else float("nan")
-        prev_end = ts[idx, 11].max()
+        prev_end = ts[idx, 14].max()
         kinds[(nt, ks, len(idx))].append(row)
     print(f"lane {a.lane} t={a.t}: {len(groups)} GEMV launches; times in us relative to the launch's first release "
           "(medians over launches of the per-launch p50 / max over CTAs)")
