@@ -275,7 +275,9 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
         *p = nv;
         if (a.xs_next) {
           sq[r] = (double)nv * (double)nv;
-          store_split(a.xs_next, a.ld_next, r, o, (float)((double)nv * (double)gn));
+          // the exact product of two floats fits a double, so the fp32 product
+          // (one rounding) equals norm_prep's (float)((double)x * (double)g)
+          store_split(a.xs_next, a.ld_next, r, o, __fmul_rn(nv, gn));
         }
       }
     }
@@ -577,6 +579,13 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
 #endif
 #ifdef HS_CTA_TRACE
     if (threadIdx.x == 0) GPH_STAMP(11)
+#ifdef HS_GEMV_FIN_TWICE
+    // experiment: the same (idempotent) finalize again -- warm caches
+    __syncthreads();
+    if (threadIdx.x == 0 && g_gph != nullptr) gph[3] = gtime();
+    finalize<EPI>(a, o, acc, yres, gn, lane, tile, inv_rms, red, nullptr);
+    if (threadIdx.x == 0 && g_gph != nullptr) gph[4] = gtime();
+#endif
 #endif
   }
   if (a.cluster && !a.push) tc::cluster_sync();   // pull style: partials stay readable until the leader is done

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--lane", default="retr")
     ap.add_argument("--t", type=int, default=3)
     ap.add_argument("--ctx", type=int, default=16384)
+    ap.add_argument("--raw", default=None, help="also save the raw [n][16] records (.npy)")
     a = ap.parse_args()
     import bench
     import paper_2404_11912_b200 as P
@@ -57,6 +58,8 @@ def main():
     lane.rollback_to(f0)
     rec = buf[4 * cap * 3:].view(-1, 16).cpu().numpy().astype(np.uint64)
     rec = rec[rec[:, 15] > 0]
+    if a.raw:
+        np.save(a.raw, rec)
     ident = rec[:, 0]
     ntiles = (ident >> np.uint64(48)).astype(int)
     split = ((ident >> np.uint64(16)) & np.uint64(0xffff)).astype(int)
