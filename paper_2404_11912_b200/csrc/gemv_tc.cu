@@ -235,6 +235,7 @@ struct GemvTcArgs {
   int ld_xs_out;
   float *partial;     // [ks][n_tiles*128][8]
   int *counters;      // [n_tiles]
+  int trig_late;      // signal programmatic launch completion after the last weight load is issued
 };
 
 // all 128 threads of the CTA call finalize (uniform control flow: the residual
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   }
 #endif
 
-  tc::grid_dep_launch();
+  if (!a.trig_late) tc::grid_dep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y;
   const int per = a.nkb / a.ks, rem = a.nkb % a.ks;
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
         tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], k, tile * TC_BM, pol);
         tc::tma_load_2d(sX + s * TC_X_BYTES, &tmX, &full[s], k, 0);
       }
+      if (a.trig_late) tc::grid_dep_launch();
     } else {
       tc::grid_dep_wait();
       HS_TRACE_RESTART
@@ -442,6 +444,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   // ---- epilogue: TMEM -> registers ---------------------------------------------------
   tc::mbar_wait(accum, 0);
   tc::fence_after();
+  if (a.trig_late) tc::grid_dep_launch();
 #ifdef HS_CTA_TRACE
   if (threadIdx.x == 0) GPH_STAMP(5)
 #endif
@@ -724,6 +727,10 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
     HS_REQUIRE(a.xs_next == nullptr || epilogue == 1, HS_ERR_VALUE, "gemv_tc: next-operand output needs epilogue 1");
     HS_REQUIRE(a.xs_next == nullptr || tiles <= 1024, HS_ERR_SHAPE, "gemv_tc: too many tiles for the norm partials");
   }
+  // programmatic launch completion once the weight stream is issued (the
+  // dependent's CTAs then start together; HS_GEMV_TRIG=0: at CTA start)
+  static const int trig_late = getenv("HS_GEMV_TRIG") ? atoi(getenv("HS_GEMV_TRIG")) : 1;
+  a.trig_late = trig_late;
   a.counters = reinterpret_cast<int *>(ws);
   a.partial = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + (size_t)TC_COUNTER_INTS * 4);
   static bool attr_set = false;
