@@ -77,6 +77,16 @@ def main():
     print(f"idle gaps > 20 us: {len(big)}, total {sum(g[0] for g in big) / 1e3:.2f} ms; largest:")
     for g, a_, b_, at in gaps[:25]:
         print(f"  {g:8.1f} us at {at:8.2f} ms  after {a_:40s} before {b_}")
+    # idle time by (previous op -> next op) pair
+    pairs = collections.defaultdict(lambda: [0, 0.0])
+    short = lambda n: n.replace("hs::", "").replace("void ", "").replace("(anonymous namespace)::", "").split("<")[0][:28]
+    for g, a_, b_, at in gaps:
+        k = (short(a_), short(b_))
+        pairs[k][0] += 1
+        pairs[k][1] += g
+    print("idle by (after -> before), all gaps:")
+    for (a_, b_), (c, g) in sorted(pairs.items(), key=lambda x: -x[1][1])[:25]:
+        print(f"  {g / 1e3:8.3f} ms  {c:6d} x  {g / c:7.1f} us  {a_:28s} -> {b_}")
 
 
 if __name__ == "__main__":
