@@ -359,6 +359,21 @@ int hs_sample(const double *probs, int V, const double *uniforms, int32_t *curso
 int hs_draft_sample(const float *logits, int V, double temperature, double *probs_out,
                     const double *uniforms, int32_t *cursor, int32_t *out, void *stream);
 
+/* one draft step through a captured one-token step graph (draft_round,
+ * speculation.py:221-226, without a host round trip per token): draft_sample
+ * of the lane's frontier row, the token also written with the step's
+ * positions into the graph's slot dyn = [frontier, window watermark, token],
+ * then the graph (cudaGraphExec_t, NULL: none) is launched on the stream;
+ * n_launch = kernels in the graph (launch accounting).                      */
+int hs_draft_step(const float *logits, int V, double temperature, double *probs_out,
+                  const double *uniforms, int32_t *cursor, int32_t *out, int32_t *dyn, int frontier,
+                  int lo, void *graph_exec, int n_launch, void *stream);
+
+/* positions (+ token >= 0, also copied to *also when non-NULL) of a step
+ * graph's slot, then the graph: the lane's catch-up over a host token.      */
+int hs_graph_step(int32_t *dyn, int frontier, int lo, int token, int32_t *also, void *graph_exec,
+                  int n_launch, void *stream);
+
 /* _verify_chain (speculation.py:187-208).  tokens[n] (device), qd [n][V],
  * pd [n+1][V].  result[0..n]: emitted tokens; result[n+1] = count emitted;
  * result[n+2] = accepted; result[n+3] = status (0 ok, HS_ERR_CONTRACT when

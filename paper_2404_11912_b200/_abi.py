@@ -102,6 +102,8 @@ _SIGS = {
     "hs_probs": (i32, [vp, i32, i32, f64, vp, vp]),
     "hs_sample": (i32, [vp, i32, vp, vp, vp, vp]),
     "hs_draft_sample": (i32, [vp, i32, f64, vp, vp, vp, vp, vp]),
+    "hs_draft_step": (i32, [vp, i32, f64, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp]),
+    "hs_graph_step": (i32, [vp, i32, i32, i32, vp, vp, i32, vp]),
     "hs_verify_chain": (i32, [vp, i32, vp, vp, i32, vp, vp, vp, vp]),
     "hs_verify_token": (i32, [i32, vp, vp, vp, vp, vp, vp]),
     "hs_correct_token": (i32, [vp, vp, i32, vp, vp, vp, vp]),

@@ -327,9 +327,12 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_kernel(const double *probs
   if (cl_leader()) { *out = tok; *cursor = cur + 1; }
 }
 
+// dyn (optional): a captured step graph's [frontier, window watermark, token]
+// slot, written together with the token (the draft lane's next step reads it)
 __global__ void __launch_bounds__(SMP_THREADS) draft_sample_kernel(const float *logits, int V, double T,
                                                                    double *probs, const double *U,
-                                                                   int32_t *cursor, int32_t *out) {
+                                                                   int32_t *cursor, int32_t *out, int32_t *dyn,
+                                                                   int dyn_frontier, int dyn_lo) {
   pdl_wait();
   HS_CL_SETUP
   extern __shared__ double sw[];
@@ -350,7 +353,21 @@ __global__ void __launch_bounds__(SMP_THREADS) draft_sample_kernel(const float *
   }
   pdl_trigger();
   cl.finish();
-  if (cl_leader()) { *out = tok; *cursor = cur + 1; }
+  if (cl_leader()) {
+    *out = tok;
+    *cursor = cur + 1;
+    if (dyn) { dyn[0] = dyn_frontier; dyn[1] = dyn_lo; dyn[2] = tok; }
+  }
+}
+
+// positions (+ token) of a captured step graph; `also` gets the token too
+__global__ void graph_step_kernel(int32_t *dyn, int frontier, int lo, int token, int32_t *also) {
+  dyn[0] = frontier;
+  dyn[1] = lo;
+  if (token >= 0) {
+    dyn[2] = token;
+    if (also) *also = token;
+  }
 }
 
 // _verify_chain: result[0..n] tokens, [n+1] count, [n+2] accepted, [n+3] status.
@@ -505,7 +522,40 @@ extern "C" int hs_draft_sample(const float *logits, int V, double temperature, d
   int rc = hs::check_vocab(V);
   if (rc != HS_OK) return rc;
   return hs::launch_rows("draft_sample", hs::draft_sample_kernel, 1, V, hs::as_stream(stream), logits, V, temperature,
-                         probs_out, uniforms, cursor, out);
+                         probs_out, uniforms, cursor, out, (int32_t *)nullptr, 0, 0);
+}
+
+static int graph_launch(void *graph_exec, int n_launch, cudaStream_t st) {
+  if (!graph_exec) return HS_OK;
+  const cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(graph_exec), st);
+  if (e != cudaSuccess) return hs::set_error(HS_ERR_CUDA, "step graph launch: %s", cudaGetErrorString(e));
+  hs::count_launch(n_launch);
+  return HS_OK;
+}
+
+extern "C" int hs_draft_step(const float *logits, int V, double temperature, double *probs_out,
+                             const double *uniforms, int32_t *cursor, int32_t *out, int32_t *dyn, int frontier, int lo,
+                             void *graph_exec, int n_launch, void *stream) {
+  if (temperature < 0) return hs::set_error(HS_ERR_VALUE, "temperature must be >= 0");
+  if (!probs_out) return hs::set_error(HS_ERR_VALUE, "draft_step: probs_out required");
+  if (!dyn) return hs::set_error(HS_ERR_VALUE, "draft_step: null step slot");
+  int rc = hs::check_vocab(V);
+  if (rc != HS_OK) return rc;
+  cudaStream_t st = hs::as_stream(stream);
+  rc = hs::launch_rows("draft_sample", hs::draft_sample_kernel, 1, V, st, logits, V, temperature, probs_out, uniforms,
+                       cursor, out, dyn, frontier, lo);
+  if (rc != HS_OK) return rc;
+  return graph_launch(graph_exec, n_launch, st);
+}
+
+extern "C" int hs_graph_step(int32_t *dyn, int frontier, int lo, int token, int32_t *also, void *graph_exec,
+                             int n_launch, void *stream) {
+  if (!dyn) return hs::set_error(HS_ERR_VALUE, "graph_step: null step slot");
+  cudaStream_t st = hs::as_stream(stream);
+  hs::graph_step_kernel<<<1, 1, 0, st>>>(dyn, frontier, lo, token, also);
+  int rc = hs::check_launch("graph_step");
+  if (rc != HS_OK) return rc;
+  return graph_launch(graph_exec, n_launch, st);
 }
 
 extern "C" int hs_verify_chain(const int32_t *tokens, int n, const double *qd, const double *pd, int V,

@@ -116,22 +116,32 @@ class _StepGraph:
                 gc.enable()
         self.n_launch = lib.hs_launch_count() - n0
         torch.cuda.current_stream().wait_stream(side)
+        # the executable graph, launched natively (hs_draft_step / hs_graph_step)
+        # right after the kernel that writes its positions -- no staging copy
+        self.exec = C.c_void_p(int(self.graph.raw_cuda_graph_exec()))
+        self.dyn_ptr = self.dyn.data_ptr()
 
-    def run(self, host_token: Optional[int] = None) -> None:
-        """Replay; the token is already in self.tok (device) or is host_token
-        (shipped with the positions in one staging copy)."""
+    def prep(self):
+        """Host checks of one step on the live state; its positions."""
+        cache = self.lane.cache
+        cache._guard(cache.frontier, cache.frontier)     # the ring keeps every exposable entry
+        return cache.frontier, cache.lo
+
+    def post(self) -> None:
         lane, cache = self.lane, self.lane.cache
-        cache._step(1)                                    # guard / capacity checks on the live state
-        if host_token is None:
-            staging.copy_into(self.dyn, [cache.frontier, cache.lo])
-        else:
-            staging.copy_into(self.dyn, [cache.frontier, cache.lo, host_token])
-        self.graph.replay()
-        lib.hs_note_launches(self.n_launch)
         STATS["alg_bytes"] += self.alg_bytes
         cache._advance(1)
         lane._has_front = True
         lane.recorder.query_position = cache.frontier - 1
+
+    def run(self, host_token: Optional[int] = None, also=None) -> None:
+        """One step; the token is already in self.tok (device) or is
+        host_token (written with the positions by one tiny kernel, and also
+        to the device int32 `also` when given)."""
+        f, lo = self.prep()
+        check(lib.hs_graph_step(self.dyn_ptr, f, lo, -1 if host_token is None else int(host_token),
+                                also, self.exec, self.n_launch, stream_ptr()))
+        self.post()
 
 
 
@@ -224,18 +234,23 @@ class Lane:
         # (tensor parallel, hs_forward_tp); None = replicated weights
         self.tp = None
 
-    def step_graph_run(self, tok) -> None:
+    def step_graph(self) -> "_StepGraph":
+        if self._graph is None:
+            self._graph = _StepGraph(self)
+        return self._graph
+
+    def step_graph_run(self, tok, also=None) -> None:
         """One-token step through the lane's captured graph.  The graph reads
         its token from a lane-owned device slot (one capture per lane, never
         per caller buffer); a device `tok` is copied into it on the stream, a
-        host int travels with the step's positions."""
-        if self._graph is None:
-            self._graph = _StepGraph(self)
+        host int travels with the step's positions (and is also written to
+        the device int32 address `also`)."""
+        g = self.step_graph()
         if isinstance(tok, torch.Tensor):
-            self._graph.tok.copy_(tok)
-            self._graph.run()
+            g.tok.copy_(tok)
+            g.run()
         else:
-            self._graph.run(host_token=int(tok))
+            g.run(host_token=int(tok), also=also)
 
     @property
     def frontier(self) -> int:
@@ -374,6 +389,10 @@ class _RoundBuffers:
         self.p = torch.empty((rows, V), dtype=torch.float64, device=dev)
         self.phat = torch.empty((rows, V), dtype=torch.float64, device=dev)
         self.xtok = torch.empty(rows, dtype=torch.int32, device=dev)
+        # retrieval-lane input of an inner round whose catch-up is one token:
+        # [catch-up token, drafted tokens...] -- written in place by the draft
+        # lane's steps, so the retrieval forward needs no concatenation
+        self.rtok = torch.empty(gamma1 + 1, dtype=torch.int32, device=dev)
         self.res = torch.zeros(rows + 4, dtype=torch.int32, device=dev)
         self.host = torch.zeros(rows + 5, dtype=torch.int32, pin_memory=True)
 
@@ -392,24 +411,40 @@ def _readback(buf: _RoundBuffers, n: int, us: UniformStream):
 
 
 def _draft_round_dev(lane: Lane, seq: Sequence[int], gamma1: int, T: float, us: UniformStream,
-                     buf: _RoundBuffers) -> None:
-    """draft_round (speculation.py:211-227) with tokens and q rows on device."""
+                     buf: _RoundBuffers, fused: bool = False) -> torch.Tensor:
+    """draft_round (speculation.py:211-227) with tokens and q rows on device;
+    returns the device tensor holding the drafted tokens.  fused: the
+    catch-up is one token, also written to buf.rtok[0], and the drafts go to
+    buf.rtok[1:] (the retrieval lane's whole input, in place)."""
     graphs = USE_GRAPHS and isinstance(lane.cache, StreamingCache)
+    fused = fused and graphs and lane.frontier + 1 == len(seq)
     if graphs and lane.frontier + 1 == len(seq):
-        lane.step_graph_run(seq[len(seq) - 1:][0])       # the usual one-token catch-up
+        # the usual one-token catch-up
+        lane.step_graph_run(seq[len(seq) - 1:][0], also=buf.rtok.data_ptr() if fused else None)
     else:
         lane.catch_up(seq)
     if not lane._has_front:
         raise ContractError("lane has no frontier logits; advance over committed tokens first")
     V = buf.V
     s = stream_ptr()
+    dtok = buf.rtok[1:] if fused else buf.dtok
+    if graphs:
+        # sample -> write token + positions into the step graph's slot -> graph,
+        # one native call per drafted token
+        sg = lane.step_graph()
+        front, qp, tp = lane._front.data_ptr(), buf.q.data_ptr(), dtok.data_ptr()
+        ub, uc = us.buf.data_ptr(), us.cursor.data_ptr()
+        for g in range(gamma1):
+            f, lo = sg.prep()
+            check(lib.hs_draft_step(front, V, float(T), qp + 8 * V * g, ub, uc, tp + 4 * g, sg.dyn_ptr, f, lo,
+                                    sg.exec, sg.n_launch, s))
+            sg.post()
+        return dtok
     for g in range(gamma1):
         check(lib.hs_draft_sample(ptr(lane._front), V, float(T), ptr(buf.q[g]), ptr(us.buf), ptr(us.cursor),
-                                  ptr(buf.dtok[g:g + 1]), s))
-        if graphs:
-            lane.step_graph_run(buf.dtok[g:g + 1])
-        else:
-            lane._forward(buf.dtok[g:g + 1])
+                                  ptr(dtok[g:g + 1]), s))
+        lane._forward(dtok[g:g + 1])
+    return dtok
 
 
 def _score_rows_dev(lane: Lane, seq: Sequence[int], tokens_dev: torch.Tensor, T: float,
@@ -440,12 +475,20 @@ def _chain_dev(tokens_dev, n, qd, pd, V, us, buf):
 
 def _inner_round_dev(retr: Lane, draft: Lane, seq, cfg: SpecConfig, us, buf, phat_off: int):
     V = buf.V
+    # both lanes sit at the same frontier: a one-token catch-up is the usual case
+    fused = retr.frontier + 1 == len(seq)
     with _nvtx("inner.draft_round"):
-        _draft_round_dev(draft, seq, cfg.gamma1, cfg.temperature, us, buf)
+        dtok = _draft_round_dev(draft, seq, cfg.gamma1, cfg.temperature, us, buf, fused=fused)
     with _nvtx("inner.retrieval_score"):
-        _score_rows_dev(retr, seq, buf.dtok, cfg.temperature, buf.p)
+        if dtok.data_ptr() != buf.dtok.data_ptr():
+            # buf.rtok = [catch-up, drafts]: one forward, gamma1 + 1 rows
+            n = cfg.gamma1
+            logits = retr._forward(buf.rtok)
+            check(lib.hs_probs(logits.data_ptr(), n + 1, V, float(cfg.temperature), buf.p.data_ptr(), stream_ptr()))
+        else:
+            _score_rows_dev(retr, seq, dtok, cfg.temperature, buf.p)
     with _nvtx("inner.verify_chain"):
-        _chain_dev(buf.dtok, cfg.gamma1, buf.q, buf.p, V, us, buf)
+        _chain_dev(dtok, cfg.gamma1, buf.q, buf.p, V, us, buf)
         # p_hat rows of the emitted tokens: copy all gamma1+1, the surplus is overwritten later
         buf.phat[phat_off:phat_off + cfg.gamma1 + 1].copy_(buf.p[:cfg.gamma1 + 1])
         return _readback(buf, cfg.gamma1, us)
