@@ -66,7 +66,7 @@ int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const floa
 int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                    uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st,
                    const GemvNorm *norm = nullptr, const float *yin = nullptr, int ldyin = 0);
-int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk, double *ssq,
+int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk,
                      cudaStream_t st);
 size_t gemv_tc_ws_bytes(int N, int nkb);
 
@@ -137,7 +137,6 @@ struct FwdWs {
   void *gemv_ws;
   size_t gemv_bytes;
   uint16_t *xd, *xf, *xa;   // split operands: normed input (xd), act (xf), attention output (xa)
-  double *ssq;              // [1024][8] row sums of squares of the residual stream
   float *x, *qkv, *q, *attn;
   void *att_ws;
   size_t att_bytes;
@@ -173,7 +172,6 @@ static size_t carve(const HsModel *m, int t, int n_view, int split, int world, c
   w->xd = (uint16_t *)take((size_t)24 * m->ld_d * 2);
   w->xf = (uint16_t *)take((size_t)24 * m->ld_ff * 2);
   w->xa = (uint16_t *)take((size_t)24 * m->ld_d * 2);
-  w->ssq = (double *)take((size_t)1024 * 8 * 8);
   w->x = (float *)take((size_t)t * d * 4);
   w->qkv = (float *)take((size_t)t * (H + 2 * KVH) * dh * 4);
   w->q = (float *)take((size_t)t * H * dh * 4);
@@ -348,7 +346,6 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
   const bool fused_split = t <= 8;   // one row block: folded norms, no split kernels
   HS_REQUIRE(tp == nullptr || (fused_split && topk_budget == 0 && probs == nullptr && probe == nullptr), HS_ERR_VALUE,
              "forward: tensor-parallel layers need a plain forward of <= 8 rows");
-  const int d_tiles = (d + 127) / 128;
   int rc;
 #define HS_TRY(call) do { if ((rc = (call)) != HS_OK) return rc; } while (0)
   if (fused_split) {
@@ -363,14 +360,14 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
                            // attention kernel, so it could not write q_stash / the rows)
                            (st->append_mode == HS_APPEND_POS || st->append_mode == HS_APPEND_LINEAR);
     HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
-    HS_TRY(launch_norm_prep(w.x, d, t, d, m->attn_norm, w.xd, m->ld_d, w.ssq, s));
+    HS_TRY(launch_norm_prep(w.x, d, t, d, m->attn_norm, w.xd, m->ld_d, s));
     for (int l = 0; l < m->n_layers; ++l) {
       const uint16_t *wqkv = m->wqkv + (size_t)l * nqkv * m->ld_d;
       const uint16_t *wo = m->wo + (size_t)l * d * m->ld_d;
       const uint16_t *wgu = m->wgu + (size_t)l * 2 * ff * m->ld_d;
       const uint16_t *wdn = m->wdown + (size_t)l * d * m->ld_ff;
       const bool last = l + 1 == m->n_layers;
-      GemvNorm in_qkv = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+      GemvNorm in_qkv = {w.x, d, d, eps, nullptr, nullptr, 0};
       if (tp) {
         int r0, n;
         tp_rows(nqkv, tp->rank, tp->world, r0, n);
@@ -418,7 +415,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       if (probe) HS_TRY(launch_probe_probs(c, l, st, H, w.q, t, probe + (size_t)l * H * st->n_view, s));
       }
       const float *gain_next = last ? m->final_norm : m->attn_norm + (size_t)(l + 1) * d;
-      GemvNorm in_gu = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+      GemvNorm in_gu = {w.x, d, d, eps, nullptr, nullptr, 0};
       if (tp) {
         int r0, n, wm;
         // w_o: residual block -> all ranks; the mlp_norm operand is rebuilt replicated
@@ -428,7 +425,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
           HS_TRY(launch_gemv_tc(w.xa, t, wo + (size_t)r0 * m->ld_d, m->ld_d, n, 1, (float *)w.tsend, wm, nullptr, 0,
                                 w.gemv_ws, w.gemv_bytes, s, nullptr, w.x + r0, d));
         HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, d, 0, w.x, d, s));
-        HS_TRY(launch_norm_prep(w.x, d, t, d, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq, s));
+        HS_TRY(launch_norm_prep(w.x, d, t, d, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, s));
         // gate|up: SwiGLU act block (split operand rows) -> all ranks
         tp_rows(2 * ff, tp->rank, tp->world, r0, n);
         wm = tp_wmax(2 * ff, tp->world);
@@ -443,17 +440,17 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
           HS_TRY(launch_gemv_tc(w.xf, t, wdn + (size_t)r0 * m->ld_ff, m->ld_ff, n, 1, (float *)w.tsend, wm, nullptr,
                                 0, w.gemv_ws, w.gemv_bytes, s, nullptr, w.x + r0, d));
         HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, d, 0, w.x, d, s));
-        HS_TRY(launch_norm_prep(w.x, d, t, d, gain_next, w.xd, m->ld_d, w.ssq, s));
+        HS_TRY(launch_norm_prep(w.x, d, t, d, gain_next, w.xd, m->ld_d, s));
         continue;
       }
-      GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, w.ssq};
+      GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d};
       HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo));
       HS_TRY(launch_gemv_tc(w.xd, t, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes, s,
                             &in_gu));
-      GemvNorm out_dn = {nullptr, 0, 1, 0.f, gain_next, w.xd, m->ld_d, w.ssq};
+      GemvNorm out_dn = {nullptr, 0, 1, 0.f, gain_next, w.xd, m->ld_d};
       HS_TRY(launch_gemv_tc(w.xf, t, wdn, m->ld_ff, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_dn));
     }
-    GemvNorm in_head = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
+    GemvNorm in_head = {w.x, d, d, eps, nullptr, nullptr, 0};
     if (tp) {
       int r0, n;
       tp_rows(m->vocab_size, tp->rank, tp->world, r0, n);
@@ -479,10 +476,10 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     const uint16_t *wgu = m->wgu + (size_t)l * 2 * ff * m->ld_d;
     const uint16_t *wdn = m->wdown + (size_t)l * d * m->ld_ff;
     const float *an = m->attn_norm + (size_t)l * d, *mn = m->mlp_norm + (size_t)l * d;
-    GemvNorm in_n = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
-      HS_TRY(launch_norm_prep(w.x + (size_t)r0 * d, d, tp, d, an, w.xd, m->ld_d, w.ssq, s));
+      const GemvNorm in_n = {w.x + (size_t)r0 * d, d, d, eps, nullptr, nullptr, 0};
+      HS_TRY(launch_norm_prep(w.x + (size_t)r0 * d, d, tp, d, an, w.xd, m->ld_d, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wqkv, m->ld_d, nqkv, 0, w.qkv + (size_t)r0 * nqkv, nqkv, nullptr, 0, w.gemv_ws,
                             w.gemv_bytes, s, &in_n));
     }
@@ -502,9 +499,10 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     for (int r0 = 0; r0 < t; r0 += 8) {
       const int tp = t - r0 < 8 ? t - r0 : 8;
       float *xr = w.x + (size_t)r0 * d;
+      const GemvNorm in_n = {xr, d, d, eps, nullptr, nullptr, 0};
       HS_TRY(launch_split_rows(w.attn + (size_t)r0 * d, d, tp, d, m->ld_d, nullptr, 0.f, w.xd, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wo, m->ld_d, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
-      HS_TRY(launch_norm_prep(xr, d, tp, d, mn, w.xd, m->ld_d, w.ssq, s));
+      HS_TRY(launch_norm_prep(xr, d, tp, d, mn, w.xd, m->ld_d, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes, s,
                             &in_n));
       HS_TRY(launch_gemv_tc(w.xf, tp, wdn, m->ld_ff, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
@@ -512,8 +510,8 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
   }
   for (int r0 = 0; r0 < t; r0 += 8) {
     const int tp = t - r0 < 8 ? t - r0 : 8;
-    GemvNorm in_n = {w.ssq, d_tiles, d, eps, nullptr, nullptr, 0, nullptr};
-    HS_TRY(launch_norm_prep(w.x + (size_t)r0 * d, d, tp, d, m->final_norm, w.xd, m->ld_d, w.ssq, s));
+    const GemvNorm in_n = {w.x + (size_t)r0 * d, d, d, eps, nullptr, nullptr, 0};
+    HS_TRY(launch_norm_prep(w.x + (size_t)r0 * d, d, tp, d, m->final_norm, w.xd, m->ld_d, s));
     HS_TRY(launch_gemv_tc(w.xd, tp, m->head, m->ld_d, m->vocab_size, 0, logits + (size_t)r0 * m->vocab_size,
                           m->vocab_size, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &in_n));
   }

@@ -176,34 +176,21 @@ __global__ void __launch_bounds__(SPLIT_THREADS) split_rows_kernel(const float *
 }
 
 // Folded-RMSNorm operand prep for rows [0, t) of x: split(fp32(x * gain))
-// into xs [24][ldk] and per-128-column-tile row sums of squares into
-// ssq [tile][8].  Thread i of a CTA owns column tile * 128 + i and the sums
-// run lanes-then-warps in the same order as the residual GEMV epilogue
-// (finalize), so both producers of an operand give identical bits.
-// grid (tiles, t), 128 threads.
+// into xs [24][ldk] -- the operand the residual GEMV epilogue writes in the
+// single-block forward (its consumer computes the RMS itself, gemv_rms).
+// grid (tiles of 128 columns, t), 128 threads.
 __global__ void __launch_bounds__(128) norm_prep_kernel(const float *x, int ldx, int K, const float *gain,
-                                                        uint16_t *xs, int ldk, double *ssq) {
+                                                        uint16_t *xs, int ldk) {
   HS_TRACE_BEGIN
-  const int tile = blockIdx.x, r = blockIdx.y, col = tile * 128 + threadIdx.x;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __shared__ double red[4];
-  double sq = 0.0;
-  if (col < K) {
-    const float v = x[(size_t)r * ldx + col];
-    sq = (double)v * (double)v;
-    store_split(xs, ldk, r, col, (float)((double)v * (double)gain[col]));
-  }
-  sq = warp_sum(sq);
-  if (lane == 0) red[w] = sq;
-  __syncthreads();
-  if (threadIdx.x == 0) ssq[(size_t)tile * TC_T + r] = (red[0] + red[1]) + (red[2] + red[3]);
+  const int r = blockIdx.y, col = blockIdx.x * 128 + threadIdx.x;
+  if (col < K) store_split(xs, ldk, r, col, __fmul_rn(x[(size_t)r * ldx + col], gain[col]));
   HS_TRACE_END(3)
 }
 
-int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk, double *ssq,
+int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk,
                      cudaStream_t st) {
   HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "norm_prep: t=%d outside [1,%d]", t, TC_T);
-  norm_prep_kernel<<<dim3((K + 127) / 128, t), 128, 0, st>>>(x, ldx, K, gain, xs, ldk, ssq);
+  norm_prep_kernel<<<dim3((K + 127) / 128, t), 128, 0, st>>>(x, ldx, K, gain, xs, ldk);
   return check_launch("norm_prep");
 }
 
@@ -213,17 +200,16 @@ struct GemvTcArgs {
   int push;           // cluster reduction by pushes into the split-0 CTA (its landing area fits two CTAs per SM)
   int nrow;           // pushed floats per row (4 when t <= 4, else 8)
   // folded RMSNorm (model.py:282-284) of this GEMV's input rows: the operand
-  // is split(x * gain) and the result is scaled by 1 / rms(x) here, with the
-  // row sums of squares given as ssq_parts per-tile partials [parts][8]
-  const double *ssq_in;
-  int ssq_parts, norm_K;
+  // is split(x * gain) and the result is scaled by 1 / rms(x) here, the RMS
+  // computed from the un-normalised rows x_in [t][ldx_in] (gemv_rms)
+  const float *x_in;
+  int ldx_in, norm_K;
   float eps;
   // residual producer (epilogue 1): also write the next GEMV's operand
-  // split(x_new * gnext) and this tile's row sums of squares of x_new
+  // split(x_new * gnext)
   const float *gnext;
   uint16_t *xs_next;
   int ld_next;
-  double *ssq_out;
   float *y;
   int ldy;
   // residual source of epilogue 1 (null: y itself, updated in place); the
@@ -248,7 +234,7 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
                                          unsigned long long *gst) {
   float v[TC_T];
 #pragma unroll
-  for (int r = 0; r < TC_T; ++r) v[r] = a.ssq_in ? (float)((double)vin[r] * inv_rms[r]) : vin[r];
+  for (int r = 0; r < TC_T; ++r) v[r] = a.x_in ? (float)((double)vin[r] * inv_rms[r]) : vin[r];
   if constexpr (EPI == 2) {
     float up[TC_T];
 #pragma unroll
@@ -266,50 +252,60 @@ __device__ __forceinline__ void finalize(const GemvTcArgs &a, int o, const float
       }
     }
   } else {
-    double sq[TC_T];
 #pragma unroll
     for (int r = 0; r < TC_T; ++r) {
-      sq[r] = 0.0;
       if (r < a.t && o < a.N) {
-        float *p = a.y + (size_t)r * a.ldy + o;
         const float nv = (EPI == 1) ? (yres[r] + v[r]) : v[r];
-        *p = nv;
-        if (a.xs_next) {
-          sq[r] = (double)nv * (double)nv;
-          // the exact product of two floats fits a double, so the fp32 product
-          // (one rounding) equals norm_prep's (float)((double)x * (double)g)
-          store_split(a.xs_next, a.ld_next, r, o, __fmul_rn(nv, gn));
-        }
+        a.y[(size_t)r * a.ldy + o] = nv;
+        // the exact product of two floats fits a double, so the fp32 product
+        // (one rounding) equals the reference's (float)((double)x * (double)g)
+        if (a.xs_next) store_split(a.xs_next, a.ld_next, r, o, __fmul_rn(nv, gn));
       }
     }
 #ifdef HS_CTA_TRACE
     if (gst && threadIdx.x == 0) gst[12] = gtime();
 #endif
-    if (a.xs_next != nullptr) {
-      // this tile's row sums of squares, fixed order: lanes, then the 4 warps
-      const int w = threadIdx.x >> 5;
-#pragma unroll
-      for (int r = 0; r < TC_T; ++r) {
-        if (r < a.t) {   // rows >= t are zero: no shuffles for them
-          const double sr = warp_sum(sq[r]);
-          if (lane == 0) red[w][r] = sr;
-        } else if (lane == 0) {
-          red[w][r] = 0.0;
-        }
-      }
-#ifdef HS_CTA_TRACE
-      if (gst && threadIdx.x == 0) gst[13] = gtime();
-#endif
-      __syncthreads();
-#ifdef HS_CTA_TRACE
-      if (gst && threadIdx.x == 0) gst[14] = gtime();
-#endif
-      if (threadIdx.x < TC_T) {
-        const int r = threadIdx.x;
-        a.ssq_out[(size_t)tile * TC_T + r] = (red[0][r] + red[1][r]) + (red[2][r] + red[3][r]);
-      }
+  }
+  (void)lane; (void)tile; (void)red;
+}
+
+// 1 / sqrt(mean(x^2) + eps) of rows [0, t) of x (model.py:282-284), computed
+// by the 64 threads of warps 2-3 while the main loop streams the weights:
+// thread j sums float4 columns 4j + 256i in fp64, then the two warps' xor
+// trees, warp 2 + warp 3.  Every consumer of a row (and every path: single
+// block, multi-block, tensor-parallel) sums in this same order.
+__device__ __forceinline__ double sq4(const float4 v) {
+  return (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+}
+__device__ __forceinline__ void gemv_rms(const GemvTcArgs &a, int j, double *inv_rms, double (*red)[TC_T]) {
+  const int lane = j & 31, w = j >> 5;
+  const int K4 = a.norm_K & ~3;
+  // rows in pairs (more loads in flight for the longer verify batches); every
+  // row accumulates its chunks in the same order either way
+  for (int r = 0; r < a.t; r += 2) {
+    const bool two = r + 1 < a.t;
+    const float *x0 = a.x_in + (size_t)r * a.ldx_in, *x1 = x0 + a.ldx_in;
+    double s0 = 0.0, s1 = 0.0;
+    for (int c = 4 * j; c < K4; c += 256) {
+      const float4 v0 = __ldcg(reinterpret_cast<const float4 *>(x0 + c));
+      const float4 v1 = two ? __ldcg(reinterpret_cast<const float4 *>(x1 + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      s0 += sq4(v0);
+      s1 += sq4(v1);
+    }
+    for (int c = K4 + j; c < a.norm_K; c += 64) {
+      const float u0 = __ldcg(x0 + c), u1 = two ? __ldcg(x1 + c) : 0.f;
+      s0 += (double)u0 * u0;
+      s1 += (double)u1 * u1;
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (lane == 0) {
+      red[w][r] = s0;
+      if (two) red[w][r + 1] = s1;
     }
   }
+  asm volatile("bar.sync 3, 64;" ::: "memory");
+  if (j < a.t) inv_rms[j] = 1.0 / sqrt((red[0][j] + red[1][j]) / (double)a.norm_K + (double)a.eps);
 }
 
 // EPI: 0 store (optionally scaled by the folded RMSNorm), 1 residual
@@ -421,11 +417,7 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
   __syncwarp();
   __shared__ double inv_rms[TC_T];
   __shared__ double red[4][TC_T];
-  if (a.ssq_in && warp == 2 && lane < TC_T) {   // folded RMSNorm: 1 / sqrt(mean(x^2) + eps) per row
-    double ss = 0.0;
-    for (int k = 0; k < a.ssq_parts; ++k) ss += __ldcg(a.ssq_in + (size_t)k * TC_T + lane);
-    inv_rms[lane] = 1.0 / sqrt(ss / (double)a.norm_K + (double)a.eps);
-  }
+  if (a.x_in && warp >= 2) gemv_rms(a, threadIdx.x - 64, inv_rms, red);   // folded RMSNorm of the input rows
   const int row = warp * 32 + lane;
   const int o = tile * TC_BM + row;
   // operands of the epilogue that do not depend on the accumulator (residual
@@ -719,13 +711,14 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   a.push = (a.cluster && push_mode && (push_mode == 2 || TC_SMEM + land <= gemv_smem_budget())) ? 1 : 0;
   a.y = y; a.ldy = ldy; a.xs_out = xs_out; a.ld_xs_out = ld_xs_out;
   a.yin = yin; a.ldyin = ldyin;
-  a.ssq_in = nullptr; a.ssq_parts = 0; a.norm_K = 1; a.eps = 0.f;
-  a.gnext = nullptr; a.xs_next = nullptr; a.ld_next = 0; a.ssq_out = nullptr;
+  a.x_in = nullptr; a.ldx_in = 0; a.norm_K = 1; a.eps = 0.f;
+  a.gnext = nullptr; a.xs_next = nullptr; a.ld_next = 0;
   if (norm) {
-    a.ssq_in = norm->ssq_in; a.ssq_parts = norm->ssq_parts; a.norm_K = norm->norm_K; a.eps = norm->eps;
-    a.gnext = norm->gnext; a.xs_next = norm->xs_next; a.ld_next = norm->ld_next; a.ssq_out = norm->ssq_out;
+    a.x_in = norm->x_in; a.ldx_in = norm->ldx_in; a.norm_K = norm->norm_K; a.eps = norm->eps;
+    a.gnext = norm->gnext; a.xs_next = norm->xs_next; a.ld_next = norm->ld_next;
+    HS_REQUIRE(a.x_in == nullptr || ((uintptr_t)a.x_in % 16 == 0 && a.ldx_in % 4 == 0), HS_ERR_VALUE,
+               "gemv_tc: norm input rows must be 16-byte aligned");
     HS_REQUIRE(a.xs_next == nullptr || epilogue == 1, HS_ERR_VALUE, "gemv_tc: next-operand output needs epilogue 1");
-    HS_REQUIRE(a.xs_next == nullptr || tiles <= 1024, HS_ERR_SHAPE, "gemv_tc: too many tiles for the norm partials");
   }
   // programmatic launch completion once the weight stream is issued (the
   // dependent's CTAs then start together; HS_GEMV_TRIG=0: at CTA start)

@@ -64,7 +64,7 @@ def main():
     torch.cuda.synchronize()
     lib.hs_cta_trace(None, 0)
     lane.rollback_to(f0)
-    rec = buf.view(-1, 3).cpu().numpy().astype(np.uint64)
+    rec = buf[:4 * cap * 3].view(-1, 3).cpu().numpy().astype(np.uint64)   # (region 5: GEMV phase records)
     rec = rec[rec[:, 1] > 0]
     kid_full = (rec[:, 0] >> np.uint64(32)).astype(int)
     kid = kid_full & 0xff
