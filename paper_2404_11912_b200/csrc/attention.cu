@@ -216,11 +216,10 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
 // out[i][h*DH + d] = sum_s w_s o_s / sum_s w_s l_s,  w_s = exp(m_s - M), splits in order.
 // packed != nullptr: write the view's partial state (M, l, o unnormalised)
 // as [rows][2 + DH] instead (sequence-shard input, hs_attention_partial).
-// Latency-shaped: every thread loads the (m, l) of a chunk of CHUNK
-// splits itself (broadcast loads) together with its own o column, all in
-// flight at once, so a view of <= CHUNK splits costs one L2 round trip
-// (CHUNK 16 for the retrieval / streaming views, 64 for the full cache up to
-// 131,072 keys);
+// Latency-shaped: the CTA loads the row's (m, l) of up to CHUNK splits once
+// into shared memory while every thread's o column of every split is in
+// flight, so a view of <= CHUNK splits costs one L2 round trip (CHUNK 16 for
+// the retrieval / streaming views, 64 for the full cache up to 131,072 keys);
 // longer views take one max pass and one sum pass per chunk.  The sums run in
 // split order with the same operations as shard_merge_kernel.
 template <int COMB_CHUNK>
@@ -234,43 +233,85 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const float *pm, cons
   const int row = blockIdx.x, d = threadIdx.x;
   const size_t ostride = (size_t)rows * DH;
   const float *pd = po + (size_t)row * DH + d;
-  float mv[COMB_CHUNK], lv[COMB_CHUNK], ov[COMB_CHUNK];
-  float M = -INFINITY;
-  const bool one = n_splits <= COMB_CHUNK;
-  if (one) {
+  float M = -INFINITY, l = 0.f, o = 0.f;
+  if (n_splits <= COMB_CHUNK) {
+    // one round trip: the row's (m, l) of every split are loaded once per CTA
+    // into shared memory (not by every thread) while each thread's o column
+    // of every split is in flight; M, the split weights and l are computed
+    // once per CTA, so a thread's work is its o chain alone
+    __shared__ float ms[COMB_CHUNK], ls[COMB_CHUNK], ws[COMB_CHUNK];
+    __shared__ float Ml[2];
+    for (int u = d; u < COMB_CHUNK; u += blockDim.x) {
+      ms[u] = u < n_splits ? __ldcg(pm + (size_t)u * rows + row) : -INFINITY;
+      ls[u] = u < n_splits ? __ldcg(pl + (size_t)u * rows + row) : 0.f;
+    }
+    float ov[COMB_CHUNK];
+    if (n_splits > 0) {
+      const int last = n_splits - 1;
+#pragma unroll
+      for (int u = 0; u < COMB_CHUNK; ++u) ov[u] = __ldcg(pd + (size_t)(u < last ? u : last) * ostride);   // (clamped: weight 0)
+    } else {
+#pragma unroll
+      for (int u = 0; u < COMB_CHUNK; ++u) ov[u] = 0.f;
+    }
+    __syncthreads();
+    const int nw = blockDim.x < 32 ? (int)blockDim.x : 32;   // the first warp (all of a small block)
+    if (d < nw) {
+      float mx = -INFINITY;
+      for (int u = d; u < COMB_CHUNK; u += nw) mx = fmaxf(mx, ms[u]);
+      if (nw == 32) {
+        mx = warp_max(mx);   // max: order-free
+      } else {
+        __shared__ float mred[32];
+        mred[d] = mx;
+        __syncwarp((1u << nw) - 1);
+        mx = -INFINITY;
+        for (int k = 0; k < nw; ++k) mx = fmaxf(mx, mred[k]);
+      }
+      for (int u = d; u < COMB_CHUNK; u += nw) ws[u] = (ms[u] == -INFINITY) ? 0.f : expf(ms[u] - mx);
+      __syncwarp(nw == 32 ? 0xffffffffu : (1u << nw) - 1);
+      if (d == 0) {
+        float lsum = 0.f;
+        for (int u = 0; u < n_splits; ++u) {
+          const float w = ws[u];
+          if (w != 0.f) lsum = fmaf(w, ls[u], lsum);
+        }
+        Ml[0] = mx;
+        Ml[1] = lsum;
+      }
+    }
+    __syncthreads();
+    M = Ml[0];
+    l = Ml[1];
 #pragma unroll
     for (int u = 0; u < COMB_CHUNK; ++u) {
-      mv[u] = u < n_splits ? __ldcg(pm + (size_t)u * rows + row) : -INFINITY;
-      lv[u] = u < n_splits ? __ldcg(pl + (size_t)u * rows + row) : 0.f;
-      ov[u] = u < n_splits ? __ldcg(pd + u * ostride) : 0.f;
+      const float w = ws[u];
+      o = (w != 0.f) ? fmaf(w, ov[u], o) : o;   // splits in order, as shard_merge_kernel
     }
-#pragma unroll
-    for (int u = 0; u < COMB_CHUNK; ++u) M = fmaxf(M, mv[u]);
   } else {
+    // longer views: one max pass and one sum pass per chunk of splits
+    float mv[COMB_CHUNK], lv[COMB_CHUNK], ov[COMB_CHUNK];
     for (int s0 = 0; s0 < n_splits; s0 += COMB_CHUNK) {
 #pragma unroll
       for (int u = 0; u < COMB_CHUNK; ++u) mv[u] = s0 + u < n_splits ? __ldcg(pm + (size_t)(s0 + u) * rows + row) : -INFINITY;
 #pragma unroll
       for (int u = 0; u < COMB_CHUNK; ++u) M = fmaxf(M, mv[u]);
     }
-  }
-  float l = 0.f, o = 0.f;
-  for (int s0 = 0; s0 < n_splits; s0 += COMB_CHUNK) {
-    if (!one) {
+    for (int s0 = 0; s0 < n_splits; s0 += COMB_CHUNK) {
 #pragma unroll
       for (int u = 0; u < COMB_CHUNK; ++u) {
-        const int s = s0 + u;
-        mv[u] = s < n_splits ? __ldcg(pm + (size_t)s * rows + row) : -INFINITY;
-        lv[u] = s < n_splits ? __ldcg(pl + (size_t)s * rows + row) : 0.f;
-        ov[u] = s < n_splits ? __ldcg(pd + s * ostride) : 0.f;
+        const int sp = s0 + u;
+        mv[u] = sp < n_splits ? __ldcg(pm + (size_t)sp * rows + row) : -INFINITY;
+        lv[u] = sp < n_splits ? __ldcg(pl + (size_t)sp * rows + row) : 0.f;
+        ov[u] = sp < n_splits ? __ldcg(pd + sp * ostride) : 0.f;
       }
-    }
 #pragma unroll
-    for (int u = 0; u < COMB_CHUNK; ++u) {
-      const float w = (mv[u] == -INFINITY) ? 0.f : expf(mv[u] - M);
-      if (w != 0.f) {
-        l = fmaf(w, lv[u], l);
-        o = fmaf(w, ov[u], o);
+      for (int u = 0; u < COMB_CHUNK; ++u) {
+        const float w = (mv[u] == -INFINITY) ? 0.f : expf(mv[u] - M);
+        if (w != 0.f) {
+          l = fmaf(w, lv[u], l);
+          o = fmaf(w, ov[u], o);
+        }
       }
     }
   }

@@ -171,17 +171,20 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
   // ---------------------------------------------------------------- TMA producer (warp 4)
   if (warp == 4) {
     if (tc::elect_one()) {
+      // K / V are streamed once: evict-first, so they do not push the split
+      // states (read back by the combine) out of L2
+      const uint64_t kv_pol = tc::policy_evict_first();
       auto load_kv = [&](uint32_t g, int row) {
         const int ks = g % AT_KSTAGES, vs = g % AT_VSTAGES;
         const uint32_t kph = (g / AT_KSTAGES) & 1, vph = (g / AT_VSTAGES) & 1;
         tc::mbar_wait(&kempty[ks], kph ^ 1);
         tc::mbar_expect_tx(&kfull[ks], AT_KV);
-        tc::tma_load_2d(sK + ks * AT_KV, &tmK, &kfull[ks], 0, row);
-        tc::tma_load_2d(sK + ks * AT_KV + AT_HALF, &tmK, &kfull[ks], 64, row);
+        tc::tma_load_2d_hint(sK + ks * AT_KV, &tmK, &kfull[ks], 0, row, kv_pol);
+        tc::tma_load_2d_hint(sK + ks * AT_KV + AT_HALF, &tmK, &kfull[ks], 64, row, kv_pol);
         tc::mbar_wait(&vempty[vs], vph ^ 1);
         tc::mbar_expect_tx(&vfull[vs], AT_KV);
-        tc::tma_load_2d(sV + vs * AT_KV, &tmV, &vfull[vs], 0, row);
-        tc::tma_load_2d(sV + vs * AT_KV + AT_HALF, &tmV, &vfull[vs], 64, row);
+        tc::tma_load_2d_hint(sV + vs * AT_KV, &tmV, &vfull[vs], 0, row, kv_pol);
+        tc::tma_load_2d_hint(sV + vs * AT_KV + AT_HALF, &tmV, &vfull[vs], 64, row, kv_pol);
       };
       // Programmatic dependent launch: the first tile of this CTA's first item
       // streams in while the RoPE kernel (and the GEMV before it) drain, when
@@ -499,16 +502,19 @@ __global__ void __launch_bounds__(AT_THREADS, 2) attn_tc_kernel(const __grid_con
     }
     group_sync(grp);
     const size_t pbase = (size_t)split * a.t * a.H;
+    // the split states stay in L2 (evict-last) for the combine that follows
+    const uint64_t st_pol = tc::policy_evict_last();
 #pragma unroll
     for (int r = 0; r < AT_GR; ++r) {
       const int rr = rb + r;
       if (rr < re) {
         const int i = (r0 + rr) / a.g, head = kh * a.g + (r0 + rr) % a.g;
         const size_t row = (size_t)i * a.H + head;
-        a.part_o[(pbase + row) * AT_DH + ltid] = o_acc[r];
+        tc::st_hint_f32(a.part_o + (pbase + row) * AT_DH + ltid, o_acc[r], st_pol);
         if (ltid == 0) {
-          a.part_m[pbase + row] = m_run[r] * 0.69314718055994530942f;   // back to natural-log units
-          a.part_l[pbase + row] = (redl[0][rr] + redl[1][rr]) + (redl[2][rr] + redl[3][rr]);
+          // m back to natural-log units
+          tc::st_hint_f32(a.part_m + pbase + row, m_run[r] * 0.69314718055994530942f, st_pol);
+          tc::st_hint_f32(a.part_l + pbase + row, (redl[0][rr] + redl[1][rr]) + (redl[2][rr] + redl[3][rr]), st_pol);
         }
       }
     }

@@ -83,6 +83,15 @@ __device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap *map, int c
                "r"(c0), "r"(c1)
                : "memory");
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// fp32 store with an L2 eviction-priority policy
+__device__ __forceinline__ void st_hint_f32(float *p, float v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(policy) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

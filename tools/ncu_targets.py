@@ -7,6 +7,8 @@ same shape, so --launch-skip picks a warm one):
                                             #   per layer gemv wqkv, attn_tc (288 items) + combine,
                                             #   gemv w_o, gemv gate|up, gemv w_down
     python tools/ncu_targets.py score       # chunk_score over 122,880 keys (2 layers)
+    python tools/ncu_targets.py full        # verify forward, t = 7, over a 122,880-key full cache
+                                            #   (attn_tc 60 splits + combine<64>)
 
 GEMV launch order per layer: wqkv, w_o, gate|up, w_down (lm_head once per
 forward), so with L layers and F warm forwards skip F*(4L+1) + k to land on
@@ -43,6 +45,18 @@ def main():
         lane = P.speculation.Lane(tw, rc)
         toks = torch.ones(3, dtype=torch.int32, device="cuda")
         f0 = rc.frontier
+        for _ in range(reps):
+            lane._forward(toks)
+            lane.rollback_to(f0)
+        torch.cuda.synchronize()
+    elif what == "full":
+        tw = P.ModelWeights.on_device(P.DeviceModel.random(cfg, seed=1))
+        n = 122880
+        full = P.FullCache.from_config(cfg)
+        full.fill_random_(n, seed=0)
+        lane = P.speculation.Lane(tw, full)
+        toks = torch.ones(7, dtype=torch.int32, device="cuda")
+        f0 = full.frontier
         for _ in range(reps):
             lane._forward(toks)
             lane.rollback_to(f0)
