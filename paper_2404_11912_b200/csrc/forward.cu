@@ -69,6 +69,18 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
 int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk,
                      cudaStream_t st);
 size_t gemv_tc_ws_bytes(int N, int nkb);
+void gemv_set_keep_l2(int keep);
+
+// weights of a model small enough to stay L2-resident between its steps (the
+// draft: 88 MB at the JF68M shape against a 126 MB L2; HS_L2_KEEP_MB overrides)
+static int keep_weights_in_l2(const HsModel *m) {
+  static const long long lim = getenv("HS_L2_KEEP_MB") ? atoll(getenv("HS_L2_KEEP_MB")) : 100;
+  const long long nqkv = (long long)(m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
+  const long long bytes = 2LL * ((long long)m->n_layers * ((nqkv + m->d_model + 2LL * m->d_ff) * m->ld_d +
+                                                         (long long)m->d_model * m->ld_ff) +
+                                 (long long)m->vocab_size * m->ld_d);
+  return bytes <= lim * 1000000LL;
+}
 
 // ---- tensor-parallel dense layers ("TP-shard the dense
 // weights"): every projection is split by output rows in whole 128-row tiles
@@ -334,6 +346,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     HS_REQUIRE(workspace_bytes >= align256(need) + topk_bytes, HS_ERR_VALUE, "forward: top-k workspace too small");
   }
   cudaStream_t s = as_stream(stream);
+  gemv_set_keep_l2(keep_weights_in_l2(m));
   const int d = m->d_model, H = m->n_heads, KVH = m->n_kv_heads, dh = m->head_dim, ff = m->d_ff;
   const int nqkv = (H + 2 * KVH) * dh;
   const float eps = m->norm_eps;

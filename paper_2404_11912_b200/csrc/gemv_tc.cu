@@ -222,6 +222,7 @@ struct GemvTcArgs {
   float *partial;     // [ks][n_tiles*128][8]
   int *counters;      // [n_tiles]
   int trig_late;      // signal programmatic launch completion after the last weight load is issued
+  int keep_l2;        // weights loaded evict-last (a small model re-read every step) instead of evict-first
 };
 
 // all 128 threads of the CTA call finalize (uniform control flow: the residual
@@ -367,7 +368,9 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
       // Programmatic dependent launch: the weights never depend on the
       // previous kernel, so the first stages' weight tiles stream in while
       // that kernel drains; only the activation tiles wait for it.
-      const uint64_t pol = tc::policy_evict_first();   // weights are streamed exactly once
+      // large models' weights are streamed exactly once per forward (evict-first);
+      // a small model's (the draft) stay in L2 between its steps
+      const uint64_t pol = a.keep_l2 ? tc::policy_evict_last() : tc::policy_evict_first();
       const int npre = nk < TC_STAGES ? nk : TC_STAGES;
       for (int i = 0; i < npre; ++i) {
         tc::mbar_expect_tx(&full[i], TC_W_BYTES + TC_X_BYTES);
@@ -684,6 +687,11 @@ int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const floa
   return check_launch("split_rows");
 }
 
+// L2 policy of the weight tiles for the GEMVs this host thread launches next
+// (set per forward: forward.cu)
+static thread_local int g_gemv_keep_l2 = 0;
+void gemv_set_keep_l2(int keep) { g_gemv_keep_l2 = keep; }
+
 // y (+)= W . x for one pass of <= 8 rows whose split operand is in xs [24][ldw]
 int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                    uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st,
@@ -724,6 +732,7 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   // dependent's CTAs then start together; HS_GEMV_TRIG=0: at CTA start)
   static const int trig_late = getenv("HS_GEMV_TRIG") ? atoi(getenv("HS_GEMV_TRIG")) : 1;
   a.trig_late = trig_late;
+  a.keep_l2 = g_gemv_keep_l2;
   a.counters = reinterpret_cast<int *>(ws);
   a.partial = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + (size_t)TC_COUNTER_INTS * 4);
   static bool attr_set = false;
