@@ -369,6 +369,10 @@ int hs_draft_step(const float *logits, int V, double temperature, double *probs_
                   const double *uniforms, int32_t *cursor, int32_t *out, int32_t *dyn, int frontier,
                   int lo, void *graph_exec, int n_launch, void *stream);
 
+/* n <= 1024 int32 host values (src, pageable) -> device dst, stream-ordered
+ * through a pinned ring (no synchronisation): a step's token ids.           */
+int hs_upload_i32(int32_t *dst, const int32_t *src, int n, void *stream);
+
 /* positions (+ token >= 0, also copied to *also when non-NULL) of a step
  * graph's slot, then the graph: the lane's catch-up over a host token.      */
 int hs_graph_step(int32_t *dyn, int frontier, int lo, int token, int32_t *also, void *graph_exec,

@@ -104,6 +104,7 @@ _SIGS = {
     "hs_draft_sample": (i32, [vp, i32, f64, vp, vp, vp, vp, vp]),
     "hs_draft_step": (i32, [vp, i32, f64, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp]),
     "hs_graph_step": (i32, [vp, i32, i32, i32, vp, vp, i32, vp]),
+    "hs_upload_i32": (i32, [vp, vp, i32, vp]),
     "hs_verify_chain": (i32, [vp, i32, vp, vp, i32, vp, vp, vp, vp]),
     "hs_verify_token": (i32, [i32, vp, vp, vp, vp, vp, vp]),
     "hs_correct_token": (i32, [vp, vp, i32, vp, vp, vp, vp]),

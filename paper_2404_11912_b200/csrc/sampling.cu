@@ -23,6 +23,8 @@
 // keeps all of a row's loads in flight at once.
 #include <cooperative_groups.h>
 
+#include <cstring>
+
 #include "hs_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -530,6 +532,42 @@ static int graph_launch(void *graph_exec, int n_launch, cudaStream_t st) {
   const cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(graph_exec), st);
   if (e != cudaSuccess) return hs::set_error(HS_ERR_CUDA, "step graph launch: %s", cudaGetErrorString(e));
   hs::count_launch(n_launch);
+  return HS_OK;
+}
+
+// small host -> device uploads (token ids of a step) through a pinned ring:
+// one call, stream-ordered, no synchronisation (a slot is reused only after
+// its previous copy ran); n <= 1024 int32 per call
+namespace {
+struct UploadRing {
+  static constexpr int kSlots = 64, kCap = 1024;
+  int32_t *host = nullptr;
+  cudaEvent_t ev[kSlots];
+  bool used[kSlots] = {};
+  int next = 0;
+};
+thread_local UploadRing g_up;
+}  // namespace
+
+extern "C" int hs_upload_i32(int32_t *dst, const int32_t *src, int n, void *stream) {
+  if (n < 0 || n > UploadRing::kCap) return hs::set_error(HS_ERR_VALUE, "upload: %d values (max %d)", n, UploadRing::kCap);
+  if (n == 0) return HS_OK;
+  UploadRing &r = g_up;
+  if (!r.host) {
+    if (cudaMallocHost(&r.host, sizeof(int32_t) * UploadRing::kSlots * UploadRing::kCap) != cudaSuccess)
+      return hs::set_error(HS_ERR_CUDA, "upload: pinned ring allocation failed");
+    for (int i = 0; i < UploadRing::kSlots; ++i) cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
+  }
+  const int slot = r.next;
+  r.next = (r.next + 1) % UploadRing::kSlots;
+  if (r.used[slot]) cudaEventSynchronize(r.ev[slot]);
+  int32_t *h = r.host + (size_t)slot * UploadRing::kCap;
+  memcpy(h, src, sizeof(int32_t) * n);
+  cudaStream_t st = hs::as_stream(stream);
+  cudaError_t e = cudaMemcpyAsync(dst, h, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return hs::set_error(HS_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
+  cudaEventRecord(r.ev[slot], st);
+  r.used[slot] = true;
   return HS_OK;
 }
 

@@ -389,10 +389,12 @@ class _RoundBuffers:
         self.p = torch.empty((rows, V), dtype=torch.float64, device=dev)
         self.phat = torch.empty((rows, V), dtype=torch.float64, device=dev)
         self.xtok = torch.empty(rows, dtype=torch.int32, device=dev)
-        # retrieval-lane input of an inner round whose catch-up is one token:
-        # [catch-up token, drafted tokens...] -- written in place by the draft
+        # retrieval-lane input of an inner round whose catch-up is 1-2 tokens:
+        # [catch-up tokens, drafted tokens...] -- written in place by the draft
         # lane's steps, so the retrieval forward needs no concatenation
-        self.rtok = torch.empty(gamma1 + 1, dtype=torch.int32, device=dev)
+        self.rtok = torch.empty(gamma1 + 2, dtype=torch.int32, device=dev)
+        # the full lane's input of an outer round: [catch-up tokens, x_hat]
+        self.ftok = torch.empty(rows + 2, dtype=torch.int32, device=dev)
         self.res = torch.zeros(rows + 4, dtype=torch.int32, device=dev)
         self.host = torch.zeros(rows + 5, dtype=torch.int32, pin_memory=True)
 
@@ -411,23 +413,28 @@ def _readback(buf: _RoundBuffers, n: int, us: UniformStream):
 
 
 def _draft_round_dev(lane: Lane, seq: Sequence[int], gamma1: int, T: float, us: UniformStream,
-                     buf: _RoundBuffers, fused: bool = False) -> torch.Tensor:
+                     buf: _RoundBuffers, fused: int = 0) -> torch.Tensor:
     """draft_round (speculation.py:211-227) with tokens and q rows on device;
-    returns the device tensor holding the drafted tokens.  fused: the
-    catch-up is one token, also written to buf.rtok[0], and the drafts go to
-    buf.rtok[1:] (the retrieval lane's whole input, in place)."""
+    returns the device tensor holding the drafted tokens.  fused = k > 0: the
+    lane's catch-up is the last k tokens of seq, also written to buf.rtok[:k],
+    and the drafts go to buf.rtok[k:] (the retrieval lane's whole input, in
+    place)."""
     graphs = USE_GRAPHS and isinstance(lane.cache, StreamingCache)
-    fused = fused and graphs and lane.frontier + 1 == len(seq)
-    if graphs and lane.frontier + 1 == len(seq):
-        # the usual one-token catch-up
-        lane.step_graph_run(seq[len(seq) - 1:][0], also=buf.rtok.data_ptr() if fused else None)
+    k = len(seq) - lane.frontier
+    fused = fused if (fused and graphs and k == fused) else 0
+    if graphs and 1 <= k <= 2:
+        # the usual one- or two-token catch-up, one graph step per token
+        rp = buf.rtok.data_ptr()
+        tail = list(seq[len(seq) - k:])
+        for i in range(k):
+            lane.step_graph_run(tail[i], also=rp + 4 * i if fused else None)
     else:
         lane.catch_up(seq)
     if not lane._has_front:
         raise ContractError("lane has no frontier logits; advance over committed tokens first")
     V = buf.V
     s = stream_ptr()
-    dtok = buf.rtok[1:] if fused else buf.dtok
+    dtok = buf.rtok[fused:fused + gamma1] if fused else buf.dtok
     if graphs:
         # sample -> write token + positions into the step graph's slot -> graph,
         # one native call per drafted token
@@ -475,16 +482,19 @@ def _chain_dev(tokens_dev, n, qd, pd, V, us, buf):
 
 def _inner_round_dev(retr: Lane, draft: Lane, seq, cfg: SpecConfig, us, buf, phat_off: int):
     V = buf.V
-    # both lanes sit at the same frontier: a one-token catch-up is the usual case
-    fused = retr.frontier + 1 == len(seq)
+    # both lanes sit at the same frontier: a one- (two-, after an all-accept
+    # outer round) token catch-up is the usual case
+    k = len(seq) - retr.frontier
+    fused = k if (1 <= k <= 2 and draft.frontier == retr.frontier) else 0
     with _nvtx("inner.draft_round"):
         dtok = _draft_round_dev(draft, seq, cfg.gamma1, cfg.temperature, us, buf, fused=fused)
     with _nvtx("inner.retrieval_score"):
         if dtok.data_ptr() != buf.dtok.data_ptr():
-            # buf.rtok = [catch-up, drafts]: one forward, gamma1 + 1 rows
+            # buf.rtok = [catch-up, drafts]: one forward, rows k-1 .. k-1+gamma1
             n = cfg.gamma1
-            logits = retr._forward(buf.rtok)
-            check(lib.hs_probs(logits.data_ptr(), n + 1, V, float(cfg.temperature), buf.p.data_ptr(), stream_ptr()))
+            logits = retr._forward(buf.rtok[:fused + n])
+            check(lib.hs_probs(logits.data_ptr() + 4 * V * (fused - 1), n + 1, V, float(cfg.temperature),
+                               buf.p.data_ptr(), stream_ptr()))
         else:
             _score_rows_dev(retr, seq, dtok, cfg.temperature, buf.p)
     with _nvtx("inner.verify_chain"):
@@ -703,10 +713,26 @@ class HierarchicalSession:
             n = len(x_hat)
             us.ensure(n + 2, cursor)
             with _nvtx("outer.verify"):
-                buf.xtok[:n].copy_(to_i32_device(x_hat))
-                COUNTERS["h2d_bytes"] += 4 * n
-                _score_rows_dev(self.full_lane, self.committed, buf.xtok[:n], cfg.temperature, buf.p)
-                _chain_dev(buf.xtok[:n], n, buf.phat, buf.p, V, us, buf)
+                # [catch-up, x_hat] in one upload, one forward
+                full = self.full_lane
+                cu = self.committed[full.frontier:]
+                k = len(cu)
+                toks = np.asarray(cu + x_hat, dtype=np.int32)
+                s = stream_ptr()
+                check(lib.hs_upload_i32(buf.ftok.data_ptr(), toks.ctypes.data, k + n, s))
+                COUNTERS["h2d_bytes"] += 4 * (k + n)
+                if k:
+                    logits = full._forward(buf.ftok[:k + n])
+                    check(lib.hs_probs(logits.data_ptr() + 4 * V * (k - 1), n + 1, V, float(cfg.temperature),
+                                       buf.p.data_ptr(), s))
+                else:
+                    if not full._has_front:
+                        raise ContractError("lane has no frontier logits; advance over committed tokens first")
+                    check(lib.hs_probs(full._front.data_ptr(), 1, V, float(cfg.temperature), buf.p.data_ptr(), s))
+                    logits = full._forward(buf.ftok[:n])
+                    check(lib.hs_probs(logits.data_ptr(), n, V, float(cfg.temperature), buf.p.data_ptr() + 8 * V, s))
+                xt = buf.ftok[k:k + n]
+                _chain_dev(xt, n, buf.phat, buf.p, V, us, buf)
                 emitted, accepted, cursor = _readback(buf, n, us)
             olabels = ["accepted"] * accepted + (["corrected"] if accepted < n else ["bonus"])
             trace.outer.rounds += 1
