@@ -222,6 +222,7 @@ struct GemvTcArgs {
   float *partial;     // [ks][n_tiles*128][8]
   int *counters;      // [n_tiles]
   int trig_late;      // signal programmatic launch completion after the last weight load is issued
+  int l2pf;           // experiment hook: weight tiles past the ring prefetched to L2 before the dependency wait
   int keep_l2;        // weights loaded evict-last (a small model re-read every step) instead of evict-first
 };
 
@@ -376,6 +377,8 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
         tc::mbar_expect_tx(&full[i], TC_W_BYTES + TC_X_BYTES);
         tc::tma_load_2d_hint(sW + i * TC_W_BYTES, &tmW, &full[i], (kb0 + i) * TC_BK, tile * TC_BM, pol);
       }
+      for (int i = npre; i < nk && i < npre + a.l2pf; ++i)   // experiment hook (HS_GEMV_L2PF)
+        tc::tma_prefetch_l2_2d(&tmW, (kb0 + i) * TC_BK, tile * TC_BM);
       tc::grid_dep_wait();
       HS_TRACE_RESTART
       GPH_STAMP(2)
@@ -733,6 +736,8 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   static const int trig_late = getenv("HS_GEMV_TRIG") ? atoi(getenv("HS_GEMV_TRIG")) : 1;
   a.trig_late = trig_late;
   a.keep_l2 = g_gemv_keep_l2;
+  static const int l2pf = getenv("HS_GEMV_L2PF") ? atoi(getenv("HS_GEMV_L2PF")) : 0;
+  a.l2pf = l2pf;
   a.counters = reinterpret_cast<int *>(ws);
   a.partial = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + (size_t)TC_COUNTER_INTS * 4);
   static bool attr_set = false;
