@@ -69,6 +69,10 @@ typedef struct {
   const uint16_t *wdown;      /* [L][d][ld_ff]                         */
   const float *rope_cos;      /* [max_seq][dh/2] fp32 (tensor.py:66-76)*/
   const float *rope_sin;
+  int blocked;         /* weight layout: bit 0 -- wqkv / wo / wgu / wdown,
+                          bit 1 -- head, stored tile-blocked: [N/128][ld/64]
+                          [128][64] (every 128 x 64 GEMV tile one contiguous
+                          16 KB block; N a multiple of 128); 0 = row-major  */
 } HsModel;
 
 /* ---- KV cache descriptor ------------------------------------------------
@@ -259,6 +263,10 @@ int hs_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int
  * ldk >= ldw, K = ldw a multiple of 64) and w bf16 [n][ldw]; all three planes
  * accumulate into one fp32 accumulator (model.py:281-285,316-328 matmuls for
  * long prompts).  accumulate = 1 adds into y (residual updates).             */
+/* row-major [N][ld] bf16 -> tile-blocked [N/128][ld/64][128][64] in place
+ * (tmp: N x ld scratch), or back (inverse = 1); N % 128 == 0, ld % 64 == 0 */
+int hs_weights_block(uint16_t *w, uint16_t *tmp, int N, int ld, int inverse, void *stream);
+
 int hs_gemm3_tc(const uint16_t *s0, const uint16_t *s1, const uint16_t *s2, int ldk, int rows,
                 const uint16_t *w, int ldw, int n, float *y, int ldy, int accumulate, void *stream);
 

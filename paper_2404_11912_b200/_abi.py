@@ -43,7 +43,8 @@ class HsModel(C.Structure):
                 ("d_ff", i32), ("vocab_size", i32), ("max_seq", i32), ("d_model", i32),
                 ("ld_d", i32), ("ld_ff", i32), ("norm_eps", f32),
                 ("emb", vp), ("head", vp), ("final_norm", vp), ("attn_norm", vp), ("mlp_norm", vp),
-                ("wqkv", vp), ("wo", vp), ("wgu", vp), ("wdown", vp), ("rope_cos", vp), ("rope_sin", vp)]
+                ("wqkv", vp), ("wo", vp), ("wgu", vp), ("wdown", vp), ("rope_cos", vp), ("rope_sin", vp),
+                ("blocked", i32)]
 
 
 class HsCache(C.Structure):
@@ -105,6 +106,7 @@ _SIGS = {
     "hs_draft_step": (i32, [vp, i32, f64, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp]),
     "hs_graph_step": (i32, [vp, i32, i32, i32, vp, vp, i32, vp]),
     "hs_upload_i32": (i32, [vp, vp, i32, vp]),
+    "hs_weights_block": (i32, [vp, vp, i32, i32, i32, vp]),
     "hs_verify_chain": (i32, [vp, i32, vp, vp, i32, vp, vp, vp, vp]),
     "hs_verify_token": (i32, [i32, vp, vp, vp, vp, vp, vp]),
     "hs_correct_token": (i32, [vp, vp, i32, vp, vp, vp, vp]),

@@ -65,7 +65,7 @@ int launch_split_rows(const float *x, int ldx, int t, int K, int ldk, const floa
                       cudaStream_t st);
 int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                    uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st,
-                   const GemvNorm *norm = nullptr, const float *yin = nullptr, int ldyin = 0);
+                   const GemvNorm *norm = nullptr, const float *yin = nullptr, int ldyin = 0, int blocked = 0);
 int launch_norm_prep(const float *x, int ldx, int t, int K, const float *gain, uint16_t *xs, int ldk,
                      cudaStream_t st);
 size_t gemv_tc_ws_bytes(int N, int nkb);
@@ -387,11 +387,11 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
         const int wm = tp_wmax(nqkv, tp->world);
         if (n > 0)
           HS_TRY(launch_gemv_tc(w.xd, t, wqkv + (size_t)r0 * m->ld_d, m->ld_d, n, 0, (float *)w.tsend, wm, nullptr,
-                                0, w.gemv_ws, w.gemv_bytes, s, &in_qkv));
+                                0, w.gemv_ws, w.gemv_bytes, s, &in_qkv, nullptr, 0, m->blocked & 1));
         HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, nqkv, 0, w.qkv, nqkv, s));
       } else {
         HS_TRY(launch_gemv_tc(w.xd, t, wqkv, m->ld_d, nqkv, 0, w.qkv, nqkv, nullptr, 0, w.gemv_ws, w.gemv_bytes, s,
-                              &in_qkv));
+                              &in_qkv, nullptr, 0, m->blocked & 1));
       }
       if (fuse_rope) {
         // RoPE + K/V append inside the tensor-core attention (its q staging
@@ -436,7 +436,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
         wm = tp_wmax(d, tp->world);
         if (n > 0)
           HS_TRY(launch_gemv_tc(w.xa, t, wo + (size_t)r0 * m->ld_d, m->ld_d, n, 1, (float *)w.tsend, wm, nullptr, 0,
-                                w.gemv_ws, w.gemv_bytes, s, nullptr, w.x + r0, d));
+                                w.gemv_ws, w.gemv_bytes, s, nullptr, w.x + r0, d, m->blocked & 1));
         HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, d, 0, w.x, d, s));
         HS_TRY(launch_norm_prep(w.x, d, t, d, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d, s));
         // gate|up: SwiGLU act block (split operand rows) -> all ranks
@@ -444,24 +444,24 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
         wm = tp_wmax(2 * ff, tp->world);
         if (n > 0)
           HS_TRY(launch_gemv_tc(w.xd, t, wgu + (size_t)r0 * m->ld_d, m->ld_d, n, 2, nullptr, 0, (uint16_t *)w.tsend,
-                                wm / 2, w.gemv_ws, w.gemv_bytes, s, &in_gu));
+                                wm / 2, w.gemv_ws, w.gemv_bytes, s, &in_gu, nullptr, 0, m->blocked & 1));
         HS_TRY(tp_exchange(tp, w.tsend, w.trecv, 3 * 8, wm / 2, 2, 2 * ff, 1, w.xf, m->ld_ff, s));
         // w_down: residual block -> all ranks; next norm operand rebuilt
         tp_rows(d, tp->rank, tp->world, r0, n);
         wm = tp_wmax(d, tp->world);
         if (n > 0)
           HS_TRY(launch_gemv_tc(w.xf, t, wdn + (size_t)r0 * m->ld_ff, m->ld_ff, n, 1, (float *)w.tsend, wm, nullptr,
-                                0, w.gemv_ws, w.gemv_bytes, s, nullptr, w.x + r0, d));
+                                0, w.gemv_ws, w.gemv_bytes, s, nullptr, w.x + r0, d, m->blocked & 1));
         HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, d, 0, w.x, d, s));
         HS_TRY(launch_norm_prep(w.x, d, t, d, gain_next, w.xd, m->ld_d, s));
         continue;
       }
       GemvNorm out_wo = {nullptr, 0, 1, 0.f, m->mlp_norm + (size_t)l * d, w.xd, m->ld_d};
-      HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo));
+      HS_TRY(launch_gemv_tc(w.xa, t, wo, m->ld_d, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_wo, nullptr, 0, m->blocked & 1));
       HS_TRY(launch_gemv_tc(w.xd, t, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes, s,
-                            &in_gu));
+                            &in_gu, nullptr, 0, m->blocked & 1));
       GemvNorm out_dn = {nullptr, 0, 1, 0.f, gain_next, w.xd, m->ld_d};
-      HS_TRY(launch_gemv_tc(w.xf, t, wdn, m->ld_ff, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_dn));
+      HS_TRY(launch_gemv_tc(w.xf, t, wdn, m->ld_ff, d, 1, w.x, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &out_dn, nullptr, 0, m->blocked & 1));
     }
     GemvNorm in_head = {w.x, d, d, eps, nullptr, nullptr, 0};
     if (tp) {
@@ -470,12 +470,12 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       const int wm = tp_wmax(m->vocab_size, tp->world);
       if (n > 0)
         HS_TRY(launch_gemv_tc(w.xd, t, m->head + (size_t)r0 * m->ld_d, m->ld_d, n, 0, (float *)w.tsend, wm, nullptr,
-                              0, w.gemv_ws, w.gemv_bytes, s, &in_head));
+                              0, w.gemv_ws, w.gemv_bytes, s, &in_head, nullptr, 0, (m->blocked >> 1) & 1));
       HS_TRY(tp_exchange(tp, w.tsend, w.trecv, t, wm, 4, m->vocab_size, 0, logits, m->vocab_size, s));
       return HS_OK;
     }
     HS_TRY(launch_gemv_tc(w.xd, t, m->head, m->ld_d, m->vocab_size, 0, logits, m->vocab_size, nullptr, 0, w.gemv_ws,
-                          w.gemv_bytes, s, &in_head));
+                          w.gemv_bytes, s, &in_head, nullptr, 0, (m->blocked >> 1) & 1));
     return HS_OK;
   }
   // ---- several row blocks (prefill-sized batches through the decode path):
@@ -494,7 +494,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       const GemvNorm in_n = {w.x + (size_t)r0 * d, d, d, eps, nullptr, nullptr, 0};
       HS_TRY(launch_norm_prep(w.x + (size_t)r0 * d, d, tp, d, an, w.xd, m->ld_d, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wqkv, m->ld_d, nqkv, 0, w.qkv + (size_t)r0 * nqkv, nqkv, nullptr, 0, w.gemv_ws,
-                            w.gemv_bytes, s, &in_n));
+                            w.gemv_bytes, s, &in_n, nullptr, 0, m->blocked & 1));
     }
     HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
     if (sharded) {
@@ -514,11 +514,13 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       float *xr = w.x + (size_t)r0 * d;
       const GemvNorm in_n = {xr, d, d, eps, nullptr, nullptr, 0};
       HS_TRY(launch_split_rows(w.attn + (size_t)r0 * d, d, tp, d, m->ld_d, nullptr, 0.f, w.xd, s));
-      HS_TRY(launch_gemv_tc(w.xd, tp, wo, m->ld_d, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
+      HS_TRY(launch_gemv_tc(w.xd, tp, wo, m->ld_d, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, nullptr, nullptr,
+                            0, m->blocked & 1));
       HS_TRY(launch_norm_prep(xr, d, tp, d, mn, w.xd, m->ld_d, s));
       HS_TRY(launch_gemv_tc(w.xd, tp, wgu, m->ld_d, 2 * ff, 2, nullptr, 0, w.xf, m->ld_ff, w.gemv_ws, w.gemv_bytes, s,
-                            &in_n));
-      HS_TRY(launch_gemv_tc(w.xf, tp, wdn, m->ld_ff, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s));
+                            &in_n, nullptr, 0, m->blocked & 1));
+      HS_TRY(launch_gemv_tc(w.xf, tp, wdn, m->ld_ff, d, 1, xr, d, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, nullptr,
+                            nullptr, 0, m->blocked & 1));
     }
   }
   for (int r0 = 0; r0 < t; r0 += 8) {
@@ -526,7 +528,8 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     const GemvNorm in_n = {w.x + (size_t)r0 * d, d, d, eps, nullptr, nullptr, 0};
     HS_TRY(launch_norm_prep(w.x + (size_t)r0 * d, d, tp, d, m->final_norm, w.xd, m->ld_d, s));
     HS_TRY(launch_gemv_tc(w.xd, tp, m->head, m->ld_d, m->vocab_size, 0, logits + (size_t)r0 * m->vocab_size,
-                          m->vocab_size, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &in_n));
+                          m->vocab_size, nullptr, 0, w.gemv_ws, w.gemv_bytes, s, &in_n, nullptr, 0,
+                          (m->blocked >> 1) & 1));
   }
 #undef HS_TRY
   return HS_OK;

@@ -46,6 +46,7 @@ struct GemmArgs {
   int n_mt, n_nt, tiles;
   float *y;
   int ldy, accumulate;
+  int blocked;             // W tile-blocked [N/128][K/64][128][64] (HsModel.blocked): loaded as 3 x 64-row boxes
 };
 
 __global__ void __launch_bounds__(GM_THREADS, 1) gemm3_tc_kernel(const __grid_constant__ CUtensorMap tA0,
@@ -94,7 +95,16 @@ __global__ void __launch_bounds__(GM_THREADS, 1) gemm3_tc_kernel(const __grid_co
           tc::tma_load_2d(st, &tA0, &full[s], ks * GM_KS, mt * GM_M);
           tc::tma_load_2d(st + GM_A, &tA1, &full[s], ks * GM_KS, mt * GM_M);
           tc::tma_load_2d(st + 2 * GM_A, &tA2, &full[s], ks * GM_KS, mt * GM_M);
-          tc::tma_load_2d(st + 3 * GM_A, &tW, &full[s], ks * GM_KS, nt * GM_BN);
+          if (a.blocked) {
+            // the 192 weight rows of this tile as three 64-row halves of 128-row blocks
+#pragma unroll
+            for (int c = 0; c < GM_BN / 64; ++c) {
+              const int r = nt * GM_BN + c * 64;
+              tc::tma_load_2d(st + 3 * GM_A + c * 64 * 128, &tW, &full[s], 0, ((r >> 7) * a.nk + ks) * 128 + (r & 127));
+            }
+          } else {
+            tc::tma_load_2d(st + 3 * GM_A, &tW, &full[s], ks * GM_KS, nt * GM_BN);
+          }
         }
       }
     }
@@ -176,21 +186,26 @@ __global__ void __launch_bounds__(GM_THREADS, 1) gemm3_tc_kernel(const __grid_co
 // Y[R][N] (ldy) (+)= W[N][ld] . (s0 + s1 + s2)[R][ld]^T with the split planes
 // at row stride ldk (elements); fp32 accumulate in TMEM
 int launch_gemm3_tc(const uint16_t *s0, const uint16_t *s1, const uint16_t *s2, int ldk, int R, const uint16_t *W,
-                    int ld, int N, float *Y, int ldy, int accumulate, cudaStream_t st) {
+                    int ld, int N, float *Y, int ldy, int accumulate, cudaStream_t st, int blocked) {
   HS_REQUIRE(ld % GM_KS == 0 && ldk >= ld && R >= 1 && N >= 1, HS_ERR_SHAPE, "gemm3_tc: bad shape (ld %d, ldk %d)", ld,
              ldk);
+  HS_REQUIRE(!blocked || N % 128 == 0, HS_ERR_SHAPE, "gemm3_tc: a blocked W needs N %% 128 == 0 (N %d)", N);
   CUtensorMap m0, m1, m2, mw;
   int rc;
   if ((rc = get_tmap_bf16(s0, ld, R, (uint64_t)ldk * 2, GM_M, &m0)) != HS_OK) return rc;
   if ((rc = get_tmap_bf16(s1, ld, R, (uint64_t)ldk * 2, GM_M, &m1)) != HS_OK) return rc;
   if ((rc = get_tmap_bf16(s2, ld, R, (uint64_t)ldk * 2, GM_M, &m2)) != HS_OK) return rc;
-  if ((rc = get_tmap_bf16(W, ld, N, (uint64_t)ld * 2, GM_BN, &mw)) != HS_OK) return rc;
+  if (blocked) {
+    if ((rc = get_tmap_bf16(W, GM_KS, (uint64_t)N * (ld / GM_KS), GM_KS * 2, 64, &mw)) != HS_OK) return rc;
+  } else if ((rc = get_tmap_bf16(W, ld, N, (uint64_t)ld * 2, GM_BN, &mw)) != HS_OK) {
+    return rc;
+  }
   GemmArgs a;
   a.R = R; a.N = N; a.nk = ld / GM_KS;
   a.n_mt = ceil_div(R, GM_M);
   a.n_nt = ceil_div(N, GM_BN);
   a.tiles = a.n_mt * a.n_nt;
-  a.y = Y; a.ldy = ldy; a.accumulate = accumulate;
+  a.y = Y; a.ldy = ldy; a.accumulate = accumulate; a.blocked = blocked;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM);
@@ -208,5 +223,5 @@ int launch_gemm3_tc(const uint16_t *s0, const uint16_t *s1, const uint16_t *s2, 
 
 extern "C" int hs_gemm3_tc(const uint16_t *s0, const uint16_t *s1, const uint16_t *s2, int ldk, int rows,
                            const uint16_t *w, int ldw, int n, float *y, int ldy, int accumulate, void *stream) {
-  return hs::launch_gemm3_tc(s0, s1, s2, ldk, rows, w, ldw, n, y, ldy, accumulate, hs::as_stream(stream));
+  return hs::launch_gemm3_tc(s0, s1, s2, ldk, rows, w, ldw, n, y, ldy, accumulate, hs::as_stream(stream), 0);
 }

@@ -222,6 +222,7 @@ struct GemvTcArgs {
   float *partial;     // [ks][n_tiles*128][8]
   int *counters;      // [n_tiles]
   int trig_late;      // signal programmatic launch completion after the last weight load is issued
+  int blocked;        // weights stored tile-blocked [N/128][K/64][128][64] (HsModel.blocked)
   int l2pf;           // experiment hook: weight tiles past the ring prefetched to L2 before the dependency wait
   int keep_l2;        // weights loaded evict-last (a small model re-read every step) instead of evict-first
 };
@@ -375,7 +376,8 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
       const int npre = nk < TC_STAGES ? nk : TC_STAGES;
       for (int i = 0; i < npre; ++i) {
         tc::mbar_expect_tx(&full[i], TC_W_BYTES + TC_X_BYTES);
-        tc::tma_load_2d_hint(sW + i * TC_W_BYTES, &tmW, &full[i], (kb0 + i) * TC_BK, tile * TC_BM, pol);
+        if (a.blocked) tc::tma_load_2d_hint(sW + i * TC_W_BYTES, &tmW, &full[i], 0, (tile * a.nkb + kb0 + i) * TC_BM, pol);
+        else tc::tma_load_2d_hint(sW + i * TC_W_BYTES, &tmW, &full[i], (kb0 + i) * TC_BK, tile * TC_BM, pol);
       }
       for (int i = npre; i < nk && i < npre + a.l2pf; ++i)   // experiment hook (HS_GEMV_L2PF)
         tc::tma_prefetch_l2_2d(&tmW, (kb0 + i) * TC_BK, tile * TC_BM);
@@ -389,7 +391,8 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
         tc::mbar_wait(&empty[s], ph ^ 1);
         tc::mbar_expect_tx(&full[s], TC_W_BYTES + TC_X_BYTES);
         const int k = (kb0 + i) * TC_BK;
-        tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], k, tile * TC_BM, pol);
+        if (a.blocked) tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], 0, (tile * a.nkb + kb0 + i) * TC_BM, pol);
+        else tc::tma_load_2d_hint(sW + s * TC_W_BYTES, &tmW, &full[s], k, tile * TC_BM, pol);
         tc::tma_load_2d(sX + s * TC_X_BYTES, &tmX, &full[s], k, 0);
       }
       if (a.trig_late) tc::grid_dep_launch();
@@ -698,7 +701,7 @@ void gemv_set_keep_l2(int keep) { g_gemv_keep_l2 = keep; }
 // y (+)= W . x for one pass of <= 8 rows whose split operand is in xs [24][ldw]
 int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                    uint16_t *xs_out, int ld_xs_out, void *ws, size_t ws_bytes, cudaStream_t st,
-                   const GemvNorm *norm, const float *yin, int ldyin) {
+                   const GemvNorm *norm, const float *yin, int ldyin, int blocked) {
   HS_REQUIRE(t >= 1 && t <= TC_T, HS_ERR_SHAPE, "gemv_tc: t=%d outside [1,%d]", t, TC_T);
   HS_REQUIRE(ldw % TC_BK == 0, HS_ERR_SHAPE, "gemv_tc: ldw %d not a multiple of %d", ldw, TC_BK);
   HS_REQUIRE(((uintptr_t)w % 16) == 0 && ((uintptr_t)xs % 16) == 0, HS_ERR_VALUE, "gemv_tc: operands must be 16B aligned");
@@ -709,12 +712,16 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   HS_REQUIRE(tiles <= TC_COUNTER_INTS, HS_ERR_SHAPE, "gemv_tc: N too large");
   HS_REQUIRE(ws_bytes >= gemv_tc_ws_bytes(N, nkb), HS_ERR_VALUE, "gemv_tc: workspace too small");
   CUtensorMap mw, mx;
-  int rc = get_tmap_bf16(w, (uint64_t)ldw, (uint64_t)N, (uint64_t)ldw * 2, TC_BM, &mw);
+  HS_REQUIRE(!blocked || N % TC_BM == 0, HS_ERR_SHAPE, "gemv_tc: a blocked matrix needs N %% 128 == 0 (N %d)", N);
+  const bool blk = blocked != 0;
+  int rc = blk ? get_tmap_bf16(w, (uint64_t)TC_BK, (uint64_t)N * nkb, (uint64_t)TC_BK * 2, TC_BM, &mw)
+               : get_tmap_bf16(w, (uint64_t)ldw, (uint64_t)N, (uint64_t)ldw * 2, TC_BM, &mw);
   if (rc != HS_OK) return rc;
   rc = get_tmap_bf16(xs, (uint64_t)ldw, (uint64_t)TC_XN, (uint64_t)ldw * 2, TC_XN, &mx);
   if (rc != HS_OK) return rc;
   GemvTcArgs a;
   a.N = N; a.nkb = nkb; a.ks = gemv_tc_ksplit(N, nkb); a.t = t; a.epilogue = epilogue; a.n_tiles = tiles;
+  a.blocked = blk ? 1 : 0;
   a.cluster = (a.ks > 1 && a.ks <= 8 && gemv_use_cluster()) ? 1 : 0;
   static const int push_mode = getenv("HS_GEMV_PUSH") ? atoi(getenv("HS_GEMV_PUSH")) : 1;   // A/B hook
   a.nrow = (t <= 4 && push_mode != 2) ? 4 : TC_T;
@@ -774,7 +781,34 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   return check_launch("gemv_tc");
 }
 
+// row-major [N][ld] <-> tile-blocked [N/128][ld/64][128][64] (one 16-byte
+// unit per thread; dst index space)
+__global__ void relayout_blocked_kernel(const uint16_t *src, uint16_t *dst, int N, int ld, int inverse) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nkb = ld / 64;
+  const size_t total = (size_t)N * ld / 8;
+  if (i >= total) return;
+  const size_t e = i * 8;   // element of the blocked layout
+  const int c = (int)(e % 64);
+  const size_t r_in_tile = (e / 64) % 128;
+  const size_t kb = (e / (64 * 128)) % nkb;
+  const size_t tile = e / ((size_t)64 * 128 * nkb);
+  const size_t rm = (tile * 128 + r_in_tile) * ld + kb * 64 + c;   // element of the row-major layout
+  if (inverse) *reinterpret_cast<uint4 *>(dst + rm) = *reinterpret_cast<const uint4 *>(src + e);
+  else *reinterpret_cast<uint4 *>(dst + e) = *reinterpret_cast<const uint4 *>(src + rm);
+}
+
 }  // namespace hs
+
+extern "C" int hs_weights_block(uint16_t *w, uint16_t *tmp, int N, int ld, int inverse, void *stream) {
+  HS_REQUIRE(N % 128 == 0 && ld % 64 == 0 && N > 0, HS_ERR_SHAPE, "weights_block: N %d / ld %d", N, ld);
+  const size_t units = (size_t)N * ld / 8;
+  cudaStream_t st = hs::as_stream(stream);
+  cudaError_t e = cudaMemcpyAsync(tmp, w, (size_t)N * ld * 2, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return hs::set_error(HS_ERR_CUDA, "weights_block: %s", cudaGetErrorString(e));
+  hs::relayout_blocked_kernel<<<(unsigned)((units + 255) / 256), 256, 0, st>>>(tmp, w, N, ld, inverse);
+  return hs::check_launch("weights_block");
+}
 
 extern "C" size_t hs_gemv_tc_workspace_bytes(int N, int ldw) { return hs::gemv_tc_ws_bytes(N, ldw / hs::TC_BK); }
 
@@ -786,5 +820,5 @@ extern "C" int hs_split_rows(const float *x, int ldx, int t, int K, int ldk, con
 extern "C" int hs_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N, int epilogue, float *y, int ldy,
                           uint16_t *xs_out, int ld_xs_out, void *workspace, size_t ws_bytes, void *stream) {
   return hs::launch_gemv_tc(xs, t, w, ldw, N, epilogue, y, ldy, xs_out, ld_xs_out, workspace, ws_bytes,
-                            hs::as_stream(stream), nullptr, nullptr, 0);
+                            hs::as_stream(stream), nullptr, nullptr, 0, 0);
 }

@@ -29,7 +29,7 @@ int launch_shard_merge(const float *parts, int G, int rows, int DH, float *out, 
                        cudaStream_t st);
 int shard_all_gather(const HsShard *sh, const void *send, void *recv, size_t bytes, cudaStream_t st);
 int launch_gemm3_tc(const uint16_t *s0, const uint16_t *s1, const uint16_t *s2, int ldk, int R, const uint16_t *W,
-                    int ld, int N, float *Y, int ldy, int accumulate, cudaStream_t st);
+                    int ld, int N, float *Y, int ldy, int accumulate, cudaStream_t st, int blocked);
 
 namespace {
 
@@ -119,8 +119,9 @@ size_t carve(const HsModel *m, int t, int n_view, int split, int world, char *ba
 
 // Y[R][N] (ldy) (+)= W[N][ld] . (s0 + s1 + s2)[R][ld]^T, fp32 accumulate (tcgen05)
 // (split_rows_n wrote the planes at row stride ld)
-int gemm3(const uint16_t *W, int ld, int N, const PfWs &w, int R, int accumulate, float *Y, int ldy, cudaStream_t s) {
-  return launch_gemm3_tc(w.s0, w.s1, w.s2, ld, R, W, ld, N, Y, ldy, accumulate, s);
+int gemm3(const uint16_t *W, int ld, int N, const PfWs &w, int R, int accumulate, float *Y, int ldy, cudaStream_t s,
+          int blocked) {
+  return launch_gemm3_tc(w.s0, w.s1, w.s2, ld, R, W, ld, N, Y, ldy, accumulate, s, blocked);
 }
 
 int split_rows_n(const float *x, int ldx, int R, int K, int ldk, const float *gain, float eps, const PfWs &w,
@@ -190,7 +191,7 @@ static int prefill_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
     for (int r0 = 0; r0 < t; r0 += PF_ROWS) {
       const int R = t - r0 < PF_ROWS ? t - r0 : PF_ROWS;
       HS_TRY(split_rows_n(w.x + (size_t)r0 * d, d, R, d, m->ld_d, an, eps, w, s));
-      HS_TRY(gemm3(wqkv, m->ld_d, nqkv, w, R, 0, w.qkv + (size_t)r0 * nqkv, nqkv, s));
+      HS_TRY(gemm3(wqkv, m->ld_d, nqkv, w, R, 0, w.qkv + (size_t)r0 * nqkv, nqkv, s, m->blocked & 1));
     }
     HS_TRY(launch_rope_append(m, c, st, l, w.qkv, t, w.q, q_stash, s));
     // causal attention: head_dim 128 on the 128-row tensor-core prefill kernel
@@ -226,20 +227,20 @@ static int prefill_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
       const int R = t - r0 < PF_ROWS ? t - r0 : PF_ROWS;
       float *xr = w.x + (size_t)r0 * d;
       HS_TRY(split_rows_n(w.attn + (size_t)r0 * d, d, R, d, m->ld_d, nullptr, 0.f, w, s));
-      HS_TRY(gemm3(wo, m->ld_d, d, w, R, 1, xr, d, s));                  // x += wo . attn
+      HS_TRY(gemm3(wo, m->ld_d, d, w, R, 1, xr, d, s, m->blocked & 1));                  // x += wo . attn
       HS_TRY(split_rows_n(xr, d, R, d, m->ld_d, mn, eps, w, s));
-      HS_TRY(gemm3(wgu, m->ld_d, 2 * ff, w, R, 0, w.gu, 2 * ff, s));
+      HS_TRY(gemm3(wgu, m->ld_d, 2 * ff, w, R, 0, w.gu, 2 * ff, s, m->blocked & 1));
       pf_swiglu_kernel<<<592, 256, 0, s>>>(w.gu, R, ff, w.act);
       HS_TRY(check_launch("prefill swiglu"));
       HS_TRY(split_rows_n(w.act, ff, R, ff, m->ld_ff, nullptr, 0.f, w, s));
-      HS_TRY(gemm3(wdn, m->ld_ff, d, w, R, 1, xr, d, s));                // x += w_down . act
+      HS_TRY(gemm3(wdn, m->ld_ff, d, w, R, 1, xr, d, s, m->blocked & 1));                // x += w_down . act
     }
   }
   for (int r0 = 0; r0 < t; r0 += PF_ROWS) {
     const int R = t - r0 < PF_ROWS ? t - r0 : PF_ROWS;
     HS_TRY(split_rows_n(w.x + (size_t)r0 * d, d, R, d, m->ld_d, m->final_norm, eps, w, s));
     HS_TRY(gemm3(m->head, m->ld_d, m->vocab_size, w, R, 0, logits + (size_t)r0 * m->vocab_size,
-                 m->vocab_size, s));
+                 m->vocab_size, s, (m->blocked >> 1) & 1));
   }
 #undef HS_TRY
   return HS_OK;

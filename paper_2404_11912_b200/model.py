@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import hashlib
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -35,6 +36,12 @@ BOS = 256
 EOS = 257
 PAD = 258
 TOKENIZER_VOCAB = 259
+
+
+# projection matrices stored tile-blocked on the device (HsModel.blocked): every
+# 128 x 64 GEMV / GEMM tile one contiguous 16 KB block, so a CTA's weight stream
+# is sequential in HBM (HS_ROWMAJOR_WEIGHTS=1: row-major, an A/B hook)
+BLOCK_WEIGHTS = os.environ.get("HS_ROWMAJOR_WEIGHTS", "0") != "1"
 
 
 def _pad64(n: int) -> int:
@@ -105,7 +112,10 @@ class DeviceModel:
     Layout (include/hs_abi.h): matrices transposed to [out][in] with the row
     stride padded to 64 elements; wq|wk|wv fused; gate/up rows interleaved
     (gate_i, up_i) so the GEMV's SwiGLU epilogue sees both halves; norms and
-    the rope table stay fp32.
+    the rope table stay fp32.  When every projection has a multiple of 128
+    rows the projections (and an untied lm_head) are then stored tile-blocked
+    ([N/128][ld/64][128][64], `blocked`): each 128 x 64 weight tile a GEMV or
+    GEMM CTA streams is one contiguous 16 KB block.
     """
 
     def __init__(self, config: ModelConfig, tensors, tied_head: bool, rope_scaling=None):
@@ -206,10 +216,50 @@ class DeviceModel:
             u = torch.randint(0, 2, (rows.numel(), d), generator=gen, device=dev).float() * 2.0 - 1.0
             self.emb[rows, :d] = (self.emb[rows, :d].float() + emb_scale * u).to(torch.bfloat16)
             hr = succ[rows]
-            self.head[hr, :d] = (self.head[hr, :d].float() + head_scale * u).to(torch.bfloat16)
+            self._set_head_rows(hr, (self._head_rows(hr)[:, :d].float() + head_scale * u).to(torch.bfloat16))
         self.planted = {"kind": "successor", "easy_frac": easy_frac, "seed": seed, "emb_scale": emb_scale,
                         "margin": margin}
         return self
+
+    def _head_rows(self, rows: torch.Tensor) -> torch.Tensor:
+        """Rows of the lm_head [n, ld] whatever its device layout."""
+        if not (getattr(self, "blocked", 0) & 2):
+            return self.head[rows]
+        ld = self.ld_d
+        hv = self.head.view(-1, ld // 64, 128, 64)
+        return hv[rows // 128, :, rows % 128, :].reshape(rows.numel(), ld)
+
+    def _set_head_rows(self, rows: torch.Tensor, vals: torch.Tensor) -> None:
+        """head[rows, :vals.shape[1]] = vals, whatever its device layout."""
+        if not (getattr(self, "blocked", 0) & 2):
+            self.head[rows, :vals.shape[1]] = vals
+            return
+        full = self._head_rows(rows)
+        full[:, :vals.shape[1]] = vals
+        ld = self.ld_d
+        hv = self.head.view(-1, ld // 64, 128, 64)
+        hv[rows // 128, :, rows % 128, :] = full.view(rows.numel(), ld // 64, 64)
+
+    def _block_weights(self) -> int:
+        """Re-lay the projection matrices (and an untied lm_head) tile-blocked
+        in place (hs_weights_block); returns HsModel.blocked."""
+        cfg = self.config
+        kv = cfg.n_kv_heads * cfg.head_dim
+        if not BLOCK_WEIGHTS or any(n % 128 for n in (cfg.d_model + 2 * kv, cfg.d_model, 2 * cfg.d_ff)):
+            return 0
+        mats = [self.wqkv, self.wo, self.wgu, self.wdown]
+        head = not self.tied_head and cfg.vocab_size % 128 == 0
+        n_tmp = max([m[0].numel() for m in mats] + ([self.head.numel()] if head else []))
+        tmp = torch.empty(n_tmp, dtype=torch.bfloat16, device=self.wqkv.device)
+        s = stream_ptr()
+        for m in mats:
+            for layer in range(m.shape[0]):
+                check(lib.hs_weights_block(m[layer].data_ptr(), tmp.data_ptr(), m.shape[1], m.shape[2], 0, s))
+        if head:
+            check(lib.hs_weights_block(self.head.data_ptr(), tmp.data_ptr(), self.head.shape[0], self.head.shape[1],
+                                       0, s))
+        torch.cuda.current_stream().synchronize()   # (tmp is freed on return)
+        return 1 | (2 if head else 0)
 
     def _finish(self):
         cfg = self.config
@@ -226,6 +276,8 @@ class DeviceModel:
         for name in ("emb", "head", "final_norm", "attn_norm", "mlp_norm", "wqkv", "wo", "wgu", "wdown",
                      "rope_cos", "rope_sin"):
             setattr(s, name, getattr(self, name).data_ptr())
+        self.blocked = self._block_weights()
+        s.blocked = self.blocked
         self.struct = s
         self.ref = C.byref(s)
 

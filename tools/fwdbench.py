@@ -25,7 +25,8 @@ def main():
     a = ap.parse_args()
     import paper_2404_11912_b200 as P
     import bench
-    tw = P.ModelWeights.on_device(P.DeviceModel.random(P.ModelConfig(**bench.TARGET_7B), seed=1))
+    tdm = P.DeviceModel.random(P.ModelConfig(**bench.TARGET_7B), seed=1)
+    tw = P.ModelWeights.on_device(tdm)
     dw = P.ModelWeights.on_device(P.DeviceModel.random(P.ModelConfig(**bench.DRAFT_68M), seed=2))
     ctx = np.random.default_rng(0).integers(1, 32000, a.ctx).tolist()
     spec = P.SpecConfig(target_len=a.ctx + 64, gamma1=2, gamma2=4,
