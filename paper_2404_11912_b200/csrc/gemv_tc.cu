@@ -66,7 +66,7 @@ constexpr int TC_T = 8;           // activation rows per pass
 constexpr int TC_STAGES = HS_TC_STAGES;   // 5 x 19 KB: two CTAs per SM (a GEMV + the next one's prefetch)
 constexpr int TC_W_BYTES = TC_BM * TC_BK * 2;    // 16 KB
 constexpr int TC_X_BYTES = TC_XN * TC_BK * 2;    // 3 KB
-constexpr int TC_SMEM = TC_STAGES * (TC_W_BYTES + TC_X_BYTES) + 1024 + 256;
+constexpr int TC_SMEM = TC_STAGES * (TC_W_BYTES + TC_X_BYTES) + 1024 + 256;   // with the worst-case alignment slack
 // + the split-0 CTA's landing area for the partials of splits 1..ks-1 (cluster split-K)
 constexpr int TC_SMEM_MAX = TC_SMEM + 7 * TC_BM * TC_T * 4;
 constexpr int TC_COUNTER_INTS = 16384;           // per-tile arrival counters at the workspace head
@@ -224,6 +224,7 @@ struct GemvTcArgs {
   int trig_late;      // signal programmatic launch completion after the last weight load is issued
   int blocked;        // weights stored tile-blocked [N/128][K/64][128][64] (HsModel.blocked)
   int l2pf;           // experiment hook: weight tiles past the ring prefetched to L2 before the dependency wait
+  int *align_probe;   // non-null: thread 0 reports the dynamic shared memory's misalignment and the CTA exits
   int keep_l2;        // weights loaded evict-last (a small model re-read every step) instead of evict-first
 };
 
@@ -320,6 +321,10 @@ __global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__
                                                          const __grid_constant__ CUtensorMap tmX, GemvTcArgs a) {
   HS_TRACE_BEGIN
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  if (a.align_probe) {
+    if (threadIdx.x == 0) *a.align_probe = (int)(reinterpret_cast<uintptr_t>(smem_raw) & 1023);
+    return;
+  }
   unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char *sW = base;
   unsigned char *sX = base + TC_STAGES * TC_W_BYTES;
@@ -632,6 +637,37 @@ static int gemv_use_cluster() {
   return on;
 }
 
+// alignment slack the ring needs: 0 when the kernel's dynamic shared memory
+// already starts 1024-byte aligned (probed once per process on every
+// instantiation, outside stream capture), else 1024
+template <int EPI>
+__global__ void __launch_bounds__(128, 2) gemv_tc_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                         const __grid_constant__ CUtensorMap tmX, GemvTcArgs a);
+static int gemv_smem_slack(cudaStream_t st) {
+  static int slack = -1;
+  if (slack >= 0) return slack;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 1024;
+  int *d = nullptr, h[3] = {1, 1, 1};
+  if (cudaMalloc(&d, sizeof(int) * 3) != cudaSuccess) { slack = 1024; return slack; }
+  CUtensorMap m;
+  memset(&m, 0, sizeof(m));
+  void (*kerns[3])(const CUtensorMap, const CUtensorMap, GemvTcArgs) = {gemv_tc_kernel<0>, gemv_tc_kernel<1>,
+                                                                          gemv_tc_kernel<2>};
+  for (int k = 0; k < 3; ++k) {
+    GemvTcArgs a;
+    memset(&a, 0, sizeof(a));
+    a.align_probe = d + k;
+    kerns[k]<<<1, 128, TC_SMEM, st>>>(m, m, a);
+  }
+  cudaMemcpyAsync(h, d, sizeof(int) * 3, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(d);
+  slack = (h[0] == 0 && h[1] == 0 && h[2] == 0) ? 0 : 1024;
+  if (getenv("HS_GEMV_DEBUG")) fprintf(stderr, "gemv_tc: dynamic smem misalignment %d %d %d -> slack %d\n", h[0], h[1], h[2], slack);
+  return slack;
+}
+
 // dynamic shared memory one GEMV CTA may use while two fit per SM (a GEMV
 // and its programmatic dependent's prefetching CTA)
 static int gemv_smem_budget() {
@@ -726,7 +762,15 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   static const int push_mode = getenv("HS_GEMV_PUSH") ? atoi(getenv("HS_GEMV_PUSH")) : 1;   // A/B hook
   a.nrow = (t <= 4 && push_mode != 2) ? 4 : TC_T;
   const int land = a.cluster ? (a.ks - 1) * TC_BM * a.nrow * 4 : 0;
-  a.push = (a.cluster && push_mode && (push_mode == 2 || TC_SMEM + land <= gemv_smem_budget())) ? 1 : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemv_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
+    cudaFuncSetAttribute(gemv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
+    cudaFuncSetAttribute(gemv_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
+    attr_set = true;
+  }
+  const int smem_base = TC_SMEM - 1024 + gemv_smem_slack(st);
+  a.push = (a.cluster && push_mode && (push_mode == 2 || smem_base + land <= gemv_smem_budget())) ? 1 : 0;
   a.y = y; a.ldy = ldy; a.xs_out = xs_out; a.ld_xs_out = ld_xs_out;
   a.yin = yin; a.ldyin = ldyin;
   a.x_in = nullptr; a.ldx_in = 0; a.norm_K = 1; a.eps = 0.f;
@@ -742,22 +786,16 @@ int launch_gemv_tc(const uint16_t *xs, int t, const uint16_t *w, int ldw, int N,
   // dependent's CTAs then start together; HS_GEMV_TRIG=0: at CTA start)
   static const int trig_late = getenv("HS_GEMV_TRIG") ? atoi(getenv("HS_GEMV_TRIG")) : 1;
   a.trig_late = trig_late;
+  a.align_probe = nullptr;
   a.keep_l2 = g_gemv_keep_l2;
   static const int l2pf = getenv("HS_GEMV_L2PF") ? atoi(getenv("HS_GEMV_L2PF")) : 0;
   a.l2pf = l2pf;
   a.counters = reinterpret_cast<int *>(ws);
   a.partial = reinterpret_cast<float *>(reinterpret_cast<char *>(ws) + (size_t)TC_COUNTER_INTS * 4);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemv_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
-    cudaFuncSetAttribute(gemv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
-    cudaFuncSetAttribute(gemv_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
-    attr_set = true;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles, a.ks, 1);
   cfg.blockDim = dim3(128, 1, 1);
-  cfg.dynamicSmemBytes = TC_SMEM + (a.push ? land : 0);
+  cfg.dynamicSmemBytes = smem_base + (a.push ? land : 0);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   int na = 0;
