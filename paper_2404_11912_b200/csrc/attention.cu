@@ -79,12 +79,21 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
     } else {
       tok_s[tid] = 0; head_s[tid] = 0; qp_s[tid] = -1;
     }
-    m_s[tid] = -INFINITY; l_s[tid] = 0.f;
+    m_s[tid] = -INFINITY; l_s[tid] = 0.f; f_s[tid] = 1.f;
   }
   __syncthreads();
-  for (int e = tid; e < ATT_QROWS * DH; e += ATT_THREADS) {
-    int rr = e / DH, d = e % DH;
-    qs[e] = rr < nrows ? a.q[((size_t)tok_s[rr] * a.H + head_s[rr]) * DH + d] : 0.f;
+  {
+    // every load of the query rows in flight at once (a step's first round
+    // trip), then the shared-memory stores
+    constexpr int QPT = ATT_QROWS * DH / ATT_THREADS;
+    float qv[QPT];
+#pragma unroll
+    for (int u = 0; u < QPT; ++u) {
+      const int e = tid + u * ATT_THREADS, rr = e / DH, d = e % DH;
+      qv[u] = rr < nrows ? a.q[((size_t)tok_s[rr] * a.H + head_s[rr]) * DH + d] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < QPT; ++u) qs[tid + u * ATT_THREADS] = qv[u];
   }
 
   float acc[RPT][2];
@@ -102,15 +111,28 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
     __syncthreads();   // previous tile fully consumed
     // ---- stage K, V (16-byte vectors) and positions ------------------------
     constexpr int VPR = DH / 8;  // 16B vectors per row
-    for (int e = tid; e < ATT_TILE * VPR; e += ATT_THREADS) {
-      int kr = e / VPR, c = e % VPR;
-      uint4 kv4 = make_uint4(0, 0, 0, 0), vv4 = make_uint4(0, 0, 0, 0);
-      if (kr < nk) {
-        kv4 = ld_stream(kbase + (size_t)(tile + kr) * DH + c * 8);
-        vv4 = ld_stream(vbase + (size_t)(tile + kr) * DH + c * 8);
+    constexpr int VPT = (ATT_TILE * VPR + ATT_THREADS - 1) / ATT_THREADS;
+    {
+      // all of this thread's K / V vectors in flight at once, then the stores
+      uint4 kv4[VPT], vv4[VPT];
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int e = tid + u * ATT_THREADS, kr = e / VPR, c = e % VPR;
+        kv4[u] = make_uint4(0, 0, 0, 0);
+        vv4[u] = make_uint4(0, 0, 0, 0);
+        if (e < ATT_TILE * VPR && kr < nk) {
+          kv4[u] = ld_stream(kbase + (size_t)(tile + kr) * DH + c * 8);
+          vv4[u] = ld_stream(vbase + (size_t)(tile + kr) * DH + c * 8);
+        }
       }
-      *reinterpret_cast<uint4 *>(&Ks[kr * KP + c * 8]) = kv4;
-      *reinterpret_cast<uint4 *>(&Vs[kr * DH + c * 8]) = vv4;
+#pragma unroll
+      for (int u = 0; u < VPT; ++u) {
+        const int e = tid + u * ATT_THREADS, kr = e / VPR, c = e % VPR;
+        if (e < ATT_TILE * VPR) {
+          *reinterpret_cast<uint4 *>(&Ks[kr * KP + c * 8]) = kv4[u];
+          *reinterpret_cast<uint4 *>(&Vs[kr * DH + c * 8]) = vv4[u];
+        }
+      }
     }
     if (tid < ATT_TILE) {
       int j = tile + tid;
@@ -149,7 +171,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
     }
     __syncthreads();
     // ---- online softmax: one warp per row -------------------------------------
-    for (int rr = warp; rr < ATT_QROWS; rr += ATT_THREADS / 32) {
+    for (int rr = warp; rr < nrows; rr += ATT_THREADS / 32) {   // (rows past nrows are never written)
       float s0 = S[rr][lane], s1 = S[rr][lane + 32];
       float tmax = warp_max(fmaxf(s0, s1));
       float m_old = m_s[rr];
@@ -181,7 +203,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
           const int rr = rg + NRG * i;
-          if (rr < ATT_QROWS) {
+          if (rr < nrows) {
             const float p = S[rr][key];
             acc[i][0] = fmaf(p, v0, acc[i][0]);
             acc[i][1] = fmaf(p, v1, acc[i][1]);
