@@ -70,6 +70,27 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
   const int r0 = rb * ATT_QROWS;
   const int nrows = min(ATT_QROWS, nrows_total - r0);
 
+  const int s_lo = split * a.split;
+  const int s_hi = min(a.n_view, s_lo + a.split);
+  const uint16_t *kbase = a.k + (size_t)kh * a.cap * DH;
+  const uint16_t *vbase = a.v + (size_t)kh * a.cap * DH;
+  constexpr int VPR = DH / 8;  // 16B vectors per row
+  constexpr int VPT = (ATT_TILE * VPR + ATT_THREADS - 1) / ATT_THREADS;
+  uint4 kv4[VPT], vv4[VPT];
+  // all of this thread's K / V vectors of a tile in flight at once
+  auto load_tile = [&](int tile, int nk) {
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int e = tid + u * ATT_THREADS, kr = e / VPR, c = e % VPR;
+      kv4[u] = make_uint4(0, 0, 0, 0);
+      vv4[u] = make_uint4(0, 0, 0, 0);
+      if (e < ATT_TILE * VPR && kr < nk) {
+        kv4[u] = ld_stream(kbase + (size_t)(tile + kr) * DH + c * 8);
+        vv4[u] = ld_stream(vbase + (size_t)(tile + kr) * DH + c * 8);
+      }
+    }
+  };
+
   // query rows: rr = i*g + gi  ->  token i, head kh*g + gi
   if (tid < ATT_QROWS) {
     int rr = r0 + tid;
@@ -83,8 +104,8 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
   }
   __syncthreads();
   {
-    // every load of the query rows in flight at once (a step's first round
-    // trip), then the shared-memory stores
+    // every load of the query rows and of the first K / V tile in flight at
+    // once (a step's first round trip), then the shared-memory stores
     constexpr int QPT = ATT_QROWS * DH / ATT_THREADS;
     float qv[QPT];
 #pragma unroll
@@ -92,6 +113,8 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
       const int e = tid + u * ATT_THREADS, rr = e / DH, d = e % DH;
       qv[u] = rr < nrows ? a.q[((size_t)tok_s[rr] * a.H + head_s[rr]) * DH + d] : 0.f;
     }
+#pragma unroll
+    if (s_lo < s_hi) load_tile(s_lo, min(ATT_TILE, s_hi - s_lo));   // (the first tile's K / V too)
 #pragma unroll
     for (int u = 0; u < QPT; ++u) qs[tid + u * ATT_THREADS] = qv[u];
   }
@@ -101,30 +124,12 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
   for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = 0.f;
   const int dp = tid % NDP, rg = tid / NDP;
 
-  const int s_lo = split * a.split;
-  const int s_hi = min(a.n_view, s_lo + a.split);
-  const uint16_t *kbase = a.k + (size_t)kh * a.cap * DH;
-  const uint16_t *vbase = a.v + (size_t)kh * a.cap * DH;
-
   for (int tile = s_lo; tile < s_hi; tile += ATT_TILE) {
     const int nk = min(ATT_TILE, s_hi - tile);
     __syncthreads();   // previous tile fully consumed
     // ---- stage K, V (16-byte vectors) and positions ------------------------
-    constexpr int VPR = DH / 8;  // 16B vectors per row
-    constexpr int VPT = (ATT_TILE * VPR + ATT_THREADS - 1) / ATT_THREADS;
+    if (tile != s_lo) load_tile(tile, nk);
     {
-      // all of this thread's K / V vectors in flight at once, then the stores
-      uint4 kv4[VPT], vv4[VPT];
-#pragma unroll
-      for (int u = 0; u < VPT; ++u) {
-        const int e = tid + u * ATT_THREADS, kr = e / VPR, c = e % VPR;
-        kv4[u] = make_uint4(0, 0, 0, 0);
-        vv4[u] = make_uint4(0, 0, 0, 0);
-        if (e < ATT_TILE * VPR && kr < nk) {
-          kv4[u] = ld_stream(kbase + (size_t)(tile + kr) * DH + c * 8);
-          vv4[u] = ld_stream(vbase + (size_t)(tile + kr) * DH + c * 8);
-        }
-      }
 #pragma unroll
       for (int u = 0; u < VPT; ++u) {
         const int e = tid + u * ATT_THREADS, kr = e / VPR, c = e % VPR;
@@ -152,6 +157,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
 #pragma unroll
         for (int i = 0; i < ATT_QROWS / 2; ++i) {
           const int rr = half + 2 * i;
+          if (rr >= nrows) break;   // (warp-uniform: half is a function of the warp)
           const float4 qa = *reinterpret_cast<const float4 *>(&qs[rr * DH + d]);
           const float4 qb = *reinterpret_cast<const float4 *>(&qs[rr * DH + d + 4]);
           float s = dot[i];
@@ -197,6 +203,9 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
         const int rr = rg + NRG * i;
         if (rr < ATT_QROWS) { const float f = f_s[rr]; acc[i][0] *= f; acc[i][1] *= f; }
       }
+      // (unrolled: the shared-memory loads of the next keys issue ahead of
+      // the accumulator chain, which stays in key order)
+#pragma unroll 8
       for (int key = 0; key < nk; ++key) {
         const uint32_t vw = *reinterpret_cast<const uint32_t *>(&Vs[key * DH + 2 * dp]);
         const float v0 = bf16_lo(vw), v1 = bf16_hi(vw);

@@ -12,6 +12,8 @@
 namespace hs {
 
 int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x, cudaStream_t st);
+int launch_embed_norm(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x, const float *gain,
+                      uint16_t *xs, int ldk, cudaStream_t st);
 int launch_rope_append(const HsModel *m, const HsCache *c, const HsStep *s, int layer, const float *qkv, int t,
                        float *q_out, float *q_stash, cudaStream_t st);
 int launch_attention_timed(const HsCache *c, int layer, const HsStep *st, int H, const float *q, int t, float *out,
@@ -372,8 +374,7 @@ static int forward_impl(const HsModel *m, const HsCache *c, const HsStep *st, co
                            dh == 128 && st->dyn == nullptr && st->n_view > 0 &&   // (an empty shard view launches no
                            // attention kernel, so it could not write q_stash / the rows)
                            (st->append_mode == HS_APPEND_POS || st->append_mode == HS_APPEND_LINEAR);
-    HS_TRY(launch_embed(m->emb, m->ld_d, d, tokens, t, w.x, s));
-    HS_TRY(launch_norm_prep(w.x, d, t, d, m->attn_norm, w.xd, m->ld_d, s));
+    HS_TRY(launch_embed_norm(m->emb, m->ld_d, d, tokens, t, w.x, m->attn_norm, w.xd, m->ld_d, s));
     for (int l = 0; l < m->n_layers; ++l) {
       const uint16_t *wqkv = m->wqkv + (size_t)l * nqkv * m->ld_d;
       const uint16_t *wo = m->wo + (size_t)l * d * m->ld_d;

@@ -22,6 +22,36 @@ int launch_embed(const uint16_t *emb, int ld, int d, const int32_t *tokens, int 
   return check_launch("embed");
 }
 
+// embedding rows + the first layer's folded-RMSNorm operand in one kernel
+// (the single-block forward): x[r] = emb[token r] and xs = split(x * gain),
+// norm_prep's arithmetic on the same fp32 values.  grid (tiles of 128
+// columns, t).  A programmatic dependent of the previous forward's last
+// kernel: scheduled while it drains, everything after griddepcontrol.wait
+// (the tokens come from the sampler, x is still read by that kernel).
+__global__ void __launch_bounds__(128) embed_norm_kernel(const uint16_t *emb, int ld, int d, const int32_t *tokens,
+                                                         float *x, const float *gain, uint16_t *xs, int ldk) {
+  HS_TRACE_BEGIN
+  pdl_wait();
+  pdl_trigger();
+  HS_TRACE_RESTART
+  const int r = blockIdx.y, col = blockIdx.x * 128 + threadIdx.x;
+  if (col < d) {
+    const float v = bf16_to_f(emb[(size_t)tokens[r] * ld + col]);
+    x[(size_t)r * d + col] = v;
+    store_split(xs, ldk, r, col, __fmul_rn(v, gain[col]));
+  }
+  HS_TRACE_END(6)
+}
+
+int launch_embed_norm(const uint16_t *emb, int ld, int d, const int32_t *tokens, int t, float *x, const float *gain,
+                      uint16_t *xs, int ldk, cudaStream_t st) {
+  HS_REQUIRE(t >= 1 && t <= 8, HS_ERR_SHAPE, "embed_norm: t=%d outside [1,8]", t);
+  cudaError_t e = launch_pdl(embed_norm_kernel, dim3((d + 127) / 128, t), dim3(128), 0, st, emb, ld, d, tokens, x,
+                             gain, xs, ldk);
+  if (e != cudaSuccess) return set_error(HS_ERR_CUDA, "embed_norm launch: %s", cudaGetErrorString(e));
+  return check_launch("embed_norm");
+}
+
 // slot of the i-th new row at position p, or -1 when this rank does not store
 // it (sequence shard of a full cache: positions [pos_base, own_hi))
 __device__ __forceinline__ int append_slot(const HsStep &s, int i, int p) {

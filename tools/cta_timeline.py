@@ -26,7 +26,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 NAMES = {1: "gemv_tc", 2: "split_rows", 3: "norm_prep", 4: "attn_tc", 5: "attn_combine", 6: "embed", 7: "rope",
-         8: "attn_partial"}
+         8: "attn_partial", 9: "gemv_cc", 10: "attn_fused"}
 
 
 def main():
@@ -37,6 +37,8 @@ def main():
     ap.add_argument("--layers", type=int, default=8, help="layers shown in detail")
     ap.add_argument("--gemv", action="store_true",
                     help="per-GEMV CTA distributions (start = dependency release, griddepcontrol.wait)")
+    ap.add_argument("--graph", action="store_true",
+                    help="draft lane, t=1: replay the lane's captured step graph instead of a direct forward")
     a = ap.parse_args()
     import bench
     import paper_2404_11912_b200 as P
@@ -53,14 +55,15 @@ def main():
     lane = {"retr": sess.retr_lane, "full": sess.full_lane, "draft": sess.draft_lane}[a.lane]
     toks = torch.ones(a.t, dtype=torch.int32, device="cuda")
     f0 = lane.frontier
+    fwd = (lambda: lane.step_graph_run(1)) if a.graph else (lambda: lane._forward(toks))
     for _ in range(3):
-        lane._forward(toks)
+        fwd()
         lane.rollback_to(f0)
     cap = 1 << 18
     buf = torch.zeros(5 * cap * 3, dtype=torch.int64, device="cuda")   # 4 TU regions + GEMV phases
     torch.cuda.synchronize()
     lib.hs_cta_trace(buf.data_ptr(), cap)
-    lane._forward(toks)
+    fwd()
     torch.cuda.synchronize()
     lib.hs_cta_trace(None, 0)
     lane.rollback_to(f0)

@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
 """Device time of single lane forwards at the Llama2-7B shape (CUDA events,
-no profiler): retrieval lane t=3, full lane t=7 (context --ctx), draft t=1.
+no profiler): retrieval lane t=3, full lane t=7 (context --ctx), draft t=1, and
+the draft's captured step graph replayed back to back (draft_graph).
 
     python tools/fwdbench.py [--ctx 16384] [--reps 10]
 """
@@ -50,6 +51,19 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         out[name] = e0.elapsed_time(e1) / a.reps
+    # the draft lane's captured one-token step, replayed back to back (device
+    # time of the step as the decode loop runs it: no host launches inside)
+    sg = sess.draft_lane.step_graph()
+    for _ in range(3):
+        sg.graph.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(a.reps * 5):
+        sg.graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    out["draft_graph"] = e0.elapsed_time(e1) / (a.reps * 5)
     w = tw.device().weight_bytes
     out["dense_GBps_retr_t3"] = w / (out["retr_t3"] * 1e-3) / 1e9
     print(json.dumps(out))
