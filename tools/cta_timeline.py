@@ -26,7 +26,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 NAMES = {1: "gemv_tc", 2: "split_rows", 3: "norm_prep", 4: "attn_tc", 5: "attn_combine", 6: "embed", 7: "rope",
-         8: "attn_partial", 9: "gemv_cc", 10: "attn_fused"}
+         8: "attn_partial"}
 
 
 def main():
