@@ -113,7 +113,6 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_partial_kernel(AttnArgs a) {
       const int e = tid + u * ATT_THREADS, rr = e / DH, d = e % DH;
       qv[u] = rr < nrows ? a.q[((size_t)tok_s[rr] * a.H + head_s[rr]) * DH + d] : 0.f;
     }
-#pragma unroll
     if (s_lo < s_hi) load_tile(s_lo, min(ATT_TILE, s_hi - s_lo));   // (the first tile's K / V too)
 #pragma unroll
     for (int u = 0; u < QPT; ++u) qs[tid + u * ATT_THREADS] = qv[u];

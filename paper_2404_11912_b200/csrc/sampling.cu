@@ -294,16 +294,55 @@ __device__ int inv_cdf(Cl &cl, const double *p, const double *q, double scale, i
   return cnt < V - 1 ? cnt : V - 1;
 }
 
-__device__ double residual_mass(Cl &cl, const double *p, const double *q, int V) {
+// the residual mass Z = sum max(p - q, 0) (correct_token, speculation.py:65-72)
+// and the residual's staging for the inverse CDF in one pass over p, q:
+// sw[j - c0] = max(p_j - q_j, 0) for this CTA's slice, Z summed in a fixed
+// order (thread's strided entries -> warp -> CTA -> rank)
+__device__ double residual_stage(Cl &cl, const double *p, const double *q, int V, double *sw) {
   int c0, c1;
   cta_range(V, c0, c1);
   double z = 0.0;
 #pragma unroll
   for (int k = 0; k < SEG_REG; ++k) {
     const int j = c0 + (int)threadIdx.x + k * SMP_THREADS;
-    if (j < c1) z += fmax(p[j] - q[j], 0.0);
+    if (j < c1) {
+      const double x = fmax(p[j] - q[j], 0.0);
+      sw[j - c0] = x;
+      z += x;
+    }
   }
-  return cl.sum(z);
+  return cl.sum(z);   // (its block barrier also orders the staging stores)
+}
+
+// inv_cdf over a slice already staged in sw (residual_stage), each entry
+// divided by scale in place first: the same values and order as inv_cdf
+__device__ int inv_cdf_staged(Cl &cl, double scale, int V, double u, double *sw) {
+  int c0, c1;
+  cta_range(V, c0, c1);
+  if (scale != 1.0)
+    for (int j = c0 + (int)threadIdx.x; j < c1; j += SMP_THREADS) sw[j - c0] = sw[j - c0] / scale;
+  __syncthreads();
+  const Seg s = my_seg(V);
+  const int n = s.j1 - s.j0;
+  double w[SEG_REG];
+  double local = 0.0;
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i) {
+    w[i] = i < n ? sw[s.j0 - c0 + i] : 0.0;
+    local += w[i];
+  }
+  double c = cl.exclusive_prefix(local);
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < SEG_REG; ++i) {
+    if (i < n) {
+      c += w[i];
+      cnt += (c <= u) ? 1 : 0;
+    }
+  }
+  cnt = cl.count(cnt);
+  __syncthreads();   // sw may be restaged by a later call
+  return cnt < V - 1 ? cnt : V - 1;
 }
 
 __device__ __forceinline__ bool cl_leader() { return cg::this_cluster().block_rank() == 0 && threadIdx.x == 0; }
@@ -384,30 +423,32 @@ __global__ void __launch_bounds__(SMP_THREADS) verify_chain_kernel(const int32_t
   pdl_wait();
   HS_CL_SETUP
   extern __shared__ double sw[];
-  __shared__ int first_s, bad_s;
+  __shared__ int first_s, zero_s;
   const int cur = *cursor;
-  if (threadIdx.x == 0) { first_s = n; bad_s = 0; }
+  if (threadIdx.x == 0) { first_s = n; zero_s = n; }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += SMP_THREADS) {
     const int x = tokens[i];
     const double qx = qd[(size_t)i * V + x];
     const double px = pd[(size_t)i * V + x];
-    const bool fail = !(qx > 0.0) || !(U[cur + i] < fmin(1.0, px / qx));
+    const bool zero = !(qx > 0.0);
+    const bool fail = zero || !(U[cur + i] < fmin(1.0, px / qx));
     if (fail) atomicMin(&first_s, i);
+    if (zero) atomicMin(&zero_s, i);
   }
   __syncthreads();
   const int r = first_s;
-  if (r < n && threadIdx.x == 0) bad_s = !(qd[(size_t)r * V + tokens[r]] > 0.0);
-  __syncthreads();
-  const int status = bad_s ? HS_ERR_CONTRACT : 0;
+  // the first failing proposal raises (verify_token's q(x) = 0 check) when its
+  // draft probability is 0
+  const int status = (r < n && zero_s == r) ? HS_ERR_CONTRACT : 0;
   int tok = 0, used = 0;
   if (!status) {
     if (r < n) {
       // correct_token: residual max(p - q, 0); Z <= 1e-12 -> sample p
       const double *p = pd + (size_t)r * V, *q = qd + (size_t)r * V;
-      const double z = residual_mass(cl, p, q, V);
+      const double z = residual_stage(cl, p, q, V, sw);
       const double u2 = U[cur + r + 1];
-      tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, u2, sw) : inv_cdf(cl, p, q, z, V, u2, sw);
+      tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, u2, sw) : inv_cdf_staged(cl, z, V, u2, sw);
       used = r + 2;
     } else {
       tok = inv_cdf(cl, pd + (size_t)n * V, nullptr, 1.0, V, U[cur + n], sw);
@@ -448,8 +489,8 @@ __global__ void __launch_bounds__(SMP_THREADS) correct_token_kernel(const double
   HS_CL_SETUP
   const int cur = *cursor;
   extern __shared__ double sw[];
-  const double z = residual_mass(cl, p, q, V);
-  const int tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, U[cur], sw) : inv_cdf(cl, p, q, z, V, U[cur], sw);
+  const double z = residual_stage(cl, p, q, V, sw);
+  const int tok = (z <= 1e-12) ? inv_cdf(cl, p, nullptr, 1.0, V, U[cur], sw) : inv_cdf_staged(cl, z, V, U[cur], sw);
   cl.finish();
   if (cl_leader()) { *out = tok; *cursor = cur + 1; }
 }

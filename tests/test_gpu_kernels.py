@@ -376,6 +376,28 @@ def test_verify_chain_randomized_against_oracle(P):
         assert r1.random() == r2.random(), case      # same number of uniforms consumed
 
 
+def test_verify_chain_zero_draft_probability(P):
+    """A drafted token the draft distribution gives probability 0 raises
+    ContractError when the chain reaches it (verify_token's check,
+    speculation.py:52-62) -- after accepted proposals too -- and does not
+    when an earlier proposal already ended the chain."""
+    from oracle import hs_oracle as O
+    from paper_2404_11912_b200 import speculation as S
+    V = 8
+    one = np.zeros(V); one[3] = 1.0
+    flat = np.full(V, 1.0 / V)
+    zq = flat.copy(); zq[5] = 0.0; zq /= zq.sum()
+    # proposal 0 always accepted (p = q one-hot), proposal 1 has q(x) = 0
+    with pytest.raises(P.ContractError):
+        S._verify_chain([3, 5], [one, zq], [one, flat, flat], np.random.default_rng(1))
+    # proposal 0 rejected (p(x) = 0 < q(x)): the chain ends before the zero
+    p0 = np.full(V, 1.0 / (V - 1)); p0[3] = 0.0
+    r1, r2 = np.random.default_rng(2), np.random.default_rng(2)
+    got = S._verify_chain([3, 5], [flat, zq], [p0, flat, flat], r1)
+    assert got == O.verify_chain([3, 5], [flat, zq], [p0, flat, flat], r2)
+    assert got[2] == 0
+
+
 def test_sampling_randomized_against_oracle(P):
     """prob_from_logits + sample_from_probs (probs_kernel / sample_kernel)
     against the oracle's fp64 softmax and inverse-CDF draw
